@@ -1,0 +1,62 @@
+"""LoRAFusion-B200: B200-native FusedLoRA / FusedMultiLoRA (arXiv 2510.00206).
+
+Public API
+  FusedLoRA, FusedMultiLoRA          nn.Modules (PEFT parameter names lora_A / lora_B)
+  fused_lora, fused_multi_lora       functional forms (autograd)
+  AdapterConfig, Segment, LayerPlan  adapter hyper-parameters and microbatch segment tables
+  dropout_keep_mask                  SPEC.md §3 mask the kernels regenerate
+  traffic, GemmShape, ...            DRAM-traffic model mirroring lorasched.costmodel
+  unfused_lora                       the PEFT-style torch baseline (cuBLAS + elementwise)
+
+The compute path is the sm_100a shared library liblorafusion_b200.so (C ABI in
+include/lorafusion_b200.h). There is no CPU fallback.
+"""
+from .errors import ExtensionMissingError, KernelError, LoRAFusionError, ValidationError
+from .functional import dropout_keep_mask, fused_lora, fused_multi_lora
+from .modules import FusedLoRA, FusedMultiLoRA
+from .plan import AdapterConfig, LayerPlan, Segment, padded_rank, segments_from_lengths
+from .traffic import (
+    B200,
+    H100_SXM,
+    VARIANTS,
+    GemmShape,
+    HardwareProfile,
+    KernelTraffic,
+    TrafficReport,
+    arithmetic_intensity,
+    down_projection_intensity,
+    lora_memory_bytes,
+    roundtrip_bytes,
+    traffic,
+)
+from .baseline import unfused_lora
+
+__all__ = [
+    "AdapterConfig",
+    "B200",
+    "ExtensionMissingError",
+    "FusedLoRA",
+    "FusedMultiLoRA",
+    "GemmShape",
+    "H100_SXM",
+    "HardwareProfile",
+    "KernelError",
+    "KernelTraffic",
+    "LayerPlan",
+    "LoRAFusionError",
+    "Segment",
+    "TrafficReport",
+    "VARIANTS",
+    "ValidationError",
+    "arithmetic_intensity",
+    "down_projection_intensity",
+    "dropout_keep_mask",
+    "fused_lora",
+    "fused_multi_lora",
+    "lora_memory_bytes",
+    "padded_rank",
+    "roundtrip_bytes",
+    "segments_from_lengths",
+    "traffic",
+    "unfused_lora",
+]

@@ -1,0 +1,421 @@
+// lf_capi.cu — the extern "C" boundary (include/lorafusion_b200.h).
+//
+// Host side only: argument validation (ValueError-class failures → LF_E_INVALID, the
+// reference's ValidationError convention, ls/errors.py:12), conversion of the segment
+// table into kernel-parameter form, TMA tensor-map encoding, grid heuristics and the
+// launches. No allocation, no host synchronisation, no global device state beyond a
+// per-device cache of the SM count.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "lf_kernels.h"
+#include "lorafusion_b200.h"
+
+namespace {
+
+thread_local std::string g_err = "no error";
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  return fail(LF_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 row-major tensor [rows, cols] (row stride ld elements), box [box_rows, box_cols]
+bool make_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_cols,
+              uint32_t box_rows, CUtensorMapSwizzle sw) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct Dev {
+  int id = -1;
+  int sms = 0;
+  int major = 0;
+  int minor = 0;
+};
+
+int current_device(Dev* d) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_fail("cudaGetDevice");
+  static Dev cache[64];
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0 || dev >= 64) return fail(LF_E_CUDA, "device ordinal %d out of range", dev);
+  if (cache[dev].id != dev) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return cuda_fail("cudaGetDeviceProperties");
+    cache[dev].id = dev;
+    cache[dev].sms = prop.multiProcessorCount;
+    cache[dev].major = prop.major;
+    cache[dev].minor = prop.minor;
+  }
+  *d = cache[dev];
+  if (d->major != 10 || d->minor != 0)
+    return fail(LF_E_UNSUPPORTED, "lorafusion_b200 kernels are built for sm_100a (B200); device is sm_%d%d",
+                d->major, d->minor);
+  return LF_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// ---------------------------------------------------------------------------------
+// validation + conversion of the problem into kernel-parameter form
+// ---------------------------------------------------------------------------------
+int validate(const LfProblem* p, bool need_routes, lf::LfSegTable* t) {
+  if (!p) return fail(LF_E_INVALID, "problem is NULL");
+  if (p->m < 1 || p->k < 1 || p->n < 1) return fail(LF_E_INVALID, "m, k, n must all be >= 1, got (%d, %d, %d)", p->m, p->k, p->n);
+  if (p->k % 8 || p->n % 8)
+    return fail(LF_E_INVALID, "k and n must be multiples of 8 (16-byte TMA row pitch), got k=%d n=%d", p->k, p->n);
+  if (p->num_segments < 0 || p->num_segments > LF_MAX_SEGMENTS)
+    return fail(LF_E_INVALID, "num_segments must be in [0, %d], got %d", LF_MAX_SEGMENTS, p->num_segments);
+  if (p->rank_total < 0 || p->rank_total > LF_MAX_RANK_TOTAL || p->rank_total % 16)
+    return fail(LF_E_INVALID, "rank_total must be a multiple of 16 in [0, %d], got %d", LF_MAX_RANK_TOTAL,
+                p->rank_total);
+  if (p->num_segments > 0 && p->rank_total < 16)
+    return fail(LF_E_INVALID, "rank_total must be >= 16 when segments are present");
+  memset(t, 0, sizeof(*t));
+  t->nseg = p->num_segments;
+  t->m = p->m;
+  t->rtot = p->rank_total;
+  bool any_dropout = false;
+  int prev_row = 0, prev_col = 0;
+  for (int i = 0; i < p->num_segments; ++i) {
+    const LfSegment& s = p->segments[i];
+    if (s.row_start < prev_row || s.row_end < s.row_start || s.row_end > p->m)
+      return fail(LF_E_INVALID,
+                  "segment %d rows [%d, %d) must be sorted, disjoint and inside [0, m=%d)", i, s.row_start, s.row_end,
+                  p->m);
+    if (s.rank < 16 || s.rank % 16 || s.col_start % 16 || s.col_start < prev_col || s.col_start + s.rank > p->rank_total)
+      return fail(LF_E_INVALID,
+                  "segment %d columns [%d, %d) must be 16-aligned, increasing and inside rank_total=%d", i, s.col_start,
+                  s.col_start + s.rank, p->rank_total);
+    if (!(s.dropout_p >= 0.f && s.dropout_p < 1.f))
+      return fail(LF_E_INVALID, "segment %d dropout_p must be in [0, 1), got %g", i, (double)s.dropout_p);
+    if (!std::isfinite(s.scaling)) return fail(LF_E_INVALID, "segment %d scaling must be finite", i);
+    prev_row = s.row_end;
+    prev_col = s.col_start + s.rank;
+    lf::LfSegDev& d = t->seg[i];
+    d.row0 = s.row_start;
+    d.row1 = s.row_end;
+    d.col0 = s.col_start;
+    d.ncol = s.rank;
+    d.scale = (float)((double)s.scaling / (1.0 - (double)s.dropout_p));
+    d.thr = (uint32_t)std::floor((double)s.dropout_p * 65536.0);
+    d.key0 = (uint32_t)(s.seed & 0xFFFFFFFFull);
+    d.key1 = (uint32_t)(s.seed >> 32);
+    d.off0 = (uint32_t)(s.offset & 0xFFFFFFFFull);
+    d.off1 = (uint32_t)(s.offset >> 32);
+    if (d.thr) any_dropout = true;
+  }
+  if (p->keep_mask) {
+    t->mask_mode = 2;
+    t->mask = p->keep_mask;
+    t->ld_mask = p->k;
+  } else {
+    t->mask_mode = any_dropout ? 1 : 0;
+  }
+  if (need_routes && p->num_segments > 0 && !p->routes) return fail(LF_E_INVALID, "routes is NULL (call lf_build_routes)");
+  return LF_OK;
+}
+
+int check_ptr(const void* ptr, const char* name) {
+  if (!ptr) return fail(LF_E_INVALID, "%s is NULL", name);
+  if (!aligned16(ptr)) return fail(LF_E_INVALID, "%s must be 16-byte aligned", name);
+  return LF_OK;
+}
+
+int check_workspace(const LfProblem* p) {
+  if (!p->workspace) return fail(LF_E_INVALID, "workspace is NULL");
+  if (p->workspace_bytes < lf_workspace_bytes(p->m, p->rank_total))
+    return fail(LF_E_INVALID, "workspace too small: %zu < %zu bytes", p->workspace_bytes,
+                lf_workspace_bytes(p->m, p->rank_total));
+  if (!aligned16(p->workspace)) return fail(LF_E_INVALID, "workspace must be 16-byte aligned");
+  return LF_OK;
+}
+
+void split_workspace(const LfProblem* p, float** ws, int32_t** counters) {
+  *ws = reinterpret_cast<float*>(p->workspace);
+  *counters = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(p->workspace) +
+                                         align_up((size_t)p->m * p->rank_total * 4, 256));
+}
+
+int occupancy_for_smem(int smem_bytes) {
+  const int per_sm = 228 * 1024;
+  int c = per_sm / (smem_bytes + 1024);
+  return c < 1 ? 1 : c;
+}
+
+#define LF_TRY(expr)             \
+  do {                           \
+    const int _rc = (expr);      \
+    if (_rc != LF_OK) return _rc; \
+  } while (0)
+
+}  // namespace
+
+// =================================================================================
+extern "C" {
+
+int lf_abi_version(void) { return LF_ABI_VERSION; }
+
+const char* lf_last_error(void) { return g_err.c_str(); }
+
+size_t lf_workspace_bytes(int32_t m, int32_t rank_total) {
+  if (m < 0 || rank_total < 0) return 0;
+  const size_t tiles = ((size_t)m + 127) / 128;
+  return align_up((size_t)m * rank_total * 4, 256) + align_up(tiles * 4, 256);
+}
+
+int lf_build_routes(const LfProblem* p, int32_t* routes_out, void* stream) {
+  lf::LfSegTable t;
+  LF_TRY(validate(p, false, &t));
+  LF_TRY(check_ptr(routes_out, "routes_out"));
+  Dev d;
+  LF_TRY(current_device(&d));
+  if (lf::routes_launch(t, routes_out, (p->m + 127) / 128, (cudaStream_t)stream)) return cuda_fail("routes launch");
+  return LF_OK;
+}
+
+int lf_dropout_mask(const LfProblem* p, uint8_t* keep_out, void* stream) {
+  lf::LfSegTable t;
+  LF_TRY(validate(p, false, &t));
+  if (!keep_out) return fail(LF_E_INVALID, "keep_out is NULL");
+  Dev d;
+  LF_TRY(current_device(&d));
+  if (lf::mask_launch(t, p->k, keep_out, (cudaStream_t)stream)) return cuda_fail("mask launch");
+  return LF_OK;
+}
+
+int lf_dropout_down_fwd(const LfProblem* p, const uint16_t* x, const uint16_t* a_cat, uint16_t* s_hat,
+                        void* stream) {
+  lf::LfSegTable t;
+  LF_TRY(validate(p, true, &t));
+  if (p->num_segments == 0) return fail(LF_E_INVALID, "lf_dropout_down_fwd needs at least one segment");
+  LF_TRY(check_ptr(x, "x"));
+  LF_TRY(check_ptr(a_cat, "a_cat"));
+  LF_TRY(check_ptr(s_hat, "s_hat"));
+  LF_TRY(check_workspace(p));
+  Dev d;
+  LF_TRY(current_device(&d));
+  CUtensorMap tx, ta;
+  if (!make_map(&tx, x, p->m, p->k, p->k, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&ta, a_cat, p->rank_total, p->k, p->k, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B))
+    return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (x / a_cat)");
+  lf::DownArgs a;
+  memset(&a, 0, sizeof(a));
+  a.m = p->m;
+  a.k = p->k;
+  a.rtot = p->rank_total;
+  a.s_hat = s_hat;
+  split_workspace(p, &a.ws, &a.counters);
+  a.routes = reinterpret_cast<const lf::LfRoute*>(p->routes);
+  a.segs = t;
+  const int tiles_m = (p->m + 127) / 128;
+  const int nkb = (p->k + 63) / 64;
+  int stages = 0, stage_bytes = 0;
+  lf::down_config(p->rank_total, &stages, &stage_bytes);
+  const int occ = occupancy_for_smem(stages * stage_bytes + 2048);
+  const int target = occ * d.sms;
+  int ksplit = (target + tiles_m - 1) / tiles_m;
+  const int max_split = nkb >= 8 ? nkb / 4 : 1;
+  if (ksplit > max_split) ksplit = max_split;
+  if (ksplit < 1) ksplit = 1;
+  a.ksplit = ksplit;
+  if (lf::down_launch(tx, ta, a, d.sms, (cudaStream_t)stream)) return cuda_fail("dropout_down launch");
+  return LF_OK;
+}
+
+int lf_base_fwd(const LfProblem* p, const uint16_t* x, const uint16_t* w, const uint16_t* s_hat,
+                const uint16_t* b_cat, uint16_t* y, void* stream) {
+  lf::LfSegTable t;
+  LF_TRY(validate(p, true, &t));
+  LF_TRY(check_ptr(x, "x"));
+  LF_TRY(check_ptr(w, "w"));
+  LF_TRY(check_ptr(y, "y"));
+  const bool lora = p->num_segments > 0;
+  if (lora) {
+    LF_TRY(check_ptr(s_hat, "s_hat"));
+    LF_TRY(check_ptr(b_cat, "b_cat"));
+  }
+  Dev d;
+  LF_TRY(current_device(&d));
+  lf::GemmMaps maps;
+  if (!make_map(&maps.a, x, p->m, p->k, p->k, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&maps.b, w, p->n, p->k, p->k, 64, 256, CU_TENSOR_MAP_SWIZZLE_128B))
+    return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (x / w)");
+  if (lora) {
+    if (!make_map(&maps.a2, s_hat, p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
+        !make_map(&maps.b2, b_cat, p->n, p->rank_total, p->rank_total, 16, 256, CU_TENSOR_MAP_SWIZZLE_32B))
+      return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (s_hat / b_cat)");
+  } else {
+    maps.a2 = maps.a;
+    maps.b2 = maps.b;
+  }
+  lf::GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = p->m;
+  a.N = p->n;
+  a.K = p->k;
+  a.ldc = p->n;
+  a.C = y;
+  a.routes = lora ? reinterpret_cast<const lf::LfRoute*>(p->routes) : nullptr;
+  a.segs = t;
+  if (lf::gemm_launch(lf::kGemmFwd, maps, a, d.sms, (cudaStream_t)stream)) return cuda_fail("base_fwd launch");
+  return LF_OK;
+}
+
+int lf_grad_up(const LfProblem* p, const uint16_t* dy, const uint16_t* b_cat, const uint16_t* s_hat, uint16_t* ds,
+               float* db_accum, void* stream) {
+  lf::LfSegTable t;
+  LF_TRY(validate(p, true, &t));
+  if (p->num_segments == 0) return fail(LF_E_INVALID, "lf_grad_up needs at least one segment");
+  LF_TRY(check_ptr(dy, "dy"));
+  LF_TRY(check_ptr(b_cat, "b_cat"));
+  LF_TRY(check_ptr(s_hat, "s_hat"));
+  LF_TRY(check_ptr(ds, "ds"));
+  LF_TRY(check_ptr(db_accum, "db_accum"));
+  LF_TRY(check_workspace(p));
+  Dev d;
+  LF_TRY(current_device(&d));
+  CUtensorMap tdy, tb, ts;
+  if (!make_map(&tdy, dy, p->m, p->n, p->n, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&tb, b_cat, p->n, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
+      !make_map(&ts, s_hat, p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B))
+    return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (dy / b_cat / s_hat)");
+  lf::GradUpArgs a;
+  memset(&a, 0, sizeof(a));
+  a.m = p->m;
+  a.n = p->n;
+  a.rtot = p->rank_total;
+  a.ds = ds;
+  a.db = db_accum;
+  split_workspace(p, &a.ws, &a.counters);
+  a.routes = reinterpret_cast<const lf::LfRoute*>(p->routes);
+  a.segs = t;
+  lf::grad_up_grid(p->m, p->n, p->rank_total, d.sms, &a.n_split, &a.m_split);
+  if (a.n_split <= 0) return fail(LF_E_INVALID, "rank_total=%d too large for grad_up TMEM budget", p->rank_total);
+  if (lf::grad_up_launch(tdy, tb, ts, a, d.sms, (cudaStream_t)stream)) return cuda_fail("grad_up launch");
+  return LF_OK;
+}
+
+int lf_grad_down(const LfProblem* p, const uint16_t* x, const uint16_t* ds, float* da_accum, void* stream) {
+  lf::LfSegTable t;
+  LF_TRY(validate(p, true, &t));
+  if (p->num_segments == 0) return fail(LF_E_INVALID, "lf_grad_down needs at least one segment");
+  LF_TRY(check_ptr(x, "x"));
+  LF_TRY(check_ptr(ds, "ds"));
+  LF_TRY(check_ptr(da_accum, "da_accum"));
+  Dev d;
+  LF_TRY(current_device(&d));
+  CUtensorMap tx, td;
+  if (!make_map(&tx, x, p->m, p->k, p->k, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&td, ds, p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B))
+    return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (x / ds)");
+  lf::GradDownArgs a;
+  memset(&a, 0, sizeof(a));
+  a.m = p->m;
+  a.k = p->k;
+  a.rtot = p->rank_total;
+  a.da = da_accum;
+  a.routes = reinterpret_cast<const lf::LfRoute*>(p->routes);
+  a.segs = t;
+  int stages = 0, stage_bytes = 0;
+  lf::grad_down_config(p->rank_total, &stages, &stage_bytes);
+  const int occ = occupancy_for_smem(stages * stage_bytes + 2048);
+  const int tiles_k = (p->k + 127) / 128;
+  const int tiles_m = (p->m + 127) / 128;
+  int ms = (occ * d.sms + tiles_k - 1) / tiles_k;
+  if (ms > tiles_m) ms = tiles_m;
+  if (ms < 1) ms = 1;
+  a.m_split = ms;
+  if (lf::grad_down_launch(tx, td, a, d.sms, (cudaStream_t)stream)) return cuda_fail("grad_down launch");
+  return LF_OK;
+}
+
+int lf_grad_input(const LfProblem* p, const uint16_t* dy, const uint16_t* w, const uint16_t* ds,
+                  const uint16_t* a_cat, uint16_t* dx, void* stream) {
+  lf::LfSegTable t;
+  LF_TRY(validate(p, true, &t));
+  LF_TRY(check_ptr(dy, "dy"));
+  LF_TRY(check_ptr(w, "w"));
+  LF_TRY(check_ptr(dx, "dx"));
+  const bool lora = p->num_segments > 0;
+  if (lora) {
+    LF_TRY(check_ptr(ds, "ds"));
+    LF_TRY(check_ptr(a_cat, "a_cat"));
+  }
+  Dev d;
+  LF_TRY(current_device(&d));
+  const bool masked = lora && t.mask_mode != 0;
+  lf::GemmMaps maps;
+  // dX[m, k] = dY[m, n] · W[n, k]: A = dY (K-major), B = W (MN-major), K = n
+  if (!make_map(&maps.a, dy, p->m, p->n, p->n, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&maps.b, w, p->n, p->k, p->k, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))
+    return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (dy / w)");
+  if (lora) {
+    if (!make_map(&maps.a2, ds, p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
+        !make_map(&maps.b2, a_cat, p->rank_total, p->k, p->k, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B))
+      return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (ds / a_cat)");
+  } else {
+    maps.a2 = maps.a;
+    maps.b2 = maps.b;
+  }
+  lf::GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = p->m;
+  a.N = p->k;
+  a.K = p->n;
+  a.ldc = p->k;
+  a.C = dx;
+  a.routes = lora ? reinterpret_cast<const lf::LfRoute*>(p->routes) : nullptr;
+  a.segs = t;
+  if (lf::gemm_launch(masked ? lf::kGemmDgradMasked : lf::kGemmDgrad, maps, a, d.sms, (cudaStream_t)stream))
+    return cuda_fail("grad_input launch");
+  return LF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,324 @@
+// lf_gradup.cu — ③ grad_up_fused: one read of dY serves both rank-R gradients.
+//
+// Reference contract: ls/costmodel.py:268-269 (R (mn + mr + rn), W (mr + rn)).
+//   dŜ     = bf16( s_seg · dY·B_cat )   (m x R; off-segment columns zero)
+//   dB_cat += dYᵀ·Ŝ                     (n x R, fp32)
+//
+// Each CTA owns a block of 128-row m-tiles x 128-column n-subtiles. Every dY tile is
+// TMA-loaded once into shared memory and consumed by two tcgen05 MMAs through two
+// descriptors over the same bytes: K-major (rows = tokens) for dŜ += dY·B_cat, and
+// MN-major (rows = out features) for dBᵀ += dYᵀ·Ŝ. Both accumulators live in TMEM:
+// dŜ double-buffered per m-tile, dB per n-subtile for the CTA's whole m-range.
+// dŜ partials over n-subtiles meet in an fp32 workspace (red.global.add); the CTA that
+// completes a tile's count finalizes it (scale, mask off-segment columns, bf16) and
+// re-zeroes the workspace.
+#include "lf_device.cuh"
+#include "lf_kernels.h"
+
+namespace lf {
+
+namespace gup {
+constexpr int DY_BYTES = 2 * 128 * 64 * 2;  // 32 KB: two 64-column SW128 boxes of 128 rows
+constexpr int MAX_SMEM = 200 * 1024;
+}  // namespace gup
+
+__device__ __forceinline__ void finalize_row_up(const LfSegTable& t, const LfRoute& rt, int row, float* ws,
+                                                __nv_bfloat16* out) {
+  const int rtot = t.rtot;
+  const int seg = find_segment(t, rt.seg_lo, rt.seg_hi, row);
+  const int own0 = seg >= 0 ? t.seg[seg].col0 : 0;
+  const int own1 = seg >= 0 ? t.seg[seg].col0 + t.seg[seg].ncol : 0;
+  const float scale = seg >= 0 ? t.seg[seg].scale : 0.f;
+  float* wrow = ws + (int64_t)row * rtot;
+  __nv_bfloat16* orow = out + (int64_t)row * rtot;
+  for (int c = 0; c < rtot; c += 8) {
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (c >= rt.col_lo && c < rt.col_hi) {
+      const float4 a = ld_cg_f4(wrow + c), b = ld_cg_f4(wrow + c + 4);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+      *reinterpret_cast<float4*>(wrow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(wrow + c + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float s = (c >= own0 && c < own1) ? scale : 0.f;
+    *reinterpret_cast<uint4*>(orow + c) = make_uint4(pack_bf16x2(v[0] * s, v[1] * s), pack_bf16x2(v[2] * s, v[3] * s),
+                                                     pack_bf16x2(v[4] * s, v[5] * s), pack_bf16x2(v[6] * s, v[7] * s));
+  }
+}
+
+__global__ void __launch_bounds__(192, 1)
+    lf_gradup_kernel(const __grid_constant__ CUtensorMap tmDy, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmS, const __grid_constant__ GradUpArgs args, int stages,
+                     int stage_bytes) {
+  using namespace gup;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int rtot = args.rtot;
+  const int sh_bytes = (rtot / 16) * 4096;
+  uint8_t* sSh0 = smem + stages * stage_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sSh0 + 2 * sh_bytes);
+  uint64_t* empty = full + stages;
+  uint64_t* sh_full = empty + stages;   // [2]
+  uint64_t* sh_empty = sh_full + 2;     // [2]
+  uint64_t* ds_full = sh_empty + 2;     // [2]
+  uint64_t* ds_empty = ds_full + 2;     // [2]
+  uint64_t* db_full = ds_empty + 2;     // [1]
+  uint64_t* tzero = db_full + 1;        // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tzero + 1);
+  volatile int* s_last = reinterpret_cast<volatile int*>(tmem_slot + 1);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int tiles_m = (args.m + 127) / 128;
+  const int tiles_n = (args.n + 127) / 128;
+  const int nt0 = (int)((int64_t)blockIdx.x * tiles_n / args.n_split);
+  const int nt1 = (int)((int64_t)(blockIdx.x + 1) * tiles_n / args.n_split);
+  const int mt0 = (int)((int64_t)blockIdx.y * tiles_m / args.m_split);
+  const int mt1 = (int)((int64_t)(blockIdx.y + 1) * tiles_m / args.m_split);
+  const int nsub = nt1 - nt0;
+  const uint32_t tmem_need = (uint32_t)((2 + nsub) * rtot);
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < tmem_need) tmem_cols <<= 1;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&sh_full[a], 1);
+      mbar_init(&sh_empty[a], 1);
+      mbar_init(&ds_full[a], 1);
+      mbar_init(&ds_empty[a], 4);
+    }
+    mbar_init(db_full, 1);
+    mbar_init(tzero, 4);
+    fence_barrier_init();
+    tma_prefetch_desc(&tmDy);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmS);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tm_ds = tmem;              // 2 x rtot columns
+  const uint32_t tm_db = tmem + 2 * rtot;   // nsub x rtot columns
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0 && nsub > 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int lm = 0;
+      for (int mt = mt0; mt < mt1; ++mt) {
+        const LfRoute rt = args.routes[mt];
+        const int N = rt.col_hi - rt.col_lo;
+        if (N <= 0) continue;
+        const int b = lm & 1;
+        const uint32_t bph = (lm >> 1) & 1;
+        ++lm;
+        mbar_wait(&sh_empty[b], bph ^ 1);
+        uint8_t* sSh = sSh0 + b * sh_bytes;
+        mbar_arrive_expect_tx(&sh_full[b], (N / 16) * 4096);
+        for (int j = 0; j < N / 16; ++j) tma_load_2d(sSh + j * 4096, &tmS, &sh_full[b], rt.col_lo + 16 * j, mt * 128);
+        for (int nt = nt0; nt < nt1; ++nt) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sDy = smem + stage * stage_bytes;
+          uint8_t* sB = sDy + DY_BYTES;
+          mbar_arrive_expect_tx(&full[stage], DY_BYTES + (N / 16) * 4096);
+          tma_load_2d(sDy, &tmDy, &full[stage], nt * 128, mt * 128);
+          tma_load_2d(sDy + 16384, &tmDy, &full[stage], nt * 128 + 64, mt * 128);
+          for (int j = 0; j < N / 16; ++j) tma_load_2d(sB + j * 4096, &tmB, &full[stage], rt.col_lo + 16 * j, nt * 128);
+          if (++stage == stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && nsub > 0) {
+      mbar_wait(tzero, 0);
+      tc_fence_after();
+      int stage = 0;
+      uint32_t phase = 0;
+      int lm = 0;
+      for (int mt = mt0; mt < mt1; ++mt) {
+        const LfRoute rt = args.routes[mt];
+        const int N = rt.col_hi - rt.col_lo;
+        if (N <= 0) continue;
+        const int b = lm & 1;
+        const uint32_t bph = (lm >> 1) & 1;
+        ++lm;
+        mbar_wait(&ds_empty[b], bph ^ 1);
+        mbar_wait(&sh_full[b], bph);
+        tc_fence_after();
+        const uint32_t sSh = smem_u32(sSh0 + b * sh_bytes);
+        const uint32_t d_ds = tm_ds + b * rtot + rt.col_lo;
+        const uint32_t idesc_ds = make_idesc_bf16(128, (uint32_t)N, false, true);
+        const uint32_t idesc_db = make_idesc_bf16(128, (uint32_t)N, true, true);
+        for (int nt = nt0; nt < nt1; ++nt) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sDy = smem_u32(smem + stage * stage_bytes);
+          const uint32_t sB = sDy + DY_BYTES;
+          // dŜ[m-tile] += dY[m-tile, n-sub] · B_cat[n-sub, cols]      (K = 128 out features)
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            umma_bf16(d_ds, make_sdesc(sDy + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, kLayoutSW128),
+                      make_sdesc(sB + kk * 512, 4096, 256, kLayoutSW32), idesc_ds, (nt > nt0 || kk > 0) ? 1u : 0u);
+          }
+          // dB_cat[n-sub, cols] += dY[m-tile, n-sub]ᵀ · Ŝ[m-tile, cols]  (K = 128 tokens)
+          const uint32_t d_db = tm_db + (nt - nt0) * rtot + rt.col_lo;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            umma_bf16(d_db, make_sdesc(sDy + kk * 2048, 16384, 1024, kLayoutSW128),
+                      make_sdesc(sSh + kk * 512, 4096, 256, kLayoutSW32), idesc_db, 1u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == stages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&ds_full[b]);
+        umma_commit(&sh_empty[b]);
+      }
+      umma_commit(db_full);
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 2..5)
+    const uint32_t q = warp & 3u;
+    const uint32_t lane_off = (q * 32u) << 16;
+    if (nsub > 0) {
+      uint32_t z[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) z[i] = 0u;
+      for (int c = 0; c < nsub * rtot; c += 16) tmem_st16(tm_db + lane_off + c, z);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tzero);
+    }
+    const int rit = (int)(q * 32 + lane);
+    int lm = 0;
+    uint32_t touched = 0;
+    for (int mt = mt0; mt < mt1; ++mt) {
+      const LfRoute rt = args.routes[mt];
+      const int N = rt.col_hi - rt.col_lo;
+      const int row = mt * 128 + rit;
+      if (N > 0 && nsub > 0) {
+        for (int c = rt.col_lo; c < rt.col_hi; c += 16) touched |= 1u << (c >> 4);
+        const int b = lm & 1;
+        const uint32_t bph = (lm >> 1) & 1;
+        ++lm;
+        mbar_wait(&ds_full[b], bph);
+        tc_fence_after();
+        float* wrow = args.ws + (int64_t)row * rtot + rt.col_lo;
+        for (int c = 0; c < N; c += 16) {
+          uint32_t v[16];
+          tmem_ld16(tm_ds + lane_off + b * rtot + rt.col_lo + c, v);
+          tmem_ld_wait();
+          if (row < args.m) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4)
+              red_add_v4(wrow + c + j, __uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                         __uint_as_float(v[j + 3]));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ds_empty[b]);
+      }
+      // tile completion across the n-split
+      __threadfence();
+      named_bar_sync(1, 128);
+      if (warp == 2 && lane == 0) {
+        const int old = atomicAdd(&args.counters[mt], nsub);
+        *s_last = (old + nsub == tiles_n) ? 1 : 0;
+      }
+      named_bar_sync(1, 128);
+      if (*s_last) {
+        __threadfence();
+        if (row < args.m) finalize_row_up(args.segs, rt, row, args.ws, reinterpret_cast<__nv_bfloat16*>(args.ds));
+        if (warp == 2 && lane == 0) args.counters[mt] = 0;
+      }
+      named_bar_sync(1, 128);
+    }
+    if (touched && nsub > 0) {
+      mbar_wait(db_full, 0);
+      tc_fence_after();
+      for (int i = 0; i < nsub; ++i) {
+        const int ncol = (nt0 + i) * 128 + rit;
+        float* drow = args.db + (int64_t)ncol * rtot;
+        for (int g = 0; g < rtot / 16; ++g) {
+          if (!((touched >> g) & 1u)) continue;
+          uint32_t v[16];
+          tmem_ld16(tm_db + lane_off + i * rtot + g * 16, v);
+          tmem_ld_wait();
+          if (ncol < args.n) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4)
+              red_add_v4(drow + g * 16 + j, __uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                         __uint_as_float(v[j + 3]));
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, tmem_cols);
+  }
+}
+
+// CTA grid: n_split x m_split blocks of (n-subtiles x m-tiles). The dB accumulators of a
+// CTA's n-range must fit TMEM next to the two dŜ buffers: (2 + nsub) * R <= 512.
+// Among admissible splits pick the smallest critical path (max units of one 32 KB dY tile
+// per CTA), then the least partial-sum traffic R * (m_split * n + n_split * m).
+void grad_up_grid(int m, int n, int rtot, int sms, int* n_split, int* m_split) {
+  const int tiles_m = (m + 127) / 128, tiles_n = (n + 127) / 128;
+  const int max_nsub = 512 / rtot - 2;
+  *n_split = 0;
+  *m_split = 0;
+  if (max_nsub < 1) return;
+  long best_units = -1;
+  double best_traffic = 0;
+  for (int ns = (tiles_n + max_nsub - 1) / max_nsub; ns <= tiles_n; ++ns) {
+    int ms = sms / ns;
+    if (ms < 1) ms = 1;
+    if (ms > tiles_m) ms = tiles_m;
+    const long units = (long)((tiles_m + ms - 1) / ms) * ((tiles_n + ns - 1) / ns);
+    const double traffic = (double)rtot * ((double)ms * n + (double)ns * m);
+    if (best_units < 0 || units < best_units || (units == best_units && traffic < best_traffic)) {
+      best_units = units;
+      best_traffic = traffic;
+      *n_split = ns;
+      *m_split = ms;
+    }
+  }
+}
+
+int grad_up_launch(const CUtensorMap& tm_dy, const CUtensorMap& tm_b, const CUtensorMap& tm_s,
+                   const GradUpArgs& args, int num_sms, cudaStream_t stream) {
+  (void)num_sms;
+  const int sh_bytes = (args.rtot / 16) * 4096;
+  const int stage_bytes = gup::DY_BYTES + sh_bytes;
+  int stages = (gup::MAX_SMEM - 2 * sh_bytes) / stage_bytes;
+  if (stages > 4) stages = 4;
+  if (stages < 2) return -1;
+  const int smem = stages * stage_bytes + 2 * sh_bytes + 1024 + 256;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(lf_gradup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gup::MAX_SMEM + 2048) !=
+        cudaSuccess)
+      return -1;
+    configured = true;
+  }
+  dim3 grid(args.n_split, args.m_split);
+  lf_gradup_kernel<<<grid, 192, smem, stream>>>(tm_dy, tm_b, tm_s, args, stages, stage_bytes);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace lf

@@ -1,0 +1,80 @@
+// lf_kernels.h — host-visible launch entry points of the sm_100a kernels (internal).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lf_params.h"
+
+namespace lf {
+
+// ② / ⑤: persistent warp-specialised tcgen05 GEMM  C[M,N] = A[M,K]·B (+ LoRA K-chunk).
+//  kind FWD       : B is K-major  (N x K, nn.Linear.weight), LoRA B2 = B_cat (N x R) K-major
+//  kind DGRAD     : B is MN-major (K x N, W as stored),      LoRA B2 = A_cat (R x N) MN-major,
+//                   LoRA term concatenated into the main accumulator (no dropout)
+//  kind DGRAD_MASK: as DGRAD but the LoRA term lands in a second TMEM accumulator and is
+//                   combined as acc + keep ⊙ acc_lora in the epilogue (dropout p > 0)
+enum GemmKind { kGemmFwd = 0, kGemmDgrad = 1, kGemmDgradMasked = 2 };
+
+struct GemmArgs {
+  int32_t M, N, K;
+  int32_t tiles_m, tiles_n;
+  int64_t ldc;
+  void* C;                // bf16 output, row-major M x N (ldc elements)
+  const LfRoute* routes;  // nullptr = no LoRA chunk
+  LfSegTable segs;        // keep-mask source for kGemmDgradMasked
+};
+
+struct GemmMaps {
+  CUtensorMap a, b, a2, b2;
+};
+
+int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& args, int num_sms, cudaStream_t stream);
+
+// ① dropout + down projection
+struct DownArgs {
+  int32_t m, k, rtot;
+  int32_t ksplit;         // CTAs along K per 128-row tile
+  void* s_hat;            // bf16 m x rtot
+  float* ws;              // fp32 m x rtot partials (zero on entry and exit)
+  int32_t* counters;      // per 128-row tile (zero on entry and exit)
+  const LfRoute* routes;
+  LfSegTable segs;
+};
+void down_config(int rtot, int* stages, int* stage_bytes);
+int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs& args, int num_sms,
+                cudaStream_t stream);
+
+// ③ fused dS / dB
+struct GradUpArgs {
+  int32_t m, n, rtot;
+  int32_t n_split, m_split;  // CTA grid
+  void* ds;                  // bf16 m x rtot
+  float* db;                 // fp32 n x rtot accumulator
+  float* ws;                 // fp32 m x rtot partials (zero on entry and exit)
+  int32_t* counters;         // per 128-row tile
+  const LfRoute* routes;
+  LfSegTable segs;
+};
+void grad_up_grid(int m, int n, int rtot, int sms, int* n_split, int* m_split);
+int grad_up_launch(const CUtensorMap& tm_dy, const CUtensorMap& tm_b, const CUtensorMap& tm_s,
+                   const GradUpArgs& args, int num_sms, cudaStream_t stream);
+
+// ④ dA
+struct GradDownArgs {
+  int32_t m, k, rtot;
+  int32_t m_split;
+  float* da;  // fp32 rtot x k accumulator
+  const LfRoute* routes;
+  LfSegTable segs;
+};
+void grad_down_config(int rtot, int* stages, int* stage_bytes);
+int grad_down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_ds, const GradDownArgs& args, int num_sms,
+                     cudaStream_t stream);
+
+// routing table + explicit mask materialisation
+int routes_launch(const LfSegTable& segs, int32_t* routes, int ntiles, cudaStream_t stream);
+int mask_launch(const LfSegTable& segs, int32_t k, uint8_t* keep, cudaStream_t stream);
+
+}  // namespace lf

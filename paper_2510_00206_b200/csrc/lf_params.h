@@ -1,0 +1,41 @@
+// lf_params.h — kernel parameter structs shared by the host launchers and the kernels.
+// Passed by value (kernel parameter space), so a launch needs no H2D copy of the
+// segment table: the per-segment data rides in the constant bank of every CTA.
+#pragma once
+
+#include <stdint.h>
+
+#define LF_MAX_SEGS 32
+#define LF_TILE_M 128
+#define LF_MAX_RANK 128
+
+namespace lf {
+
+// Device-side view of one LfSegment (include/lorafusion_b200.h) with the derived
+// quantities precomputed on the host: scale = scaling / (1 - p) as fp32 and the
+// integer dropout threshold thr = floor(p * 65536) (SPEC.md §3).
+struct LfSegDev {
+  int32_t row0, row1;  // token rows [row0, row1)
+  int32_t col0, ncol;  // rank-concat columns [col0, col0 + ncol)
+  float scale;         // scaling / (1 - p)
+  uint32_t thr;        // keep iff u16 >= thr
+  uint32_t key0, key1; // Philox key (seed)
+  uint32_t off0, off1; // Philox counter words 2,3 (offset)
+};
+
+struct LfSegTable {
+  int32_t nseg;
+  int32_t m;
+  int32_t rtot;         // rank-concat width R
+  int32_t mask_mode;    // 0 = no dropout anywhere, 1 = Philox, 2 = explicit uint8 mask
+  const uint8_t* mask;  // explicit keep mask (m x ld_mask) when mask_mode == 2
+  int64_t ld_mask;
+  LfSegDev seg[LF_MAX_SEGS];
+};
+
+// per-128-row routing entry (16 B): segments [seg_lo, seg_hi], columns [col_lo, col_hi)
+struct LfRoute {
+  int32_t seg_lo, seg_hi, col_lo, col_hi;
+};
+
+}  // namespace lf

@@ -1,0 +1,193 @@
+"""Functional FusedLoRA / FusedMultiLoRA (forward + backward through the sm_100a kernels).
+
+Forward:  ① lf_dropout_down_fwd   Ŝ = s·(M⊙X)·Aᵀ
+                               ② lf_base_fwd           Y = X·Wᵀ + Ŝ·Bᵀ   (one write of Y)
+Backward:  ③ lf_grad_up            dŜ = s·dY·B, dB += dYᵀ·Ŝ   (one read of dY)
+                               ④ lf_grad_down          dA += dŜᵀ·(M⊙X)
+                               ⑤ lf_grad_input         dX = dY·W + M⊙(dŜ·A)       (one write of dX)
+
+The base weight is frozen (LoRA fine-tuning); there is no CPU path — tensors must live on
+a B200 and the shared library must be built, otherwise the call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Callable, Sequence
+
+import torch
+
+from . import _lib
+from .errors import ValidationError
+from .plan import AdapterConfig, LayerPlan, Segment
+
+_BF16 = torch.bfloat16
+
+
+def _ptr(t: torch.Tensor | None) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+def _stream() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _check_operand(t: torch.Tensor, name: str, shape: tuple | None = None) -> None:
+    if not isinstance(t, torch.Tensor):
+        raise ValidationError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValidationError(f"{name} must be a CUDA tensor on a B200 (no CPU fallback)")
+    if t.dtype != _BF16:
+        raise ValidationError(f"{name} must be bfloat16, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValidationError(f"{name} must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValidationError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+
+
+class _FusedLoRAFn(torch.autograd.Function):
+    """Autograd node over the five kernels. Inputs: x (m,k), w (n,k), a_cat (R,k), b_cat (n,R)."""
+
+    @staticmethod
+    def forward(ctx, x, w, a_cat, b_cat, plan: LayerPlan, grad_sink):
+        lib = _lib.load()
+        m, k, n, R = plan.m, plan.k, plan.n, plan.rank_total
+        pp = ctypes.byref(plan.problem)
+        y = torch.empty((m, n), dtype=_BF16, device=x.device)
+        s_hat = None
+        if plan.has_lora:
+            s_hat = torch.empty((m, R), dtype=_BF16, device=x.device)
+            _lib.check(lib.lf_dropout_down_fwd(pp, _ptr(x), _ptr(a_cat), _ptr(s_hat), _stream()), "dropout_down_fwd")
+        _lib.check(lib.lf_base_fwd(pp, _ptr(x), _ptr(w), _ptr(s_hat), _ptr(b_cat), _ptr(y), _stream()), "base_fwd")
+        ctx.plan = plan
+        ctx.grad_sink = grad_sink
+        ctx.save_for_backward(x, w, a_cat, b_cat, s_hat)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        lib = _lib.load()
+        plan: LayerPlan = ctx.plan
+        x, w, a_cat, b_cat, s_hat = ctx.saved_tensors
+        m, k, n, R = plan.m, plan.k, plan.n, plan.rank_total
+        dy = dy.to(_BF16).contiguous()
+        pp = ctypes.byref(plan.problem)
+        da = db = ds = None
+        if plan.has_lora:
+            ds = torch.empty((m, R), dtype=_BF16, device=dy.device)
+            db = torch.zeros((n, R), dtype=torch.float32, device=dy.device)
+            da = torch.zeros((R, k), dtype=torch.float32, device=dy.device)
+            _lib.check(lib.lf_grad_up(pp, _ptr(dy), _ptr(b_cat), _ptr(s_hat), _ptr(ds), _ptr(db), _stream()), "grad_up")
+            _lib.check(lib.lf_grad_down(pp, _ptr(x), _ptr(ds), _ptr(da), _stream()), "grad_down")
+        dx = None
+        if ctx.needs_input_grad[0]:
+            dx = torch.empty((m, k), dtype=_BF16, device=dy.device)
+            _lib.check(lib.lf_grad_input(pp, _ptr(dy), _ptr(w), _ptr(ds), _ptr(a_cat), _ptr(dx), _stream()),
+                       "grad_input")
+        if ctx.grad_sink is not None and plan.has_lora:
+            ctx.grad_sink(plan, da, db)
+        return dx, None, da, db, None, None
+
+
+def _flatten_input(x: torch.Tensor, k: int) -> tuple[torch.Tensor, tuple]:
+    if x.shape[-1] != k:
+        raise ValidationError(f"input last dim {x.shape[-1]} != in_features {k}")
+    lead = tuple(x.shape[:-1])
+    x2 = x.reshape(-1, k)
+    if x2.dtype != _BF16:
+        raise ValidationError(f"input must be bfloat16, got {x2.dtype}")
+    return x2.contiguous(), lead
+
+
+def _check_frozen(weight: torch.Tensor) -> None:
+    if weight.requires_grad:
+        raise ValidationError(
+            "the base weight must be frozen (requires_grad=False): FusedLoRA trains only the adapters"
+        )
+
+
+def fused_lora(
+    x: torch.Tensor,
+    weight: torch.Tensor,
+    lora_a: torch.Tensor,
+    lora_b: torch.Tensor,
+    scaling: float,
+    dropout_p: float = 0.0,
+    seed: int = 0,
+    offset: int = 0,
+    keep_mask: torch.Tensor | None = None,
+    training: bool = True,
+) -> torch.Tensor:
+    """Y = X·Wᵀ + scaling·dropout(X)·Aᵀ·Bᵀ  (Eq. 1) on one adapter.
+
+    x (..., k) bf16; weight (n, k) = nn.Linear.weight (frozen); lora_a (r, k) =
+    lora_A.weight; lora_b (n, r) = lora_B.weight. Dropout uses SPEC.md §3's Philox mask
+    keyed by (seed, offset) unless ``keep_mask`` (uint8, m x k) is given.
+    """
+    k = weight.shape[1]
+    x2, lead = _flatten_input(x, k)
+    m = x2.shape[0]
+    adapter = AdapterConfig(rank=lora_a.shape[0], scaling=float(scaling), dropout_p=float(dropout_p), seed=int(seed))
+    plan = LayerPlan(m, k, weight.shape[0], [adapter], [Segment(0, 0, m)] if m > 0 else [], offset=offset,
+                     training=training, keep_mask=keep_mask)
+    return _run(x2, weight, [lora_a], [lora_b], plan, lead, None)
+
+
+def fused_multi_lora(
+    x: torch.Tensor,
+    weight: torch.Tensor,
+    lora_a: Sequence[torch.Tensor],
+    lora_b: Sequence[torch.Tensor],
+    adapters: Sequence[AdapterConfig],
+    segments: Sequence[Segment],
+    offset: int = 0,
+    keep_mask: torch.Tensor | None = None,
+    training: bool = True,
+    grad_sink: Callable | None = None,
+) -> torch.Tensor:
+    """Mixed-adapter microbatch: rows of ``segments`` route to their adapter's A/B, scale
+    and dropout; the frozen W is streamed once for all of them.
+
+    ``grad_sink(plan, dA_cat, dB_cat)`` (optional) receives the fp32 rank-concat gradients
+    so a caller can keep per-(adapter, global batch) slots (plan.segment_grad_slices()).
+    """
+    k = weight.shape[1]
+    x2, lead = _flatten_input(x, k)
+    if len(lora_a) != len(adapters) or len(lora_b) != len(adapters):
+        raise ValidationError("lora_a, lora_b and adapters must have one entry per adapter slot")
+    plan = LayerPlan(x2.shape[0], k, weight.shape[0], adapters, segments, offset=offset, training=training,
+                     keep_mask=keep_mask)
+    return _run(x2, weight, lora_a, lora_b, plan, lead, grad_sink)
+
+
+def _run(x2, weight, lora_a, lora_b, plan: LayerPlan, lead, grad_sink):
+    _check_operand(x2, "x")
+    _check_operand(weight, "weight", (plan.n, plan.k))
+    _check_frozen(weight)
+    for i, (a, b) in enumerate(zip(lora_a, lora_b)):
+        r = plan.adapters[i].rank
+        if tuple(a.shape) != (r, plan.k):
+            raise ValidationError(f"lora_a[{i}] must have shape ({r}, {plan.k}), got {tuple(a.shape)}")
+        if tuple(b.shape) != (plan.n, r):
+            raise ValidationError(f"lora_b[{i}] must have shape ({plan.n}, {r}), got {tuple(b.shape)}")
+        if not (a.is_cuda and b.is_cuda):
+            raise ValidationError("adapter weights must be CUDA tensors")
+    if plan.m == 0:
+        return x2.new_empty(lead + (plan.n,))
+    plan.bind(x2.device)
+    if plan.has_lora:
+        a_cat = plan.gather_a(lora_a)
+        b_cat = plan.gather_b(lora_b)
+    else:
+        a_cat = torch.empty((0, plan.k), dtype=_BF16, device=x2.device)
+        b_cat = torch.empty((plan.n, 0), dtype=_BF16, device=x2.device)
+    y = _FusedLoRAFn.apply(x2, weight, a_cat, b_cat, plan, grad_sink)
+    return y.reshape(lead + (plan.n,))
+
+
+def dropout_keep_mask(m: int, k: int, adapters: Sequence[AdapterConfig], segments: Sequence[Segment],
+                      offset: int = 0, device: torch.device | str = "cuda") -> torch.Tensor:
+    """The SPEC.md §3 keep mask (uint8, m x k) the kernels regenerate, materialised on device."""
+    plan = LayerPlan(m, k, 8, adapters, segments, offset=offset)
+    keep = torch.empty((m, k), dtype=torch.uint8, device=device)
+    _lib.check(_lib.load().lf_dropout_mask(ctypes.byref(plan.problem), _ptr(keep), _stream()), "dropout_mask")
+    return keep

@@ -1,0 +1,188 @@
+"""``FusedLoRA`` and ``FusedMultiLoRA`` modules (PEFT-compatible parameter names).
+
+Both wrap a frozen ``nn.Linear`` (or its weight) and keep adapter parameters under the
+PEFT names ``lora_A.weight`` (r x k) and ``lora_B.weight`` (n x r), so a PEFT/HF LoRA
+layer's state dict maps onto them directly. Adapter parameters default to fp32 master
+weights (cast to bf16 per call, gradients arrive in fp32 for the optimizer and the DP
+all-reduce); the base weight and activations are bf16.
+
+Dropout masks come from SPEC.md §3's counter-based Philox stream: each training forward
+uses (seed, offset) with ``offset`` advanced once per call, and backward reuses the
+forward's pair, so no mask is ever stored.
+"""
+from __future__ import annotations
+
+import math
+from typing import Sequence
+
+import torch
+from torch import nn
+
+from .errors import ValidationError
+from .functional import fused_lora, fused_multi_lora
+from .plan import AdapterConfig, LayerPlan, Segment
+
+
+def _init_lora(a: nn.Linear, b: nn.Linear, init: str, generator: torch.Generator | None = None) -> None:
+    with torch.no_grad():
+        if init == "peft":
+            # PEFT default: kaiming-uniform A, zero B
+            nn.init.kaiming_uniform_(a.weight, a=math.sqrt(5), generator=generator)
+            nn.init.zeros_(b.weight)
+        elif init == "gaussian":
+            k = a.weight.shape[1]
+            a.weight.uniform_(-1.0 / math.sqrt(k), 1.0 / math.sqrt(k), generator=generator)
+            b.weight.normal_(0.0, 1.0 / math.sqrt(b.weight.shape[1]), generator=generator)
+        else:
+            raise ValidationError(f"unknown init {init!r} (expected 'peft' or 'gaussian')")
+
+
+def _frozen_base(base: nn.Linear | torch.Tensor) -> tuple[torch.Tensor, torch.Tensor | None]:
+    if isinstance(base, nn.Linear):
+        w, bias = base.weight, base.bias
+    elif isinstance(base, torch.Tensor):
+        w, bias = base, None
+    else:
+        raise ValidationError("base must be an nn.Linear or a weight tensor of shape (out_features, in_features)")
+    if w.dim() != 2:
+        raise ValidationError("base weight must be 2-D (out_features, in_features)")
+    return w, bias
+
+
+class FusedLoRA(nn.Module):
+    """Single-adapter LoRA linear: Y = X·Wᵀ (+ bias) + scaling·dropout(X)·Aᵀ·Bᵀ."""
+
+    def __init__(
+        self,
+        base: nn.Linear | torch.Tensor,
+        rank: int,
+        scaling: float | None = None,
+        dropout_p: float = 0.0,
+        *,
+        alpha: float | None = None,
+        seed: int = 0,
+        init: str = "peft",
+        dtype: torch.dtype = torch.float32,
+        generator: torch.Generator | None = None,
+    ):
+        super().__init__()
+        w, bias = _frozen_base(base)
+        w.requires_grad_(False)
+        self.base = base if isinstance(base, nn.Linear) else None
+        self.register_buffer("weight", w, persistent=False) if self.base is None else None
+        self.out_features, self.in_features = w.shape
+        if scaling is None:
+            scaling = (alpha if alpha is not None else 32.0) / rank
+        self.config = AdapterConfig(rank=rank, scaling=float(scaling), dropout_p=float(dropout_p), seed=int(seed))
+        dev = w.device
+        self.lora_A = nn.Linear(self.in_features, rank, bias=False, device=dev, dtype=dtype)
+        self.lora_B = nn.Linear(rank, self.out_features, bias=False, device=dev, dtype=dtype)
+        _init_lora(self.lora_A, self.lora_B, init, generator)
+        self._offset = 0
+
+    @property
+    def base_weight(self) -> torch.Tensor:
+        return self.base.weight if self.base is not None else self.weight
+
+    @property
+    def base_bias(self) -> torch.Tensor | None:
+        return self.base.bias if self.base is not None else None
+
+    def next_offset(self) -> int:
+        off = self._offset
+        self._offset += 1
+        return off
+
+    def forward(self, x: torch.Tensor, keep_mask: torch.Tensor | None = None) -> torch.Tensor:
+        c = self.config
+        y = fused_lora(
+            x,
+            self.base_weight,
+            self.lora_A.weight,
+            self.lora_B.weight,
+            c.scaling,
+            c.dropout_p,
+            seed=c.seed,
+            offset=self.next_offset() if self.training else 0,
+            keep_mask=keep_mask,
+            training=self.training,
+        )
+        if self.base_bias is not None:
+            y = y + self.base_bias
+        return y
+
+    def extra_repr(self) -> str:
+        c = self.config
+        return (f"in_features={self.in_features}, out_features={self.out_features}, rank={c.rank}, "
+                f"scaling={c.scaling}, dropout_p={c.dropout_p}")
+
+
+class FusedMultiLoRA(nn.Module):
+    """Several adapters sharing one frozen base linear; each microbatch row segment is
+    routed to its adapter (rank, scaling, dropout) inside the same fused launches."""
+
+    def __init__(
+        self,
+        base: nn.Linear | torch.Tensor,
+        adapters: Sequence[AdapterConfig],
+        *,
+        init: str = "peft",
+        dtype: torch.dtype = torch.float32,
+        track_slot_grads: bool = False,
+        generator: torch.Generator | None = None,
+    ):
+        super().__init__()
+        if not adapters:
+            raise ValidationError("FusedMultiLoRA needs at least one adapter")
+        w, bias = _frozen_base(base)
+        w.requires_grad_(False)
+        self.base = base if isinstance(base, nn.Linear) else None
+        self.register_buffer("weight", w, persistent=False) if self.base is None else None
+        self.out_features, self.in_features = w.shape
+        self.adapters = list(adapters)
+        dev = w.device
+        self.lora_A = nn.ModuleList(
+            nn.Linear(self.in_features, a.rank, bias=False, device=dev, dtype=dtype) for a in self.adapters)
+        self.lora_B = nn.ModuleList(
+            nn.Linear(a.rank, self.out_features, bias=False, device=dev, dtype=dtype) for a in self.adapters)
+        for la, lb in zip(self.lora_A, self.lora_B):
+            _init_lora(la, lb, init, generator)
+        self._offset = 0
+        self.track_slot_grads = track_slot_grads
+        # (adapter slot, global batch) -> [dA (r x k) fp32, dB (n x r) fp32]
+        self.slot_grads: dict[tuple[int, int], list[torch.Tensor]] = {}
+
+    @property
+    def base_weight(self) -> torch.Tensor:
+        return self.base.weight if self.base is not None else self.weight
+
+    def _sink(self, plan: LayerPlan, da: torch.Tensor, db: torch.Tensor) -> None:
+        for adapter, batch, c0, r in plan.segment_grad_slices():
+            ga, gb = da[c0:c0 + r], db[:, c0:c0 + r]
+            slot = self.slot_grads.get((adapter, batch))
+            if slot is None:
+                self.slot_grads[(adapter, batch)] = [ga.clone(), gb.clone()]
+            else:
+                slot[0].add_(ga)
+                slot[1].add_(gb)
+
+    def forward(self, x: torch.Tensor, segments: Sequence[Segment],
+                keep_mask: torch.Tensor | None = None) -> torch.Tensor:
+        off = self._offset if self.training else 0
+        if self.training:
+            self._offset += 1
+        y = fused_multi_lora(
+            x,
+            self.base_weight,
+            [la.weight for la in self.lora_A],
+            [lb.weight for lb in self.lora_B],
+            self.adapters,
+            segments,
+            offset=off,
+            keep_mask=keep_mask,
+            training=self.training,
+            grad_sink=self._sink if self.track_slot_grads else None,
+        )
+        if self.base is not None and self.base.bias is not None:
+            y = y + self.base.bias
+        return y

@@ -1,0 +1,245 @@
+"""Segment tables and per-call problem plans.
+
+A microbatch is a sequence of *segments*: contiguous token rows that belong to one
+(adapter, global batch) pair — lorasched's ``MicrobatchSegment`` (ls/packing.py:41-60),
+whose rows are padded to the adapter's ``padding_multiple`` (ls/packing.py:30-32) and
+ordered by (adapter, global batch) (ls/packing.py:251-258). Each segment gets its own
+column block in a rank-concatenated low-rank dimension, so one fused launch handles
+every adapter present: Ŝ and dŜ are (m x R) with each row non-zero only in its own
+segment's block, A_cat (R x k) and B_cat (n x R) stack the segments' adapter weights.
+A tile that straddles two segments (P = 64 < 128-row tiles) simply runs both blocks.
+
+``LayerPlan`` owns everything one layer call needs on the device besides the tensors:
+the C ``LfProblem`` (segment table by value), the 16-byte-per-128-row routing table
+(ls/costmodel.py:23-26, 279-281) and a self-cleaning split-K workspace.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import torch
+
+from . import _lib
+from .errors import ValidationError
+
+RANK_ALIGN = 16  # one bf16 tcgen05 MMA-K step
+
+
+def padded_rank(rank: int) -> int:
+    """Adapter rank rounded up to the MMA-K granularity (16)."""
+    return -(-int(rank) // RANK_ALIGN) * RANK_ALIGN
+
+
+@dataclass(frozen=True)
+class AdapterConfig:
+    """Per-adapter hyper-parameters the kernels route on.
+
+    Mirrors the fields of lorasched's AdapterSpec (ls/workload.py:25-48) that reach the
+    FusedMultiLoRA lookup table: ``rank`` = lora_rank, ``scaling`` = Eq. 1
+    alpha (PEFT convention alpha / r, see SPEC.md §1), ``dropout_p``, plus the dropout seed.
+    """
+
+    rank: int
+    scaling: float = 2.0
+    dropout_p: float = 0.0
+    seed: int = 0
+
+    def __post_init__(self):
+        if int(self.rank) < 1:
+            raise ValidationError(f"rank must be >= 1, got {self.rank}")
+        if not math.isfinite(float(self.scaling)):
+            raise ValidationError(f"scaling must be finite, got {self.scaling}")
+        if not 0.0 <= float(self.dropout_p) < 1.0:
+            raise ValidationError(f"dropout_p must be in [0, 1), got {self.dropout_p}")
+        if not 0 <= int(self.seed) < 2**64:
+            raise ValidationError(f"seed must be a 64-bit unsigned integer, got {self.seed}")
+
+    @classmethod
+    def from_adapter_spec(cls, spec, seed: int = 0) -> "AdapterConfig":
+        """Build from a lorasched ``AdapterSpec``-like object (lora_rank, alpha, dropout_p)."""
+        rank = int(spec.lora_rank)
+        return cls(rank=rank, scaling=float(spec.alpha) / rank, dropout_p=float(spec.dropout_p), seed=seed)
+
+
+@dataclass(frozen=True)
+class Segment:
+    """Token rows [row_start, row_end) of one (adapter slot, global batch) pair."""
+
+    adapter: int
+    row_start: int
+    row_end: int
+    batch: int = 0
+
+    @property
+    def rows(self) -> int:
+        return self.row_end - self.row_start
+
+
+def segments_from_lengths(adapters: Sequence[int], lengths: Sequence[int], batches: Sequence[int] | None = None,
+                          start: int = 0) -> list[Segment]:
+    """Consecutive segments of the given (padded) token lengths."""
+    segs, row = [], start
+    batches = list(batches) if batches is not None else [0] * len(adapters)
+    for a, n, b in zip(adapters, lengths, batches):
+        segs.append(Segment(int(a), row, row + int(n), int(b)))
+        row += int(n)
+    return segs
+
+
+def validate_segments(segments: Sequence[Segment], m: int, num_adapters: int) -> None:
+    if len(segments) > _lib.LF_MAX_SEGMENTS:
+        raise ValidationError(f"at most {_lib.LF_MAX_SEGMENTS} segments per microbatch, got {len(segments)}")
+    prev = 0
+    for i, s in enumerate(segments):
+        if not 0 <= s.adapter < num_adapters:
+            raise ValidationError(f"segment {i}: adapter slot {s.adapter} out of range [0, {num_adapters})")
+        if s.row_start < prev or s.row_end < s.row_start or s.row_end > m:
+            raise ValidationError(
+                f"segment {i}: rows [{s.row_start}, {s.row_end}) must be sorted, disjoint and inside [0, {m})"
+            )
+        prev = s.row_end
+
+
+def routing_table(segments: Sequence[Segment], col_starts: Sequence[int], ranks: Sequence[int], m: int) -> list[tuple]:
+    """Host restatement of the device routing table (used for the tile-level cost
+    accounting; the kernels consume the table lf_build_routes writes)."""
+    out = []
+    for t in range(-(-m // _lib.ROUTE_TILE_ROWS)):
+        r0, r1 = t * _lib.ROUTE_TILE_ROWS, min(m, (t + 1) * _lib.ROUTE_TILE_ROWS)
+        hit = [i for i, s in enumerate(segments) if s.row_start < s.row_end and s.row_start < r1 and s.row_end > r0]
+        if not hit:
+            out.append((0, -1, 0, 0))
+        else:
+            lo, hi = hit[0], hit[-1]
+            out.append((lo, hi, col_starts[lo], col_starts[hi] + ranks[hi]))
+    return out
+
+
+_WORKSPACES: dict[tuple[int, int], torch.Tensor] = {}
+
+
+def workspace(device: torch.device, stream: torch.cuda.Stream, nbytes: int) -> torch.Tensor:
+    """Zero-initialised scratch owned per (device, stream). Kernels return it to zero."""
+    key = (device.index if device.index is not None else torch.cuda.current_device(), stream.cuda_stream)
+    buf = _WORKSPACES.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.zeros(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
+        _WORKSPACES[key] = buf
+    return buf
+
+
+class LayerPlan:
+    """Device-side plan of one fused LoRA layer call (forward and its backward)."""
+
+    def __init__(
+        self,
+        m: int,
+        k: int,
+        n: int,
+        adapters: Sequence[AdapterConfig],
+        segments: Sequence[Segment],
+        *,
+        offset: int = 0,
+        training: bool = True,
+        keep_mask: torch.Tensor | None = None,
+        device: torch.device | None = None,
+    ):
+        self.m, self.k, self.n = int(m), int(k), int(n)
+        self.adapters = list(adapters)
+        self.segments = list(segments)
+        self.offset = int(offset)
+        self.training = bool(training)
+        validate_segments(self.segments, self.m, len(self.adapters))
+        self.ranks = [padded_rank(self.adapters[s.adapter].rank) for s in self.segments]
+        self.col_starts = []
+        c = 0
+        for r in self.ranks:
+            self.col_starts.append(c)
+            c += r
+        self.rank_total = c
+        if self.rank_total > _lib.LF_MAX_RANK_TOTAL:
+            raise ValidationError(
+                f"sum of padded segment ranks {self.rank_total} exceeds {_lib.LF_MAX_RANK_TOTAL}; "
+                "split the microbatch"
+            )
+        self.keep_mask = keep_mask
+        if keep_mask is not None:
+            if keep_mask.dtype != torch.uint8 or tuple(keep_mask.shape) != (self.m, self.k):
+                raise ValidationError(f"keep_mask must be uint8 of shape ({self.m}, {self.k})")
+            if not keep_mask.is_contiguous():
+                raise ValidationError("keep_mask must be contiguous")
+        self.device = device
+        self.problem = _lib.LfProblem()
+        p = self.problem
+        p.m, p.k, p.n = self.m, self.k, self.n
+        p.rank_total = self.rank_total
+        p.num_segments = len(self.segments)
+        for i, (s, c0, r) in enumerate(zip(self.segments, self.col_starts, self.ranks)):
+            a = self.adapters[s.adapter]
+            d = p.segments[i]
+            d.row_start, d.row_end = s.row_start, s.row_end
+            d.col_start, d.rank = c0, r
+            d.scaling = float(a.scaling)
+            d.dropout_p = float(a.dropout_p) if self.training else 0.0
+            d.seed = int(a.seed) & (2**64 - 1)
+            d.offset = self.offset & (2**64 - 1)
+        p.keep_mask = keep_mask.data_ptr() if (keep_mask is not None and self.training) else None
+        self.routes: torch.Tensor | None = None
+        self._ws: torch.Tensor | None = None
+
+    # -- derived ------------------------------------------------------------------
+    @property
+    def has_lora(self) -> bool:
+        return len(self.segments) > 0
+
+    @property
+    def num_tiles(self) -> int:
+        return -(-self.m // _lib.ROUTE_TILE_ROWS)
+
+    def host_routes(self) -> list[tuple]:
+        return routing_table(self.segments, self.col_starts, self.ranks, self.m)
+
+    # -- device ---------------------------------------------------------------------
+    def bind(self, device: torch.device, stream: torch.cuda.Stream | None = None) -> "LayerPlan":
+        """Build the routing table and attach the workspace on ``device``/``stream``."""
+        stream = stream or torch.cuda.current_stream(device)
+        self.device = device
+        lib = _lib.load()
+        self.routes = torch.empty((max(self.num_tiles, 1), 4), dtype=torch.int32, device=device)
+        nbytes = _lib.workspace_bytes(self.m, self.rank_total)
+        self._ws = workspace(device, stream, nbytes)
+        self.problem.routes = self.routes.data_ptr()
+        self.problem.workspace = self._ws.data_ptr()
+        self.problem.workspace_bytes = self._ws.numel()
+        if self.has_lora:
+            _lib.check(lib.lf_build_routes(ctypes.byref(self.problem), self.routes.data_ptr(),
+                                           ctypes.c_void_p(stream.cuda_stream)), "lf_build_routes")
+        return self
+
+    def gather_a(self, lora_a: Sequence[torch.Tensor]) -> torch.Tensor:
+        """A_cat (R x k, bf16): each segment's adapter lora_A.weight, zero-padded to its block."""
+        blocks = []
+        for s, r in zip(self.segments, self.ranks):
+            a = lora_a[s.adapter].to(torch.bfloat16)
+            if a.shape[0] != r:
+                a = torch.nn.functional.pad(a, (0, 0, 0, r - a.shape[0]))
+            blocks.append(a)
+        return torch.cat(blocks, 0).contiguous() if len(blocks) > 1 else blocks[0].contiguous()
+
+    def gather_b(self, lora_b: Sequence[torch.Tensor]) -> torch.Tensor:
+        """B_cat (n x R, bf16): each segment's adapter lora_B.weight, zero-padded to its block."""
+        blocks = []
+        for s, r in zip(self.segments, self.ranks):
+            b = lora_b[s.adapter].to(torch.bfloat16)
+            if b.shape[1] != r:
+                b = torch.nn.functional.pad(b, (0, r - b.shape[1]))
+            blocks.append(b)
+        return torch.cat(blocks, 1).contiguous() if len(blocks) > 1 else blocks[0].contiguous()
+
+    def segment_grad_slices(self) -> list[tuple[int, int, int, int]]:
+        """(adapter, batch, col_start, rank) for routing dA/dB columns to (adapter, batch) slots."""
+        return [(s.adapter, s.batch, c0, self.adapters[s.adapter].rank)
+                for s, c0 in zip(self.segments, self.col_starts)]
