@@ -1,0 +1,534 @@
+"""Benchmark of the FusedLoRA hot path (BASELINE.json metric) — one JSON line on rank 0.
+
+Metric: "LoRA linear fwd+bwd tokens/s & TFLOP/s (8B/70B shapes), % of bf16 peak".
+Workload (default, BASELINE.json configs[1]): one step = forward + backward of the seven
+LLaMa-3.1-8B LoRA linears (q, k, v, o, gate, up, down; hidden 4096, kv 1024, ffn 14336),
+r = 16, scaling 2.0, dropout p = 0.1, 8192 tokens per GPU, bf16, frozen W, random init,
+synthetic inputs. q/k/v share the attention input and gate/up the MLP input, as in the
+decoder. With N GPUs (torchrun, one process per GPU) every rank runs its own 8192 tokens
+(weak scaling, data parallel) and the fp32 dA/dB of all seven adapters are NCCL
+all-reduced once per step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c4] [--impl ours|reference]
+
+`--impl reference` times the reference CPU path of this hot path (the oracle port in
+oracle/, numpy, all host threads) on a bounded token sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HIDDEN_8B, KV_8B, FFN_8B = 4096, 1024, 14336
+HIDDEN_70B, KV_70B, FFN_70B = 8192, 1024, 28672
+
+
+def projections(config: str):
+    """(name, k, n, input group) of each LoRA linear of one decoder layer."""
+    if config in ("c2", "c1"):
+        h, kv, f = HIDDEN_8B, KV_8B, FFN_8B
+    elif config == "c4":
+        h, kv, f = HIDDEN_70B, KV_70B, FFN_70B
+    else:
+        raise SystemExit(f"unknown config {config}")
+    if config == "c1":
+        return [("linear", 4096, 4096, "x")]
+    return [("q", h, h, "attn"), ("k", h, kv, "attn"), ("v", h, kv, "attn"), ("o", h, h, "o"),
+            ("gate", h, f, "mlp"), ("up", h, f, "mlp"), ("down", f, h, "down")]
+
+
+def tokens_per_gpu(config: str) -> int:
+    return {"c1": 2048, "c2": 8192, "c4": 16384}[config]
+
+
+def step_flops(config: str, m: int, r: int) -> float:
+    return float(sum(4 * m * k * n + 6 * m * r * (k + n) for _, k, n, _ in projections(config)))
+
+
+def gemm_flops(config: str, m: int, r: int) -> dict:
+    """Algorithmic FLOPs of the two tcgen05 GEMM launchers per step."""
+    fwd = sum(2 * m * k * n + 2 * m * r * n for _, k, n, _ in projections(config))
+    dgrad = sum(2 * m * n * k + 2 * m * r * k for _, k, n, _ in projections(config))
+    return {"base_fwd": float(fwd), "grad_input": float(dgrad)}
+
+
+def lowrank_bytes(config: str, m: int, r: int) -> dict:
+    """Algorithmic HBM bytes of the memory-bound launchers per step."""
+    k1 = sum(2 * m * k + 2 * k * r + 2 * m * r for _, k, n, _ in projections(config))
+    k3 = sum(2 * (m * n + r * n + m * r) + 2 * m * r + 4 * r * n for _, k, n, _ in projections(config))
+    k4 = sum(2 * (m * k + m * r) + 4 * k * r for _, k, n, _ in projections(config))
+    return {"dropout_down_fwd": float(k1), "grad_up": float(k3), "grad_down": float(k4)}
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "source": "MEASURED_PEAKS.json (measured)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "source": "B200_PROFILING.md fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------------
+# reference arm: the CPU oracle (numpy port) on the host cores
+# --------------------------------------------------------------------------------------
+def cpu_reference_step(config: str, sample_tokens: int, r: int, p: float, seed: int = 0) -> float:
+    """One fwd+bwd of every projection on a `sample_tokens`-row sample with the oracle;
+    returns the wall seconds."""
+    import numpy as np
+
+    from oracle import lora as olora
+    from oracle import philox as ophilox
+
+    rng = np.random.default_rng(seed)
+    t0 = time.perf_counter()
+    total = 0.0
+    inputs = {}
+    for name, k, n, grp in projections(config):
+        m = sample_tokens
+        if grp not in inputs:
+            inputs[grp] = olora.bf16_round(rng.standard_normal((m, k), dtype=np.float32))
+        x = inputs[grp]
+        w = olora.bf16_round(rng.standard_normal((n, k), dtype=np.float32) / np.sqrt(k))
+        a = olora.bf16_round((rng.random((r, k), dtype=np.float32) * 2 - 1) / np.sqrt(k))
+        b = olora.bf16_round(rng.standard_normal((n, r), dtype=np.float32) / np.sqrt(r))
+        dy = olora.bf16_round(rng.standard_normal((m, n), dtype=np.float32))
+        seg = [olora.OracleSegment(0, m, 0, r, 2.0, p, 1234)]
+        t1 = time.perf_counter()
+        keep = ophilox.keep_mask_rows(np.arange(m), k, p, 1234, 0)
+        y, s_hat = olora.forward(x, w, a, b, seg, keep)
+        olora.backward(dy, x, w, a, b, s_hat, seg, keep)
+        total += time.perf_counter() - t1
+    del t0
+    return total
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    sample = args.cpu_sample_tokens
+    r, p = 16, 0.1
+    for _ in range(max(1, min(args.warmup, 1))):
+        cpu_reference_step(args.config, 64, r, p)
+    times = [cpu_reference_step(args.config, sample, r, p, seed=i) for i in range(args.steps)]
+    t = sum(times) / len(times)
+    value = sample / t
+    line = {
+        "impl": "reference",
+        "metric": "LoRA linear fwd+bwd tokens/s & TFLOP/s (8B/70B shapes), % of bf16 peak",
+        "value": value,
+        "unit": "tokens/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": workload_name(args.config) + f" — CPU oracle on a {sample}-token sample",
+                   "tokens_per_step": sample, "rank": r, "dropout_p": p},
+        "tflops": step_flops(args.config, sample, r) / t / 1e12,
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample} tokens of each projection, fwd+bwd, numpy float64 oracle (oracle/lora.py)"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_name(config: str) -> str:
+    return {
+        "c2": "LLaMa-3.1-8B layer shapes (q/k/v/o, gate/up/down) FusedLoRA r=16, 8192 tokens, bf16, 1 B200",
+        "c1": "single FusedLoRA linear fwd+bwd: tokens=2048, k=n=4096, r=16, dropout=0.1",
+        "c4": "LLaMa-3.1-70B layer shapes FusedLoRA r=16, 16384 tokens per GPU",
+    }[config]
+
+
+# --------------------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------------------
+def build_layers(config: str, m: int, r: int, p: float, device, gen, use_fused: bool = True):
+    import torch
+
+    from paper_2510_00206_b200 import FusedLoRA
+
+    layers, inputs, grads = {}, {}, {}
+    for i, (name, k, n, grp) in enumerate(projections(config)):
+        w = (torch.randn(n, k, generator=gen, device=device, dtype=torch.float32) / k**0.5).to(torch.bfloat16)
+        layer = FusedLoRA(w, rank=r, scaling=2.0, dropout_p=p, seed=1234 + i, init="gaussian",
+                          generator=gen).to(device)
+        layers[name] = layer
+        if grp not in inputs:
+            # activations come from the previous layer: they need dX (⑤ runs every step)
+            inputs[grp] = torch.randn(m, k, generator=gen, device=device, dtype=torch.float32).to(
+                torch.bfloat16).requires_grad_(True)
+        grads[name] = torch.randn(m, n, generator=gen, device=device, dtype=torch.float32).to(torch.bfloat16)
+    return layers, inputs, grads
+
+
+def fused_step(config, layers, inputs, grads, world, flat_grad=None):
+    """fwd+bwd of every projection through the public module API; grads all-reduced if world>1."""
+    import torch
+
+    for name, k, n, grp in projections(config):
+        layer = layers[name]
+        x = inputs[grp]
+        y = layer(x)
+        y.backward(grads[name])
+    if world > 1:
+        import torch.distributed as dist
+
+        params = [p for nm in layers for p in (layers[nm].lora_A.weight, layers[nm].lora_B.weight)]
+        flat = torch.cat([p.grad.reshape(-1) for p in params])
+        dist.all_reduce(flat)
+        off = 0
+        for p in params:
+            n_ = p.numel()
+            p.grad.copy_(flat[off:off + n_].view_as(p))
+            off += n_
+
+
+def zero_grads(layers, inputs=None):
+    for layer in layers.values():
+        layer.lora_A.weight.grad = None
+        layer.lora_B.weight.grad = None
+    for t in (inputs or {}).values():
+        t.grad = None
+
+
+def unfused_step(config, base, inputs, grads, p):
+    """PEFT-style torch LoRA: cuBLAS F.linear + F.dropout + add/scale, autograd, W frozen."""
+    from paper_2510_00206_b200 import unfused_lora
+
+    for name, k, n, grp in projections(config):
+        w, a, b = base[name]
+        y = unfused_lora(inputs[grp], w, a, b, 2.0, p, training=True)
+        y.backward(grads[name])
+        a.grad = None
+        b.grad = None
+
+
+def time_loop(fn, steps, warmup, sync_barrier):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    sync_barrier()
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(steps):
+        fn()
+    stop.record()
+    torch.cuda.synchronize()
+    sync_barrier()
+    return start.elapsed_time(stop) / steps
+
+
+def run_ours(args, rank: int, world: int, local_rank: int) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_00206_b200 import _lib
+    from paper_2510_00206_b200 import functional as F_
+
+    _lib.load()  # fail loudly without the sm_100a library
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    gen = torch.Generator(device=device).manual_seed(1000 + rank)
+    r, p = 16, args.dropout
+    m = tokens_per_gpu(args.config)
+    layers, inputs, grads = build_layers(args.config, m, r, p, device, gen)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def step():
+        zero_grads(layers, inputs)
+        fused_step(args.config, layers, inputs, grads, world)
+
+    # ---- device-resident timed region (value) ----------------------------------------
+    for _ in range(args.warmup):
+        step()
+    stats = F_.LaunchStats(timed=True)
+    clocks = ClockSampler(local_rank)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    F_.set_launch_stats(stats)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        step()
+    t1.record()
+    torch.cuda.synchronize()
+    F_.set_launch_stats(None)
+    clk = clocks.stop()
+    barrier()
+    ms = max_over_ranks(t0.elapsed_time(t1) / args.steps)
+    durs = stats.durations_ms()
+    launches = stats.total_launches()
+
+    # ---- per-kernel roofline ----------------------------------------------------------
+    peaks = measured_peaks()
+    gfl = gemm_flops(args.config, m, r)
+    lrb = lowrank_bytes(args.config, m, r)
+    kernels = {}
+    for name, lst in durs.items():
+        tot = sum(lst) / args.steps  # ms per step spent in this launcher
+        ent = {"ms_per_step": tot, "launches_per_step": len(lst) / args.steps}
+        if name in gfl:
+            ent["tflops"] = gfl[name] / (tot * 1e-3) / 1e12
+        if name in lrb:
+            ent["gbs"] = lrb[name] / (tot * 1e-3) / 1e9
+        kernels[name] = ent
+    gemm_ms = sum(kernels[n]["ms_per_step"] for n in ("base_fwd", "grad_input") if n in kernels)
+    gemm_tf = (gfl["base_fwd"] + gfl["grad_input"]) / (gemm_ms * 1e-3) / 1e12 if gemm_ms else 0.0
+    roofline = {
+        "bound": "tensor",
+        "kernel": "lf_gemm_kernel (② base_fwd + ⑤ grad_input)",
+        "achieved": gemm_tf,
+        "peak": peaks["bf16_tflops_sustained"],
+        "peak_kind": "bf16_tflops_sustained, " + peaks["source"] + " (kernels timed inside a long step)",
+        "unit": "TFLOP/s",
+        "frac": gemm_tf / peaks["bf16_tflops_sustained"],
+        "frac_of_burst": gemm_tf / peaks["bf16_tflops"],
+        "share_of_step": gemm_ms / ms,
+        "traffic": None,
+        "per_kernel": kernels,
+    }
+
+    # ---- unfused torch baseline (same box, same shapes) -------------------------------
+    base = {}
+    for name, k, n, grp in projections(args.config):
+        layer = layers[name]
+        a = layer.lora_A.weight.detach().to(torch.bfloat16).clone().requires_grad_(True)
+        b = layer.lora_B.weight.detach().to(torch.bfloat16).clone().requires_grad_(True)
+        base[name] = (layer.base_weight, a, b)
+    unf_ms = time_loop(lambda: unfused_step(args.config, base, inputs, grads, p), max(2, args.steps // 2),
+                       args.warmup, barrier)
+    unf_ms = max_over_ranks(unf_ms)
+
+    # ---- end to end through the public API: pinned host inputs -> H2D, D2H of grads ---
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, layers, inputs, grads, device, world, barrier, max_over_ranks)
+
+    flops = step_flops(args.config, m, r)
+    value = world * m / (ms * 1e-3)
+    if rank == 0:
+        line = {
+            "metric": "LoRA linear fwd+bwd tokens/s & TFLOP/s (8B/70B shapes), % of bf16 peak",
+            "value": value,
+            "unit": "tokens/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic",
+            "config": {
+                "workload": workload_name(args.config),
+                "projections": [[nm, k, n] for nm, k, n, _ in projections(args.config)],
+                "tokens_per_gpu": m,
+                "global_tokens": m * world,
+                "rank": r,
+                "scaling": 2.0,
+                "dropout_p": p,
+                "parallelism": f"dp{world}",
+                "l2": "inputs larger than L2 (≈2 GB touched per step vs 126 MB L2)",
+            },
+            "tflops": world * flops / (ms * 1e-3) / 1e12,
+            "tflops_per_gpu": flops / (ms * 1e-3) / 1e12,
+            "frac_of_bf16_peak": flops / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+            "unfused_torch": {"ms_per_step": unf_ms, "tokens_per_s": world * m / (unf_ms * 1e-3),
+                              "speedup": unf_ms / ms},
+            "roofline": roofline,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        if e2e is not None:
+            line["e2e"] = e2e
+        if not args.no_cpu_baseline:
+            cores = len(os.sched_getaffinity(0))
+            ts = cpu_reference_step(args.config, args.cpu_sample_tokens, r, p)
+            line["cpu_baseline"] = {
+                "value": args.cpu_sample_tokens / ts, "unit": "tokens/s", "cores": cores, "kind": "port",
+                "sample": f"{args.cpu_sample_tokens} tokens of each projection, fwd+bwd, numpy float64 oracle",
+            }
+        print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, layers, inputs, grads, device, world, barrier, max_over_ranks):
+    """Same step through the module API, with every input copied H2D from pinned host
+    memory (copy stream, overlapped with compute) and all adapter grads read back D2H."""
+    import torch
+
+    host_in = {g: t.detach().cpu().pin_memory() for g, t in inputs.items()}
+    host_dy = {nm: t.cpu().pin_memory() for nm, t in grads.items()}
+    dev_in = {g: torch.empty_like(t) for g, t in inputs.items()}
+    dev_dy = {nm: torch.empty_like(t) for nm, t in grads.items()}
+    params = [p for nm in layers for p in (layers[nm].lora_A.weight, layers[nm].lora_B.weight)]
+    host_out = torch.empty(sum(p.numel() for p in params), dtype=torch.float32).pin_memory()
+    copy = torch.cuda.Stream(device)
+    order = projections(args.config)
+    h2d = sum(t.numel() * t.element_size() for t in host_in.values()) + \
+        sum(t.numel() * t.element_size() for t in host_dy.values())
+    d2h = host_out.numel() * 4
+
+    def step():
+        zero_grads(layers)
+        ready = {}
+        with torch.cuda.stream(copy):
+            for name, k, n, grp in order:
+                if grp not in ready:
+                    dev_in[grp].copy_(host_in[grp], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(copy)
+                    ready[grp] = ev
+                dev_dy[name].copy_(host_dy[name], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+                ready[name] = ev
+        cur = torch.cuda.current_stream(device)
+        leaves = {}
+        for name, k, n, grp in order:
+            cur.wait_event(ready[grp])
+            cur.wait_event(ready[name])
+            if grp not in leaves:  # activation leaf: dX is computed as in a real layer
+                leaves[grp] = dev_in[grp].detach().requires_grad_(True)
+            y = layers[name](leaves[grp])
+            y.backward(dev_dy[name])
+        if world > 1:
+            import torch.distributed as dist
+
+            flat = torch.cat([p.grad.reshape(-1) for p in params])
+            dist.all_reduce(flat)
+        else:
+            flat = torch.cat([p.grad.reshape(-1) for p in params])
+        host_out.copy_(flat, non_blocking=True)
+        # the copy stream must not overwrite inputs of this step before compute used them
+        copy.wait_stream(cur)
+
+    ms = time_loop(step, max(2, args.steps // 2), args.warmup, barrier)
+    ms = max_over_ranks(ms)
+    m = tokens_per_gpu(args.config)
+    return {"value": world * m / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "path": "FusedLoRA modules (public API), pinned host inputs H2D on a copy stream, fp32 grads D2H"}
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dropout", type=float, default=0.1)
+    ap.add_argument("--cpu-sample-tokens", type=int, default=256)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -48,7 +48,7 @@ extern "C" {
 #define LF_API
 #endif
 
-#define LF_ABI_VERSION 1
+#define LF_ABI_VERSION 2
 #define LF_MAX_SEGMENTS 32
 #define LF_MAX_RANK_TOTAL 128
 #define LF_ROUTE_TILE_ROWS 128 /* ls/costmodel.py:25 ROUTING_TILE_ROWS */
@@ -84,6 +84,11 @@ typedef struct LfProblem {
   const uint8_t* keep_mask; /* device, optional explicit m x k keep mask (1 keep, 0 drop); NULL = Philox */
   void* workspace;          /* device scratch, zero-filled once, >= lf_workspace_bytes(); kernels leave it zeroed */
   size_t workspace_bytes;
+  /* device, optional m x (k/8) bytes: the Philox keep mask bit-packed (bit e of byte
+   * [row][col/8] = column col/8*8+e). lf_dropout_down_fwd writes it for rows of segments
+   * with p > 0; lf_grad_down / lf_grad_input read it instead of re-running Philox.
+   * NULL: every kernel regenerates the mask. Ignored when keep_mask is set. */
+  uint8_t* keep_bits;
 } LfProblem;
 
 /* Bytes of zero-initialised scratch one problem needs (split-K partials + tile counters). */

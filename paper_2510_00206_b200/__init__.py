@@ -15,7 +15,7 @@ from .errors import ExtensionMissingError, KernelError, LoRAFusionError, Validat
 from .functional import dropout_keep_mask, fused_lora, fused_multi_lora
 from .modules import FusedLoRA, FusedMultiLoRA
 from .plan import AdapterConfig, LayerPlan, Segment, padded_rank, segments_from_lengths
-from .traffic import (
+from .costmodel import (
     B200,
     H100_SXM,
     VARIANTS,

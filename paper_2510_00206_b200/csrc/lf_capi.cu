@@ -157,6 +157,11 @@ int validate(const LfProblem* p, bool need_routes, lf::LfSegTable* t) {
     t->ld_mask = p->k;
   } else {
     t->mask_mode = any_dropout ? 1 : 0;
+    if (any_dropout && p->keep_bits) {
+      if (!aligned16(p->keep_bits)) return fail(LF_E_INVALID, "keep_bits must be 16-byte aligned");
+      t->bits = p->keep_bits;
+      t->ld_bits = p->k / 8;
+    }
   }
   if (need_routes && p->num_segments > 0 && !p->routes) return fail(LF_E_INVALID, "routes is NULL (call lf_build_routes)");
   return LF_OK;
@@ -260,7 +265,7 @@ int lf_dropout_down_fwd(const LfProblem* p, const uint16_t* x, const uint16_t* a
   lf::down_config(p->rank_total, &stages, &stage_bytes);
   const int occ = occupancy_for_smem(stages * stage_bytes + 2048);
   const int target = occ * d.sms;
-  int ksplit = (target + tiles_m - 1) / tiles_m;
+  int ksplit = target / tiles_m;  // one resident wave: no tail CTAs
   const int max_split = nkb >= 8 ? nkb / 4 : 1;
   if (ksplit > max_split) ksplit = max_split;
   if (ksplit < 1) ksplit = 1;

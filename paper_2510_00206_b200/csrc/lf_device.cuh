@@ -152,6 +152,17 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------------
@@ -277,6 +288,53 @@ __device__ __forceinline__ uint4 apply_keep8(uint4 v, uint32_t bits) {
     w[i] &= (lo | hi);
   }
   return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// keep bits of 64 consecutive columns [col, col+64) of one row: byte c = chunk c
+__device__ __forceinline__ uint64_t keep_bits64(const LfSegTable& t, int seg, int row, int col, int ncols) {
+  uint64_t bits = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int cc = col + 8 * c;
+    const uint32_t b = (t.mask_mode == 2) ? explicit_keep8(t.mask + (int64_t)row * t.ld_mask, cc, ncols)
+                                           : philox_keep8((uint32_t)cc >> 3, (uint32_t)row, t.seg[seg]);
+    bits |= (uint64_t)b << (8 * c);
+  }
+  return bits;
+}
+
+// 8 bytes of a bit-packed mask row starting at byte b0 (bounded by the row length)
+__device__ __forceinline__ uint64_t load_bits64(const uint8_t* row_bits, int b0, int row_bytes) {
+  const uint8_t* p = row_bits + b0;
+  if (b0 + 8 <= row_bytes && ((reinterpret_cast<uintptr_t>(p) & 7u) == 0))
+    return *reinterpret_cast<const uint64_t*>(p);
+  uint64_t v = 0;
+  for (int i = 0; i < 8; ++i)
+    if (b0 + i < row_bytes) v |= (uint64_t)p[i] << (8 * i);
+  return v;
+}
+
+__device__ __forceinline__ void store_bits64(uint8_t* row_bits, int b0, int row_bytes, uint64_t v) {
+  uint8_t* p = row_bits + b0;
+  if (b0 + 8 <= row_bytes && ((reinterpret_cast<uintptr_t>(p) & 7u) == 0)) {
+    *reinterpret_cast<uint64_t*>(p) = v;
+    return;
+  }
+  for (int i = 0; i < 8; ++i)
+    if (b0 + i < row_bytes) p[i] = (uint8_t)(v >> (8 * i));
+}
+
+// zero the dropped bf16 elements of one 128-byte row of an SW128 tile (64 columns)
+__device__ __forceinline__ void apply_row_sw128(uint8_t* tile, int rit, uint64_t bits) {
+  uint8_t* rowp = tile + rit * 128;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint32_t b = (uint32_t)(bits >> (8 * c)) & 0xFFu;
+    if (b != 0xFFu) {
+      uint4* p = reinterpret_cast<uint4*>(rowp + ((c ^ (rit & 7)) << 4));
+      *p = apply_keep8(*p, b);
+    }
+  }
 }
 
 // index of the segment holding `row` among [lo, hi] (sorted, disjoint), or -1

@@ -6,27 +6,33 @@
 //
 // B200 design: persistent, warp-specialised tcgen05 GEMM, one CTA per SM.
 //   warp 0      TMA producer (one lane): A/B tiles into a STAGES-deep smem ring
-//   warp 1      MMA issuer (one lane): tcgen05.mma 128xBNx16, fp32 accumulators in TMEM,
+//   warp 1      MMA issuer (one lane): tcgen05.mma 128x256x16, fp32 accumulators in TMEM,
 //               double-buffered so the epilogue of tile i overlaps the main loop of tile i+1
-//   warps 2..5  epilogue: tcgen05.ld -> (mask ⊙ LoRA accumulator) -> bf16 -> global
-// The low-rank up-projection is NOT an epilogue GEMM: [X | Ŝ]·[W | B_cat]ᵀ — the
-// rank-R LoRA operands are streamed as extra K-blocks into the same accumulator, so
-// the output tile is written exactly once and the epilogue stays a pure convert.
-// With dropout in the backward (⑤, p > 0) the mask multiplies the LoRA term only,
-// so that term goes to a second TMEM accumulator and is folded in by the epilogue.
+//   warps 2..5  epilogue: tcgen05.ld -> bf16 -> global (and, for ⑤ with dropout, the mask pass)
+// The low-rank up-projection is NOT an epilogue GEMM: [X | Ŝ]·[W | B_cat]ᵀ — the rank-R
+// LoRA operands are streamed as extra K-blocks into the same accumulator, so the output
+// tile is written exactly once and the epilogue stays a pure convert.
+//
+// ⑤ with dropout: the mask multiplies only the LoRA term (dX = dY·W + M ⊙ (dŜ·A_cat)),
+// so the LoRA K-block of a tile is issued FIRST into its (empty) accumulator, the
+// epilogue warps zero the dropped elements of that partial in TMEM (tcgen05.ld → keep
+// bits → tcgen05.st), and only then is the main dY·W loop accumulated on top. The LoRA
+// block of tile i+1 is issued half-way through tile i's main loop, so its mask pass
+// runs while the tensor pipe is busy with tile i — same 128x256 tiles and TMEM budget
+// as the dropout-free path, no second accumulator.
 #include "lf_device.cuh"
 #include "lf_kernels.h"
 
 namespace lf {
 
-template <int BN, bool B_MN, bool MASKED, int STAGES>
+template <int BN, bool B_MN, int STAGES>
 struct GemmCfg {
   static constexpr int BM = 128;
   static constexpr int BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;  // 16 KB, K-major SW128
   static constexpr int B_BYTES = BN * BK * 2;  // BN x 128 B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int ACC_COLS = MASKED ? 2 * BN : BN;
+  static constexpr int ACC_COLS = BN;
   static constexpr int TMEM_COLS = 2 * ACC_COLS;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
   static_assert(TMEM_COLS <= 512 && (TMEM_COLS & (TMEM_COLS - 1)) == 0, "TMEM budget");
@@ -45,19 +51,65 @@ __device__ __forceinline__ void gemm_tile_coords(int t, int tiles_m, int tiles_n
   nb = r / gm;
 }
 
+struct TileInfo {
+  int mb, nb;
+  int col_lo, col_hi;  // LoRA K-range (empty if none)
+  __device__ bool lora() const { return col_hi > col_lo; }
+};
+
+__device__ __forceinline__ TileInfo tile_info(const GemmArgs& a, int t) {
+  TileInfo ti;
+  gemm_tile_coords(t, a.tiles_m, a.tiles_n, ti.mb, ti.nb);
+  if (a.routes) {
+    const LfRoute rt = a.routes[ti.mb];
+    ti.col_lo = rt.col_lo;
+    ti.col_hi = rt.col_hi;
+  } else {
+    ti.col_lo = ti.col_hi = 0;
+  }
+  return ti;
+}
+
+// keep bits (4 bytes = 32 columns, byte j = columns col+8j..col+8j+7) of one row for the
+// ⑤ mask pass: bit-packed mask written by ① if present, else Philox / explicit mask
+__device__ __forceinline__ uint32_t dgrad_keep32(const LfSegTable& t, int seg, int row, int col, int ncols) {
+  if (t.mask_mode == 1 && t.bits) {
+    const uint8_t* rb = t.bits + (int64_t)row * t.ld_bits;
+    const int b0 = col >> 3;
+    const int nb = (int)t.ld_bits;
+    if (b0 + 4 <= nb && ((reinterpret_cast<uintptr_t>(rb + b0) & 3u) == 0))
+      return *reinterpret_cast<const uint32_t*>(rb + b0);
+    uint32_t v = 0;
+    for (int i = 0; i < 4; ++i)
+      if (b0 + i < nb) v |= (uint32_t)rb[b0 + i] << (8 * i);
+    return v;
+  }
+  uint32_t v = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int cc = col + 8 * j;
+    const uint32_t b = (t.mask_mode == 2) ? explicit_keep8(t.mask + (int64_t)row * t.ld_mask, cc, ncols)
+                                           : philox_keep8((uint32_t)cc >> 3, (uint32_t)row, t.seg[seg]);
+    v |= b << (8 * j);
+  }
+  return v;
+}
+
 template <int BN, bool B_MN, bool MASKED, int STAGES>
 __global__ void __launch_bounds__(192, 1)
     lf_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                    const __grid_constant__ GemmArgs args) {
-  using Cfg = GemmCfg<BN, B_MN, MASKED, STAGES>;
+  using Cfg = GemmCfg<BN, B_MN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = empty + STAGES;  // [2] main loop done  (MMA -> epilogue)
+  uint64_t* tempty = tfull + 2;      // [2] accumulator drained (epilogue -> MMA)
+  uint64_t* lfull = tempty + 2;      // [2] LoRA partial ready (MMA -> mask pass)      MASKED only
+  uint64_t* lmasked = lfull + 2;     // [2] LoRA partial masked (mask pass -> MMA)     MASKED only
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lmasked + 2);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -70,6 +122,8 @@ __global__ void __launch_bounds__(192, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
+      mbar_init(&lfull[a], 1);
+      mbar_init(&lmasked[a], 4);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmA);
@@ -87,50 +141,63 @@ __global__ void __launch_bounds__(192, 1)
 
   const int tiles = args.tiles_m * args.tiles_n;
   const int nkb = (args.K + Cfg::BK - 1) / Cfg::BK;
+  const int jmid = nkb / 2;  // MASKED: where the next tile's LoRA block is interleaved
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        int mb, nb;
-        gemm_tile_coords(t, args.tiles_m, args.tiles_n, mb, nb);
-        const int m0 = mb * Cfg::BM, n0 = nb * BN;
-        for (int kb = 0; kb < nkb; ++kb) {
+      auto load_main = [&](const TileInfo& ti, int kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
+        uint8_t* sB = sA + Cfg::A_BYTES;
+        mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+        tma_load_2d(sA, &tmA, &full[stage], kb * Cfg::BK, ti.mb * Cfg::BM);
+        if constexpr (!B_MN) {
+          tma_load_2d(sB, &tmB, &full[stage], kb * Cfg::BK, ti.nb * BN);
+        } else {
+#pragma unroll
+          for (int i = 0; i < BN / 64; ++i)
+            tma_load_2d(sB + i * 8192, &tmB, &full[stage], ti.nb * BN + 64 * i, kb * Cfg::BK);
+        }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      };
+      auto load_lora = [&](const TileInfo& ti) {
+        for (int c = ti.col_lo; c < ti.col_hi; c += 64) {
+          const int nsub = min(4, (ti.col_hi - c) >> 4);
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sB = sA + Cfg::A_BYTES;
-          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-          tma_load_2d(sA, &tmA, &full[stage], kb * Cfg::BK, m0);
-          if constexpr (!B_MN) {
-            tma_load_2d(sB, &tmB, &full[stage], kb * Cfg::BK, n0);
-          } else {
+          mbar_arrive_expect_tx(&full[stage], nsub * (Cfg::BM * 32 + BN * 32));
+          for (int j = 0; j < nsub; ++j) {
+            tma_load_2d(sA + j * (Cfg::BM * 32), &tmA2, &full[stage], c + 16 * j, ti.mb * Cfg::BM);
+            if constexpr (!B_MN) {
+              tma_load_2d(sB + j * (BN * 32), &tmB2, &full[stage], c + 16 * j, ti.nb * BN);
+            } else {
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i) tma_load_2d(sB + i * 8192, &tmB, &full[stage], n0 + 64 * i, kb * Cfg::BK);
+              for (int i = 0; i < BN / 64; ++i)
+                tma_load_2d(sB + j * (BN / 64) * 2048 + i * 2048, &tmB2, &full[stage], ti.nb * BN + 64 * i,
+                            c + 16 * j);
+            }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        if (args.routes) {
-          const LfRoute rt = args.routes[mb];
-          for (int c = rt.col_lo; c < rt.col_hi; c += 64) {
-            const int nsub = min(4, (rt.col_hi - c) >> 4);
-            mbar_wait(&empty[stage], phase ^ 1);
-            uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
-            uint8_t* sB = sA + Cfg::A_BYTES;
-            mbar_arrive_expect_tx(&full[stage], nsub * (Cfg::BM * 32 + BN * 32));
-            for (int j = 0; j < nsub; ++j) {
-              tma_load_2d(sA + j * (Cfg::BM * 32), &tmA2, &full[stage], c + 16 * j, m0);
-              if constexpr (!B_MN) {
-                tma_load_2d(sB + j * (BN * 32), &tmB2, &full[stage], c + 16 * j, n0);
-              } else {
-#pragma unroll
-                for (int i = 0; i < BN / 64; ++i)
-                  tma_load_2d(sB + j * (BN / 64) * 2048 + i * 2048, &tmB2, &full[stage], n0 + 64 * i, c + 16 * j);
-              }
-            }
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      };
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const TileInfo ti = tile_info(args, t);
+        if constexpr (MASKED) {
+          if (t == (int)blockIdx.x && ti.lora()) load_lora(ti);
+          const bool has_next = t + (int)gridDim.x < tiles;
+          const TileInfo tn = has_next ? tile_info(args, t + gridDim.x) : ti;
+          for (int kb = 0; kb < nkb; ++kb) {
+            if (kb == jmid && has_next && tn.lora()) load_lora(tn);
+            load_main(ti, kb);
           }
+          if (jmid >= nkb && has_next && tn.lora()) load_lora(tn);
+        } else {
+          for (int kb = 0; kb < nkb; ++kb) load_main(ti, kb);
+          if (ti.lora()) load_lora(ti);
         }
       }
     }
@@ -141,50 +208,75 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t idesc = make_idesc_bf16(Cfg::BM, BN, false, B_MN);
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-        int mb, nb;
-        gemm_tile_coords(t, args.tiles_m, args.tiles_n, mb, nb);
-        const int acc = it & 1;
-        const uint32_t aph = (it >> 1) & 1;
-        mbar_wait(&tempty[acc], aph ^ 1);
+      uint32_t lora_uses[2] = {0, 0};  // MASKED: LoRA partials produced per accumulator buffer
+      auto mma_main_block = [&](uint32_t d, int kb, bool acc_any) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * Cfg::ACC_COLS;
-        for (int kb = 0; kb < nkb; ++kb) {
+        const uint32_t sA = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+        const uint32_t sB = sA + Cfg::A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t ad = make_sdesc(sA + kk * 32, 16, 1024, kLayoutSW128);
+          const uint64_t bd = B_MN ? make_sdesc(sB + kk * 2048, 8192, 1024, kLayoutSW128)
+                                   : make_sdesc(sB + kk * 32, 16, 1024, kLayoutSW128);
+          umma_bf16(d, ad, bd, idesc, (acc_any || (kb | kk) != 0) ? 1u : 0u);
+        }
+        umma_commit(&empty[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      };
+      auto mma_lora = [&](const TileInfo& ti, uint32_t d, bool acc_any) {
+        uint32_t accum = acc_any ? 1u : 0u;
+        for (int c = ti.col_lo; c < ti.col_hi; c += 64) {
+          const int nsub = min(4, (ti.col_hi - c) >> 4);
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t sA = smem_u32(smem + stage * Cfg::STAGE_BYTES);
           const uint32_t sB = sA + Cfg::A_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ad = make_sdesc(sA + kk * 32, 16, 1024, kLayoutSW128);
-            const uint64_t bd = B_MN ? make_sdesc(sB + kk * 2048, 8192, 1024, kLayoutSW128)
-                                     : make_sdesc(sB + kk * 32, 16, 1024, kLayoutSW128);
-            umma_bf16(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          for (int j = 0; j < nsub; ++j) {
+            const uint64_t ad = make_sdesc(sA + j * (Cfg::BM * 32), 16, 256, kLayoutSW32);
+            const uint64_t bd = B_MN ? make_sdesc(sB + j * (BN / 64) * 2048, 2048, 1024, kLayoutSW128)
+                                     : make_sdesc(sB + j * (BN * 32), 16, 256, kLayoutSW32);
+            umma_bf16(d, ad, bd, idesc, accum);
+            accum = 1u;
           }
           umma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        if (args.routes) {
-          const LfRoute rt = args.routes[mb];
-          const uint32_t dl = MASKED ? d + BN : d;
-          uint32_t accum = MASKED ? 0u : 1u;
-          for (int c = rt.col_lo; c < rt.col_hi; c += 64) {
-            const int nsub = min(4, (rt.col_hi - c) >> 4);
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            const uint32_t sA = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-            const uint32_t sB = sA + Cfg::A_BYTES;
-            for (int j = 0; j < nsub; ++j) {
-              const uint64_t ad = make_sdesc(sA + j * (Cfg::BM * 32), 16, 256, kLayoutSW32);
-              const uint64_t bd = B_MN ? make_sdesc(sB + j * (BN / 64) * 2048, 2048, 1024, kLayoutSW128)
-                                       : make_sdesc(sB + j * (BN * 32), 16, 256, kLayoutSW32);
-              umma_bf16(dl, ad, bd, idesc, accum);
-              accum = 1u;
-            }
-            umma_commit(&empty[stage]);
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      };
+      // MASKED: LoRA partial of local tile `it` into its (drained) buffer, then signal the mask pass
+      auto issue_lora_first = [&](const TileInfo& ti, int it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        mma_lora(ti, tmem_base + acc * Cfg::ACC_COLS, false);
+        umma_commit(&lfull[acc]);
+      };
+      int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        const TileInfo ti = tile_info(args, t);
+        const int acc = it & 1;
+        const uint32_t d = tmem_base + acc * Cfg::ACC_COLS;
+        if constexpr (MASKED) {
+          if (it == 0 && ti.lora()) issue_lora_first(ti, 0);
+          if (ti.lora()) {
+            mbar_wait(&lmasked[acc], lora_uses[acc] & 1);
+            ++lora_uses[acc];
+          } else {
+            mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
           }
+          tc_fence_after();
+          const bool has_next = t + (int)gridDim.x < tiles;
+          const TileInfo tn = has_next ? tile_info(args, t + gridDim.x) : ti;
+          for (int kb = 0; kb < nkb; ++kb) {
+            if (kb == jmid && has_next && tn.lora()) issue_lora_first(tn, it + 1);
+            mma_main_block(d, kb, ti.lora());
+          }
+          if (jmid >= nkb && has_next && tn.lora()) issue_lora_first(tn, it + 1);
+        } else {
+          mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+          tc_fence_after();
+          for (int kb = 0; kb < nkb; ++kb) mma_main_block(d, kb, false);
+          if (ti.lora()) mma_lora(ti, d, true);
         }
         umma_commit(&tfull[acc]);
       }
@@ -193,23 +285,52 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..5)
     const uint32_t q = warp & 3u;  // TMEM lane quadrant this warp may access
+    uint32_t lora_uses[2] = {0, 0};
+    // MASKED: zero the dropped elements of tile `it`'s LoRA partial in place
+    auto mask_pass = [&](const TileInfo& ti, int it) {
+      const int acc = it & 1;
+      mbar_wait(&lfull[acc], lora_uses[acc] & 1);
+      ++lora_uses[acc];
+      tc_fence_after();
+      const int row = ti.mb * Cfg::BM + (int)(q * 32 + lane);
+      const LfRoute rt = args.routes[ti.mb];
+      const int seg = row < args.M ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
+      const bool active = seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0);
+      // tcgen05.ld/st are warp-collective (.sync.aligned): every branch around them is warp-uniform
+      if (__any_sync(0xFFFFFFFFu, active)) {
+        const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * Cfg::ACC_COLS;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          const uint32_t keep = active ? dgrad_keep32(args.segs, seg, row, ti.nb * BN + c, args.N) : 0xFFFFFFFFu;
+          if (__all_sync(0xFFFFFFFFu, keep == 0xFFFFFFFFu)) continue;
+          uint32_t v[32];
+          tmem_ld32(taddr + c, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (!((keep >> i) & 1u)) v[i] = 0u;
+          tmem_st32(taddr + c, v);
+        }
+        tmem_st_wait();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&lmasked[acc]);
+    };
     int it = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-      int mb, nb;
-      gemm_tile_coords(t, args.tiles_m, args.tiles_n, mb, nb);
+      const TileInfo ti = tile_info(args, t);
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
-      const int row = mb * Cfg::BM + (int)(q * 32 + lane);
-      const int n0 = nb * BN;
-      bool lora_on = false;
-      int seg = -1;
       if constexpr (MASKED) {
-        if (args.routes) {
-          const LfRoute rt = args.routes[mb];
-          lora_on = rt.col_lo < rt.col_hi;
-          seg = find_segment(args.segs, rt.seg_lo, rt.seg_hi, row);
+        if (it == 0 && ti.lora()) mask_pass(ti, 0);
+        if (t + (int)gridDim.x < tiles) {
+          const TileInfo tn = tile_info(args, t + gridDim.x);
+          if (tn.lora()) mask_pass(tn, it + 1);
         }
       }
+      const int row = ti.mb * Cfg::BM + (int)(q * 32 + lane);
+      const int n0 = ti.nb * BN;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * Cfg::ACC_COLS;
@@ -218,42 +339,16 @@ __global__ void __launch_bounds__(192, 1)
       for (int c = 0; c < BN; c += 32) {
         uint32_t v[32];
         tmem_ld32(taddr + c, v);
-        float f[32];
-        if constexpr (MASKED) {
-          uint32_t u[32];
-          if (lora_on) tmem_ld32(taddr + BN + c, u);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-          if (lora_on && seg >= 0) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int col = n0 + c + 8 * j;
-              uint32_t bits;
-              if (args.segs.mask_mode == 2) {
-                bits = (row < args.M) ? explicit_keep8(args.segs.mask + (int64_t)row * args.segs.ld_mask, col, args.N)
-                                      : 0u;
-              } else {
-                const LfSegDev& s = args.segs.seg[seg];
-                bits = s.thr ? philox_keep8((uint32_t)col >> 3, (uint32_t)row, s) : 0xFFu;
-              }
-#pragma unroll
-              for (int e = 0; e < 8; ++e)
-                if ((bits >> e) & 1u) f[8 * j + e] += __uint_as_float(u[8 * j + e]);
-            }
-          }
-        } else {
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-        }
+        tmem_ld_wait();
         if (row < args.M) {
           const int col0 = n0 + c;
           uint4 pk[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            pk[j] = make_uint4(pack_bf16x2(f[8 * j + 0], f[8 * j + 1]), pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
-                               pack_bf16x2(f[8 * j + 4], f[8 * j + 5]), pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
+            pk[j] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1])),
+                               pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
+                               pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
+                               pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             if (col0 + 8 * j < args.N) *reinterpret_cast<uint4*>(crow + col0 + 8 * j) = pk[j];
@@ -275,7 +370,7 @@ __global__ void __launch_bounds__(192, 1)
 
 template <int BN, bool B_MN, bool MASKED, int STAGES>
 static int launch_one(const GemmMaps& maps, const GemmArgs& args, int num_sms, cudaStream_t stream) {
-  using Cfg = GemmCfg<BN, B_MN, MASKED, STAGES>;
+  using Cfg = GemmCfg<BN, B_MN, STAGES>;
   auto kern = lf_gemm_kernel<BN, B_MN, MASKED, STAGES>;
   static bool configured = false;  // per instantiation; attribute set is idempotent
   if (!configured) {
@@ -291,19 +386,15 @@ static int launch_one(const GemmMaps& maps, const GemmArgs& args, int num_sms, c
 
 int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_sms, cudaStream_t stream) {
   GemmArgs args = a;
+  args.tiles_m = (args.M + 127) / 128;
+  args.tiles_n = (args.N + 255) / 256;
   switch (kind) {
     case kGemmFwd:
-      args.tiles_m = (args.M + 127) / 128;
-      args.tiles_n = (args.N + 255) / 256;
       return launch_one<256, false, false, 4>(maps, args, num_sms, stream);
     case kGemmDgrad:
-      args.tiles_m = (args.M + 127) / 128;
-      args.tiles_n = (args.N + 255) / 256;
       return launch_one<256, true, false, 4>(maps, args, num_sms, stream);
     case kGemmDgradMasked:
-      args.tiles_m = (args.M + 127) / 128;
-      args.tiles_n = (args.N + 127) / 128;
-      return launch_one<128, true, true, 6>(maps, args, num_sms, stream);
+      return launch_one<256, true, true, 4>(maps, args, num_sms, stream);
   }
   return -1;
 }

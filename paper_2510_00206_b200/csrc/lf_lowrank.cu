@@ -30,26 +30,6 @@ __device__ __forceinline__ bool tile_needs_mask(const LfSegTable& t, const LfRou
   return false;
 }
 
-// zero dropped elements of one row of an SW128 tile (64 bf16 columns starting at col)
-__device__ __forceinline__ void mask_row_sw128(uint8_t* tile, int rit, int row, int col, int ncols,
-                                               const LfSegTable& t, int seg) {
-  uint8_t* rowp = tile + rit * 128;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int cc = col + 8 * c;
-    uint32_t bits;
-    if (t.mask_mode == 2) {
-      bits = explicit_keep8(t.mask + (int64_t)row * t.ld_mask, cc, ncols);
-    } else {
-      bits = philox_keep8((uint32_t)cc >> 3, (uint32_t)row, t.seg[seg]);
-    }
-    if (bits != 0xFFu) {
-      uint4* p = reinterpret_cast<uint4*>(rowp + ((c ^ (rit & 7)) << 4));
-      *p = apply_keep8(*p, bits);
-    }
-  }
-}
-
 // finalize one row of a split-K reduced m x R result: scale own-segment columns, zero the
 // rest, write bf16, and return the partial-sum workspace to zero.
 __device__ __forceinline__ void finalize_row(const LfSegTable& t, const LfRoute& rt, int row, float* ws,
@@ -185,7 +165,13 @@ __global__ void __launch_bounds__(192, 2)
       uint32_t phase = 0;
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
-        if (my_mask) mask_row_sw128(smem + stage * STAGE_BYTES, rit, row, kb * 64, args.k, args.segs, seg);
+        if (my_mask) {
+          const uint64_t bits = keep_bits64(args.segs, seg, row, kb * 64, args.k);
+          apply_row_sw128(smem + stage * STAGE_BYTES, rit, bits);
+          // Philox runs once per step: ④ and ⑤ read these bits instead
+          if (args.segs.mask_mode == 1 && args.segs.bits)
+            store_bits64(args.segs.bits + (int64_t)row * args.segs.ld_bits, kb * 8, (int)args.segs.ld_bits, bits);
+        }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&masked[stage]);
@@ -372,8 +358,17 @@ __global__ void __launch_bounds__(192, 2)
         mbar_wait(&full[stage], phase);
         if (seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0)) {
           uint8_t* sX = smem + stage * stage_bytes;
-          mask_row_sw128(sX, rit, row, kt * 128, args.k, args.segs, seg);
-          mask_row_sw128(sX + 16384, rit, row, kt * 128 + 64, args.k, args.segs, seg);
+          uint64_t b0, b1;
+          if (args.segs.mask_mode == 1 && args.segs.bits) {
+            const uint8_t* rb = args.segs.bits + (int64_t)row * args.segs.ld_bits;
+            b0 = load_bits64(rb, kt * 16, (int)args.segs.ld_bits);
+            b1 = load_bits64(rb, kt * 16 + 8, (int)args.segs.ld_bits);
+          } else {
+            b0 = keep_bits64(args.segs, seg, row, kt * 128, args.k);
+            b1 = keep_bits64(args.segs, seg, row, kt * 128 + 64, args.k);
+          }
+          apply_row_sw128(sX, rit, b0);
+          apply_row_sw128(sX + 16384, rit, b1);
         }
         fence_proxy_async_smem();
         __syncwarp();

@@ -30,6 +30,8 @@ struct LfSegTable {
   int32_t mask_mode;    // 0 = no dropout anywhere, 1 = Philox, 2 = explicit uint8 mask
   const uint8_t* mask;  // explicit keep mask (m x ld_mask) when mask_mode == 2
   int64_t ld_mask;
+  uint8_t* bits;        // bit-packed Philox keep mask (m x ld_bits bytes) when mask_mode == 1, or null
+  int64_t ld_bits;      // = k / 8
   LfSegDev seg[LF_MAX_SEGS];
 };
 

@@ -31,6 +31,55 @@ def _stream() -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+class LaunchStats:
+    """Counts kernel launches and (optionally) times each launcher with CUDA events on the
+    launching stream. Install with ``set_launch_stats``; used by bench.py."""
+
+    def __init__(self, timed: bool = False):
+        self.timed = timed
+        self.launches: dict[str, int] = {}
+        self.events: dict[str, list] = {}
+
+    def begin(self, name: str):
+        self.launches[name] = self.launches.get(name, 0) + 1
+        if not self.timed:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        return ev
+
+    def end(self, name: str, start) -> None:
+        if start is None:
+            return
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.events.setdefault(name, []).append((start, ev))
+
+    def total_launches(self) -> int:
+        return sum(self.launches.values())
+
+    def durations_ms(self) -> dict[str, list[float]]:
+        torch.cuda.synchronize()
+        return {k: [a.elapsed_time(b) for a, b in v] for k, v in self.events.items()}
+
+
+_STATS: LaunchStats | None = None
+
+
+def set_launch_stats(stats: LaunchStats | None) -> None:
+    global _STATS
+    _STATS = stats
+
+
+def _call(name: str, fn, *args) -> None:
+    st = _STATS
+    tok = st.begin(name) if st is not None else None
+    rc = fn(*args)
+    if st is not None:
+        st.end(name, tok)
+    _lib.check(rc, name)
+
+
 def _check_operand(t: torch.Tensor, name: str, shape: tuple | None = None) -> None:
     if not isinstance(t, torch.Tensor):
         raise ValidationError(f"{name} must be a torch.Tensor")
@@ -45,21 +94,30 @@ def _check_operand(t: torch.Tensor, name: str, shape: tuple | None = None) -> No
 
 
 class _FusedLoRAFn(torch.autograd.Function):
-    """Autograd node over the five kernels. Inputs: x (m,k), w (n,k), a_cat (R,k), b_cat (n,R)."""
+    """Autograd node over the five kernels.
+
+    Inputs: x (m,k) bf16, w (n,k) bf16 frozen, the plan, an optional per-slot gradient sink,
+    then the adapter parameters lora_A[0..a) and lora_B[0..a) in their own dtype (fp32
+    master weights are cast to the bf16 rank-concat operands inside, outside autograd, so
+    their gradients come back in fp32 without a bf16 round trip)."""
 
     @staticmethod
-    def forward(ctx, x, w, a_cat, b_cat, plan: LayerPlan, grad_sink):
+    def forward(ctx, x, w, plan: LayerPlan, grad_sink, n_adapters: int, *params):
         lib = _lib.load()
         m, k, n, R = plan.m, plan.k, plan.n, plan.rank_total
         pp = ctypes.byref(plan.problem)
         y = torch.empty((m, n), dtype=_BF16, device=x.device)
-        s_hat = None
+        s_hat = a_cat = b_cat = None
         if plan.has_lora:
+            a_cat = plan.gather_a(params[:n_adapters])
+            b_cat = plan.gather_b(params[n_adapters:])
             s_hat = torch.empty((m, R), dtype=_BF16, device=x.device)
-            _lib.check(lib.lf_dropout_down_fwd(pp, _ptr(x), _ptr(a_cat), _ptr(s_hat), _stream()), "dropout_down_fwd")
-        _lib.check(lib.lf_base_fwd(pp, _ptr(x), _ptr(w), _ptr(s_hat), _ptr(b_cat), _ptr(y), _stream()), "base_fwd")
+            _call("dropout_down_fwd", lib.lf_dropout_down_fwd, pp, _ptr(x), _ptr(a_cat), _ptr(s_hat), _stream())
+        _call("base_fwd", lib.lf_base_fwd, pp, _ptr(x), _ptr(w), _ptr(s_hat), _ptr(b_cat), _ptr(y), _stream())
         ctx.plan = plan
         ctx.grad_sink = grad_sink
+        ctx.n_adapters = n_adapters
+        ctx.param_dtypes = [p.dtype for p in params]
         ctx.save_for_backward(x, w, a_cat, b_cat, s_hat)
         return y
 
@@ -76,16 +134,28 @@ class _FusedLoRAFn(torch.autograd.Function):
             ds = torch.empty((m, R), dtype=_BF16, device=dy.device)
             db = torch.zeros((n, R), dtype=torch.float32, device=dy.device)
             da = torch.zeros((R, k), dtype=torch.float32, device=dy.device)
-            _lib.check(lib.lf_grad_up(pp, _ptr(dy), _ptr(b_cat), _ptr(s_hat), _ptr(ds), _ptr(db), _stream()), "grad_up")
-            _lib.check(lib.lf_grad_down(pp, _ptr(x), _ptr(ds), _ptr(da), _stream()), "grad_down")
+            _call("grad_up", lib.lf_grad_up, pp, _ptr(dy), _ptr(b_cat), _ptr(s_hat), _ptr(ds), _ptr(db), _stream())
+            _call("grad_down", lib.lf_grad_down, pp, _ptr(x), _ptr(ds), _ptr(da), _stream())
         dx = None
         if ctx.needs_input_grad[0]:
             dx = torch.empty((m, k), dtype=_BF16, device=dy.device)
-            _lib.check(lib.lf_grad_input(pp, _ptr(dy), _ptr(w), _ptr(ds), _ptr(a_cat), _ptr(dx), _stream()),
-                       "grad_input")
+            _call("grad_input", lib.lf_grad_input, pp, _ptr(dy), _ptr(w), _ptr(ds), _ptr(a_cat), _ptr(dx), _stream())
         if ctx.grad_sink is not None and plan.has_lora:
             ctx.grad_sink(plan, da, db)
-        return dx, None, da, db, None, None
+        # route the rank-concat gradients back to each adapter's parameters (summing the
+        # segments that share an adapter, e.g. two global batches in one microbatch)
+        na = ctx.n_adapters
+        ga: list = [None] * na
+        gb: list = [None] * na
+        if plan.has_lora:
+            for adapter, _batch, c0, r in plan.segment_grad_slices():
+                a_part, b_part = da[c0:c0 + r], db[:, c0:c0 + r]
+                ga[adapter] = a_part if ga[adapter] is None else ga[adapter] + a_part
+                gb[adapter] = b_part if gb[adapter] is None else gb[adapter] + b_part
+        dts = ctx.param_dtypes
+        ga = [g.to(dts[i]) if g is not None else None for i, g in enumerate(ga)]
+        gb = [g.to(dts[na + i]) if g is not None else None for i, g in enumerate(gb)]
+        return (dx, None, None, None, None, *ga, *gb)
 
 
 def _flatten_input(x: torch.Tensor, k: int) -> tuple[torch.Tensor, tuple]:
@@ -174,13 +244,7 @@ def _run(x2, weight, lora_a, lora_b, plan: LayerPlan, lead, grad_sink):
     if plan.m == 0:
         return x2.new_empty(lead + (plan.n,))
     plan.bind(x2.device)
-    if plan.has_lora:
-        a_cat = plan.gather_a(lora_a)
-        b_cat = plan.gather_b(lora_b)
-    else:
-        a_cat = torch.empty((0, plan.k), dtype=_BF16, device=x2.device)
-        b_cat = torch.empty((plan.n, 0), dtype=_BF16, device=x2.device)
-    y = _FusedLoRAFn.apply(x2, weight, a_cat, b_cat, plan, grad_sink)
+    y = _FusedLoRAFn.apply(x2, weight, plan, grad_sink, len(lora_a), *lora_a, *lora_b)
     return y.reshape(lead + (plan.n,))
 
 

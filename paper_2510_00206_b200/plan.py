@@ -189,6 +189,10 @@ class LayerPlan:
         p.keep_mask = keep_mask.data_ptr() if (keep_mask is not None and self.training) else None
         self.routes: torch.Tensor | None = None
         self._ws: torch.Tensor | None = None
+        # ① writes the Philox keep mask bit-packed (m x k/8 bytes); ④/⑤ read it back
+        self.needs_keep_bits = (self.training and keep_mask is None and
+                                any(p.segments[i].dropout_p > 0 for i in range(p.num_segments)))
+        self.keep_bits: torch.Tensor | None = None
 
     # -- derived ------------------------------------------------------------------
     @property
@@ -214,9 +218,14 @@ class LayerPlan:
         self.problem.routes = self.routes.data_ptr()
         self.problem.workspace = self._ws.data_ptr()
         self.problem.workspace_bytes = self._ws.numel()
+        if self.needs_keep_bits:
+            self.keep_bits = torch.empty((self.m, self.k // 8), dtype=torch.uint8, device=device)
+            self.problem.keep_bits = self.keep_bits.data_ptr()
         if self.has_lora:
-            _lib.check(lib.lf_build_routes(ctypes.byref(self.problem), self.routes.data_ptr(),
-                                           ctypes.c_void_p(stream.cuda_stream)), "lf_build_routes")
+            from .functional import _call
+
+            _call("build_routes", lib.lf_build_routes, ctypes.byref(self.problem), self.routes.data_ptr(),
+                  ctypes.c_void_p(stream.cuda_stream))
         return self
 
     def gather_a(self, lora_a: Sequence[torch.Tensor]) -> torch.Tensor:

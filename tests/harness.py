@@ -81,7 +81,7 @@ def run_oracle(case: Case, x, w, dy, a_cat, b_cat, keep=None):
     return dict(y=y, s_hat=s_hat, dx=dx, da=da, db=db, ds=ds, keep=keep)
 
 
-def make_problem(case: Case, device, keep_mask=None):
+def make_problem(case: Case, device, keep_mask=None, use_bits=False):
     from paper_2510_00206_b200 import _lib
 
     segs, R = oracle_segments(case)
@@ -99,16 +99,21 @@ def make_problem(case: Case, device, keep_mask=None):
     p.workspace = ws.data_ptr()
     p.workspace_bytes = ws.numel()
     p.keep_mask = keep_mask.data_ptr() if keep_mask is not None else None
+    bits = None
+    if use_bits:
+        bits = torch.full((case.m, case.k // 8), 0xAA, dtype=torch.uint8, device=device)
+        p.keep_bits = bits.data_ptr()
+    p._bits_ref = bits  # keep alive
     return p, routes, ws, R
 
 
-def run_device(case: Case, x, w, dy, a_cat, b_cat, keep_mask=None, device="cuda"):
+def run_device(case: Case, x, w, dy, a_cat, b_cat, keep_mask=None, device="cuda", use_bits=False):
     """Run all five launchers through the C ABI; returns every intermediate on the host."""
     from paper_2510_00206_b200 import _lib
 
     lib = _lib.load()
     dev = torch.device(device)
-    p, routes, ws, R = make_problem(case, dev, keep_mask)
+    p, routes, ws, R = make_problem(case, dev, keep_mask, use_bits)
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     P = lambda t: ctypes.c_void_p(t.data_ptr())
     xd, wd, dyd = x.to(dev).contiguous(), w.to(dev).contiguous(), dy.to(dev).contiguous()

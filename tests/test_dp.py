@@ -1,0 +1,68 @@
+"""Data-parallel host logic on CPU: microbatch assignment and the bucketed adapter-gradient
+all-reduce over a world_size-2 gloo group (the NCCL path on the B200 box is identical)."""
+from __future__ import annotations
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2510_00206_b200 import dp
+
+
+def test_assign_microbatches_balances_and_covers():
+    counts = [8192, 8000, 7800, 4096, 4096, 2048, 1024, 512, 8192, 6000, 300, 64]
+    for world in (1, 2, 4, 8):
+        a = dp.assign_microbatches(counts, world)
+        flat = sorted(i for r in a for i in r)
+        assert flat == list(range(len(counts)))
+        loads = dp.rank_loads(counts, a)
+        # LPT bound: max load <= mean + largest item
+        assert max(loads) <= sum(counts) / world + max(counts)
+        assert a == dp.assign_microbatches(counts, world)  # deterministic
+    assert dp.imbalance([10, 10]) == 0.0
+    assert dp.imbalance([10, 5]) == pytest.approx(1 - 7.5 / 10)
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank: int, world: int, port: int, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.manual_seed(rank)
+        params = [torch.nn.Parameter(torch.zeros(16, 40)), torch.nn.Parameter(torch.zeros(72, 16)),
+                  torch.nn.Parameter(torch.zeros(8, 8))]
+        for i, p in enumerate(params):
+            p.grad = torch.full_like(p, float(rank + 1) * (i + 1))
+        params[2].grad = None  # a parameter without a gradient this step contributes zeros
+        red = dp.AdapterGradReducer(params, bucket_bytes=3000)  # forces several buckets
+        assert len(red.buckets) >= 2
+        red.reduce()
+        tot = sum(r + 1 for r in range(world))
+        ok = all(torch.allclose(p.grad, torch.full_like(p, tot * (i + 1.0))) for i, p in enumerate(params[:2]))
+        ok = ok and torch.count_nonzero(params[2].grad) == 0
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_adapter_grad_allreduce_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}

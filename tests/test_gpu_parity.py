@@ -1,0 +1,281 @@
+"""Parity of the sm_100a kernels with the CPU oracle (SPEC.md §5 tolerances), through the
+C ABI and through the public module/functional API. Needs a B200."""
+from __future__ import annotations
+
+import ctypes
+import glob
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import tests.harness as H
+from oracle import lora as olora
+from oracle import philox as ophilox
+from oracle import routing as orouting
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+def _lib():
+    from paper_2510_00206_b200 import _lib
+
+    return _lib
+
+
+def _check_all(out, ref, tag):
+    for key in ("s_hat", "y", "ds", "dx"):
+        H.assert_close_bf16(out[key], ref[key], f"{tag}:{key}")
+    for key in ("da", "db"):
+        H.assert_close_bf16(out[key], ref[key], f"{tag}:{key}")
+
+
+CASES = {
+    "single_r16_p0": H.Case(256, 512, 384, (16,), (256,), (2.0,), (0.0,), (11,)),
+    "single_r16_p01": H.Case(256, 512, 384, (16,), (256,), (2.0,), (0.1,), (12,)),
+    "single_r8_odd": H.Case(130, 72, 200, (8,), (130,), (2.0,), (0.1,), (13,)),
+    "single_r32": H.Case(384, 256, 520, (32,), (384,), (0.5,), (0.05,), (14,)),
+    "single_r64": H.Case(200, 1024, 256, (64,), (200,), (1.0,), (0.1,), (15,)),
+    "one_row": H.Case(1, 64, 64, (16,), (1,), (2.0,), (0.5,), (16,)),
+    "multi4_aligned": H.Case(1024, 512, 512, (8, 16, 32, 64), (448, 304, 176, 96), (2.0,) * 4,
+                             (0.0, 0.05, 0.1, 0.1), (1, 2, 3, 4)),
+    "multi4_straddle_p64": H.Case(1088, 256, 264, (8, 16, 32, 64), (320, 448, 192, 128), (2.0, 1.0, 0.5, 2.0),
+                                  (0.1, 0.0, 0.1, 0.2), (5, 6, 7, 8)),
+    "rows_without_adapter": H.Case(640, 256, 256, (16, 16), (100, 300), (2.0, 2.0), (0.1, 0.0), (9, 10)),
+    "c1": H.Case(2048, 4096, 4096, (16,), (2048,), (2.0,), (0.1,), (1234,)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+@pytest.mark.parametrize("use_bits", [False, True], ids=["philox", "packed"])
+def test_kernels_match_oracle(name, use_bits):
+    case = CASES[name]
+    x, w, dy, a_list, b_list = H.make_inputs(case, seed=hash(name) % 1000)
+    a_cat, b_cat = H.cat_weights(case, a_list, b_list)
+    ref = H.run_oracle(case, x, w, dy, a_cat, b_cat)
+    out = H.run_device(case, x, w, dy, a_cat, b_cat, use_bits=use_bits)
+    _check_all(out, ref, name)
+    segs, _ = H.oracle_segments(case)
+    r_ref = orouting.routes([(s.row_start, s.row_end) for s in segs], [(s.col_start, s.rank) for s in segs], case.m)
+    assert np.array_equal(out["routes"], r_ref)
+    assert out["ws_clean"], "split-K workspace must be returned to zero"
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_dropout_mask_bit_exact(name):
+    case = CASES[name]
+    L = _lib()
+    p, routes, ws, R = H.make_problem(case, torch.device(DEV))
+    keep = torch.empty((case.m, case.k), dtype=torch.uint8, device=DEV)
+    L.check(L.load().lf_dropout_mask(ctypes.byref(p), ctypes.c_void_p(keep.data_ptr()), None), "mask")
+    segs, _ = H.oracle_segments(case)
+    assert np.array_equal(keep.cpu().numpy(), H.oracle_keep(case, segs))
+
+
+def test_packed_bits_written_by_forward_match_oracle():
+    case = CASES["multi4_straddle_p64"]
+    x, w, dy, a_list, b_list = H.make_inputs(case)
+    a_cat, b_cat = H.cat_weights(case, a_list, b_list)
+    L = _lib()
+    lib = L.load()
+    p, routes, ws, R = H.make_problem(case, torch.device(DEV), use_bits=True)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    xd, ad = x.to(DEV), a_cat.to(DEV)
+    s_hat = torch.empty((case.m, R), dtype=torch.bfloat16, device=DEV)
+    L.check(lib.lf_build_routes(ctypes.byref(p), P(routes), None), "routes")
+    L.check(lib.lf_dropout_down_fwd(ctypes.byref(p), P(xd), P(ad), P(s_hat), None), "down")
+    bits = p._bits_ref.cpu().numpy()
+    segs, _ = H.oracle_segments(case)
+    keep = H.oracle_keep(case, segs)
+    for s in segs:
+        if s.dropout_p == 0:
+            continue
+        rows = slice(s.row_start, s.row_end)
+        unpacked = np.unpackbits(bits[rows], axis=1, bitorder="little")[:, :case.k]
+        assert np.array_equal(unpacked, keep[rows])
+
+
+def test_explicit_keep_mask():
+    case = CASES["single_r16_p01"]
+    x, w, dy, a_list, b_list = H.make_inputs(case)
+    a_cat, b_cat = H.cat_weights(case, a_list, b_list)
+    rng = np.random.default_rng(0)
+    keep = (rng.random((case.m, case.k)) > 0.3).astype(np.uint8)
+    ref = H.run_oracle(case, x, w, dy, a_cat, b_cat, keep=keep)
+    out = H.run_device(case, x, w, dy, a_cat, b_cat, keep_mask=torch.from_numpy(keep).to(DEV))
+    _check_all(out, ref, "explicit")
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "numeric_*.npz"))),
+                         ids=os.path.basename)
+def test_golden_vectors(path):
+    """Committed oracle vectors: exact bf16 inputs, bit-exact mask, outputs within tolerance."""
+    d = np.load(path)
+    f = lambda k: torch.from_numpy(olora.from_bf16_bits(d[k])).to(torch.bfloat16)
+    st = d["seg_table"]
+    sp = d["seg_params"]
+    m, k = d["x"].shape
+    n = d["w"].shape[0]
+    used = int(st[-1, 1])
+    lengths = tuple(int(r1 - r0) for r0, r1, _, _ in st)
+    case = H.Case(m, k, n, tuple(int(r) for r in st[:, 3]), lengths, tuple(float(v) for v in sp[:, 0]),
+                  tuple(float(v) for v in sp[:, 1]), tuple(int(v) for v in d["seg_seeds"]), int(d["offset"][0]),
+                  m - used)
+    out = H.run_device(case, f("x"), f("w"), f("dy"), f("a_cat"), f("b_cat"))
+    ref = {kk: olora.from_bf16_bits(d[kk]) for kk in ("y", "s_hat", "dx", "ds")}
+    ref.update(da=d["da"], db=d["db"])
+    _check_all(out, ref, os.path.basename(path))
+
+
+def test_module_api_fused_lora_matches_oracle():
+    from paper_2510_00206_b200 import FusedLoRA
+
+    case = H.Case(512, 256, 384, (16,), (512,), (2.0,), (0.1,), (21,))
+    x, w, dy, a_list, b_list = H.make_inputs(case)
+    layer = FusedLoRA(w.to(DEV), rank=16, scaling=2.0, dropout_p=0.1, seed=21).to(DEV)
+    with torch.no_grad():
+        layer.lora_A.weight.copy_(a_list[0].float())
+        layer.lora_B.weight.copy_(b_list[0].float())
+    layer._offset = case.offset
+    xd = x.to(DEV).requires_grad_(True)
+    y = layer(xd)
+    y.backward(dy.to(DEV))
+    a_cat, b_cat = H.cat_weights(case, a_list, b_list)
+    ref = H.run_oracle(case, x, w, dy, a_cat, b_cat)
+    H.assert_close_bf16(y.detach().float().cpu().numpy(), ref["y"], "api:y")
+    H.assert_close_bf16(xd.grad.float().cpu().numpy(), ref["dx"], "api:dx")
+    H.assert_close_bf16(layer.lora_A.weight.grad.cpu().numpy(), ref["da"], "api:dA")
+    H.assert_close_bf16(layer.lora_B.weight.grad.cpu().numpy(), ref["db"], "api:dB")
+    assert layer._offset == case.offset + 1
+    # eval: no dropout, no offset advance
+    layer.eval()
+    with torch.no_grad():
+        y2 = layer(xd)
+    case0 = H.Case(512, 256, 384, (16,), (512,), (2.0,), (0.0,), (21,))
+    ref0 = H.run_oracle(case0, x, w, dy, a_cat, b_cat)
+    H.assert_close_bf16(y2.float().cpu().numpy(), ref0["y"], "api:eval_y")
+
+
+def test_module_api_multi_lora_slots():
+    from paper_2510_00206_b200 import AdapterConfig, FusedMultiLoRA, segments_from_lengths
+
+    case = CASES["multi4_straddle_p64"]
+    x, w, dy, a_list, b_list = H.make_inputs(case)
+    ads = [AdapterConfig(r, s, p, sd) for r, s, p, sd in zip(case.ranks, case.scalings, case.ps, case.seeds)]
+    layer = FusedMultiLoRA(w.to(DEV), ads, track_slot_grads=True).to(DEV)
+    with torch.no_grad():
+        for i in range(4):
+            layer.lora_A[i].weight.copy_(a_list[i].float())
+            layer.lora_B[i].weight.copy_(b_list[i].float())
+    layer._offset = case.offset
+    segs = segments_from_lengths([0, 1, 2, 3], case.lengths, batches=[7, 7, 7, 7])
+    xd = x.to(DEV).requires_grad_(True)
+    y = layer(xd, segs)
+    y.backward(dy.to(DEV))
+    a_cat, b_cat = H.cat_weights(case, a_list, b_list)
+    ref = H.run_oracle(case, x, w, dy, a_cat, b_cat)
+    H.assert_close_bf16(y.detach().float().cpu().numpy(), ref["y"], "multi:y")
+    H.assert_close_bf16(xd.grad.float().cpu().numpy(), ref["dx"], "multi:dx")
+    oseg, _ = H.oracle_segments(case)
+    for i, s in enumerate(oseg):
+        r = case.ranks[i]
+        H.assert_close_bf16(layer.lora_A[i].weight.grad.cpu().numpy(), ref["da"][s.col_start:s.col_start + r],
+                            f"multi:dA{i}")
+        H.assert_close_bf16(layer.lora_B[i].weight.grad.cpu().numpy(), ref["db"][:, s.col_start:s.col_start + r],
+                            f"multi:dB{i}")
+        ga, gb = layer.slot_grads[(i, 7)]
+        assert torch.equal(ga, layer.lora_A[i].weight.grad) and torch.equal(gb, layer.lora_B[i].weight.grad)
+
+
+def test_same_adapter_two_batches_keeps_separate_slots():
+    """lorasched can put two global batches of one adapter in a microbatch (SURVEY §7 hard
+    part 6): their gradients land in separate (adapter, batch) slots and sum in .grad."""
+    from paper_2510_00206_b200 import AdapterConfig, FusedMultiLoRA, Segment
+
+    torch.manual_seed(0)
+    w = (torch.randn(256, 128) / 11).to(torch.bfloat16).to(DEV)
+    layer = FusedMultiLoRA(w, [AdapterConfig(16, 2.0, 0.0, 1)], init="gaussian", track_slot_grads=True).to(DEV)
+    x = torch.randn(384, 128, device=DEV).to(torch.bfloat16).requires_grad_(True)
+    segs = [Segment(0, 0, 128, 0), Segment(0, 128, 384, 1)]
+    y = layer(x, segs)
+    y.backward(torch.randn_like(y))
+    g0a, g0b = layer.slot_grads[(0, 0)]
+    g1a, g1b = layer.slot_grads[(0, 1)]
+    torch.testing.assert_close(g0a + g1a, layer.lora_A[0].weight.grad, rtol=1e-5, atol=1e-5)
+    torch.testing.assert_close(g0b + g1b, layer.lora_B[0].weight.grad, rtol=1e-5, atol=1e-5)
+    assert not torch.allclose(g0a, g1a)
+
+
+def test_frozen_linear_no_adapter_matches_fp32_torch():
+    """num_segments = 0: the tcgen05 GEMMs alone (Y = X·Wᵀ, dX = dY·W) vs a torch fp32 reference."""
+    from paper_2510_00206_b200 import AdapterConfig, fused_multi_lora
+
+    torch.manual_seed(1)
+    for m, k, n in [(8192, 4096, 1024), (300, 264, 136)]:
+        x = torch.randn(m, k, device=DEV).to(torch.bfloat16).requires_grad_(True)
+        w = (torch.randn(n, k, device=DEV) / k**0.5).to(torch.bfloat16)
+        a = torch.zeros(16, k, device=DEV, requires_grad=True)
+        b = torch.zeros(n, 16, device=DEV, requires_grad=True)
+        y = fused_multi_lora(x, w, [a], [b], [AdapterConfig(16)], [])
+        dy = torch.randn(m, n, device=DEV).to(torch.bfloat16)
+        y.backward(dy)
+        yr = x.detach().float() @ w.float().T
+        dxr = dy.float() @ w.float()
+        H.assert_close_bf16(y.detach().float().cpu().numpy(), yr.cpu().numpy(), "frozen:y")
+        H.assert_close_bf16(x.grad.float().cpu().numpy(), dxr.cpu().numpy(), "frozen:dx")
+
+
+@pytest.mark.parametrize("shape", [(8192, 4096, 14336), (8192, 14336, 4096), (8192, 4096, 1024)],
+                         ids=["gate_up", "down", "kv"])
+def test_full_size_llama8b_shapes_vs_fp32_torch(shape):
+    """BASELINE C2 sizes (too big for the CPU oracle in a test): compare against a torch fp32
+    reference of Eq. 1 on the same device, using the kernels' own keep mask, which is pinned
+    bit-exact to the oracle by test_dropout_mask_bit_exact."""
+    from paper_2510_00206_b200 import AdapterConfig, Segment, dropout_keep_mask, fused_lora
+
+    m, k, n = shape
+    g = torch.Generator(device=DEV).manual_seed(3)
+    x = torch.randn(m, k, device=DEV, generator=g).to(torch.bfloat16).requires_grad_(True)
+    w = (torch.randn(n, k, device=DEV, generator=g) / k**0.5).to(torch.bfloat16)
+    a = ((torch.rand(16, k, device=DEV, generator=g) * 2 - 1) / k**0.5).requires_grad_(True)
+    b = (torch.randn(n, 16, device=DEV, generator=g) / 4).requires_grad_(True)
+    dy = torch.randn(m, n, device=DEV, generator=g).to(torch.bfloat16)
+    y = fused_lora(x, w, a, b, 2.0, 0.1, seed=99, offset=3)
+    y.backward(dy)
+    keep = dropout_keep_mask(m, k, [AdapterConfig(16, 2.0, 0.1, 99)], [Segment(0, 0, m)], offset=3, device=DEV)
+    xf = x.detach().float()
+    ab, bb = a.detach().bfloat16().float(), b.detach().bfloat16().float()
+    xm = xf * keep.float()
+    s = (xm @ ab.T) * (2.0 / 0.9)
+    yr = xf @ w.float().T + s.bfloat16().float() @ bb.T
+    ds = ((dy.float() @ bb) * (2.0 / 0.9))
+    dxr = dy.float() @ w.float() + keep.float() * (ds.bfloat16().float() @ ab)
+    dar = ds.bfloat16().float().T @ xm
+    dbr = dy.float().T @ s.bfloat16().float()
+    rel = lambda g_, r_: float((g_ - r_).norm() / r_.norm())
+    assert rel(y.detach().float(), yr) < 4e-3
+    assert rel(x.grad.float(), dxr) < 4e-3
+    assert rel(a.grad, dar) < 4e-3
+    assert rel(b.grad, dbr) < 4e-3
+    assert abs(keep.float().mean().item() - 0.9) < 2e-3
+
+
+def test_errors_are_loud_and_typed():
+    from paper_2510_00206_b200 import ValidationError, fused_lora
+
+    x = torch.randn(64, 64, device=DEV).to(torch.bfloat16)
+    w = torch.randn(64, 64, device=DEV).to(torch.bfloat16)
+    a = torch.randn(16, 64, device=DEV)
+    b = torch.randn(64, 16, device=DEV)
+    with pytest.raises(ValidationError, match="bfloat16"):
+        fused_lora(x.float(), w, a, b, 2.0)
+    with pytest.raises(ValidationError, match="frozen"):
+        fused_lora(x, w.clone().requires_grad_(True), a, b, 2.0)
+    with pytest.raises(ValidationError, match="shape"):
+        fused_lora(x, w, a[:, :32], b, 2.0)
+    with pytest.raises(ValidationError, match="multiples of 8"):
+        xx = torch.randn(64, 60, device=DEV).to(torch.bfloat16)
+        fused_lora(xx, torch.randn(64, 60, device=DEV).to(torch.bfloat16), a[:, :60].contiguous(), b, 2.0)

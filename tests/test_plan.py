@@ -1,0 +1,140 @@
+"""Host-side segment tables, routing and schedule ingestion (no GPU)."""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import routing as orouting
+from paper_2510_00206_b200 import AdapterConfig, LayerPlan, Segment, padded_rank, segments_from_lengths
+from paper_2510_00206_b200 import schedule as sched
+from paper_2510_00206_b200.errors import ValidationError
+
+GOLD_SCHED = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "schedule_reference.json")))
+
+
+def test_padded_rank():
+    assert [padded_rank(r) for r in (1, 8, 16, 17, 32, 64)] == [16, 16, 16, 32, 32, 64]
+
+
+def test_adapter_config_validation():
+    with pytest.raises(ValidationError):
+        AdapterConfig(rank=0)
+    with pytest.raises(ValidationError):
+        AdapterConfig(rank=8, dropout_p=1.0)
+    with pytest.raises(ValidationError):
+        AdapterConfig(rank=8, scaling=float("inf"))
+
+    class Spec:  # lorasched AdapterSpec fields (ls/workload.py:25-48)
+        lora_rank, alpha, dropout_p = 16, 32.0, 0.05
+
+    c = AdapterConfig.from_adapter_spec(Spec(), seed=3)
+    assert (c.rank, c.scaling, c.dropout_p, c.seed) == (16, 2.0, 0.05, 3)
+
+
+def test_plan_columns_and_problem():
+    ads = [AdapterConfig(8, 2.0, 0.0, 1), AdapterConfig(16, 1.0, 0.1, 2), AdapterConfig(64, 0.5, 0.1, 3)]
+    segs = segments_from_lengths([0, 1, 2, 1], [100, 200, 300, 50], batches=[0, 0, 0, 1])
+    plan = LayerPlan(700, 256, 128, ads, segs, offset=5)
+    assert plan.ranks == [16, 16, 64, 16]
+    assert plan.col_starts == [0, 16, 32, 96]
+    assert plan.rank_total == 112
+    p = plan.problem
+    assert p.num_segments == 4 and p.rank_total == 112
+    assert (p.segments[2].row_start, p.segments[2].row_end, p.segments[2].col_start, p.segments[2].rank) == (300, 600,
+                                                                                                           32, 64)
+    assert p.segments[1].seed == 2 and p.segments[3].offset == 5
+    assert plan.needs_keep_bits
+    assert plan.segment_grad_slices() == [(0, 0, 0, 8), (1, 0, 16, 16), (2, 0, 32, 64), (1, 1, 96, 16)]
+    # eval mode: no dropout anywhere
+    ev = LayerPlan(700, 256, 128, ads, segs, training=False)
+    assert not ev.needs_keep_bits and all(ev.problem.segments[i].dropout_p == 0 for i in range(4))
+
+
+def test_plan_rejects_bad_tables():
+    ads = [AdapterConfig(16)]
+    with pytest.raises(ValidationError):
+        LayerPlan(100, 64, 64, ads, [Segment(0, 0, 120)])
+    with pytest.raises(ValidationError):
+        LayerPlan(100, 64, 64, ads, [Segment(1, 0, 50)])
+    with pytest.raises(ValidationError):
+        LayerPlan(100, 64, 64, ads, [Segment(0, 50, 100), Segment(0, 0, 50)])
+    with pytest.raises(ValidationError):  # R > 128
+        LayerPlan(300, 64, 64, [AdapterConfig(64)] * 3, segments_from_lengths([0, 1, 2], [100, 100, 100]))
+    with pytest.raises(ValidationError):
+        LayerPlan(64, 64, 64, ads * 33, segments_from_lengths(list(range(33)), [1] * 33))
+
+
+@pytest.mark.parametrize("lengths", [(3584, 2432, 1408, 768), (3520, 2496, 1408, 768), (100, 0, 5, 300)])
+def test_host_routes_match_oracle(lengths):
+    ads = [AdapterConfig(r) for r in (8, 16, 32, 64)]
+    segs = segments_from_lengths([0, 1, 2, 3], lengths)
+    m = sum(lengths) + 77
+    plan = LayerPlan(m, 64, 64, ads, segs)
+    ref = orouting.routes([(s.row_start, s.row_end) for s in segs], list(zip(plan.col_starts, plan.ranks)), m)
+    assert np.array_equal(np.array(plan.host_routes(), np.int32), ref)
+    assert len(plan.host_routes()) * orouting.ENTRY_BYTES == orouting.table_bytes(m)
+
+
+def test_straddling_tiles_with_p64():
+    """P = 64 padding (ls/workload.py:31) puts two segments in one 128-row tile."""
+    segs = segments_from_lengths([0, 1, 2, 3], [3520, 2496, 1408, 768])
+    plan = LayerPlan(8192, 64, 64, [AdapterConfig(r) for r in (8, 16, 32, 64)], segs)
+    routes = plan.host_routes()
+    straddle = [t for t, r in enumerate(routes) if r[1] > r[0]]
+    assert straddle == [27]  # rows 3456..3583 hold segments 0 and 1
+    assert routes[27] == (0, 1, 0, 32)
+
+
+def test_schedule_document_ingestion():
+    """A real lorasched schedule (tests/golden/schedule_reference.json, produced by the
+    reference planner) becomes segment tables whose padded lengths match the document."""
+    ids, cfgs = sched.adapters_from_doc(GOLD_SCHED)
+    assert ids == [a["adapter_id"] for a in GOLD_SCHED["adapters"]]
+    assert all(c.scaling == a["alpha"] / a["lora_rank"] for c, a in zip(cfgs, GOLD_SCHED["adapters"]))
+    mbs = sched.microbatches_from_doc(GOLD_SCHED)
+    entries = [e for e in GOLD_SCHED["entries"] if e["kind"] == "microbatch"]
+    assert len(mbs) == len(entries)
+    for mb, e in zip(mbs, entries):
+        assert mb.rows == e["total_padded_tokens"] <= GOLD_SCHED["capacity"]
+        assert mb.raw_tokens == e["total_raw_tokens"]
+        assert [s.rows for s in mb.segments] == [s["padded_tokens"] for s in e["segments"]]
+        assert [s.batch for s in mb.segments] == [s["global_batch_index"] for s in e["segments"]]
+        assert [ids[s.adapter] for s in mb.segments] == [s["adapter_id"] for s in e["segments"]]
+        plan = LayerPlan(mb.rows, 4096, 4096, cfgs, list(mb.segments))
+        ref = orouting.routes([(s.row_start, s.row_end) for s in mb.segments],
+                              list(zip(plan.col_starts, plan.ranks)), mb.rows)
+        assert np.array_equal(np.array(plan.host_routes(), np.int32), ref)
+
+
+def test_schedule_validation():
+    bad = json.loads(json.dumps(GOLD_SCHED))
+    bad["schema_version"] = 2
+    with pytest.raises(ValidationError, match="schema_version"):
+        sched.microbatches_from_doc(bad)
+    bad = json.loads(json.dumps(GOLD_SCHED))
+    bad["entries"][0]["segments"][0]["padded_tokens"] += 64
+    with pytest.raises(ValidationError, match="padded_tokens"):
+        sched.microbatches_from_doc(bad)
+    bad = json.loads(json.dumps(GOLD_SCHED))
+    bad["entries"][0]["segments"][0]["adapter_id"] = "nope"
+    with pytest.raises(ValidationError, match="unknown adapter"):
+        sched.microbatches_from_doc(bad)
+    bad = json.loads(json.dumps(GOLD_SCHED))
+    del bad["entries"][0]["group_id"]
+    with pytest.raises(ValidationError, match="group_id"):
+        sched.microbatches_from_doc(bad)
+
+
+def test_segments_from_microbatch_objects():
+    class Seg:
+        def __init__(self, a, b, n):
+            self.adapter_id, self.global_batch_index, self.padded_tokens = a, b, n
+
+    class MB:
+        segments = (Seg("a0", 3, 128), Seg("a2", 3, 64), Seg("a2", 4, 192))
+
+    segs = sched.segments_from_microbatch(MB(), ["a0", "a1", "a2"])
+    assert segs == [Segment(0, 0, 128, 3), Segment(2, 128, 192, 3), Segment(2, 192, 384, 4)]

@@ -82,6 +82,25 @@ def run_case(name: str) -> dict:
     for key in ("s_hat", "y", "ds", "db", "da", "dx"):
         res[key + "_relfro"] = olora.rel_fro(out[key], o[key])
     res["ws_clean"] = out["ws_clean"]
+    if any(p > 0 for p in ps):  # packed-mask path: ① writes bits, ④/⑤ read them
+        out = H.run_device(case, x, w, dy, a_cat, b_cat, use_bits=True)
+        for key in ("s_hat", "da", "dx"):
+            res[key + "_bits_relfro"] = olora.rel_fro(out[key], o[key])
+    # module API end to end (autograd, fp32 master adapter weights)
+    if len(ranks) == 1 and lengths[0] == m:
+        from paper_2510_00206_b200 import fused_lora
+
+        xd = x.to(dev).requires_grad_(True)
+        a = a_list[0].to(dev).float().requires_grad_(True)
+        b = b_list[0].to(dev).float().requires_grad_(True)
+        y = fused_lora(xd, w.to(dev), a, b, 2.0, ps[0], seed=case.seeds[0], offset=case.offset)
+        y.backward(dy.to(dev))
+        torch.cuda.synchronize()
+        r0 = ranks[0]
+        res["api_y_relfro"] = olora.rel_fro(y.detach().float().cpu().numpy(), o["y"])
+        res["api_dx_relfro"] = olora.rel_fro(xd.grad.float().cpu().numpy(), o["dx"])
+        res["api_da_relfro"] = olora.rel_fro(a.grad.cpu().numpy(), o["da"][:r0])
+        res["api_db_relfro"] = olora.rel_fro(b.grad.cpu().numpy(), o["db"][:, :r0])
     return res
 
 
