@@ -118,6 +118,11 @@ int validate(const LfProblem* p, bool need_routes, lf::LfSegTable* t) {
   if (p->num_segments > 0 && p->rank_total < 16)
     return fail(LF_E_INVALID, "rank_total must be >= 16 when segments are present");
   memset(t, 0, sizeof(*t));
+  static const int debug_flags = [] {
+    const char* e = getenv("LF_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  t->debug = debug_flags;
   t->nseg = p->num_segments;
   t->m = p->m;
   t->rtot = p->rank_total;
@@ -341,7 +346,7 @@ int lf_grad_up(const LfProblem* p, const uint16_t* dy, const uint16_t* b_cat, co
   split_workspace(p, &a.ws, &a.counters);
   a.routes = reinterpret_cast<const lf::LfRoute*>(p->routes);
   a.segs = t;
-  lf::grad_up_grid(p->m, p->n, p->rank_total, d.sms, &a.n_split, &a.m_split);
+  lf::grad_up_grid(p->m, p->n, p->rank_total, d.sms, &a.n_split, &a.m_split, &a.nacc);
   if (a.n_split <= 0) return fail(LF_E_INVALID, "rank_total=%d too large for grad_up TMEM budget", p->rank_total);
   if (lf::grad_up_launch(tdy, tb, ts, a, d.sms, (cudaStream_t)stream)) return cuda_fail("grad_up launch");
   return LF_OK;
@@ -373,7 +378,7 @@ int lf_grad_down(const LfProblem* p, const uint16_t* x, const uint16_t* ds, floa
   const int occ = occupancy_for_smem(stages * stage_bytes + 2048);
   const int tiles_k = (p->k + 127) / 128;
   const int tiles_m = (p->m + 127) / 128;
-  int ms = (occ * d.sms + tiles_k - 1) / tiles_k;
+  int ms = occ * d.sms / tiles_k;  // one resident wave
   if (ms > tiles_m) ms = tiles_m;
   if (ms < 1) ms = 1;
   a.m_split = ms;

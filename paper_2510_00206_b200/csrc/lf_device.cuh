@@ -22,6 +22,24 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// 1024-byte aligned view of dynamic shared memory (SW128 atoms). Pointer arithmetic on the
+// __shared__ array keeps the shared address space visible to the compiler (an integer
+// round-trip would turn every access into a generic LD.E/ST.E).
+__device__ __forceinline__ uint8_t* align_smem_1024(uint8_t* raw) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(raw));
+  return raw + ((1024u - (a & 1023u)) & 1023u);
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
 __device__ __forceinline__ uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
@@ -262,6 +280,56 @@ __device__ __forceinline__ uint32_t philox_keep8(uint32_t col8, uint32_t row, co
   return bits;
 }
 
+// Per-(segment, row) Philox state hoisted out of the column loop: the round keys, the
+// constant counter words (row, offset) and the packed 16-bit threshold. One call then
+// costs 10 x (2 IMAD.WIDE + 2 LOP3) plus a SIMD compare of the eight 16-bit lanes.
+struct PhiloxRow {
+  uint32_t k0[10], k1[10];
+  uint32_t c1, c2, c3;
+  uint32_t thr2;  // thr in both 16-bit halves
+};
+
+__device__ __forceinline__ PhiloxRow philox_row(const LfSegDev& s, uint32_t row) {
+  PhiloxRow pr;
+  uint32_t a = s.key0, b = s.key1;
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    pr.k0[i] = a;
+    pr.k1[i] = b;
+    a += 0x9E3779B9u;
+    b += 0xBB67AE85u;
+  }
+  pr.c1 = row;
+  pr.c2 = s.off0;
+  pr.c3 = s.off1;
+  pr.thr2 = s.thr | (s.thr << 16);
+  return pr;
+}
+
+// 0x00/0x01 per byte (4 lanes) -> 4 bits
+__device__ __forceinline__ uint32_t gather_lsb4(uint32_t x) { return ((x & 0x01010101u) * 0x01020408u) >> 24; }
+
+__device__ __forceinline__ uint32_t philox_row_keep8(const PhiloxRow& pr, uint32_t col8) {
+  uint32_t c0 = col8, c1 = pr.c1, c2 = pr.c2, c3 = pr.c3;
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ pr.k0[i];
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ pr.k1[i];
+    c1 = (uint32_t)p1;
+    c3 = (uint32_t)p0;
+    c0 = n0;
+    c2 = n2;
+  }
+  // per 16-bit lane: 0xFFFF where lane >= thr; gather one byte per lane, then one bit per byte
+  const uint32_t r0 = __vcmpgeu2(c0, pr.thr2), r1 = __vcmpgeu2(c1, pr.thr2);
+  const uint32_t r2 = __vcmpgeu2(c2, pr.thr2), r3 = __vcmpgeu2(c3, pr.thr2);
+  const uint32_t lo = __byte_perm(r0, r1, 0x6420);  // lanes 0..3
+  const uint32_t hi = __byte_perm(r2, r3, 0x6420);  // lanes 4..7
+  return gather_lsb4(lo) | (gather_lsb4(hi) << 4);
+}
+
 // keep bits for 8 consecutive columns from an explicit uint8 mask row (col multiple of 8)
 __device__ __forceinline__ uint32_t explicit_keep8(const uint8_t* mask_row, uint32_t col, uint32_t ncols) {
   uint32_t bits = 0;
@@ -290,16 +358,48 @@ __device__ __forceinline__ uint4 apply_keep8(uint4 v, uint32_t bits) {
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// keep bits of 64 consecutive columns [col, col+64) of one row: byte c = chunk c
-__device__ __forceinline__ uint64_t keep_bits64(const LfSegTable& t, int seg, int row, int col, int ncols) {
+// keep bits of 64 consecutive columns [col, col+64) of one row: byte c = chunk c.
+// The eight Philox streams (counters col/8 .. col/8+7) advance round by round in lockstep,
+// so every round exposes 8 independent IMAD.WIDE/LOP3 chains to the scheduler.
+__device__ __forceinline__ uint64_t keep_bits64_philox(const PhiloxRow& pr, int col) {
+  uint32_t c0[8], c1[8], c2[8], c3[8];
+  const uint32_t base = (uint32_t)col >> 3;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    c0[j] = base + j;
+    c1[j] = pr.c1;
+    c2[j] = pr.c2;
+    c3[j] = pr.c3;
+  }
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint64_t p0 = (uint64_t)0xD2511F53u * c0[j];
+      const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2[j];
+      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1[j] ^ pr.k0[i];
+      const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3[j] ^ pr.k1[i];
+      c1[j] = (uint32_t)p1;
+      c3[j] = (uint32_t)p0;
+      c0[j] = n0;
+      c2[j] = n2;
+    }
+  }
   uint64_t bits = 0;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int cc = col + 8 * c;
-    const uint32_t b = (t.mask_mode == 2) ? explicit_keep8(t.mask + (int64_t)row * t.ld_mask, cc, ncols)
-                                           : philox_keep8((uint32_t)cc >> 3, (uint32_t)row, t.seg[seg]);
-    bits |= (uint64_t)b << (8 * c);
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t r0 = __vcmpgeu2(c0[j], pr.thr2), r1 = __vcmpgeu2(c1[j], pr.thr2);
+    const uint32_t r2 = __vcmpgeu2(c2[j], pr.thr2), r3 = __vcmpgeu2(c3[j], pr.thr2);
+    const uint32_t b = gather_lsb4(__byte_perm(r0, r1, 0x6420)) | (gather_lsb4(__byte_perm(r2, r3, 0x6420)) << 4);
+    bits |= (uint64_t)b << (8 * j);
   }
+  return bits;
+}
+__device__ __forceinline__ uint64_t keep_bits64_explicit(const LfSegTable& t, int row, int col, int ncols) {
+  uint64_t bits = 0;
+  const uint8_t* mrow = t.mask + (int64_t)row * t.ld_mask;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) bits |= (uint64_t)explicit_keep8(mrow, col + 8 * c, ncols) << (8 * c);
   return bits;
 }
 
@@ -324,16 +424,18 @@ __device__ __forceinline__ void store_bits64(uint8_t* row_bits, int b0, int row_
     if (b0 + i < row_bytes) p[i] = (uint8_t)(v >> (8 * i));
 }
 
-// zero the dropped bf16 elements of one 128-byte row of an SW128 tile (64 columns)
+// zero the dropped bf16 elements of one 128-byte row of an SW128 tile (64 columns):
+// all eight 16-byte chunks are loaded first (ld.shared), masked, then stored back
 __device__ __forceinline__ void apply_row_sw128(uint8_t* tile, int rit, uint64_t bits) {
-  uint8_t* rowp = tile + rit * 128;
+  if (bits == ~0ull) return;
+  const uint32_t rowa = smem_u32(tile) + (uint32_t)rit * 128u;
+  uint4 v[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) v[c] = lds128(rowa + (uint32_t)((c ^ (rit & 7)) << 4));
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     const uint32_t b = (uint32_t)(bits >> (8 * c)) & 0xFFu;
-    if (b != 0xFFu) {
-      uint4* p = reinterpret_cast<uint4*>(rowp + ((c ^ (rit & 7)) << 4));
-      *p = apply_keep8(*p, b);
-    }
+    sts128(rowa + (uint32_t)((c ^ (rit & 7)) << 4), apply_keep8(v[c], b));
   }
 }
 

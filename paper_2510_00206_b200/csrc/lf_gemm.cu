@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(192, 1)
                    const __grid_constant__ GemmArgs args) {
   using Cfg = GemmCfg<BN, B_MN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2] main loop done  (MMA -> epilogue)
@@ -289,26 +289,31 @@ __global__ void __launch_bounds__(192, 1)
     // MASKED: zero the dropped elements of tile `it`'s LoRA partial in place
     auto mask_pass = [&](const TileInfo& ti, int it) {
       const int acc = it & 1;
-      mbar_wait(&lfull[acc], lora_uses[acc] & 1);
-      ++lora_uses[acc];
-      tc_fence_after();
       const int row = ti.mb * Cfg::BM + (int)(q * 32 + lane);
       const LfRoute rt = args.routes[ti.mb];
       const int seg = row < args.M ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
       const bool active = seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0);
+      // keep bits of the row's BN columns, fetched before waiting on the LoRA partial
+      uint32_t keep[BN / 32];
+#pragma unroll
+      for (int j = 0; j < BN / 32; ++j)
+        keep[j] = active ? dgrad_keep32(args.segs, seg, row, ti.nb * BN + 32 * j, args.N) : 0xFFFFFFFFu;
+      mbar_wait(&lfull[acc], lora_uses[acc] & 1);
+      ++lora_uses[acc];
+      tc_fence_after();
       // tcgen05.ld/st are warp-collective (.sync.aligned): every branch around them is warp-uniform
       if (__any_sync(0xFFFFFFFFu, active)) {
         const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * Cfg::ACC_COLS;
-#pragma unroll 1
+#pragma unroll
         for (int c = 0; c < BN; c += 32) {
-          const uint32_t keep = active ? dgrad_keep32(args.segs, seg, row, ti.nb * BN + c, args.N) : 0xFFFFFFFFu;
-          if (__all_sync(0xFFFFFFFFu, keep == 0xFFFFFFFFu)) continue;
+          const uint32_t kp = keep[c / 32];
+          if (__all_sync(0xFFFFFFFFu, kp == 0xFFFFFFFFu)) continue;
           uint32_t v[32];
           tmem_ld32(taddr + c, v);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i)
-            if (!((keep >> i) & 1u)) v[i] = 0u;
+            if (!((kp >> i) & 1u)) v[i] = 0u;
           tmem_st32(taddr + c, v);
         }
         tmem_st_wait();

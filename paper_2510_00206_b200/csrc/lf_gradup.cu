@@ -9,9 +9,9 @@
 // descriptors over the same bytes: K-major (rows = tokens) for dŜ += dY·B_cat, and
 // MN-major (rows = out features) for dBᵀ += dYᵀ·Ŝ. Both accumulators live in TMEM:
 // dŜ double-buffered per m-tile, dB per n-subtile for the CTA's whole m-range.
-// dŜ partials over n-subtiles meet in an fp32 workspace (red.global.add); the CTA that
-// completes a tile's count finalizes it (scale, mask off-segment columns, bf16) and
-// re-zeroes the workspace.
+// dŜ partials over n-subtiles meet in an fp32 workspace (red.global.add); the split-K
+// epilogue kernel (lf_finalize_kernel, lf_lowrank.cu) then scales, masks off-segment
+// columns, converts to bf16 and re-zeroes the workspace.
 #include "lf_device.cuh"
 #include "lf_kernels.h"
 
@@ -22,37 +22,13 @@ constexpr int DY_BYTES = 2 * 128 * 64 * 2;  // 32 KB: two 64-column SW128 boxes 
 constexpr int MAX_SMEM = 200 * 1024;
 }  // namespace gup
 
-__device__ __forceinline__ void finalize_row_up(const LfSegTable& t, const LfRoute& rt, int row, float* ws,
-                                                __nv_bfloat16* out) {
-  const int rtot = t.rtot;
-  const int seg = find_segment(t, rt.seg_lo, rt.seg_hi, row);
-  const int own0 = seg >= 0 ? t.seg[seg].col0 : 0;
-  const int own1 = seg >= 0 ? t.seg[seg].col0 + t.seg[seg].ncol : 0;
-  const float scale = seg >= 0 ? t.seg[seg].scale : 0.f;
-  float* wrow = ws + (int64_t)row * rtot;
-  __nv_bfloat16* orow = out + (int64_t)row * rtot;
-  for (int c = 0; c < rtot; c += 8) {
-    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (c >= rt.col_lo && c < rt.col_hi) {
-      const float4 a = ld_cg_f4(wrow + c), b = ld_cg_f4(wrow + c + 4);
-      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-      *reinterpret_cast<float4*>(wrow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-      *reinterpret_cast<float4*>(wrow + c + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    const float s = (c >= own0 && c < own1) ? scale : 0.f;
-    *reinterpret_cast<uint4*>(orow + c) = make_uint4(pack_bf16x2(v[0] * s, v[1] * s), pack_bf16x2(v[2] * s, v[3] * s),
-                                                     pack_bf16x2(v[4] * s, v[5] * s), pack_bf16x2(v[6] * s, v[7] * s));
-  }
-}
-
 __global__ void __launch_bounds__(192, 1)
     lf_gradup_kernel(const __grid_constant__ CUtensorMap tmDy, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmS, const __grid_constant__ GradUpArgs args, int stages,
                      int stage_bytes) {
   using namespace gup;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const int rtot = args.rtot;
   const int sh_bytes = (rtot / 16) * 4096;
   uint8_t* sSh0 = smem + stages * stage_bytes;
@@ -65,7 +41,6 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* db_full = ds_empty + 2;     // [1]
   uint64_t* tzero = db_full + 1;        // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tzero + 1);
-  volatile int* s_last = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int tiles_m = (args.m + 127) / 128;
@@ -75,7 +50,11 @@ __global__ void __launch_bounds__(192, 1)
   const int mt0 = (int)((int64_t)blockIdx.y * tiles_m / args.m_split);
   const int mt1 = (int)((int64_t)(blockIdx.y + 1) * tiles_m / args.m_split);
   const int nsub = nt1 - nt0;
-  const uint32_t tmem_need = (uint32_t)((2 + nsub) * rtot);
+  // NA independent accumulators per chain (consecutive K-steps rotate through them): small-N
+  // MMAs into a single accumulator serialise on its latency
+  const int NA = args.nacc;
+  const int AW = NA * rtot;  // TMEM columns of one (multi-)accumulator
+  const uint32_t tmem_need = (uint32_t)((2 + nsub) * AW);
   uint32_t tmem_cols = 32;
   while (tmem_cols < tmem_need) tmem_cols <<= 1;
 
@@ -102,8 +81,8 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tm_ds = tmem;              // 2 x rtot columns
-  const uint32_t tm_db = tmem + 2 * rtot;   // nsub x rtot columns
+  const uint32_t tm_ds = tmem;            // 2 buffers x AW columns
+  const uint32_t tm_db = tmem + 2 * AW;   // nsub x AW columns
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -154,7 +133,7 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&sh_full[b], bph);
         tc_fence_after();
         const uint32_t sSh = smem_u32(sSh0 + b * sh_bytes);
-        const uint32_t d_ds = tm_ds + b * rtot + rt.col_lo;
+        const uint32_t d_ds = tm_ds + b * AW + rt.col_lo;
         const uint32_t idesc_ds = make_idesc_bf16(128, (uint32_t)N, false, true);
         const uint32_t idesc_db = make_idesc_bf16(128, (uint32_t)N, true, true);
         for (int nt = nt0; nt < nt1; ++nt) {
@@ -162,18 +141,19 @@ __global__ void __launch_bounds__(192, 1)
           tc_fence_after();
           const uint32_t sDy = smem_u32(smem + stage * stage_bytes);
           const uint32_t sB = sDy + DY_BYTES;
-          // dŜ[m-tile] += dY[m-tile, n-sub] · B_cat[n-sub, cols]      (K = 128 out features)
+          const uint32_t d_db = tm_db + (nt - nt0) * AW + rt.col_lo;
+          // the two chains share each dY K-step and are issued interleaved:
+          //   dŜ[m-tile]        += dY[m-tile, n-sub]  · B_cat[n-sub, cols]   (K = 128 out features)
+          //   dB_cat[n-sub, ..] += dY[m-tile, n-sub]ᵀ · Ŝ[m-tile, cols]      (K = 128 tokens)
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            umma_bf16(d_ds, make_sdesc(sDy + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, kLayoutSW128),
-                      make_sdesc(sB + kk * 512, 4096, 256, kLayoutSW32), idesc_ds, (nt > nt0 || kk > 0) ? 1u : 0u);
-          }
-          // dB_cat[n-sub, cols] += dY[m-tile, n-sub]ᵀ · Ŝ[m-tile, cols]  (K = 128 tokens)
-          const uint32_t d_db = tm_db + (nt - nt0) * rtot + rt.col_lo;
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            umma_bf16(d_db, make_sdesc(sDy + kk * 2048, 16384, 1024, kLayoutSW128),
-                      make_sdesc(sSh + kk * 512, 4096, 256, kLayoutSW32), idesc_db, 1u);
+            const uint32_t a = (uint32_t)(kk % NA) * rtot;
+            if (!(args.segs.debug & 1))
+              umma_bf16(d_ds + a, make_sdesc(sDy + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, kLayoutSW128),
+                        make_sdesc(sB + kk * 512, 4096, 256, kLayoutSW32), idesc_ds, (nt > nt0 || kk >= NA) ? 1u : 0u);
+            if (!(args.segs.debug & 32))
+              umma_bf16(d_db + a, make_sdesc(sDy + kk * 2048, 16384, 1024, kLayoutSW128),
+                        make_sdesc(sSh + kk * 512, 4096, 256, kLayoutSW32), idesc_db, 1u);
           }
           umma_commit(&empty[stage]);
           if (++stage == stages) { stage = 0; phase ^= 1; }
@@ -192,7 +172,7 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t z[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) z[i] = 0u;
-      for (int c = 0; c < nsub * rtot; c += 16) tmem_st16(tm_db + lane_off + c, z);
+      for (int c = 0; c < nsub * AW; c += 16) tmem_st16(tm_db + lane_off + c, z);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -214,34 +194,25 @@ __global__ void __launch_bounds__(192, 1)
         tc_fence_after();
         float* wrow = args.ws + (int64_t)row * rtot + rt.col_lo;
         for (int c = 0; c < N; c += 16) {
-          uint32_t v[16];
-          tmem_ld16(tm_ds + lane_off + b * rtot + rt.col_lo + c, v);
-          tmem_ld_wait();
-          if (row < args.m) {
+          float s[16];
 #pragma unroll
-            for (int j = 0; j < 16; j += 4)
-              red_add_v4(wrow + c + j, __uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
-                         __uint_as_float(v[j + 3]));
+          for (int j = 0; j < 16; ++j) s[j] = 0.f;
+          for (int a = 0; a < NA; ++a) {
+            uint32_t v[16];
+            tmem_ld16(tm_ds + lane_off + b * AW + a * rtot + rt.col_lo + c, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) s[j] += __uint_as_float(v[j]);
+          }
+          if (row < args.m && !(args.segs.debug & 2)) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) red_add_v4(wrow + c + j, s[j], s[j + 1], s[j + 2], s[j + 3]);
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&ds_empty[b]);
       }
-      // tile completion across the n-split
-      __threadfence();
-      named_bar_sync(1, 128);
-      if (warp == 2 && lane == 0) {
-        const int old = atomicAdd(&args.counters[mt], nsub);
-        *s_last = (old + nsub == tiles_n) ? 1 : 0;
-      }
-      named_bar_sync(1, 128);
-      if (*s_last) {
-        __threadfence();
-        if (row < args.m) finalize_row_up(args.segs, rt, row, args.ws, reinterpret_cast<__nv_bfloat16*>(args.ds));
-        if (warp == 2 && lane == 0) args.counters[mt] = 0;
-      }
-      named_bar_sync(1, 128);
     }
     if (touched && nsub > 0) {
       mbar_wait(db_full, 0);
@@ -251,18 +222,25 @@ __global__ void __launch_bounds__(192, 1)
         float* drow = args.db + (int64_t)ncol * rtot;
         for (int g = 0; g < rtot / 16; ++g) {
           if (!((touched >> g) & 1u)) continue;
-          uint32_t v[16];
-          tmem_ld16(tm_db + lane_off + i * rtot + g * 16, v);
-          tmem_ld_wait();
-          if (ncol < args.n) {
+          float s[16];
 #pragma unroll
-            for (int j = 0; j < 16; j += 4)
-              red_add_v4(drow + g * 16 + j, __uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
-                         __uint_as_float(v[j + 3]));
+          for (int j = 0; j < 16; ++j) s[j] = 0.f;
+          for (int a = 0; a < NA; ++a) {
+            uint32_t v[16];
+            tmem_ld16(tm_db + lane_off + i * AW + a * rtot + g * 16, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) s[j] += __uint_as_float(v[j]);
+          }
+          if (ncol < args.n && !(args.segs.debug & 2)) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) red_add_v4(drow + g * 16 + j, s[j], s[j + 1], s[j + 2], s[j + 3]);
           }
         }
       }
     }
+    // dŜ partials over the n-split are complete once the grid retires; lf_finalize_kernel
+    // (launched behind this grid) scales, masks, converts and re-zeroes the workspace
   }
 
   tc_fence_before();
@@ -277,9 +255,12 @@ __global__ void __launch_bounds__(192, 1)
 // CTA's n-range must fit TMEM next to the two dŜ buffers: (2 + nsub) * R <= 512.
 // Among admissible splits pick the smallest critical path (max units of one 32 KB dY tile
 // per CTA), then the least partial-sum traffic R * (m_split * n + n_split * m).
-void grad_up_grid(int m, int n, int rtot, int sms, int* n_split, int* m_split) {
+void grad_up_grid(int m, int n, int rtot, int sms, int* n_split, int* m_split, int* nacc) {
   const int tiles_m = (m + 127) / 128, tiles_n = (n + 127) / 128;
-  const int max_nsub = 512 / rtot - 2;
+  // measured on B200: rotating K-steps over several accumulators does not speed the
+  // small-N chains up (the pipelines are TMA-bound), so one accumulator keeps TMEM free
+  *nacc = 1;
+  const int max_nsub = 512 / (*nacc * rtot) - 2;
   *n_split = 0;
   *m_split = 0;
   if (max_nsub < 1) return;
@@ -306,9 +287,9 @@ int grad_up_launch(const CUtensorMap& tm_dy, const CUtensorMap& tm_b, const CUte
   const int sh_bytes = (args.rtot / 16) * 4096;
   const int stage_bytes = gup::DY_BYTES + sh_bytes;
   int stages = (gup::MAX_SMEM - 2 * sh_bytes) / stage_bytes;
-  if (stages > 4) stages = 4;
+  if (stages > 6) stages = 6;  // deep ring: ~180 KB of dY in flight per SM
   if (stages < 2) return -1;
-  const int smem = stages * stage_bytes + 2 * sh_bytes + 1024 + 256;
+  const int smem = stages * stage_bytes + 2 * sh_bytes + 1024 + 1024;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(lf_gradup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gup::MAX_SMEM + 2048) !=
@@ -318,7 +299,8 @@ int grad_up_launch(const CUtensorMap& tm_dy, const CUtensorMap& tm_b, const CUte
   }
   dim3 grid(args.n_split, args.m_split);
   lf_gradup_kernel<<<grid, 192, smem, stream>>>(tm_dy, tm_b, tm_s, args, stages, stage_bytes);
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  return finalize_launch(args.segs, args.routes, args.ws, args.ds, stream);
 }
 
 }  // namespace lf

@@ -50,6 +50,7 @@ int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs
 struct GradUpArgs {
   int32_t m, n, rtot;
   int32_t n_split, m_split;  // CTA grid
+  int32_t nacc;              // independent accumulators per MMA chain
   void* ds;                  // bf16 m x rtot
   float* db;                 // fp32 n x rtot accumulator
   float* ws;                 // fp32 m x rtot partials (zero on entry and exit)
@@ -57,7 +58,7 @@ struct GradUpArgs {
   const LfRoute* routes;
   LfSegTable segs;
 };
-void grad_up_grid(int m, int n, int rtot, int sms, int* n_split, int* m_split);
+void grad_up_grid(int m, int n, int rtot, int sms, int* n_split, int* m_split, int* nacc);
 int grad_up_launch(const CUtensorMap& tm_dy, const CUtensorMap& tm_b, const CUtensorMap& tm_s,
                    const GradUpArgs& args, int num_sms, cudaStream_t stream);
 
@@ -72,6 +73,9 @@ struct GradDownArgs {
 void grad_down_config(int rtot, int* stages, int* stage_bytes);
 int grad_down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_ds, const GradDownArgs& args, int num_sms,
                      cudaStream_t stream);
+
+// split-K epilogue of ① and ③: fp32 partials (ws) -> scaled bf16 m x R, workspace re-zeroed
+int finalize_launch(const LfSegTable& segs, const LfRoute* routes, float* ws, void* out, cudaStream_t stream);
 
 // routing table + explicit mask materialisation
 int routes_launch(const LfSegTable& segs, int32_t* routes, int ntiles, cudaStream_t stream);

@@ -63,13 +63,14 @@ __device__ __forceinline__ void finalize_row(const LfSegTable& t, const LfRoute&
 // ------------------------------------------------------------------------------------
 namespace down {
 constexpr int X_BYTES = 128 * 64 * 2;  // 16 KB
-constexpr int SMEM_BUDGET = 74 * 1024;  // 3 CTAs / SM at R = 16
+// 2 CTAs / SM (register bound): ~2 x 100 KB of X tiles in flight per SM
+constexpr int SMEM_BUDGET = 100 * 1024;
 }  // namespace down
 
 void down_config(int rtot, int* stages, int* stage_bytes) {
   *stage_bytes = down::X_BYTES + rtot * 128;
   int s = down::SMEM_BUDGET / *stage_bytes;
-  *stages = s < 2 ? 2 : (s > 6 ? 6 : s);
+  *stages = s < 2 ? 2 : (s > 8 ? 8 : s);
 }
 
 __global__ void __launch_bounds__(192, 2)
@@ -77,13 +78,12 @@ __global__ void __launch_bounds__(192, 2)
                    const __grid_constant__ DownArgs args, int STAGES, int STAGE_BYTES) {
   using namespace down;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* masked = empty + STAGES;
   uint64_t* tfull = masked + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
-  volatile int* s_last = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int mt = blockIdx.x;
@@ -109,8 +109,11 @@ __global__ void __launch_bounds__(192, 2)
       tma_prefetch_desc(&tmA);
     }
   }
+  // Consecutive K-steps go to NACC independent accumulators (summed in the epilogue): with
+  // N = R this small, back-to-back MMAs into one accumulator serialise on its latency.
+  const int NACC = 4 * args.rtot <= 256 ? 4 : 2;
   uint32_t tmem_cols = 32;
-  while ((int)tmem_cols < args.rtot) tmem_cols <<= 1;
+  while ((int)tmem_cols < NACC * args.rtot) tmem_cols <<= 1;
   if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
   tc_fence_before();
   __syncthreads();
@@ -144,8 +147,9 @@ __global__ void __launch_bounds__(192, 2)
         const uint32_t sA = sX + X_BYTES;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          umma_bf16(tmem, make_sdesc(sX + kk * 32, 16, 1024, kLayoutSW128), make_sdesc(sA + kk * 32, 16, 1024, kLayoutSW128),
-                    idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          if (!(args.segs.debug & 1))
+          umma_bf16(tmem + (kk % NACC) * args.rtot, make_sdesc(sX + kk * 32, 16, 1024, kLayoutSW128),
+                    make_sdesc(sA + kk * 32, 16, 1024, kLayoutSW128), idesc, (kb > kb0 || kk >= NACC) ? 1u : 0u);
         }
         umma_commit(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -161,18 +165,24 @@ __global__ void __launch_bounds__(192, 2)
     const int seg = row < args.m ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
     if (need_mask) {
       const bool my_mask = seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0);
+      const bool explicit_mask = args.segs.mask_mode == 2;
+      const PhiloxRow pr = philox_row(args.segs.seg[seg >= 0 ? seg : 0], (uint32_t)row);
+      uint8_t* bits_row = args.segs.bits ? args.segs.bits + (int64_t)row * args.segs.ld_bits : nullptr;
       int stage = 0;
       uint32_t phase = 0;
       for (int kb = kb0; kb < kb1; ++kb) {
+        // the keep bits depend only on (row, column, seed, offset): generate them while the
+        // tile is still in flight, so Philox latency overlaps the TMA instead of adding to it
+        uint64_t bits = ~0ull;
+        if (my_mask)
+          bits = explicit_mask ? keep_bits64_explicit(args.segs, row, kb * 64, args.k) : keep_bits64_philox(pr, kb * 64);
         mbar_wait(&full[stage], phase);
         if (my_mask) {
-          const uint64_t bits = keep_bits64(args.segs, seg, row, kb * 64, args.k);
-          apply_row_sw128(smem + stage * STAGE_BYTES, rit, bits);
+          if (!(args.segs.debug & 8)) apply_row_sw128(smem + stage * STAGE_BYTES, rit, bits);
           // Philox runs once per step: ④ and ⑤ read these bits instead
-          if (args.segs.mask_mode == 1 && args.segs.bits)
-            store_bits64(args.segs.bits + (int64_t)row * args.segs.ld_bits, kb * 8, (int)args.segs.ld_bits, bits);
+          if (!explicit_mask && bits_row) store_bits64(bits_row, kb * 8, (int)args.segs.ld_bits, bits);
         }
-        fence_proxy_async_smem();
+        if (!(args.segs.debug & 4)) fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&masked[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -184,31 +194,24 @@ __global__ void __launch_bounds__(192, 2)
       const uint32_t taddr = tmem + ((q * 32u) << 16);
       float* wrow = args.ws + (int64_t)row * args.rtot + rt.col_lo;
       for (int c = 0; c < N; c += 16) {
-        uint32_t v[16];
-        tmem_ld16(taddr + c, v);
-        tmem_ld_wait();
-        if (row < args.m) {
+        float s[16];
 #pragma unroll
-          for (int j = 0; j < 16; j += 4)
-            red_add_v4(wrow + c + j, __uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
-                       __uint_as_float(v[j + 3]));
+        for (int j = 0; j < 16; ++j) s[j] = 0.f;
+        for (int a = 0; a < NACC; ++a) {
+          uint32_t v[16];
+          tmem_ld16(taddr + a * args.rtot + c, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) s[j] += __uint_as_float(v[j]);
+        }
+        if (row < args.m && !(args.segs.debug & 2)) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) red_add_v4(wrow + c + j, s[j], s[j + 1], s[j + 2], s[j + 3]);
         }
       }
     }
-    // split-K completion: the last CTA of this row tile finalizes it
-    __threadfence();
-    named_bar_sync(1, 128);
-    if (warp == 2 && lane == 0) {
-      const int old = atomicAdd(&args.counters[mt], 1);
-      *s_last = (old == args.ksplit - 1) ? 1 : 0;
-    }
-    named_bar_sync(1, 128);
-    if (*s_last) {
-      __threadfence();
-      if (row < args.m)
-        finalize_row(args.segs, rt, row, args.ws, reinterpret_cast<__nv_bfloat16*>(args.s_hat));
-      if (warp == 2 && lane == 0) args.counters[mt] = 0;
-    }
+    // split-K partials are complete in the workspace once this grid retires; the
+    // lf_finalize_kernel launched behind it scales, masks and converts them
   }
 
   tc_fence_before();
@@ -217,6 +220,23 @@ __global__ void __launch_bounds__(192, 2)
     tc_fence_after();
     tmem_dealloc(tmem, tmem_cols);
   }
+}
+
+// Split-K epilogue shared by ① and ③: per row, scale the own-segment columns of the fp32
+// partial sums by s = scaling / (1 - p), zero every other column, write bf16, and return
+// the workspace to zero. One thread per row.
+__global__ void __launch_bounds__(128) lf_finalize_kernel(const __grid_constant__ LfSegTable segs,
+                                                          const LfRoute* __restrict__ routes, float* ws,
+                                                          __nv_bfloat16* out) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= segs.m || (segs.debug & 16)) return;
+  finalize_row(segs, routes[row / LF_TILE_M], row, ws, out);
+}
+
+int finalize_launch(const LfSegTable& segs, const LfRoute* routes, float* ws, void* out, cudaStream_t stream) {
+  lf_finalize_kernel<<<(segs.m + 127) / 128, 128, 0, stream>>>(segs, routes, ws,
+                                                                 reinterpret_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs& args, int num_sms,
@@ -232,7 +252,8 @@ int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs
   }
   dim3 grid((args.m + 127) / 128, args.ksplit);
   lf_down_kernel<<<grid, 192, smem, stream>>>(tm_x, tm_a, args, stages, stage_bytes);
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  return finalize_launch(args.segs, args.routes, args.ws, args.s_hat, stream);
 }
 
 // ------------------------------------------------------------------------------------
@@ -248,7 +269,7 @@ __global__ void __launch_bounds__(192, 2)
                       const __grid_constant__ GradDownArgs args, int stages, int stage_bytes) {
   using namespace dga;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
   uint64_t* empty = full + stages;
   uint64_t* masked = empty + stages;
@@ -262,8 +283,10 @@ __global__ void __launch_bounds__(192, 2)
   const int mt0 = (int)((int64_t)blockIdx.y * tiles_m / args.m_split);
   const int mt1 = (int)((int64_t)(blockIdx.y + 1) * tiles_m / args.m_split);
   const int rtot = args.rtot;
+  // independent accumulators for consecutive K-steps (see ①); 2 CTAs / SM share 512 columns
+  const int NACC = 4 * rtot <= 256 ? 4 : 2;
   uint32_t tmem_cols = 32;
-  while ((int)tmem_cols < rtot) tmem_cols <<= 1;
+  while ((int)tmem_cols < NACC * rtot) tmem_cols <<= 1;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -320,7 +343,8 @@ __global__ void __launch_bounds__(192, 2)
         const uint32_t idesc = make_idesc_bf16(128, (uint32_t)N, true, true);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          umma_bf16(tmem + rt.col_lo, make_sdesc(sX + kk * 2048, 16384, 1024, kLayoutSW128),
+          if (!(args.segs.debug & 1))
+          umma_bf16(tmem + (kk % NACC) * rtot + rt.col_lo, make_sdesc(sX + kk * 2048, 16384, 1024, kLayoutSW128),
                     make_sdesc(sD + kk * 512, 4096, 256, kLayoutSW32), idesc, 1u);
         }
         umma_commit(&empty[stage]);
@@ -337,44 +361,70 @@ __global__ void __launch_bounds__(192, 2)
       uint32_t z[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) z[i] = 0u;
-      for (int c = 0; c < rtot; c += 16) tmem_st16(taddr + c, z);
+      for (int c = 0; c < NACC * rtot; c += 16) tmem_st16(taddr + c, z);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tzero);
     }
     const int rit = (int)(q * 32 + lane);
+    // keep bits of this thread's row in m-tile `mt` (128 columns of k-tile kt); false = keep all
+    auto fetch_bits = [&](int mt, uint64_t& b0, uint64_t& b1) -> bool {
+      b0 = b1 = ~0ull;
+      const LfRoute rt = args.routes[mt];
+      if (!tile_needs_mask(args.segs, rt)) return false;
+      const int row = mt * 128 + rit;
+      const int seg = row < args.m ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
+      if (!(seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0))) return false;
+      if (args.segs.mask_mode == 1 && args.segs.bits) {
+        const uint8_t* rb = args.segs.bits + (int64_t)row * args.segs.ld_bits;
+        b0 = load_bits64(rb, kt * 16, (int)args.segs.ld_bits);
+        b1 = load_bits64(rb, kt * 16 + 8, (int)args.segs.ld_bits);
+      } else if (args.segs.mask_mode == 2) {
+        b0 = keep_bits64_explicit(args.segs, row, kt * 128, args.k);
+        b1 = keep_bits64_explicit(args.segs, row, kt * 128 + 64, args.k);
+      } else {
+        const PhiloxRow pr = philox_row(args.segs.seg[seg], (uint32_t)row);
+        b0 = keep_bits64_philox(pr, kt * 128);
+        b1 = keep_bits64_philox(pr, kt * 128 + 64);
+      }
+      return true;
+    };
+    auto next_tile = [&](int mt) {
+      while (mt < mt1 && args.routes[mt].col_hi <= args.routes[mt].col_lo) ++mt;
+      return mt;
+    };
     int stage = 0;
     uint32_t phase = 0;
     uint32_t touched = 0;  // 16-column groups that received contributions
-    for (int mt = mt0; mt < mt1; ++mt) {
-      const LfRoute rt = args.routes[mt];
-      const int N = rt.col_hi - rt.col_lo;
-      if (N <= 0) continue;
+    // software pipeline: the keep bits of the next m-tile are fetched while this one is masked
+    int cur = next_tile(mt0);
+    uint64_t cb0 = ~0ull, cb1 = ~0ull;
+    bool cmask = cur < mt1 ? fetch_bits(cur, cb0, cb1) : false;
+    while (cur < mt1) {
+      const int nxt = next_tile(cur + 1);
+      uint64_t nb0 = ~0ull, nb1 = ~0ull;
+      const bool nmask = nxt < mt1 ? fetch_bits(nxt, nb0, nb1) : false;
+      const LfRoute rt = args.routes[cur];
       for (int c = rt.col_lo; c < rt.col_hi; c += 16) touched |= 1u << (c >> 4);
       if (tile_needs_mask(args.segs, rt)) {
-        const int row = mt * 128 + rit;
-        const int seg = row < args.m ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
         mbar_wait(&full[stage], phase);
-        if (seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0)) {
+        if (cmask) {
           uint8_t* sX = smem + stage * stage_bytes;
-          uint64_t b0, b1;
-          if (args.segs.mask_mode == 1 && args.segs.bits) {
-            const uint8_t* rb = args.segs.bits + (int64_t)row * args.segs.ld_bits;
-            b0 = load_bits64(rb, kt * 16, (int)args.segs.ld_bits);
-            b1 = load_bits64(rb, kt * 16 + 8, (int)args.segs.ld_bits);
-          } else {
-            b0 = keep_bits64(args.segs, seg, row, kt * 128, args.k);
-            b1 = keep_bits64(args.segs, seg, row, kt * 128 + 64, args.k);
+          if (!(args.segs.debug & 8)) {
+            apply_row_sw128(sX, rit, cb0);
+            apply_row_sw128(sX + 16384, rit, cb1);
           }
-          apply_row_sw128(sX, rit, b0);
-          apply_row_sw128(sX + 16384, rit, b1);
         }
-        fence_proxy_async_smem();
+        if (!(args.segs.debug & 4)) fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&masked[stage]);
       }
       if (++stage == stages) { stage = 0; phase ^= 1; }
+      cur = nxt;
+      cb0 = nb0;
+      cb1 = nb1;
+      cmask = nmask;
     }
     if (touched) {
       mbar_wait(tfull, 0);
@@ -382,12 +432,19 @@ __global__ void __launch_bounds__(192, 2)
       const int kcol = kt * 128 + rit;
       for (int g = 0; g < rtot / 16; ++g) {
         if (!((touched >> g) & 1u)) continue;
-        uint32_t v[16];
-        tmem_ld16(taddr + g * 16, v);
-        tmem_ld_wait();
+        float s[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) s[j] = 0.f;
+        for (int a = 0; a < NACC; ++a) {
+          uint32_t v[16];
+          tmem_ld16(taddr + a * rtot + g * 16, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) s[j] += __uint_as_float(v[j]);
+        }
         if (kcol < args.k) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) red_add_f32(args.da + (int64_t)(g * 16 + j) * args.k + kcol, __uint_as_float(v[j]));
+          for (int j = 0; j < 16; ++j) red_add_f32(args.da + (int64_t)(g * 16 + j) * args.k + kcol, s[j]);
         }
       }
     }

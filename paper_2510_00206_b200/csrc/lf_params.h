@@ -32,6 +32,8 @@ struct LfSegTable {
   int64_t ld_mask;
   uint8_t* bits;        // bit-packed Philox keep mask (m x ld_bits bytes) when mask_mode == 1, or null
   int64_t ld_bits;      // = k / 8
+  int32_t debug;        // profiling knobs (env LF_DEBUG, default 0): skip pipeline pieces, results invalid
+  int32_t pad_;
   LfSegDev seg[LF_MAX_SEGS];
 };
 

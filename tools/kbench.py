@@ -1,0 +1,104 @@
+"""Per-launcher microbenchmark through the C ABI (CUDA events, rotating inputs > L2).
+
+    python tools/kbench.py --m 8192 --k 4096 --n 4096 --r 16 --p 0.1 [--bits]
+
+Prints one JSON line per launcher: µs per call, algorithmic GB/s (memory-bound kernels)
+or TFLOP/s (GEMMs).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--m", type=int, default=8192)
+    ap.add_argument("--k", type=int, default=4096)
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--r", type=int, default=16)
+    ap.add_argument("--p", type=float, default=0.1)
+    ap.add_argument("--bits", action="store_true", help="① writes packed keep bits, ④/⑤ read them")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    import torch
+
+    from paper_2510_00206_b200 import _lib
+
+    lib = _lib.load()
+    dev = torch.device("cuda")
+    m, k, n, r = args.m, args.k, args.n, args.r
+    R = -(-r // 16) * 16
+    nbuf = max(2, int(-(-300e6 // (2 * m * max(k, n)))))  # > L2 worth of activations
+    g = torch.Generator(device=dev).manual_seed(0)
+    X = [torch.randn(m, k, device=dev, generator=g).to(torch.bfloat16) for _ in range(nbuf)]
+    DY = [torch.randn(m, n, device=dev, generator=g).to(torch.bfloat16) for _ in range(nbuf)]
+    W = (torch.randn(n, k, device=dev, generator=g) / k**0.5).to(torch.bfloat16)
+    A = (torch.randn(R, k, device=dev, generator=g) / k**0.5).to(torch.bfloat16)
+    B = (torch.randn(n, R, device=dev, generator=g) / 4).to(torch.bfloat16)
+    S = torch.randn(m, R, device=dev, generator=g).to(torch.bfloat16)
+    DS = torch.randn(m, R, device=dev, generator=g).to(torch.bfloat16)
+    Y = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
+    DX = torch.empty(m, k, device=dev, dtype=torch.bfloat16)
+    DA = torch.zeros(R, k, device=dev)
+    DB = torch.zeros(n, R, device=dev)
+    p = _lib.LfProblem()
+    p.m, p.k, p.n, p.rank_total, p.num_segments = m, k, n, R, 1
+    s = p.segments[0]
+    s.row_start, s.row_end, s.col_start, s.rank, s.scaling, s.dropout_p, s.seed, s.offset = 0, m, 0, R, 2.0, args.p, 5, 1
+    routes = torch.empty((-(-m // 128), 4), dtype=torch.int32, device=dev)
+    ws = torch.zeros(_lib.workspace_bytes(m, R), dtype=torch.uint8, device=dev)
+    bits = torch.zeros((m, k // 8), dtype=torch.uint8, device=dev)
+    p.routes, p.workspace, p.workspace_bytes = routes.data_ptr(), ws.data_ptr(), ws.numel()
+    if args.bits:
+        p.keep_bits = bits.data_ptr()
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    pp = ctypes.byref(p)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _lib.check(lib.lf_build_routes(pp, P(routes), st), "routes")
+    launches = {
+        "dropout_down_fwd": (lambda i: lib.lf_dropout_down_fwd(pp, P(X[i]), P(A), P(S), st),
+                             "gbs", 2 * m * k + 2 * k * R + 2 * m * R),
+        "base_fwd": (lambda i: lib.lf_base_fwd(pp, P(X[i]), P(W), P(S), P(B), P(Y), st),
+                     "tflops", 2 * m * k * n + 2 * m * R * n),
+        "grad_up": (lambda i: lib.lf_grad_up(pp, P(DY[i]), P(B), P(S), P(DS), P(DB), st),
+                    "gbs", 2 * (m * n + R * n + m * R) + 2 * m * R + 4 * R * n),
+        "grad_down": (lambda i: lib.lf_grad_down(pp, P(X[i]), P(DS), P(DA), st), "gbs", 2 * (m * k + m * R) + 4 * k * R),
+        "grad_input": (lambda i: lib.lf_grad_input(pp, P(DY[i]), P(W), P(DS), P(A), P(DX), st),
+                       "tflops", 2 * m * n * k + 2 * m * R * k),
+    }
+    OUT = torch.empty_like(X[0])
+    launches["torch_copy_x"] = (lambda i: (OUT.copy_(X[i]), 0)[1], "gbs", 4 * m * k)
+    launches["torch_sum_x"] = (lambda i: (X[i].sum(dtype=torch.float32), 0)[1], "gbs", 2 * m * k)
+    WT = W.t()
+    launches["cublas_fwd"] = (lambda i: (torch.mm(X[i], WT, out=Y), 0)[1], "tflops", 2 * m * k * n)
+    launches["cublas_dgrad"] = (lambda i: (torch.mm(DY[i], W, out=DX), 0)[1], "tflops", 2 * m * k * n)
+    # ① once so packed bits exist for ④/⑤
+    _lib.check(lib.lf_dropout_down_fwd(pp, P(X[0]), P(A), P(S), st), "down")
+    for name, (fn, unit, work) in launches.items():
+        if args.only and name not in args.only.split(","):
+            continue
+        for i in range(3):
+            _lib.check(fn(i % nbuf), name)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.iters):
+            fn(i % nbuf)
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / args.iters
+        val = work / (us * 1e-6) / (1e9 if unit == "gbs" else 1e12)
+        print(json.dumps({"kernel": name, "m": m, "k": k, "n": n, "r": R, "p": args.p, "bits": args.bits,
+                          "us": round(us, 2), unit: round(val, 1)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

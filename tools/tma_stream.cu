@@ -1,0 +1,149 @@
+// tma_stream.cu — microbenchmark: how fast can TMA stream a bf16 matrix [rows, cols] through
+// a STAGES-deep smem ring on B200, as a function of box shape and CTAs per SM?
+// Consumer = one warp that waits each stage and releases it (optionally reads 4 bytes).
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2510_00206_b200/csrc \
+//        tma_stream.cu -o tma_stream -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include "lf_device.cuh"
+
+using namespace lf;
+
+struct Cfg {
+  int box_cols, box_rows, boxes_per_stage;  // boxes laid side by side along columns
+  int stages;
+  int swizzle;  // 0 none, 3 = 128B
+};
+
+__global__ void __launch_bounds__(64) stream_kernel(const __grid_constant__ CUtensorMap map, int rows, int cols,
+                                                    int box_cols, int box_rows, int bps, int stages, int stage_bytes,
+                                                    int mode, unsigned long long* sink) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+  uint64_t* empty = full + stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int tiles_c = cols / (box_cols * bps);
+  const int tiles_r = rows / box_rows;
+  const int total = tiles_c * tiles_r;
+  unsigned long long acc = 0;
+  if (warp == 0 && lane == 0) {
+    int stage = 0;
+    uint32_t phase = 0;
+    const int per = (total + gridDim.x - 1) / gridDim.x;
+    for (int i = 0; i < per; ++i) {
+      int t = mode == 0 ? blockIdx.x + i * gridDim.x : blockIdx.x * per + i;
+      if (t >= total) break;
+      int tr = t / tiles_c, tc = t % tiles_c;
+      if (mode == 2) { tr = t % tiles_r; tc = t / tiles_r; }
+      mbar_wait(&empty[stage], phase ^ 1);
+      mbar_arrive_expect_tx(&full[stage], stage_bytes);
+      for (int b = 0; b < bps; ++b)
+        tma_load_2d(smem + stage * stage_bytes + b * box_cols * box_rows * 2, &map, &full[stage],
+                    (tc * bps + b) * box_cols, tr * box_rows);
+      if (++stage == stages) { stage = 0; phase ^= 1; }
+    }
+  } else if (warp == 1 && lane == 0) {
+    int stage = 0;
+    uint32_t phase = 0;
+    const int per = (total + gridDim.x - 1) / gridDim.x;
+    for (int i = 0; i < per; ++i) {
+      int t = mode == 0 ? blockIdx.x + i * gridDim.x : blockIdx.x * per + i;
+      if (t >= total) break;
+      mbar_wait(&full[stage], phase);
+      acc += *reinterpret_cast<volatile uint32_t*>(smem + stage * stage_bytes);
+      mbar_arrive(&empty[stage]);
+      if (++stage == stages) { stage = 0; phase ^= 1; }
+    }
+    if (acc == 0x12345) sink[0] = acc;
+  }
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int main(int argc, char** argv) {
+  const long rows = 8192, cols = 4096;  // 64 MB bf16; 4 rotating copies > L2
+  const int NB = 4;
+  void* bufs[NB];
+  for (int i = 0; i < NB; ++i) {
+    cudaMalloc(&bufs[i], rows * cols * 2);
+    cudaMemset(bufs[i], 1, rows * cols * 2);
+  }
+  unsigned long long* sink;
+  cudaMalloc(&sink, 8);
+  void* fnp = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &q);
+  EncodeFn enc = (EncodeFn)fnp;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  struct V {
+    int bc, br, bps, stages, ctas_per_sm, sw, mode;
+  } vars[] = {
+      {64, 128, 2, 3, 1, 3, 0}, {64, 128, 2, 3, 1, 3, 1}, {64, 128, 2, 3, 1, 3, 2},
+      {64, 128, 1, 6, 1, 3, 0}, {64, 128, 1, 6, 1, 3, 1}, {64, 128, 1, 6, 1, 3, 2},
+      {64, 128, 2, 3, 2, 3, 1}, {64, 128, 1, 5, 2, 3, 1},
+  };
+  struct V0 { int a; } unused[] = {
+{0}};
+  (void)unused;
+  for (auto& v : vars) {
+    const int stage_bytes = v.bc * v.br * 2 * v.bps;
+    const int smem = v.stages * stage_bytes + 1024 + 256;
+    if (smem * v.ctas_per_sm > 227 * 1024) {
+      printf("skip %d %d %d %d %d\n", v.bc, v.br, v.bps, v.stages, v.ctas_per_sm);
+      continue;
+    }
+    CUtensorMap maps[NB];
+    for (int i = 0; i < NB; ++i) {
+      cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+      cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+      cuuint32_t box[2] = {(cuuint32_t)v.bc, (cuuint32_t)v.br};
+      cuuint32_t es[2] = {1, 1};
+      CUresult r = enc(&maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, bufs[i], dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       v.sw == 3 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) {
+        printf("encode failed %d\n", (int)r);
+        return 1;
+      }
+    }
+    const int grid = sms * v.ctas_per_sm;
+    for (int i = 0; i < 3; ++i)
+      stream_kernel<<<grid, 64, smem>>>(maps[i % NB], rows, cols, v.bc, v.br, v.bps, v.stages, stage_bytes, v.mode, sink);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 20;
+    cudaEventRecord(e0);
+    for (int i = 0; i < iters; ++i)
+      stream_kernel<<<grid, 64, smem>>>(maps[i % NB], rows, cols, v.bc, v.br, v.bps, v.stages, stage_bytes, v.mode, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double us = ms * 1e3 / iters;
+    const cudaError_t err = cudaGetLastError();
+    printf("{\"box\": [%d, %d], \"boxes_per_stage\": %d, \"stage_kb\": %d, \"stages\": %d, \"ctas_per_sm\": %d, "
+           "\"swizzle\": %d, \"mode\": %d, \"us\": %.2f, \"gbs\": %.1f, \"err\": \"%s\"}\n",
+           v.bc, v.br, v.bps, stage_bytes / 1024, v.stages, v.ctas_per_sm, v.sw, v.mode, us, rows * cols * 2 / (us * 1e3),
+           cudaGetErrorString(err));
+  }
+  return 0;
+}
