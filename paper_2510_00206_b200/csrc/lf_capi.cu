@@ -295,11 +295,11 @@ int lf_base_fwd(const LfProblem* p, const uint16_t* x, const uint16_t* w, const 
   LF_TRY(current_device(&d));
   lf::GemmMaps maps;
   if (!make_map(&maps.a, x, p->m, p->k, p->k, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&maps.b, w, p->n, p->k, p->k, 64, 256, CU_TENSOR_MAP_SWIZZLE_128B))
+      !make_map(&maps.b, w, p->n, p->k, p->k, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))
     return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (x / w)");
   if (lora) {
     if (!make_map(&maps.a2, s_hat, p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
-        !make_map(&maps.b2, b_cat, p->n, p->rank_total, p->rank_total, 16, 256, CU_TENSOR_MAP_SWIZZLE_32B))
+        !make_map(&maps.b2, b_cat, p->n, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B))
       return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (s_hat / b_cat)");
   } else {
     maps.a2 = maps.a;

@@ -4,10 +4,14 @@
 // ls/costmodel.py:273-277 (dX = dY·Wᵀ + mask ⊙ LoRA term, one dX write);
 // paper design PAPER.md:457-463.
 //
-// B200 design: persistent, warp-specialised tcgen05 GEMM, one CTA per SM.
-//   warp 0      TMA producer (one lane): A/B tiles into a STAGES-deep smem ring
-//   warp 1      MMA issuer (one lane): tcgen05.mma 128x256x16, fp32 accumulators in TMEM,
-//               double-buffered so the epilogue of tile i overlaps the main loop of tile i+1
+// B200 design: persistent, warp-specialised tcgen05 GEMM on CTA pairs (cluster 2x1x1,
+// cta_group::2). A pair owns a 256x256 output tile: each CTA TMA-loads its 128-row half of
+// A and its 128-column half of B into its own shared memory (completion counted on the
+// leader's mbarrier), the leader issues tcgen05.mma M=256 N=256 K=16 over both halves, and
+// each CTA's TMEM holds the fp32 accumulator of its 128 rows (double-buffered, 2 x 256
+// columns) — half the shared-memory operand traffic per FLOP of a single-CTA 128x256 tile.
+//   warp 0      TMA producer (one lane per CTA)
+//   warp 1      MMA issuer (one lane, leader CTA only) + TMEM allocation (both CTAs)
 //   warps 2..5  epilogue: tcgen05.ld -> bf16 -> global (and, for ⑤ with dropout, the mask pass)
 // The low-rank up-projection is NOT an epilogue GEMM: [X | Ŝ]·[W | B_cat]ᵀ — the rank-R
 // LoRA operands are streamed as extra K-blocks into the same accumulator, so the output
@@ -18,25 +22,24 @@
 // epilogue warps zero the dropped elements of that partial in TMEM (tcgen05.ld → keep
 // bits → tcgen05.st), and only then is the main dY·W loop accumulated on top. The LoRA
 // block of tile i+1 is issued half-way through tile i's main loop, so its mask pass
-// runs while the tensor pipe is busy with tile i — same 128x256 tiles and TMEM budget
-// as the dropout-free path, no second accumulator.
+// runs while the tensor pipe is busy with tile i.
 #include "lf_device.cuh"
 #include "lf_kernels.h"
 
 namespace lf {
 
-template <int BN, bool B_MN, int STAGES>
+template <bool B_MN, int STAGES>
 struct GemmCfg {
-  static constexpr int BM = 128;
+  static constexpr int BM = 128;                  // rows per CTA (pair tile: 256)
+  static constexpr int BN = 256;                  // pair tile columns; each CTA loads BN/2 of B
+  static constexpr int HBN = BN / 2;
   static constexpr int BK = 64;
-  static constexpr int A_BYTES = BM * BK * 2;  // 16 KB, K-major SW128
-  static constexpr int B_BYTES = BN * BK * 2;  // BN x 128 B
+  static constexpr int A_BYTES = BM * BK * 2;     // 16 KB, K-major SW128
+  static constexpr int B_BYTES = HBN * BK * 2;    // 16 KB
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int ACC_COLS = BN;
-  static constexpr int TMEM_COLS = 2 * ACC_COLS;
+  static constexpr int TMEM_COLS = 2 * ACC_COLS;  // 512
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
-  static_assert(TMEM_COLS <= 512 && (TMEM_COLS & (TMEM_COLS - 1)) == 0, "TMEM budget");
-  static_assert(BN % 64 == 0 && BN <= 256, "BN");
 };
 
 // grouped raster: GROUP m-tiles share each n-column sweep so W tiles stay L2-hot
@@ -52,20 +55,30 @@ __device__ __forceinline__ void gemm_tile_coords(int t, int tiles_m, int tiles_n
 }
 
 struct TileInfo {
-  int mb, nb;
-  int col_lo, col_hi;  // LoRA K-range (empty if none)
+  int mb, nb;          // 256 x 256 pair-tile coordinates
+  int col_lo, col_hi;  // LoRA K-range: union over the tile's two 128-row routes
   __device__ bool lora() const { return col_hi > col_lo; }
 };
 
 __device__ __forceinline__ TileInfo tile_info(const GemmArgs& a, int t) {
   TileInfo ti;
   gemm_tile_coords(t, a.tiles_m, a.tiles_n, ti.mb, ti.nb);
+  ti.col_lo = ti.col_hi = 0;
   if (a.routes) {
-    const LfRoute rt = a.routes[ti.mb];
-    ti.col_lo = rt.col_lo;
-    ti.col_hi = rt.col_hi;
-  } else {
-    ti.col_lo = ti.col_hi = 0;
+    const int tiles128 = (a.M + 127) / 128;
+    for (int h = 0; h < 2; ++h) {
+      const int r = 2 * ti.mb + h;
+      if (r >= tiles128) break;
+      const LfRoute rt = a.routes[r];
+      if (rt.col_hi <= rt.col_lo) continue;
+      if (ti.col_hi <= ti.col_lo) {
+        ti.col_lo = rt.col_lo;
+        ti.col_hi = rt.col_hi;
+      } else {
+        ti.col_lo = min(ti.col_lo, rt.col_lo);
+        ti.col_hi = max(ti.col_hi, rt.col_hi);
+      }
+    }
   }
   return ti;
 }
@@ -95,24 +108,27 @@ __device__ __forceinline__ uint32_t dgrad_keep32(const LfSegTable& t, int seg, i
   return v;
 }
 
-template <int BN, bool B_MN, bool MASKED, int STAGES>
-__global__ void __launch_bounds__(192, 1)
+template <bool B_MN, bool MASKED, int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     lf_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                    const __grid_constant__ GemmArgs args) {
-  using Cfg = GemmCfg<BN, B_MN, STAGES>;
+  using Cfg = GemmCfg<B_MN, STAGES>;
+  constexpr int BN = Cfg::BN, HBN = Cfg::HBN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;  // [2] main loop done  (MMA -> epilogue)
-  uint64_t* tempty = tfull + 2;      // [2] accumulator drained (epilogue -> MMA)
-  uint64_t* lfull = tempty + 2;      // [2] LoRA partial ready (MMA -> mask pass)      MASKED only
-  uint64_t* lmasked = lfull + 2;     // [2] LoRA partial masked (mask pass -> MMA)     MASKED only
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);  // leader: both halves landed
+  uint64_t* empty = full + STAGES;   // both CTAs: stage consumed (multicast commit)
+  uint64_t* tfull = empty + STAGES;  // [2] both CTAs: main loop done
+  uint64_t* tempty = tfull + 2;      // [2] leader: both CTAs drained the accumulator (count 8)
+  uint64_t* lfull = tempty + 2;      // [2] both CTAs: LoRA partial ready                 MASKED
+  uint64_t* lmasked = lfull + 2;     // [2] leader: both CTAs masked their partial (8)   MASKED
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lmasked + 2);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -121,9 +137,9 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 8);
       mbar_init(&lfull[a], 1);
-      mbar_init(&lmasked[a], 4);
+      mbar_init(&lmasked[a], 8);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmA);
@@ -133,63 +149,72 @@ __global__ void __launch_bounds__(192, 1)
       tma_prefetch_desc(&tmB2);
     }
   }
-  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if (warp == 1) tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const int tiles = args.tiles_m * args.tiles_n;
+  const int pair = blockIdx.x >> 1;
+  const int npairs = gridDim.x >> 1;
   const int nkb = (args.K + Cfg::BK - 1) / Cfg::BK;
-  const int jmid = nkb / 2;  // MASKED: where the next tile's LoRA block is interleaved
+  // MASKED: where the next tile's LoRA block is interleaved (debug 256: after the main loop,
+  // 512: a quarter in, 1024: three quarters in)
+  const int jmid = (args.segs.debug & 256) ? nkb : (args.segs.debug & 512) ? nkb / 4
+                   : (args.segs.debug & 1024) ? (3 * nkb) / 4 : nkb / 2;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      auto load_main = [&](const TileInfo& ti, int kb) {
+      const int row_half = (int)rank * Cfg::BM;  // this CTA's rows of the 256-row tile
+      const int col_half = (int)rank * HBN;      // this CTA's columns of the 256-column tile
+      auto begin_stage = [&](uint32_t bytes) {
         mbar_wait(&empty[stage], phase ^ 1);
+        if (leader) mbar_arrive_expect_tx(&full[stage], 2 * bytes);
+      };
+      auto load_main = [&](const TileInfo& ti, int kb) {
+        begin_stage(Cfg::STAGE_BYTES);
         uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
         uint8_t* sB = sA + Cfg::A_BYTES;
-        mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-        tma_load_2d(sA, &tmA, &full[stage], kb * Cfg::BK, ti.mb * Cfg::BM);
+        tma_load_2d_pair(sA, &tmA, &full[stage], kb * Cfg::BK, ti.mb * 256 + row_half);
         if constexpr (!B_MN) {
-          tma_load_2d(sB, &tmB, &full[stage], kb * Cfg::BK, ti.nb * BN);
+          tma_load_2d_pair(sB, &tmB, &full[stage], kb * Cfg::BK, ti.nb * BN + col_half);
         } else {
 #pragma unroll
-          for (int i = 0; i < BN / 64; ++i)
-            tma_load_2d(sB + i * 8192, &tmB, &full[stage], ti.nb * BN + 64 * i, kb * Cfg::BK);
+          for (int i = 0; i < HBN / 64; ++i)
+            tma_load_2d_pair(sB + i * 8192, &tmB, &full[stage], ti.nb * BN + col_half + 64 * i, kb * Cfg::BK);
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       };
       auto load_lora = [&](const TileInfo& ti) {
         for (int c = ti.col_lo; c < ti.col_hi; c += 64) {
           const int nsub = min(4, (ti.col_hi - c) >> 4);
-          mbar_wait(&empty[stage], phase ^ 1);
+          begin_stage(nsub * (Cfg::BM * 32 + HBN * 32));
           uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sB = sA + Cfg::A_BYTES;
-          mbar_arrive_expect_tx(&full[stage], nsub * (Cfg::BM * 32 + BN * 32));
           for (int j = 0; j < nsub; ++j) {
-            tma_load_2d(sA + j * (Cfg::BM * 32), &tmA2, &full[stage], c + 16 * j, ti.mb * Cfg::BM);
+            tma_load_2d_pair(sA + j * (Cfg::BM * 32), &tmA2, &full[stage], c + 16 * j, ti.mb * 256 + row_half);
             if constexpr (!B_MN) {
-              tma_load_2d(sB + j * (BN * 32), &tmB2, &full[stage], c + 16 * j, ti.nb * BN);
+              tma_load_2d_pair(sB + j * (HBN * 32), &tmB2, &full[stage], c + 16 * j, ti.nb * BN + col_half);
             } else {
 #pragma unroll
-              for (int i = 0; i < BN / 64; ++i)
-                tma_load_2d(sB + j * (BN / 64) * 2048 + i * 2048, &tmB2, &full[stage], ti.nb * BN + 64 * i,
-                            c + 16 * j);
+              for (int i = 0; i < HBN / 64; ++i)
+                tma_load_2d_pair(sB + j * (HBN / 64) * 2048 + i * 2048, &tmB2, &full[stage],
+                                 ti.nb * BN + col_half + 64 * i, c + 16 * j);
             }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       };
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = pair; t < tiles; t += npairs) {
         const TileInfo ti = tile_info(args, t);
         if constexpr (MASKED) {
-          if (t == (int)blockIdx.x && ti.lora()) load_lora(ti);
-          const bool has_next = t + (int)gridDim.x < tiles;
-          const TileInfo tn = has_next ? tile_info(args, t + gridDim.x) : ti;
+          if (t == pair && ti.lora()) load_lora(ti);
+          const bool has_next = t + npairs < tiles;
+          const TileInfo tn = has_next ? tile_info(args, t + npairs) : ti;
           for (int kb = 0; kb < nkb; ++kb) {
             if (kb == jmid && has_next && tn.lora()) load_lora(tn);
             load_main(ti, kb);
@@ -203,12 +228,12 @@ __global__ void __launch_bounds__(192, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc_bf16(Cfg::BM, BN, false, B_MN);
+    // ------------------------------------------------------------ MMA issuer (leader CTA)
+    if (lane == 0 && leader) {
+      const uint32_t idesc = make_idesc_bf16(256, BN, false, B_MN);
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t lora_uses[2] = {0, 0};  // MASKED: LoRA partials produced per accumulator buffer
+      uint32_t lora_uses0 = 0, lora_uses1 = 0;  // MASKED: LoRA partials produced per accumulator buffer
       auto mma_main_block = [&](uint32_t d, int kb, bool acc_any) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
@@ -219,9 +244,9 @@ __global__ void __launch_bounds__(192, 1)
           const uint64_t ad = make_sdesc(sA + kk * 32, 16, 1024, kLayoutSW128);
           const uint64_t bd = B_MN ? make_sdesc(sB + kk * 2048, 8192, 1024, kLayoutSW128)
                                    : make_sdesc(sB + kk * 32, 16, 1024, kLayoutSW128);
-          umma_bf16(d, ad, bd, idesc, (acc_any || (kb | kk) != 0) ? 1u : 0u);
+          umma_bf16_pair(d, ad, bd, idesc, (acc_any || (kb | kk) != 0) ? 1u : 0u);
         }
-        umma_commit(&empty[stage]);
+        umma_commit_pair(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       };
       auto mma_lora = [&](const TileInfo& ti, uint32_t d, bool acc_any) {
@@ -234,12 +259,12 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t sB = sA + Cfg::A_BYTES;
           for (int j = 0; j < nsub; ++j) {
             const uint64_t ad = make_sdesc(sA + j * (Cfg::BM * 32), 16, 256, kLayoutSW32);
-            const uint64_t bd = B_MN ? make_sdesc(sB + j * (BN / 64) * 2048, 2048, 1024, kLayoutSW128)
-                                     : make_sdesc(sB + j * (BN * 32), 16, 256, kLayoutSW32);
-            umma_bf16(d, ad, bd, idesc, accum);
+            const uint64_t bd = B_MN ? make_sdesc(sB + j * (HBN / 64) * 2048, 2048, 1024, kLayoutSW128)
+                                     : make_sdesc(sB + j * (HBN * 32), 16, 256, kLayoutSW32);
+            umma_bf16_pair(d, ad, bd, idesc, accum);
             accum = 1u;
           }
-          umma_commit(&empty[stage]);
+          umma_commit_pair(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       };
@@ -249,24 +274,25 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         mma_lora(ti, tmem_base + acc * Cfg::ACC_COLS, false);
-        umma_commit(&lfull[acc]);
+        umma_commit_pair(&lfull[acc]);
       };
       int it = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      for (int t = pair; t < tiles; t += npairs, ++it) {
         const TileInfo ti = tile_info(args, t);
         const int acc = it & 1;
         const uint32_t d = tmem_base + acc * Cfg::ACC_COLS;
         if constexpr (MASKED) {
           if (it == 0 && ti.lora()) issue_lora_first(ti, 0);
           if (ti.lora()) {
-            mbar_wait(&lmasked[acc], lora_uses[acc] & 1);
-            ++lora_uses[acc];
+            uint32_t& lu = acc ? lora_uses1 : lora_uses0;
+            mbar_wait(&lmasked[acc], lu & 1);
+            ++lu;
           } else {
             mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
           }
           tc_fence_after();
-          const bool has_next = t + (int)gridDim.x < tiles;
-          const TileInfo tn = has_next ? tile_info(args, t + gridDim.x) : ti;
+          const bool has_next = t + npairs < tiles;
+          const TileInfo tn = has_next ? tile_info(args, t + npairs) : ti;
           for (int kb = 0; kb < nkb; ++kb) {
             if (kb == jmid && has_next && tn.lora()) issue_lora_first(tn, it + 1);
             mma_main_block(d, kb, ti.lora());
@@ -278,28 +304,39 @@ __global__ void __launch_bounds__(192, 1)
           for (int kb = 0; kb < nkb; ++kb) mma_main_block(d, kb, false);
           if (ti.lora()) mma_lora(ti, d, true);
         }
-        umma_commit(&tfull[acc]);
+        umma_commit_pair(&tfull[acc]);
       }
     }
     __syncwarp();
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2..5)
+    // ------------------------------------------------------------ epilogue (warps 2..5, both CTAs)
     const uint32_t q = warp & 3u;  // TMEM lane quadrant this warp may access
-    uint32_t lora_uses[2] = {0, 0};
+    const uint32_t tempty_leader[2] = {mapa_shared(smem_u32(&tempty[0]), 0), mapa_shared(smem_u32(&tempty[1]), 0)};
+    const uint32_t lmasked_leader[2] = {mapa_shared(smem_u32(&lmasked[0]), 0),
+                                        mapa_shared(smem_u32(&lmasked[1]), 0)};
+    uint32_t lora_uses0 = 0, lora_uses1 = 0;
     // MASKED: zero the dropped elements of tile `it`'s LoRA partial in place
     auto mask_pass = [&](const TileInfo& ti, int it) {
       const int acc = it & 1;
-      const int row = ti.mb * Cfg::BM + (int)(q * 32 + lane);
-      const LfRoute rt = args.routes[ti.mb];
-      const int seg = row < args.M ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
-      const bool active = seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0);
+      const int row = ti.mb * 256 + (int)rank * Cfg::BM + (int)(q * 32 + lane);
+      const int rt_idx = 2 * ti.mb + (int)rank;
+      const bool in_m = row < args.M;
+      int seg = -1;
+      if (in_m) {
+        const LfRoute rt = args.routes[rt_idx];
+        seg = find_segment(args.segs, rt.seg_lo, rt.seg_hi, row);
+      }
+      bool active = seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0);
       // keep bits of the row's BN columns, fetched before waiting on the LoRA partial
       uint32_t keep[BN / 32];
 #pragma unroll
       for (int j = 0; j < BN / 32; ++j)
-        keep[j] = active ? dgrad_keep32(args.segs, seg, row, ti.nb * BN + 32 * j, args.N) : 0xFFFFFFFFu;
-      mbar_wait(&lfull[acc], lora_uses[acc] & 1);
-      ++lora_uses[acc];
+        keep[j] = (active && !(args.segs.debug & 128)) ? dgrad_keep32(args.segs, seg, row, ti.nb * BN + 32 * j, args.N)
+                                                       : 0x7FFFFFFFu;
+      if (args.segs.debug & 64) active = false;
+      uint32_t& lu = acc ? lora_uses1 : lora_uses0;
+      mbar_wait(&lfull[acc], lu & 1);
+      ++lu;
       tc_fence_after();
       // tcgen05.ld/st are warp-collective (.sync.aligned): every branch around them is warp-uniform
       if (__any_sync(0xFFFFFFFFu, active)) {
@@ -320,21 +357,21 @@ __global__ void __launch_bounds__(192, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&lmasked[acc]);
+      if (lane == 0) mbar_arrive_cluster(lmasked_leader[acc]);
     };
     int it = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+    for (int t = pair; t < tiles; t += npairs, ++it) {
       const TileInfo ti = tile_info(args, t);
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       if constexpr (MASKED) {
         if (it == 0 && ti.lora()) mask_pass(ti, 0);
-        if (t + (int)gridDim.x < tiles) {
-          const TileInfo tn = tile_info(args, t + gridDim.x);
+        if (t + npairs < tiles) {
+          const TileInfo tn = tile_info(args, t + npairs);
           if (tn.lora()) mask_pass(tn, it + 1);
         }
       }
-      const int row = ti.mb * Cfg::BM + (int)(q * 32 + lane);
+      const int row = ti.mb * 256 + (int)rank * Cfg::BM + (int)(q * 32 + lane);
       const int n0 = ti.nb * BN;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
@@ -361,22 +398,22 @@ __global__ void __launch_bounds__(192, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) mbar_arrive_cluster(tempty_leader[acc]);
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
   }
 }
 
-template <int BN, bool B_MN, bool MASKED, int STAGES>
+template <bool B_MN, bool MASKED, int STAGES>
 static int launch_one(const GemmMaps& maps, const GemmArgs& args, int num_sms, cudaStream_t stream) {
-  using Cfg = GemmCfg<BN, B_MN, STAGES>;
-  auto kern = lf_gemm_kernel<BN, B_MN, MASKED, STAGES>;
+  using Cfg = GemmCfg<B_MN, STAGES>;
+  auto kern = lf_gemm_kernel<B_MN, MASKED, STAGES>;
   static bool configured = false;  // per instantiation; attribute set is idempotent
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) != cudaSuccess)
@@ -384,22 +421,22 @@ static int launch_one(const GemmMaps& maps, const GemmArgs& args, int num_sms, c
     configured = true;
   }
   const int tiles = args.tiles_m * args.tiles_n;
-  const int grid = tiles < num_sms ? tiles : num_sms;
-  kern<<<grid, 192, Cfg::SMEM_BYTES, stream>>>(maps.a, maps.b, maps.a2, maps.b2, args);
+  const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  kern<<<2 * pairs, 192, Cfg::SMEM_BYTES, stream>>>(maps.a, maps.b, maps.a2, maps.b2, args);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_sms, cudaStream_t stream) {
   GemmArgs args = a;
-  args.tiles_m = (args.M + 127) / 128;
+  args.tiles_m = (args.M + 255) / 256;
   args.tiles_n = (args.N + 255) / 256;
   switch (kind) {
     case kGemmFwd:
-      return launch_one<256, false, false, 4>(maps, args, num_sms, stream);
+      return launch_one<false, false, 6>(maps, args, num_sms, stream);
     case kGemmDgrad:
-      return launch_one<256, true, false, 4>(maps, args, num_sms, stream);
+      return launch_one<true, false, 6>(maps, args, num_sms, stream);
     case kGemmDgradMasked:
-      return launch_one<256, true, true, 4>(maps, args, num_sms, stream);
+      return launch_one<true, true, 6>(maps, args, num_sms, stream);
   }
   return -1;
 }
