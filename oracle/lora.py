@@ -105,6 +105,33 @@ def backward(dy, x, w, a_cat, b_cat, s_hat, segments: Sequence[OracleSegment], k
     return bf16_round(_f32(dx)), da, db, ds
 
 
+def base_forward(x, w, s_hat, b_cat) -> np.ndarray:
+    """② alone: Y = bf16(X·Wᵀ + Ŝ·B_catᵀ) for a given (device-produced) Ŝ."""
+    y = np.asarray(x, np.float64) @ np.asarray(w, np.float64).T
+    if s_hat.shape[1]:
+        y = y + np.asarray(s_hat, np.float64) @ np.asarray(b_cat, np.float64).T
+    return bf16_round(_f32(y))
+
+
+def grads_given(dy, x, w, a_cat, s_hat, ds, keep):
+    """③'s dB, ④ and ⑤ alone, for given (device-produced) Ŝ and dŜ: returns (dx, da, db)."""
+    dy = np.asarray(dy, np.float64)
+    keep64 = np.asarray(keep, np.float64)
+    xm = np.asarray(x, np.float64) * keep64
+    ds64 = np.asarray(ds, np.float64)
+    db = _f32(dy.T @ np.asarray(s_hat, np.float64))
+    da = _f32(ds64.T @ xm)
+    dx = dy @ np.asarray(w, np.float64) + keep64 * (ds64 @ np.asarray(a_cat, np.float64))
+    return bf16_round(_f32(dx)), da, db
+
+
+def bf16_ulp(a) -> np.ndarray:
+    """Spacing of bf16 values at |a| (8 significant bits)."""
+    a = np.abs(np.asarray(a, np.float64))
+    e = np.floor(np.log2(np.where(a > 0, a, 1.0)))
+    return np.where(a > 0, 2.0 ** (e - 7), 2.0**-133)
+
+
 def rel_fro(got, ref) -> float:
     got = np.asarray(got, np.float64)
     ref = np.asarray(ref, np.float64)

@@ -331,8 +331,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       uint32_t keep[BN / 32];
 #pragma unroll
       for (int j = 0; j < BN / 32; ++j)
-        keep[j] = (active && !(args.segs.debug & 128)) ? dgrad_keep32(args.segs, seg, row, ti.nb * BN + 32 * j, args.N)
-                                                       : 0x7FFFFFFFu;
+        keep[j] = !active ? 0xFFFFFFFFu
+                  : (args.segs.debug & 128) ? 0x7FFFFFFFu  // profiling: skip the bit loads, keep the TMEM pass
+                                            : dgrad_keep32(args.segs, seg, row, ti.nb * BN + 32 * j, args.N);
       if (args.segs.debug & 64) active = false;
       uint32_t& lu = acc ? lora_uses1 : lora_uses0;
       mbar_wait(&lfull[acc], lu & 1);
