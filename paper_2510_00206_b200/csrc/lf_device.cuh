@@ -417,14 +417,15 @@ __device__ __forceinline__ uint4 apply_keep8(uint4 v, uint32_t bits) {
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// keep bits of 64 consecutive columns [col, col+64) of one row: byte c = chunk c.
-// The eight Philox streams (counters col/8 .. col/8+7) advance round by round in lockstep,
-// so every round exposes 8 independent IMAD.WIDE/LOP3 chains to the scheduler.
-__device__ __forceinline__ uint64_t keep_bits64_philox(const PhiloxRow& pr, int col) {
-  uint32_t c0[8], c1[8], c2[8], c3[8];
+// keep bits of CH*8 consecutive columns [col, col + 8*CH) of one row: byte c = chunk c.
+// The CH Philox streams (counters col/8 .. col/8+CH-1) advance round by round in lockstep,
+// so every round exposes CH independent IMAD.WIDE/LOP3 chains to the scheduler.
+template <int CH>
+__device__ __forceinline__ uint64_t keep_bits_philox(const PhiloxRow& pr, int col) {
+  uint32_t c0[CH], c1[CH], c2[CH], c3[CH];
   const uint32_t base = (uint32_t)col >> 3;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
+  for (int j = 0; j < CH; ++j) {
     c0[j] = base + j;
     c1[j] = pr.c1;
     c2[j] = pr.c2;
@@ -433,7 +434,7 @@ __device__ __forceinline__ uint64_t keep_bits64_philox(const PhiloxRow& pr, int 
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < CH; ++j) {
       const uint64_t p0 = (uint64_t)0xD2511F53u * c0[j];
       const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2[j];
       const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1[j] ^ pr.k0[i];
@@ -446,13 +447,27 @@ __device__ __forceinline__ uint64_t keep_bits64_philox(const PhiloxRow& pr, int 
   }
   uint64_t bits = 0;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
+  for (int j = 0; j < CH; ++j) {
     const uint32_t r0 = __vcmpgeu2(c0[j], pr.thr2), r1 = __vcmpgeu2(c1[j], pr.thr2);
     const uint32_t r2 = __vcmpgeu2(c2[j], pr.thr2), r3 = __vcmpgeu2(c3[j], pr.thr2);
     const uint32_t b = gather_lsb4(__byte_perm(r0, r1, 0x6420)) | (gather_lsb4(__byte_perm(r2, r3, 0x6420)) << 4);
     bits |= (uint64_t)b << (8 * j);
   }
   return bits;
+}
+__device__ __forceinline__ uint64_t keep_bits64_philox(const PhiloxRow& pr, int col) {
+  return keep_bits_philox<8>(pr, col);
+}
+
+// zero the dropped bf16 elements of chunks [c0, c0 + CH) of one 128-byte SW128 tile row
+template <int CH>
+__device__ __forceinline__ void apply_chunks_sw128(uint8_t* tile, int rit, int c0, uint32_t bits) {
+  const uint32_t rowa = smem_u32(tile) + (uint32_t)rit * 128u;
+  uint4 v[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) v[c] = lds128(rowa + (uint32_t)(((c0 + c) ^ (rit & 7)) << 4));
+#pragma unroll
+  for (int c = 0; c < CH; ++c) sts128(rowa + (uint32_t)(((c0 + c) ^ (rit & 7)) << 4), apply_keep8(v[c], (bits >> (8 * c)) & 0xFFu));
 }
 __device__ __forceinline__ uint64_t keep_bits64_explicit(const LfSegTable& t, int row, int col, int ncols) {
   uint64_t bits = 0;

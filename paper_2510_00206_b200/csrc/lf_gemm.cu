@@ -39,7 +39,7 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int ACC_COLS = BN;
   static constexpr int TMEM_COLS = 2 * ACC_COLS;  // 512
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 512 * 16;  // + routing cache
 };
 
 // grouped raster: GROUP m-tiles share each n-column sweep so W tiles stay L2-hot
@@ -60,16 +60,24 @@ struct TileInfo {
   __device__ bool lora() const { return col_hi > col_lo; }
 };
 
-__device__ __forceinline__ TileInfo tile_info(const GemmArgs& a, int t) {
+constexpr int kSmemRoutes = 512;  // routing entries staged in smem (m <= 65536); beyond: global
+
+// the single-thread producer / MMA roles must not stall on a dependent global load per
+// tile: the routing table is staged in shared memory once per CTA
+__device__ __forceinline__ LfRoute route_at(const GemmArgs& a, const LfRoute* s_routes, int r) {
+  return r < kSmemRoutes ? s_routes[r] : a.routes[r];
+}
+
+__device__ __forceinline__ TileInfo tile_info(const GemmArgs& a, const LfRoute* s_routes, int t) {
   TileInfo ti;
   gemm_tile_coords(t, a.tiles_m, a.tiles_n, ti.mb, ti.nb);
   ti.col_lo = ti.col_hi = 0;
-  if (a.routes) {
+  if (a.routes && !(a.segs.debug & 2048)) {
     const int tiles128 = (a.M + 127) / 128;
     for (int h = 0; h < 2; ++h) {
       const int r = 2 * ti.mb + h;
       if (r >= tiles128) break;
-      const LfRoute rt = a.routes[r];
+      const LfRoute rt = route_at(a, s_routes, r);
       if (rt.col_hi <= rt.col_lo) continue;
       if (ti.col_hi <= ti.col_lo) {
         ti.col_lo = rt.col_lo;
@@ -83,8 +91,23 @@ __device__ __forceinline__ TileInfo tile_info(const GemmArgs& a, int t) {
   return ti;
 }
 
+// Fallback keep bits when ① did not leave a packed mask (explicit uint8 mask, or Philox
+// regenerated here). Kept out of line: inlined into the unrolled mask pass it multiplies the
+// kernel's code size ~15x and the epilogue warps' instruction fetch starts evicting the
+// single-thread producer / MMA loops from the instruction cache.
+__device__ __noinline__ uint32_t dgrad_keep32_slow(const LfSegTable& t, int seg, int row, int col, int ncols) {
+  uint32_t v = 0;
+  for (int j = 0; j < 4; ++j) {
+    const int cc = col + 8 * j;
+    const uint32_t b = (t.mask_mode == 2) ? explicit_keep8(t.mask + (int64_t)row * t.ld_mask, cc, ncols)
+                                           : philox_keep8((uint32_t)cc >> 3, (uint32_t)row, t.seg[seg]);
+    v |= b << (8 * j);
+  }
+  return v;
+}
+
 // keep bits (4 bytes = 32 columns, byte j = columns col+8j..col+8j+7) of one row for the
-// ⑤ mask pass: bit-packed mask written by ① if present, else Philox / explicit mask
+// ⑤ mask pass: the bit-packed mask written by ① when present
 __device__ __forceinline__ uint32_t dgrad_keep32(const LfSegTable& t, int seg, int row, int col, int ncols) {
   if (t.mask_mode == 1 && t.bits) {
     const uint8_t* rb = t.bits + (int64_t)row * t.ld_bits;
@@ -97,15 +120,7 @@ __device__ __forceinline__ uint32_t dgrad_keep32(const LfSegTable& t, int seg, i
       if (b0 + i < nb) v |= (uint32_t)rb[b0 + i] << (8 * i);
     return v;
   }
-  uint32_t v = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int cc = col + 8 * j;
-    const uint32_t b = (t.mask_mode == 2) ? explicit_keep8(t.mask + (int64_t)row * t.ld_mask, cc, ncols)
-                                           : philox_keep8((uint32_t)cc >> 3, (uint32_t)row, t.seg[seg]);
-    v |= b << (8 * j);
-  }
-  return v;
+  return dgrad_keep32_slow(t, seg, row, col, ncols);
 }
 
 template <bool B_MN, bool MASKED, int STAGES>
@@ -124,6 +139,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   uint64_t* lfull = tempty + 2;      // [2] both CTAs: LoRA partial ready                 MASKED
   uint64_t* lmasked = lfull + 2;     // [2] leader: both CTAs masked their partial (8)   MASKED
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lmasked + 2);
+  LfRoute* s_routes = reinterpret_cast<LfRoute*>(smem + STAGES * Cfg::STAGE_BYTES + 256);  // [kSmemRoutes]
+  if (args.routes) {
+    const int nr = min((args.M + 127) / 128, kSmemRoutes);
+    for (int i = (int)threadIdx.x; i < nr; i += (int)blockDim.x) s_routes[i] = args.routes[i];
+  }
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -210,11 +230,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         }
       };
       for (int t = pair; t < tiles; t += npairs) {
-        const TileInfo ti = tile_info(args, t);
+        const TileInfo ti = tile_info(args, s_routes, t);
         if constexpr (MASKED) {
           if (t == pair && ti.lora()) load_lora(ti);
           const bool has_next = t + npairs < tiles;
-          const TileInfo tn = has_next ? tile_info(args, t + npairs) : ti;
+          const TileInfo tn = has_next ? tile_info(args, s_routes, t + npairs) : ti;
           for (int kb = 0; kb < nkb; ++kb) {
             if (kb == jmid && has_next && tn.lora()) load_lora(tn);
             load_main(ti, kb);
@@ -278,7 +298,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       };
       int it = 0;
       for (int t = pair; t < tiles; t += npairs, ++it) {
-        const TileInfo ti = tile_info(args, t);
+        const TileInfo ti = tile_info(args, s_routes, t);
         const int acc = it & 1;
         const uint32_t d = tmem_base + acc * Cfg::ACC_COLS;
         if constexpr (MASKED) {
@@ -292,7 +312,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           }
           tc_fence_after();
           const bool has_next = t + npairs < tiles;
-          const TileInfo tn = has_next ? tile_info(args, t + npairs) : ti;
+          const TileInfo tn = has_next ? tile_info(args, s_routes, t + npairs) : ti;
           for (int kb = 0; kb < nkb; ++kb) {
             if (kb == jmid && has_next && tn.lora()) issue_lora_first(tn, it + 1);
             mma_main_block(d, kb, ti.lora());
@@ -323,7 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       const bool in_m = row < args.M;
       int seg = -1;
       if (in_m) {
-        const LfRoute rt = args.routes[rt_idx];
+        const LfRoute rt = route_at(args, s_routes, rt_idx);
         seg = find_segment(args.segs, rt.seg_lo, rt.seg_hi, row);
       }
       bool active = seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0);
@@ -362,13 +382,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     };
     int it = 0;
     for (int t = pair; t < tiles; t += npairs, ++it) {
-      const TileInfo ti = tile_info(args, t);
+      const TileInfo ti = tile_info(args, s_routes, t);
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       if constexpr (MASKED) {
         if (it == 0 && ti.lora()) mask_pass(ti, 0);
         if (t + npairs < tiles) {
-          const TileInfo tn = tile_info(args, t + npairs);
+          const TileInfo tn = tile_info(args, s_routes, t + npairs);
           if (tn.lora()) mask_pass(tn, it + 1);
         }
       }

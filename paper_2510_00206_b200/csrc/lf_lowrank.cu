@@ -73,7 +73,9 @@ void down_config(int rtot, int* stages, int* stage_bytes) {
   *stages = s < 2 ? 2 : (s > 8 ? 8 : s);
 }
 
-__global__ void __launch_bounds__(192, 2)
+constexpr int kDownThreads = 320;  // producer, MMA, 8 mask warps (2 per row quadrant; 4 also do the epilogue)
+
+__global__ void __launch_bounds__(kDownThreads, 2)
     lf_down_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ DownArgs args, int STAGES, int STAGE_BYTES) {
   using namespace down;
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(192, 2)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&masked[s], 4);
+      mbar_init(&masked[s], 8);
     }
     mbar_init(tfull, 1);
     fence_barrier_init();
@@ -109,9 +111,9 @@ __global__ void __launch_bounds__(192, 2)
       tma_prefetch_desc(&tmA);
     }
   }
-  // Consecutive K-steps go to NACC independent accumulators (summed in the epilogue): with
-  // N = R this small, back-to-back MMAs into one accumulator serialise on its latency.
-  const int NACC = 4 * args.rtot <= 256 ? 4 : 2;
+  // one accumulator: spreading the K-steps over several (summed in the epilogue) was
+  // measured to make no difference on B200 — these pipelines are TMA/mask bound
+  constexpr int NACC = 1;
   uint32_t tmem_cols = 32;
   while ((int)tmem_cols < NACC * args.rtot) tmem_cols <<= 1;
   if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
@@ -158,8 +160,10 @@ __global__ void __launch_bounds__(192, 2)
     }
     __syncwarp();
   } else {
-    // mask + epilogue warps (2..5): thread <-> tile row 32*(warp&3) + lane
+    // mask warps 2..9: thread <-> tile row 32*(warp&3) + lane, half = which 4 of the row's 8
+    // 16-byte chunks it masks; warps 2..5 (half 0) also run the epilogue
     const uint32_t q = warp & 3u;
+    const int half = warp >= 6 ? 1 : 0;
     const int rit = (int)(q * 32 + lane);
     const int row = m0 + rit;
     const int seg = row < args.m ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
@@ -173,14 +177,32 @@ __global__ void __launch_bounds__(192, 2)
       for (int kb = kb0; kb < kb1; ++kb) {
         // the keep bits depend only on (row, column, seed, offset): generate them while the
         // tile is still in flight, so Philox latency overlaps the TMA instead of adding to it
-        uint64_t bits = ~0ull;
-        if (my_mask)
-          bits = explicit_mask ? keep_bits64_explicit(args.segs, row, kb * 64, args.k) : keep_bits64_philox(pr, kb * 64);
+        const int col = kb * 64 + 32 * half;
+        uint32_t bits = ~0u;
+        if (my_mask) {
+          if (explicit_mask) {
+            const uint8_t* mrow = args.segs.mask + (int64_t)row * args.segs.ld_mask;
+            bits = 0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) bits |= explicit_keep8(mrow, col + 8 * c, args.k) << (8 * c);
+          } else {
+            bits = (uint32_t)keep_bits_philox<4>(pr, col);
+          }
+        }
         mbar_wait(&full[stage], phase);
         if (my_mask) {
-          if (!(args.segs.debug & 8)) apply_row_sw128(smem + stage * STAGE_BYTES, rit, bits);
+          if (!(args.segs.debug & 8) && bits != ~0u)
+            apply_chunks_sw128<4>(smem + stage * STAGE_BYTES, rit, 4 * half, bits);
           // Philox runs once per step: ④ and ⑤ read these bits instead
-          if (!explicit_mask && bits_row) store_bits64(bits_row, kb * 8, (int)args.segs.ld_bits, bits);
+          if (!explicit_mask && bits_row) {
+            const int b0 = kb * 8 + 4 * half;
+            if (b0 + 4 <= (int)args.segs.ld_bits && ((reinterpret_cast<uintptr_t>(bits_row + b0) & 3u) == 0)) {
+              *reinterpret_cast<uint32_t*>(bits_row + b0) = bits;
+            } else {
+              for (int i = 0; i < 4; ++i)
+                if (b0 + i < (int)args.segs.ld_bits) bits_row[b0 + i] = (uint8_t)(bits >> (8 * i));
+            }
+          }
         }
         if (!(args.segs.debug & 4)) fence_proxy_async_smem();
         __syncwarp();
@@ -188,7 +210,7 @@ __global__ void __launch_bounds__(192, 2)
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-    if (has_work) {
+    if (has_work && half == 0) {
       mbar_wait(tfull, 0);
       tc_fence_after();
       const uint32_t taddr = tmem + ((q * 32u) << 16);
@@ -251,7 +273,7 @@ int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs
     configured = true;
   }
   dim3 grid((args.m + 127) / 128, args.ksplit);
-  lf_down_kernel<<<grid, 192, smem, stream>>>(tm_x, tm_a, args, stages, stage_bytes);
+  lf_down_kernel<<<grid, kDownThreads, smem, stream>>>(tm_x, tm_a, args, stages, stage_bytes);
   if (cudaGetLastError() != cudaSuccess) return -1;
   return finalize_launch(args.segs, args.routes, args.ws, args.s_hat, stream);
 }
@@ -259,6 +281,20 @@ int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs
 // ------------------------------------------------------------------------------------
 // ④ dA_cat += dŜᵀ · (M⊙X)
 // ------------------------------------------------------------------------------------
+// ④ keep bits without ①'s packed mask (explicit uint8 mask or Philox regenerated): out of
+// line so the rarely used path does not bloat the kernel's hot loops
+__device__ __noinline__ void dgrad_a_keep_slow(const LfSegTable& t, int seg, int row, int col, int ncols,
+                                               uint64_t& b0, uint64_t& b1) {
+  if (t.mask_mode == 2) {
+    b0 = keep_bits64_explicit(t, row, col, ncols);
+    b1 = keep_bits64_explicit(t, row, col + 64, ncols);
+  } else {
+    const PhiloxRow pr = philox_row(t.seg[seg], (uint32_t)row);
+    b0 = keep_bits64_philox(pr, col);
+    b1 = keep_bits64_philox(pr, col + 64);
+  }
+}
+
 namespace dga {
 constexpr int X_BYTES = 2 * 128 * 64 * 2;  // two 64-column SW128 boxes of 128 rows = 32 KB
 constexpr int MAX_SMEM = 200 * 1024;
@@ -380,13 +416,8 @@ __global__ void __launch_bounds__(192, 2)
         const uint8_t* rb = args.segs.bits + (int64_t)row * args.segs.ld_bits;
         b0 = load_bits64(rb, kt * 16, (int)args.segs.ld_bits);
         b1 = load_bits64(rb, kt * 16 + 8, (int)args.segs.ld_bits);
-      } else if (args.segs.mask_mode == 2) {
-        b0 = keep_bits64_explicit(args.segs, row, kt * 128, args.k);
-        b1 = keep_bits64_explicit(args.segs, row, kt * 128 + 64, args.k);
       } else {
-        const PhiloxRow pr = philox_row(args.segs.seg[seg], (uint32_t)row);
-        b0 = keep_bits64_philox(pr, kt * 128);
-        b1 = keep_bits64_philox(pr, kt * 128 + 64);
+        dgrad_a_keep_slow(args.segs, seg, row, kt * 128, args.k, b0, b1);
       }
       return true;
     };

@@ -55,8 +55,11 @@ class LaunchStats:
         ev.record()
         self.events.setdefault(name, []).append((start, ev))
 
+    # device kernels each C entry point launches (① and ③ add the split-K finalize kernel)
+    KERNELS_PER_CALL = {"dropout_down_fwd": 2, "grad_up": 2}
+
     def total_launches(self) -> int:
-        return sum(self.launches.values())
+        return sum(n * self.KERNELS_PER_CALL.get(k, 1) for k, n in self.launches.items())
 
     def durations_ms(self) -> dict[str, list[float]]:
         torch.cuda.synchronize()
@@ -132,8 +135,10 @@ class _FusedLoRAFn(torch.autograd.Function):
         da = db = ds = None
         if plan.has_lora:
             ds = torch.empty((m, R), dtype=_BF16, device=dy.device)
-            db = torch.zeros((n, R), dtype=torch.float32, device=dy.device)
-            da = torch.zeros((R, k), dtype=torch.float32, device=dy.device)
+            # one zero-fill for both fp32 accumulators
+            acc = torch.zeros(R * k + n * R, dtype=torch.float32, device=dy.device)
+            da = acc[:R * k].view(R, k)
+            db = acc[R * k:].view(n, R)
             _call("grad_up", lib.lf_grad_up, pp, _ptr(dy), _ptr(b_cat), _ptr(s_hat), _ptr(ds), _ptr(db), _stream())
             _call("grad_down", lib.lf_grad_down, pp, _ptr(x), _ptr(ds), _ptr(da), _stream())
         dx = None

@@ -119,6 +119,8 @@ def routing_table(segments: Sequence[Segment], col_starts: Sequence[int], ranks:
 
 
 _WORKSPACES: dict[tuple[int, int], torch.Tensor] = {}
+_ROUTES: dict[tuple, torch.Tensor] = {}
+_ROUTES_MAX = 256
 
 
 def workspace(device: torch.device, stream: torch.cuda.Stream, nbytes: int) -> torch.Tensor:
@@ -212,7 +214,19 @@ class LayerPlan:
         stream = stream or torch.cuda.current_stream(device)
         self.device = device
         lib = _lib.load()
-        self.routes = torch.empty((max(self.num_tiles, 1), 4), dtype=torch.int32, device=device)
+        # the routing table depends only on the segment table: built once per (device,
+        # stream, m, segments) and reused by every later call with the same microbatch layout
+        dev_index = device.index if device.index is not None else torch.cuda.current_device()
+        key = (dev_index, stream.cuda_stream, self.m,
+               tuple((s.row_start, s.row_end) for s in self.segments), tuple(self.col_starts), tuple(self.ranks))
+        cached = _ROUTES.get(key)
+        fresh = cached is None
+        if fresh:
+            if len(_ROUTES) >= _ROUTES_MAX:
+                _ROUTES.pop(next(iter(_ROUTES)))
+            cached = torch.empty((max(self.num_tiles, 1), 4), dtype=torch.int32, device=device)
+            _ROUTES[key] = cached
+        self.routes = cached
         nbytes = _lib.workspace_bytes(self.m, self.rank_total)
         self._ws = workspace(device, stream, nbytes)
         self.problem.routes = self.routes.data_ptr()
@@ -221,7 +235,7 @@ class LayerPlan:
         if self.needs_keep_bits:
             self.keep_bits = torch.empty((self.m, self.k // 8), dtype=torch.uint8, device=device)
             self.problem.keep_bits = self.keep_bits.data_ptr()
-        if self.has_lora:
+        if self.has_lora and fresh:
             from .functional import _call
 
             _call("build_routes", lib.lf_build_routes, ctypes.byref(self.problem), self.routes.data_ptr(),
