@@ -82,12 +82,13 @@ def test_b200_minimal_formulas():
 @given(m=st.integers(1, 1 << 14), k=st.integers(1, 1 << 13), n=st.integers(1, 1 << 13), r=st.integers(1, 64))
 @settings(max_examples=100, deadline=None)
 def test_b200_design_never_exceeds_reference_fused(m, k, n, r):
-    """The built design never moves more than the reference's fused model plus rank-sized
-    terms (ours − ref = 2r(m+k+n) − 8mk); for r <= min(m, k, n)/4 it moves strictly less."""
+    """The built design differs from the reference's fused model by rank-sized terms only:
+    ours − ref = 2r(m+k+n) − 8mk (it drops the stored mask, X̂ and the mk-sized LoRA
+    input-gradient), so it moves strictly less whenever r(m+k+n) < 4mk."""
     s = _shape(m, k, n, r, 2)
     ours, ref = T.roundtrip_bytes(s, "b200_minimal"), T.roundtrip_bytes(s, "fused_lora")
     assert ours - ref == 2 * r * (m + k + n) - 8 * m * k
-    if 4 * r <= min(m, k, n):
+    if r * (m + k + n) < 4 * m * k:
         assert ours < ref
 
 
