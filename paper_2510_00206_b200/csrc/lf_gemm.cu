@@ -235,11 +235,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           if (t == pair && ti.lora()) load_lora(ti);
           const bool has_next = t + npairs < tiles;
           const TileInfo tn = has_next ? tile_info(args, s_routes, t + npairs) : ti;
-          for (int kb = 0; kb < nkb; ++kb) {
-            if (kb == jmid && has_next && tn.lora()) load_lora(tn);
-            load_main(ti, kb);
-          }
-          if (jmid >= nkb && has_next && tn.lora()) load_lora(tn);
+          const bool lora_next = has_next && tn.lora();
+          const int split = lora_next ? min(jmid, nkb) : nkb;
+          int kb = 0;
+          for (; kb < split; ++kb) load_main(ti, kb);
+          if (lora_next) load_lora(tn);
+          for (; kb < nkb; ++kb) load_main(ti, kb);
         } else {
           for (int kb = 0; kb < nkb; ++kb) load_main(ti, kb);
           if (ti.lora()) load_lora(ti);
@@ -301,7 +302,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         const TileInfo ti = tile_info(args, s_routes, t);
         const int acc = it & 1;
         const uint32_t d = tmem_base + acc * Cfg::ACC_COLS;
-        if constexpr (MASKED) {
+        if (MASKED && (args.segs.debug & 4096)) {  // profiling: plain k-loop in the masked kernel
+          mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+          tc_fence_after();
+          for (int kb = 0; kb < nkb; ++kb) mma_main_block(d, kb, false);
+        } else if constexpr (MASKED) {
           if (it == 0 && ti.lora()) issue_lora_first(ti, 0);
           if (ti.lora()) {
             uint32_t& lu = acc ? lora_uses1 : lora_uses0;
@@ -313,11 +318,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           tc_fence_after();
           const bool has_next = t + npairs < tiles;
           const TileInfo tn = has_next ? tile_info(args, s_routes, t + npairs) : ti;
-          for (int kb = 0; kb < nkb; ++kb) {
-            if (kb == jmid && has_next && tn.lora()) issue_lora_first(tn, it + 1);
-            mma_main_block(d, kb, ti.lora());
-          }
-          if (jmid >= nkb && has_next && tn.lora()) issue_lora_first(tn, it + 1);
+          const bool lora_next = has_next && tn.lora();
+          const int split = lora_next ? min(jmid, nkb) : nkb;
+          const bool acc_any = ti.lora();
+          int kb = 0;
+          for (; kb < split; ++kb) mma_main_block(d, kb, acc_any);
+          if (lora_next) issue_lora_first(tn, it + 1);
+          for (; kb < nkb; ++kb) mma_main_block(d, kb, acc_any);
         } else {
           mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
           tc_fence_after();

@@ -112,8 +112,10 @@ class _FusedLoRAFn(torch.autograd.Function):
         y = torch.empty((m, n), dtype=_BF16, device=x.device)
         s_hat = a_cat = b_cat = None
         if plan.has_lora:
-            a_cat = plan.gather_a(params[:n_adapters])
-            b_cat = plan.gather_b(params[n_adapters:])
+            # bf16 operand copies: the module's cached shadows when given, else cast here
+            shadows = plan.weights_bf16
+            a_cat = plan.gather_a(shadows[0] if shadows else params[:n_adapters])
+            b_cat = plan.gather_b(shadows[1] if shadows else params[n_adapters:])
             s_hat = torch.empty((m, R), dtype=_BF16, device=x.device)
             _call("dropout_down_fwd", lib.lf_dropout_down_fwd, pp, _ptr(x), _ptr(a_cat), _ptr(s_hat), _stream())
         _call("base_fwd", lib.lf_base_fwd, pp, _ptr(x), _ptr(w), _ptr(s_hat), _ptr(b_cat), _ptr(y), _stream())
@@ -191,12 +193,15 @@ def fused_lora(
     offset: int = 0,
     keep_mask: torch.Tensor | None = None,
     training: bool = True,
+    weights_bf16: tuple | None = None,
 ) -> torch.Tensor:
     """Y = X·Wᵀ + scaling·dropout(X)·Aᵀ·Bᵀ  (Eq. 1) on one adapter.
 
     x (..., k) bf16; weight (n, k) = nn.Linear.weight (frozen); lora_a (r, k) =
     lora_A.weight; lora_b (n, r) = lora_B.weight. Dropout uses SPEC.md §3's Philox mask
     keyed by (seed, offset) unless ``keep_mask`` (uint8, m x k) is given.
+    ``weights_bf16 = (a_bf16, b_bf16)``: bf16 copies of fp32 master weights kept current by
+    the caller (the modules refresh them when the parameters change); default: cast here.
     """
     k = weight.shape[1]
     x2, lead = _flatten_input(x, k)
@@ -204,6 +209,8 @@ def fused_lora(
     adapter = AdapterConfig(rank=lora_a.shape[0], scaling=float(scaling), dropout_p=float(dropout_p), seed=int(seed))
     plan = LayerPlan(m, k, weight.shape[0], [adapter], [Segment(0, 0, m)] if m > 0 else [], offset=offset,
                      training=training, keep_mask=keep_mask)
+    if weights_bf16 is not None:
+        plan.weights_bf16 = ([weights_bf16[0]], [weights_bf16[1]])
     return _run(x2, weight, [lora_a], [lora_b], plan, lead, None)
 
 
@@ -218,6 +225,7 @@ def fused_multi_lora(
     keep_mask: torch.Tensor | None = None,
     training: bool = True,
     grad_sink: Callable | None = None,
+    weights_bf16: tuple | None = None,
 ) -> torch.Tensor:
     """Mixed-adapter microbatch: rows of ``segments`` route to their adapter's A/B, scale
     and dropout; the frozen W is streamed once for all of them.
@@ -231,6 +239,8 @@ def fused_multi_lora(
         raise ValidationError("lora_a, lora_b and adapters must have one entry per adapter slot")
     plan = LayerPlan(x2.shape[0], k, weight.shape[0], adapters, segments, offset=offset, training=training,
                      keep_mask=keep_mask)
+    if weights_bf16 is not None:
+        plan.weights_bf16 = (list(weights_bf16[0]), list(weights_bf16[1]))
     return _run(x2, weight, lora_a, lora_b, plan, lead, grad_sink)
 
 

@@ -37,6 +37,25 @@ def _init_lora(a: nn.Linear, b: nn.Linear, init: str, generator: torch.Generator
             raise ValidationError(f"unknown init {init!r} (expected 'peft' or 'gaussian')")
 
 
+class _Bf16Shadow:
+    """bf16 operand copies of fp32 master parameters, refreshed only when a parameter
+    changes (its storage or in-place version), as a mixed-precision optimizer would keep
+    its model weights. bf16 parameters are used as they are."""
+
+    def __init__(self):
+        self._cache: dict[int, tuple] = {}
+
+    def __call__(self, p: torch.Tensor) -> torch.Tensor:
+        if p.dtype == torch.bfloat16:
+            return p.detach()
+        key = (p.data_ptr(), p._version, tuple(p.shape))
+        hit = self._cache.get(id(p))
+        if hit is None or hit[0] != key:
+            hit = (key, p.detach().to(torch.bfloat16))
+            self._cache[id(p)] = hit
+        return hit[1]
+
+
 def _frozen_base(base: nn.Linear | torch.Tensor) -> tuple[torch.Tensor, torch.Tensor | None]:
     if isinstance(base, nn.Linear):
         w, bias = base.weight, base.bias
@@ -79,6 +98,7 @@ class FusedLoRA(nn.Module):
         self.lora_B = nn.Linear(rank, self.out_features, bias=False, device=dev, dtype=dtype)
         _init_lora(self.lora_A, self.lora_B, init, generator)
         self._offset = 0
+        self._shadow = _Bf16Shadow()
 
     @property
     def base_weight(self) -> torch.Tensor:
@@ -106,6 +126,7 @@ class FusedLoRA(nn.Module):
             offset=self.next_offset() if self.training else 0,
             keep_mask=keep_mask,
             training=self.training,
+            weights_bf16=(self._shadow(self.lora_A.weight), self._shadow(self.lora_B.weight)),
         )
         if self.base_bias is not None:
             y = y + self.base_bias
@@ -148,6 +169,7 @@ class FusedMultiLoRA(nn.Module):
         for la, lb in zip(self.lora_A, self.lora_B):
             _init_lora(la, lb, init, generator)
         self._offset = 0
+        self._shadow = _Bf16Shadow()
         self.track_slot_grads = track_slot_grads
         # (adapter slot, global batch) -> [dA (r x k) fp32, dB (n x r) fp32]
         self.slot_grads: dict[tuple[int, int], list[torch.Tensor]] = {}
@@ -182,6 +204,7 @@ class FusedMultiLoRA(nn.Module):
             keep_mask=keep_mask,
             training=self.training,
             grad_sink=self._sink if self.track_slot_grads else None,
+            weights_bf16=([self._shadow(la.weight) for la in self.lora_A], [self._shadow(lb.weight) for lb in self.lora_B]),
         )
         if self.base is not None and self.base.bias is not None:
             y = y + self.base.bias

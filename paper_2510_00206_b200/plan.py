@@ -195,6 +195,9 @@ class LayerPlan:
         self.needs_keep_bits = (self.training and keep_mask is None and
                                 any(p.segments[i].dropout_p > 0 for i in range(p.num_segments)))
         self.keep_bits: torch.Tensor | None = None
+        # optional bf16 copies of the adapter weights (lora_A list, lora_B list) kept by a
+        # module in step with its fp32 master parameters; None = cast on every call
+        self.weights_bf16: tuple | None = None
 
     # -- derived ------------------------------------------------------------------
     @property
