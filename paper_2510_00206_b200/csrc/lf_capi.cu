@@ -69,6 +69,26 @@ bool make_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, u
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 2-D map over a row-major uint8 array (the packed keep bits); ld in bytes, multiple of 16
+bool make_map_u8(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_cols,
+                 uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// tuning override from the environment (profiling sweeps), read once per name
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
 struct Dev {
   int id = -1;
   int sms = 0;
@@ -269,12 +289,13 @@ int lf_dropout_down_fwd(const LfProblem* p, const uint16_t* x, const uint16_t* a
   int stages = 0, stage_bytes = 0;
   lf::down_config(p->rank_total, &stages, &stage_bytes);
   const int occ = occupancy_for_smem(stages * stage_bytes + 2048);
-  const int target = occ * d.sms;
-  int ksplit = target / tiles_m;  // one resident wave: no tail CTAs
-  const int max_split = nkb >= 8 ? nkb / 4 : 1;
-  if (ksplit > max_split) ksplit = max_split;
-  if (ksplit < 1) ksplit = 1;
-  a.ksplit = ksplit;
+  // one resident wave sharing the units evenly (stream-K); at least 4 k-blocks per CTA so
+  // the split-K partial traffic stays small next to the X stream
+  const long units = (long)tiles_m * nkb;
+  long ctas = (long)occ * d.sms;
+  if (ctas > units / 4) ctas = units / 4;
+  if (ctas < 1) ctas = 1;
+  a.ctas = (int)ctas;
   if (lf::down_launch(tx, ta, a, d.sms, (cudaStream_t)stream)) return cuda_fail("dropout_down launch");
   return LF_OK;
 }
@@ -361,12 +382,20 @@ int lf_grad_down(const LfProblem* p, const uint16_t* x, const uint16_t* ds, floa
   LF_TRY(check_ptr(da_accum, "da_accum"));
   Dev d;
   LF_TRY(current_device(&d));
-  CUtensorMap tx, td;
+  CUtensorMap tx, td, tk;
   if (!make_map(&tx, x, p->m, p->k, p->k, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&td, ds, p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B))
     return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (x / ds)");
   lf::GradDownArgs a;
   memset(&a, 0, sizeof(a));
+  // ①'s packed keep bits ride in each stage by TMA (16 B x 128 rows per unit) when the
+  // bit rows are 16-byte pitched; otherwise the mask warps read them from global memory
+  tk = tx;
+  if (t.mask_mode == 1 && t.bits && t.ld_bits % 16 == 0) {
+    if (!make_map_u8(&tk, t.bits, p->m, t.ld_bits, t.ld_bits, 16, 128))
+      return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (keep bits)");
+    a.bits_tma = 1;
+  }
   a.m = p->m;
   a.k = p->k;
   a.rtot = p->rank_total;
@@ -374,15 +403,15 @@ int lf_grad_down(const LfProblem* p, const uint16_t* x, const uint16_t* ds, floa
   a.routes = reinterpret_cast<const lf::LfRoute*>(p->routes);
   a.segs = t;
   int stages = 0, stage_bytes = 0;
-  lf::grad_down_config(p->rank_total, &stages, &stage_bytes);
+  lf::grad_down_config(p->rank_total, a.bits_tma != 0, &stages, &stage_bytes);
   const int occ = occupancy_for_smem(stages * stage_bytes + 2048);
   const int tiles_k = (p->k + 127) / 128;
   const int tiles_m = (p->m + 127) / 128;
-  int ms = occ * d.sms / tiles_k;  // one resident wave
-  if (ms > tiles_m) ms = tiles_m;
-  if (ms < 1) ms = 1;
-  a.m_split = ms;
-  if (lf::grad_down_launch(tx, td, a, d.sms, (cudaStream_t)stream)) return cuda_fail("grad_down launch");
+  // one resident wave sharing the units evenly (stream-K)
+  long ctas = (long)occ * d.sms;
+  if (ctas > (long)tiles_m * tiles_k) ctas = (long)tiles_m * tiles_k;
+  a.ctas = (int)ctas;
+  if (lf::grad_down_launch(tx, td, tk, a, d.sms, (cudaStream_t)stream)) return cuda_fail("grad_down launch");
   return LF_OK;
 }
 

@@ -35,6 +35,11 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ uint64_t lds64(uint32_t addr) {
+  uint64_t v;
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
@@ -139,6 +144,26 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+// Whole-warp forms: called by all 32 lanes of a converged warp with warp-uniform operands;
+// one elected lane (always the same, the lowest) issues. Keeping the issuing loop warp-wide
+// lets ptxas hold descriptors in uniform registers instead of a per-MMA R2UR waterfall.
+__device__ __forceinline__ void umma_bf16_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
 
 // 32 lanes x 32 bit, 16 consecutive columns per thread
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
@@ -241,6 +266,26 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       "h"((uint16_t)0x3)
       : "memory");
 }
+// whole-warp forms (see umma_bf16_warp)
+__device__ __forceinline__ void umma_bf16_pair_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                    uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
 
 // ---------------------------------------------------------------------------------
 // UMMA descriptors
@@ -260,6 +305,10 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
   d |= (uint64_t)layout << 61;
   return d;
 }
+
+// descriptor of the same layout `bytes` further on (start-address field = addr >> 4 in bits
+// 0..13; shared-window addresses stay below 256 KB, so the field never carries)
+__device__ __forceinline__ uint64_t sdesc_add(uint64_t d, uint32_t bytes) { return d + (uint64_t)(bytes >> 4); }
 
 // Instruction descriptor, kind::f16 with bf16 A/B and fp32 D.
 __host__ __device__ constexpr uint32_t make_idesc_bf16(uint32_t M, uint32_t N, bool a_mn_major, bool b_mn_major) {
@@ -405,16 +454,20 @@ __device__ __forceinline__ uint32_t explicit_keep8(const uint8_t* mask_row, uint
   return bits;
 }
 
-// zero the bf16 lanes of a 16-byte chunk whose keep bit is clear
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+// zero the bf16 lanes of a 16-byte chunk whose keep bit is clear. The 8 bits are spread to
+// the sign bits of 8 bytes (byte j of p/q: 0x80-ish iff bit j / j+4 is set), then prmt's
+// sign-replicate selectors (nibble bit 3) expand them to 0xFFFF / 0x0000 bf16 lanes.
 __device__ __forceinline__ uint4 apply_keep8(uint4 v, uint32_t bits) {
-  uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t lo = (bits >> (2 * i)) & 1u ? 0x0000FFFFu : 0u;
-    const uint32_t hi = (bits >> (2 * i + 1)) & 1u ? 0xFFFF0000u : 0u;
-    w[i] &= (lo | hi);
-  }
-  return make_uint4(w[0], w[1], w[2], w[3]);
+  const uint32_t t = bits * 0x01010101u;
+  const uint32_t p = (t & 0x08040201u) + 0x7F7F7F7Fu;
+  const uint32_t q = (t & 0x80402010u) + 0x7F7F7F7Fu;
+  return make_uint4(v.x & prmt(p, 0, 0x9988u), v.y & prmt(p, 0, 0xBBAAu), v.z & prmt(q, 0, 0x9988u),
+                    v.w & prmt(q, 0, 0xBBAAu));
 }
 
 // keep bits of CH*8 consecutive columns [col, col + 8*CH) of one row: byte c = chunk c.

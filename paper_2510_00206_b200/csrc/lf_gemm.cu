@@ -249,8 +249,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (leader CTA)
-    if (lane == 0 && leader) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA, whole warp; one elected lane issues)
+    if (leader) {
       const uint32_t idesc = make_idesc_bf16(256, BN, false, B_MN);
       int stage = 0;
       uint32_t phase = 0;
@@ -260,14 +260,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         tc_fence_after();
         const uint32_t sA = smem_u32(smem + stage * Cfg::STAGE_BYTES);
         const uint32_t sB = sA + Cfg::A_BYTES;
+        const uint64_t ad0 = make_sdesc(sA, 16, 1024, kLayoutSW128);
+        const uint64_t bd0 = B_MN ? make_sdesc(sB, 8192, 1024, kLayoutSW128) : make_sdesc(sB, 16, 1024, kLayoutSW128);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t ad = make_sdesc(sA + kk * 32, 16, 1024, kLayoutSW128);
-          const uint64_t bd = B_MN ? make_sdesc(sB + kk * 2048, 8192, 1024, kLayoutSW128)
-                                   : make_sdesc(sB + kk * 32, 16, 1024, kLayoutSW128);
-          umma_bf16_pair(d, ad, bd, idesc, (acc_any || (kb | kk) != 0) ? 1u : 0u);
-        }
-        umma_commit_pair(&empty[stage]);
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16_pair_warp(d, sdesc_add(ad0, kk * 32), sdesc_add(bd0, B_MN ? kk * 2048 : kk * 32), idesc,
+                              (acc_any || (kb | kk) != 0) ? 1u : 0u);
+        umma_commit_pair_warp(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       };
       auto mma_lora = [&](const TileInfo& ti, uint32_t d, bool acc_any) {
@@ -282,10 +281,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
             const uint64_t ad = make_sdesc(sA + j * (Cfg::BM * 32), 16, 256, kLayoutSW32);
             const uint64_t bd = B_MN ? make_sdesc(sB + j * (HBN / 64) * 2048, 2048, 1024, kLayoutSW128)
                                      : make_sdesc(sB + j * (HBN * 32), 16, 256, kLayoutSW32);
-            umma_bf16_pair(d, ad, bd, idesc, accum);
+            umma_bf16_pair_warp(d, ad, bd, idesc, accum);
             accum = 1u;
           }
-          umma_commit_pair(&empty[stage]);
+          umma_commit_pair_warp(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       };
@@ -295,7 +294,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         mma_lora(ti, tmem_base + acc * Cfg::ACC_COLS, false);
-        umma_commit_pair(&lfull[acc]);
+        umma_commit_pair_warp(&lfull[acc]);
       };
       int it = 0;
       for (int t = pair; t < tiles; t += npairs, ++it) {
@@ -331,7 +330,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           for (int kb = 0; kb < nkb; ++kb) mma_main_block(d, kb, false);
           if (ti.lora()) mma_lora(ti, d, true);
         }
-        umma_commit_pair(&tfull[acc]);
+        umma_commit_pair_warp(&tfull[acc]);
       }
     }
     __syncwarp();

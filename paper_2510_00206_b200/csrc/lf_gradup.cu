@@ -115,8 +115,8 @@ __global__ void __launch_bounds__(192, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && nsub > 0) {
+    // ------------------------------------------------------------ MMA issuer (whole warp, one lane issues)
+    if (nsub > 0) {
       mbar_wait(tzero, 0);
       tc_fence_after();
       int stage = 0;
@@ -145,23 +145,26 @@ __global__ void __launch_bounds__(192, 1)
           // the two chains share each dY K-step and are issued interleaved:
           //   dŜ[m-tile]        += dY[m-tile, n-sub]  · B_cat[n-sub, cols]   (K = 128 out features)
           //   dB_cat[n-sub, ..] += dY[m-tile, n-sub]ᵀ · Ŝ[m-tile, cols]      (K = 128 tokens)
+          const uint64_t a_ds = make_sdesc(sDy, 16, 1024, kLayoutSW128);
+          const uint64_t b_ds = make_sdesc(sB, 4096, 256, kLayoutSW32);
+          const uint64_t a_db = make_sdesc(sDy, 16384, 1024, kLayoutSW128);
+          const uint64_t b_db = make_sdesc(sSh, 4096, 256, kLayoutSW32);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t a = (uint32_t)(kk % NA) * rtot;
             if (!(args.segs.debug & 1))
-              umma_bf16(d_ds + a, make_sdesc(sDy + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, kLayoutSW128),
-                        make_sdesc(sB + kk * 512, 4096, 256, kLayoutSW32), idesc_ds, (nt > nt0 || kk >= NA) ? 1u : 0u);
+              umma_bf16_warp(d_ds + a, sdesc_add(a_ds, (kk >> 2) * 16384 + (kk & 3) * 32), sdesc_add(b_ds, kk * 512),
+                             idesc_ds, (nt > nt0 || kk >= NA) ? 1u : 0u);
             if (!(args.segs.debug & 32))
-              umma_bf16(d_db + a, make_sdesc(sDy + kk * 2048, 16384, 1024, kLayoutSW128),
-                        make_sdesc(sSh + kk * 512, 4096, 256, kLayoutSW32), idesc_db, 1u);
+              umma_bf16_warp(d_db + a, sdesc_add(a_db, kk * 2048), sdesc_add(b_db, kk * 512), idesc_db, 1u);
           }
-          umma_commit(&empty[stage]);
+          umma_commit_warp(&empty[stage]);
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&ds_full[b]);
-        umma_commit(&sh_empty[b]);
+        umma_commit_warp(&ds_full[b]);
+        umma_commit_warp(&sh_empty[b]);
       }
-      umma_commit(db_full);
+      umma_commit_warp(db_full);
     }
     __syncwarp();
   } else {

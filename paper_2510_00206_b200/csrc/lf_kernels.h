@@ -35,7 +35,7 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& args, int n
 // ① dropout + down projection
 struct DownArgs {
   int32_t m, k, rtot;
-  int32_t ksplit;         // CTAs along K per 128-row tile
+  int32_t ctas;           // persistent CTAs sharing the (row tile, k-block) units
   void* s_hat;            // bf16 m x rtot
   float* ws;              // fp32 m x rtot partials (zero on entry and exit)
   int32_t* counters;      // per 128-row tile (zero on entry and exit)
@@ -65,14 +65,15 @@ int grad_up_launch(const CUtensorMap& tm_dy, const CUtensorMap& tm_b, const CUte
 // ④ dA
 struct GradDownArgs {
   int32_t m, k, rtot;
-  int32_t m_split;
+  int32_t ctas;      // persistent CTAs sharing the (k-tile, row tile) units
+  int32_t bits_tma;  // keep bits arrive in each stage by TMA (tmK valid)
   float* da;  // fp32 rtot x k accumulator
   const LfRoute* routes;
   LfSegTable segs;
 };
-void grad_down_config(int rtot, int* stages, int* stage_bytes);
-int grad_down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_ds, const GradDownArgs& args, int num_sms,
-                     cudaStream_t stream);
+void grad_down_config(int rtot, bool bits_tma, int* stages, int* stage_bytes);
+int grad_down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_ds, const CUtensorMap& tm_bits,
+                     const GradDownArgs& args, int num_sms, cudaStream_t stream);
 
 // split-K epilogue of ① and ③: fp32 partials (ws) -> scaled bf16 m x R, workspace re-zeroed
 int finalize_launch(const LfSegTable& segs, const LfRoute* routes, float* ws, void* out, cudaStream_t stream);

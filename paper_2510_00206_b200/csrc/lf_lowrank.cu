@@ -75,6 +75,29 @@ void down_config(int rtot, int* stages, int* stage_bytes) {
 
 constexpr int kDownThreads = 320;  // producer, MMA, 8 mask warps (2 per row quadrant; 4 also do the epilogue)
 
+// Stream-K work split shared by ① and ④: the (tile, k-block) units are laid out tile-major
+// and every CTA takes one contiguous, equal share, so a single resident wave of CTAs moves
+// the same number of bytes each (a per-tile split leaves SMs with 2 CTAs next to SMs with 1).
+// A share crossing a tile boundary is walked as per-tile spans, each flushed on its own.
+struct UnitSpan {
+  int tile, k0, k1;
+};
+struct UnitWalker {
+  int u, u1, per_tile;
+  __device__ UnitWalker(int units, int ctas, int cta, int per_tile_) : per_tile(per_tile_) {
+    u = (int)((int64_t)cta * units / ctas);
+    u1 = (int)((int64_t)(cta + 1) * units / ctas);
+  }
+  __device__ bool next(UnitSpan& sp) {
+    if (u >= u1) return false;
+    sp.tile = u / per_tile;
+    sp.k0 = u - sp.tile * per_tile;
+    sp.k1 = min(per_tile, sp.k0 + (u1 - u));
+    u += sp.k1 - sp.k0;
+    return true;
+  }
+};
+
 __global__ void __launch_bounds__(kDownThreads, 2)
     lf_down_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ DownArgs args, int STAGES, int STAGE_BYTES) {
@@ -84,19 +107,14 @@ __global__ void __launch_bounds__(kDownThreads, 2)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* masked = empty + STAGES;
-  uint64_t* tfull = masked + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tfull = masked + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int mt = blockIdx.x;
-  const int m0 = mt * 128;
   const int nkb = (args.k + 63) / 64;
-  const int kb0 = (int)((int64_t)blockIdx.y * nkb / args.ksplit);
-  const int kb1 = (int)((int64_t)(blockIdx.y + 1) * nkb / args.ksplit);
-  const LfRoute rt = args.routes[mt];
-  const int N = rt.col_hi - rt.col_lo;
-  const bool has_work = N > 0 && kb1 > kb0;
-  const bool need_mask = has_work && tile_needs_mask(args.segs, rt);
+  const int tiles_m = (args.m + 127) / 128;
+  const int units = tiles_m * nkb;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -104,133 +122,160 @@ __global__ void __launch_bounds__(kDownThreads, 2)
       mbar_init(&empty[s], 1);
       mbar_init(&masked[s], 8);
     }
-    mbar_init(tfull, 1);
-    fence_barrier_init();
-    if (has_work) {
-      tma_prefetch_desc(&tmX);
-      tma_prefetch_desc(&tmA);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
     }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmA);
   }
-  // one accumulator: spreading the K-steps over several (summed in the epilogue) was
-  // measured to make no difference on B200 — these pipelines are TMA/mask bound
-  constexpr int NACC = 1;
+  // two accumulators (R columns each): a span's flush overlaps the next span's MMAs
   uint32_t tmem_cols = 32;
-  while ((int)tmem_cols < NACC * args.rtot) tmem_cols <<= 1;
+  while ((int)tmem_cols < 2 * args.rtot) tmem_cols <<= 1;
   if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  UnitWalker walk(units, (int)gridDim.x, (int)blockIdx.x, nkb);
+  UnitSpan sp;
   if (warp == 0) {
-    if (lane == 0 && has_work) {
+    if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* sX = smem + stage * STAGE_BYTES;
-        uint8_t* sA = sX + X_BYTES;
-        mbar_arrive_expect_tx(&full[stage], X_BYTES + N * 128);
-        tma_load_2d(sX, &tmX, &full[stage], kb * 64, m0);
-        for (int j = 0; j < N / 16; ++j) tma_load_2d(sA + j * 2048, &tmA, &full[stage], kb * 64, rt.col_lo + 16 * j);
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      while (walk.next(sp)) {
+        const LfRoute rt = args.routes[sp.tile];
+        const int N = rt.col_hi - rt.col_lo;
+        if (N <= 0) continue;
+        for (int kb = sp.k0; kb < sp.k1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sX = smem + stage * STAGE_BYTES;
+          uint8_t* sA = sX + X_BYTES;
+          mbar_arrive_expect_tx(&full[stage], X_BYTES + N * 128);
+          tma_load_2d(sX, &tmX, &full[stage], kb * 64, sp.tile * 128);
+          for (int j = 0; j < N / 16; ++j) tma_load_2d(sA + j * 2048, &tmA, &full[stage], kb * 64, rt.col_lo + 16 * j);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0 && has_work) {
+    // whole warp, one elected lane issues (uniform-datapath descriptors)
+    int stage = 0, it = 0;
+    uint32_t phase = 0;
+    while (walk.next(sp)) {
+      const LfRoute rt = args.routes[sp.tile];
+      const int N = rt.col_hi - rt.col_lo;
+      if (N <= 0) continue;
+      const bool need_mask = tile_needs_mask(args.segs, rt);
+      const int b = it & 1;
+      mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem + b * args.rtot;
       const uint32_t idesc = make_idesc_bf16(128, (uint32_t)N, false, false);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int kb = kb0; kb < kb1; ++kb) {
+      for (int kb = sp.k0; kb < sp.k1; ++kb) {
         mbar_wait(need_mask ? &masked[stage] : &full[stage], phase);
         tc_fence_after();
         const uint32_t sX = smem_u32(smem + stage * STAGE_BYTES);
-        const uint32_t sA = sX + X_BYTES;
+        const uint64_t ax = make_sdesc(sX, 16, 1024, kLayoutSW128);
+        const uint64_t ba = make_sdesc(sX + X_BYTES, 16, 1024, kLayoutSW128);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
           if (!(args.segs.debug & 1))
-          umma_bf16(tmem + (kk % NACC) * args.rtot, make_sdesc(sX + kk * 32, 16, 1024, kLayoutSW128),
-                    make_sdesc(sA + kk * 32, 16, 1024, kLayoutSW128), idesc, (kb > kb0 || kk >= NACC) ? 1u : 0u);
+            umma_bf16_warp(d, sdesc_add(ax, kk * 32), sdesc_add(ba, kk * 32), idesc,
+                           (kb > sp.k0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit(&empty[stage]);
+        umma_commit_warp(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      umma_commit(tfull);
+      umma_commit_warp(&tfull[b]);
+      ++it;
     }
     __syncwarp();
   } else {
     // mask warps 2..9: thread <-> tile row 32*(warp&3) + lane, half = which 4 of the row's 8
-    // 16-byte chunks it masks; warps 2..5 (half 0) also run the epilogue
+    // 16-byte chunks it masks; warps 2..5 (half 0) also flush each span's partial sums
     const uint32_t q = warp & 3u;
     const int half = warp >= 6 ? 1 : 0;
     const int rit = (int)(q * 32 + lane);
-    const int row = m0 + rit;
-    const int seg = row < args.m ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
-    if (need_mask) {
-      const bool my_mask = seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0);
-      const bool explicit_mask = args.segs.mask_mode == 2;
-      const PhiloxRow pr = philox_row(args.segs.seg[seg >= 0 ? seg : 0], (uint32_t)row);
-      uint8_t* bits_row = args.segs.bits ? args.segs.bits + (int64_t)row * args.segs.ld_bits : nullptr;
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        // the keep bits depend only on (row, column, seed, offset): generate them while the
-        // tile is still in flight, so Philox latency overlaps the TMA instead of adding to it
-        const int col = kb * 64 + 32 * half;
-        uint32_t bits = ~0u;
-        if (my_mask) {
-          if (explicit_mask) {
-            const uint8_t* mrow = args.segs.mask + (int64_t)row * args.segs.ld_mask;
-            bits = 0;
+    const bool explicit_mask = args.segs.mask_mode == 2;
+    int stage = 0, it = 0;
+    uint32_t phase = 0;
+    while (walk.next(sp)) {
+      const LfRoute rt = args.routes[sp.tile];
+      const int N = rt.col_hi - rt.col_lo;
+      if (N <= 0) continue;
+      const int row = sp.tile * 128 + rit;
+      if (tile_needs_mask(args.segs, rt)) {
+        const int seg = row < args.m ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
+        const bool my_mask = seg >= 0 && (explicit_mask || args.segs.seg[seg].thr != 0);
+        const PhiloxRow pr = philox_row(args.segs.seg[seg >= 0 ? seg : 0], (uint32_t)row);
+        uint8_t* bits_row = args.segs.bits ? args.segs.bits + (int64_t)row * args.segs.ld_bits : nullptr;
+        for (int kb = sp.k0; kb < sp.k1; ++kb) {
+          // the keep bits depend only on (row, column, seed, offset): generate them while the
+          // tile is still in flight, so Philox latency overlaps the TMA instead of adding to it
+          const int col = kb * 64 + 32 * half;
+          uint32_t bits = ~0u;
+          if (my_mask) {
+            if (explicit_mask) {
+              const uint8_t* mrow = args.segs.mask + (int64_t)row * args.segs.ld_mask;
+              bits = 0;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) bits |= explicit_keep8(mrow, col + 8 * c, args.k) << (8 * c);
-          } else {
-            bits = (uint32_t)keep_bits_philox<4>(pr, col);
-          }
-        }
-        mbar_wait(&full[stage], phase);
-        if (my_mask) {
-          if (!(args.segs.debug & 8) && bits != ~0u)
-            apply_chunks_sw128<4>(smem + stage * STAGE_BYTES, rit, 4 * half, bits);
-          // Philox runs once per step: ④ and ⑤ read these bits instead
-          if (!explicit_mask && bits_row) {
-            const int b0 = kb * 8 + 4 * half;
-            if (b0 + 4 <= (int)args.segs.ld_bits && ((reinterpret_cast<uintptr_t>(bits_row + b0) & 3u) == 0)) {
-              *reinterpret_cast<uint32_t*>(bits_row + b0) = bits;
+              for (int c = 0; c < 4; ++c) bits |= explicit_keep8(mrow, col + 8 * c, args.k) << (8 * c);
             } else {
-              for (int i = 0; i < 4; ++i)
-                if (b0 + i < (int)args.segs.ld_bits) bits_row[b0 + i] = (uint8_t)(bits >> (8 * i));
+              bits = (uint32_t)keep_bits_philox<4>(pr, col);
             }
           }
+          mbar_wait(&full[stage], phase);
+          if (my_mask) {
+            if (!(args.segs.debug & 8) && bits != ~0u)
+              apply_chunks_sw128<4>(smem + stage * STAGE_BYTES, rit, 4 * half, bits);
+            // Philox runs once per step: ④ and ⑤ read these bits instead
+            if (!explicit_mask && bits_row) {
+              const int b0 = kb * 8 + 4 * half;
+              if (b0 + 4 <= (int)args.segs.ld_bits && ((reinterpret_cast<uintptr_t>(bits_row + b0) & 3u) == 0)) {
+                *reinterpret_cast<uint32_t*>(bits_row + b0) = bits;
+              } else {
+                for (int i = 0; i < 4; ++i)
+                  if (b0 + i < (int)args.segs.ld_bits) bits_row[b0 + i] = (uint8_t)(bits >> (8 * i));
+              }
+            }
+          }
+          if (!(args.segs.debug & 4)) fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&masked[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        if (!(args.segs.debug & 4)) fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&masked[stage]);
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      } else {
+        // unmasked span: the MMA consumes the stages straight from `full`; keep the ring
+        // position in step with it
+        for (int kb = sp.k0; kb < sp.k1; ++kb)
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-    }
-    if (has_work && half == 0) {
-      mbar_wait(tfull, 0);
-      tc_fence_after();
-      const uint32_t taddr = tmem + ((q * 32u) << 16);
-      float* wrow = args.ws + (int64_t)row * args.rtot + rt.col_lo;
-      for (int c = 0; c < N; c += 16) {
-        float s[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) s[j] = 0.f;
-        for (int a = 0; a < NACC; ++a) {
+      if (half == 0) {
+        const int b = it & 1;
+        mbar_wait(&tfull[b], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem + ((q * 32u) << 16) + b * args.rtot;
+        float* wrow = args.ws + (int64_t)row * args.rtot + rt.col_lo;
+        for (int c = 0; c < N; c += 16) {
           uint32_t v[16];
-          tmem_ld16(taddr + a * args.rtot + c, v);
+          tmem_ld16(taddr + c, v);
           tmem_ld_wait();
+          if (row < args.m && !(args.segs.debug & 2)) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) s[j] += __uint_as_float(v[j]);
+            for (int j = 0; j < 16; j += 4)
+              red_add_v4(wrow + c + j, __uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                         __uint_as_float(v[j + 3]));
+          }
         }
-        if (row < args.m && !(args.segs.debug & 2)) {
-#pragma unroll
-          for (int j = 0; j < 16; j += 4) red_add_v4(wrow + c + j, s[j], s[j + 1], s[j + 2], s[j + 3]);
-        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[b]);
       }
+      ++it;
     }
     // split-K partials are complete in the workspace once this grid retires; the
     // lf_finalize_kernel launched behind it scales, masks and converts them
@@ -272,8 +317,7 @@ int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs
       return -1;
     configured = true;
   }
-  dim3 grid((args.m + 127) / 128, args.ksplit);
-  lf_down_kernel<<<grid, kDownThreads, smem, stream>>>(tm_x, tm_a, args, stages, stage_bytes);
+  lf_down_kernel<<<args.ctas, kDownThreads, smem, stream>>>(tm_x, tm_a, args, stages, stage_bytes);
   if (cudaGetLastError() != cudaSuccess) return -1;
   return finalize_launch(args.segs, args.routes, args.ws, args.s_hat, stream);
 }
@@ -295,46 +339,61 @@ __device__ __noinline__ void dgrad_a_keep_slow(const LfSegTable& t, int seg, int
   }
 }
 
+constexpr int kDgaThreads = 320;  // producer, MMA, 8 mask warps (2 per row quadrant; 4 also flush)
+
 namespace dga {
 constexpr int X_BYTES = 2 * 128 * 64 * 2;  // two 64-column SW128 boxes of 128 rows = 32 KB
 constexpr int MAX_SMEM = 200 * 1024;
 }  // namespace dga
 
-__global__ void __launch_bounds__(192, 2)
+__global__ void __launch_bounds__(kDgaThreads, 2)
     lf_dgrad_a_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmD,
-                      const __grid_constant__ GradDownArgs args, int stages, int stage_bytes) {
+                      const __grid_constant__ CUtensorMap tmK, const __grid_constant__ GradDownArgs args, int stages,
+                      int stage_bytes) {
   using namespace dga;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
   uint64_t* empty = full + stages;
   uint64_t* masked = empty + stages;
-  uint64_t* tfull = masked + stages;
-  uint64_t* tzero = tfull + 1;
+  uint64_t* tfull = masked + stages;  // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint64_t* tzero = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tzero + 1);
 
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int kt = blockIdx.x;
   const int tiles_m = (args.m + 127) / 128;
-  const int mt0 = (int)((int64_t)blockIdx.y * tiles_m / args.m_split);
-  const int mt1 = (int)((int64_t)(blockIdx.y + 1) * tiles_m / args.m_split);
+  const int tiles_k = (args.k + 127) / 128;
   const int rtot = args.rtot;
-  // independent accumulators for consecutive K-steps (see ①); 2 CTAs / SM share 512 columns
-  const int NACC = 4 * rtot <= 256 ? 4 : 2;
+  const int KBITS_OFF = X_BYTES + (rtot / 16) * 4096;  // stage: X | dŜ columns | keep bits (16 B x 128 rows)
+  // stream-K over (k-tile, m-tile) units, k-tile major: a span = one k-tile's dAᵀ columns
+  // summed over a run of m-tiles. Two zero-initialised accumulators (R columns each).
+  const int u0 = (int)((int64_t)blockIdx.x * tiles_m * tiles_k / gridDim.x);
+  const int u1 = (int)((int64_t)(blockIdx.x + 1) * tiles_m * tiles_k / gridDim.x);
   uint32_t tmem_cols = 32;
-  while ((int)tmem_cols < NACC * rtot) tmem_cols <<= 1;
+  while ((int)tmem_cols < 2 * rtot) tmem_cols <<= 1;
+  // profiling bit 64: stages bypass the mask warps (results invalid)
+  auto needs_mask = [&](const LfRoute& rt) { return !(args.segs.debug & 64) && tile_needs_mask(args.segs, rt); };
+  auto live = [&](int u) {  // next unit at or after u whose row tile carries adapters
+    while (u < u1 && args.routes[u % tiles_m].col_hi <= args.routes[u % tiles_m].col_lo) ++u;
+    return u;
+  };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&masked[s], 4);
+      mbar_init(&masked[s], 8);
     }
-    mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
     mbar_init(tzero, 4);
     fence_barrier_init();
     tma_prefetch_desc(&tmX);
     tma_prefetch_desc(&tmD);
+    if (args.bits_tma) tma_prefetch_desc(&tmK);
   }
   if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
   tc_fence_before();
@@ -346,138 +405,139 @@ __global__ void __launch_bounds__(192, 2)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int mt = mt0; mt < mt1; ++mt) {
+      for (int u = live(u0); u < u1; u = live(u + 1)) {
+        const int mt = u % tiles_m, kt = u / tiles_m;
         const LfRoute rt = args.routes[mt];
         const int N = rt.col_hi - rt.col_lo;
-        if (N <= 0) continue;
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sX = smem + stage * stage_bytes;
         uint8_t* sD = sX + X_BYTES;
-        mbar_arrive_expect_tx(&full[stage], X_BYTES + (N / 16) * 4096);
+        const bool kbits = args.bits_tma && needs_mask(rt);
+        mbar_arrive_expect_tx(&full[stage], X_BYTES + (N / 16) * 4096 + (kbits ? 2048 : 0));
         tma_load_2d(sX, &tmX, &full[stage], kt * 128, mt * 128);
         tma_load_2d(sX + 16384, &tmX, &full[stage], kt * 128 + 64, mt * 128);
         for (int j = 0; j < N / 16; ++j) tma_load_2d(sD + j * 4096, &tmD, &full[stage], rt.col_lo + 16 * j, mt * 128);
+        if (kbits) tma_load_2d(sX + KBITS_OFF, &tmK, &full[stage], kt * 16, mt * 128);
         if (++stage == stages) { stage = 0; phase ^= 1; }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      mbar_wait(tzero, 0);
-      tc_fence_after();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int mt = mt0; mt < mt1; ++mt) {
-        const LfRoute rt = args.routes[mt];
-        const int N = rt.col_hi - rt.col_lo;
-        if (N <= 0) continue;
-        const bool need_mask = tile_needs_mask(args.segs, rt);
-        mbar_wait(need_mask ? &masked[stage] : &full[stage], phase);
+    // whole warp, one elected lane issues (uniform-datapath descriptors)
+    mbar_wait(tzero, 0);
+    tc_fence_after();
+    int stage = 0, it = 0;
+    uint32_t phase = 0;
+    bool open = false;
+    for (int u = live(u0); u < u1;) {
+      const int mt = u % tiles_m, kt = u / tiles_m;
+      const int nxt = live(u + 1);
+      const int b = it & 1;
+      if (!open) {
+        mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t sX = smem_u32(smem + stage * stage_bytes);
-        const uint32_t sD = sX + X_BYTES;
-        const uint32_t idesc = make_idesc_bf16(128, (uint32_t)N, true, true);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          if (!(args.segs.debug & 1))
-          umma_bf16(tmem + (kk % NACC) * rtot + rt.col_lo, make_sdesc(sX + kk * 2048, 16384, 1024, kLayoutSW128),
-                    make_sdesc(sD + kk * 512, 4096, 256, kLayoutSW32), idesc, 1u);
-        }
-        umma_commit(&empty[stage]);
-        if (++stage == stages) { stage = 0; phase ^= 1; }
+        open = true;
       }
-      umma_commit(tfull);
+      const LfRoute rt = args.routes[mt];
+      const int N = rt.col_hi - rt.col_lo;
+      const bool need_mask = needs_mask(rt);
+      mbar_wait(need_mask ? &masked[stage] : &full[stage], phase);
+      tc_fence_after();
+      const uint32_t sX = smem_u32(smem + stage * stage_bytes);
+      const uint64_t ax = make_sdesc(sX, 16384, 1024, kLayoutSW128);
+      const uint64_t bd = make_sdesc(sX + X_BYTES, 4096, 256, kLayoutSW32);
+      const uint32_t idesc = make_idesc_bf16(128, (uint32_t)N, true, true);
+      const uint32_t d = tmem + b * rtot + rt.col_lo;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        if (!(args.segs.debug & 1))
+          umma_bf16_warp(d, sdesc_add(ax, kk * 2048), sdesc_add(bd, kk * 512), idesc, 1u);
+      }
+      umma_commit_warp(&empty[stage]);
+      if (++stage == stages) { stage = 0; phase ^= 1; }
+      if (nxt >= u1 || nxt / tiles_m != kt) {  // span ends: hand the accumulator to the flush
+        umma_commit_warp(&tfull[b]);
+        ++it;
+        open = false;
+      }
+      u = nxt;
     }
     __syncwarp();
   } else {
     const uint32_t q = warp & 3u;
     const uint32_t taddr = tmem + ((q * 32u) << 16);
-    // zero the accumulator so every MMA may accumulate
-    {
-      uint32_t z[16];
+    uint32_t z[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) z[i] = 0u;
-      for (int c = 0; c < NACC * rtot; c += 16) tmem_st16(taddr + c, z);
+    for (int i = 0; i < 16; ++i) z[i] = 0u;
+    // zero both accumulators so every MMA may accumulate (warps 2..5: one per lane quadrant)
+    if (warp < 6) {
+      for (int c = 0; c < 2 * rtot; c += 16) tmem_st16(taddr + c, z);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tzero);
     }
     const int rit = (int)(q * 32 + lane);
-    // keep bits of this thread's row in m-tile `mt` (128 columns of k-tile kt); false = keep all
-    auto fetch_bits = [&](int mt, uint64_t& b0, uint64_t& b1) -> bool {
-      b0 = b1 = ~0ull;
-      const LfRoute rt = args.routes[mt];
-      if (!tile_needs_mask(args.segs, rt)) return false;
-      const int row = mt * 128 + rit;
-      const int seg = row < args.m ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
-      if (!(seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0))) return false;
-      if (args.segs.mask_mode == 1 && args.segs.bits) {
-        const uint8_t* rb = args.segs.bits + (int64_t)row * args.segs.ld_bits;
-        b0 = load_bits64(rb, kt * 16, (int)args.segs.ld_bits);
-        b1 = load_bits64(rb, kt * 16 + 8, (int)args.segs.ld_bits);
-      } else {
-        dgrad_a_keep_slow(args.segs, seg, row, kt * 128, args.k, b0, b1);
-      }
-      return true;
-    };
-    auto next_tile = [&](int mt) {
-      while (mt < mt1 && args.routes[mt].col_hi <= args.routes[mt].col_lo) ++mt;
-      return mt;
-    };
-    int stage = 0;
+    const int half = warp >= 6 ? 1 : 0;  // which 64-column box of the unit this warp masks
+    int stage = 0, it = 0;
     uint32_t phase = 0;
-    uint32_t touched = 0;  // 16-column groups that received contributions
-    // software pipeline: the keep bits of the next m-tile are fetched while this one is masked
-    int cur = next_tile(mt0);
-    uint64_t cb0 = ~0ull, cb1 = ~0ull;
-    bool cmask = cur < mt1 ? fetch_bits(cur, cb0, cb1) : false;
-    while (cur < mt1) {
-      const int nxt = next_tile(cur + 1);
-      uint64_t nb0 = ~0ull, nb1 = ~0ull;
-      const bool nmask = nxt < mt1 ? fetch_bits(nxt, nb0, nb1) : false;
-      const LfRoute rt = args.routes[cur];
+    uint32_t touched = 0;  // 16-column groups of the open span that received contributions
+    for (int cur = live(u0); cur < u1;) {
+      const int nxt = live(cur + 1);
+      const int mt = cur % tiles_m, kt = cur / tiles_m;
+      const LfRoute rt = args.routes[mt];
       for (int c = rt.col_lo; c < rt.col_hi; c += 16) touched |= 1u << (c >> 4);
-      if (tile_needs_mask(args.segs, rt)) {
-        mbar_wait(&full[stage], phase);
-        if (cmask) {
-          uint8_t* sX = smem + stage * stage_bytes;
-          if (!(args.segs.debug & 8)) {
-            apply_row_sw128(sX, rit, cb0);
-            apply_row_sw128(sX + 16384, rit, cb1);
+      if (needs_mask(rt)) {
+        const int row = mt * 128 + rit;
+        const int seg = row < args.m ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
+        const bool mine = seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0);
+        uint64_t bits = ~0ull;
+        if (mine && !args.bits_tma) {  // fallback: fetched before the wait so it overlaps the TMA
+          if (args.segs.mask_mode == 1 && args.segs.bits) {
+            bits = load_bits64(args.segs.bits + (int64_t)row * args.segs.ld_bits, kt * 16 + 8 * half,
+                               (int)args.segs.ld_bits);
+          } else {
+            uint64_t b0, b1;
+            dgrad_a_keep_slow(args.segs, seg, row, kt * 128, args.k, b0, b1);
+            bits = half ? b1 : b0;
           }
+        }
+        mbar_wait(&full[stage], phase);
+        if (mine) {
+          uint8_t* sX = smem + stage * stage_bytes;
+          if (args.bits_tma) bits = lds64(smem_u32(sX + KBITS_OFF) + (uint32_t)(rit * 16 + half * 8));
+          if (!(args.segs.debug & 8)) apply_row_sw128(sX + half * 16384, rit, bits);
         }
         if (!(args.segs.debug & 4)) fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&masked[stage]);
       }
       if (++stage == stages) { stage = 0; phase ^= 1; }
-      cur = nxt;
-      cb0 = nb0;
-      cb1 = nb1;
-      cmask = nmask;
-    }
-    if (touched) {
-      mbar_wait(tfull, 0);
-      tc_fence_after();
-      const int kcol = kt * 128 + rit;
-      for (int g = 0; g < rtot / 16; ++g) {
-        if (!((touched >> g) & 1u)) continue;
-        float s[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) s[j] = 0.f;
-        for (int a = 0; a < NACC; ++a) {
+      if (half == 0 && (nxt >= u1 || nxt / tiles_m != kt)) {
+        // flush the span: dA_catᵀ rows of this k-tile += accumulator, then re-zero it
+        const int b = it & 1;
+        mbar_wait(&tfull[b], (it >> 1) & 1);
+        tc_fence_after();
+        const int kcol = kt * 128 + rit;
+        for (int g = 0; g < rtot / 16; ++g) {
+          if (!((touched >> g) & 1u)) continue;
           uint32_t v[16];
-          tmem_ld16(taddr + a * rtot + g * 16, v);
+          tmem_ld16(taddr + b * rtot + g * 16, v);
           tmem_ld_wait();
+          if (kcol < args.k && !(args.segs.debug & 2)) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) s[j] += __uint_as_float(v[j]);
+            for (int j = 0; j < 16; ++j) red_add_f32(args.da + (int64_t)(g * 16 + j) * args.k + kcol, __uint_as_float(v[j]));
+          }
+          tmem_st16(taddr + b * rtot + g * 16, z);
         }
-        if (kcol < args.k) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) red_add_f32(args.da + (int64_t)(g * 16 + j) * args.k + kcol, s[j]);
-        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[b]);
+        ++it;
+        touched = 0;
       }
+      cur = nxt;
     }
   }
 
@@ -489,17 +549,19 @@ __global__ void __launch_bounds__(192, 2)
   }
 }
 
-void grad_down_config(int rtot, int* stages, int* stage_bytes) {
-  *stage_bytes = dga::X_BYTES + (rtot / 16) * 4096;
-  int s = (110 * 1024) / *stage_bytes;
-  *stages = s < 2 ? 2 : (s > 4 ? 4 : s);
+// Two layouts: without TMA'd keep bits, 2 CTAs / SM x ~110 KB rings; with them (2 KB more
+// per stage) 3 stages no longer fit twice, so 1 CTA / SM with a ~200 KB ring.
+void grad_down_config(int rtot, bool bits_tma, int* stages, int* stage_bytes) {
+  *stage_bytes = dga::X_BYTES + (rtot / 16) * 4096 + (bits_tma ? 2048 : 0);
+  int s = (bits_tma ? 196 * 1024 : 110 * 1024) / *stage_bytes;
+  *stages = s < 2 ? 2 : (s > 6 ? 6 : s);
 }
 
-int grad_down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_ds, const GradDownArgs& args, int num_sms,
-                     cudaStream_t stream) {
+int grad_down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_ds, const CUtensorMap& tm_bits,
+                     const GradDownArgs& args, int num_sms, cudaStream_t stream) {
   (void)num_sms;
   int stages = 0, stage_bytes = 0;
-  grad_down_config(args.rtot, &stages, &stage_bytes);
+  grad_down_config(args.rtot, args.bits_tma != 0, &stages, &stage_bytes);
   const int smem = stages * stage_bytes + 1024 + 256;
   static int configured = 0;
   if (configured < smem) {
@@ -508,8 +570,7 @@ int grad_down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_ds, const Gr
       return -1;
     configured = dga::MAX_SMEM + 2048;
   }
-  dim3 grid((args.k + 127) / 128, args.m_split);
-  lf_dgrad_a_kernel<<<grid, 192, smem, stream>>>(tm_x, tm_ds, args, stages, stage_bytes);
+  lf_dgrad_a_kernel<<<args.ctas, kDgaThreads, smem, stream>>>(tm_x, tm_ds, tm_bits, args, stages, stage_bytes);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
