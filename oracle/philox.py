@@ -41,10 +41,13 @@ def philox4x32_10(ctr: np.ndarray, key) -> np.ndarray:
 
 
 def dropout_threshold(p: float) -> int:
-    """Integer threshold of SPEC.md §3: keep iff the 16-bit lane >= floor(p * 65536)."""
+    """Integer threshold of SPEC.md §3: keep iff the 16-bit lane >= 2 * floor(p * 32768).
+
+    The threshold is even (p quantised to 2^-15) so ``u16 >= thr`` equals
+    ``(u16 >> 1) >= thr / 2``, the borrow-free two-lanes-per-word test the kernels use."""
     if not 0.0 <= p < 1.0:
         raise ValueError(f"dropout_p must be in [0, 1), got {p}")
-    return int(np.floor(np.float64(np.float32(p)) * 65536.0))
+    return 2 * int(np.floor(np.float64(np.float32(p)) * 32768.0))
 
 
 def keep_mask_rows(rows: np.ndarray, k: int, p: float, seed: int, offset: int) -> np.ndarray:

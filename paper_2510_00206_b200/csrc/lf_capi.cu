@@ -169,7 +169,7 @@ int validate(const LfProblem* p, bool need_routes, lf::LfSegTable* t) {
     d.col0 = s.col_start;
     d.ncol = s.rank;
     d.scale = (float)((double)s.scaling / (1.0 - (double)s.dropout_p));
-    d.thr = (uint32_t)std::floor((double)s.dropout_p * 65536.0);
+    d.thr = 2u * (uint32_t)std::floor((double)s.dropout_p * 32768.0);  // even: SPEC.md §3
     d.key0 = (uint32_t)(s.seed & 0xFFFFFFFFull);
     d.key1 = (uint32_t)(s.seed >> 32);
     d.off0 = (uint32_t)(s.offset & 0xFFFFFFFFull);

@@ -394,7 +394,8 @@ __device__ __forceinline__ uint32_t philox_keep8(uint32_t col8, uint32_t row, co
 struct PhiloxRow {
   uint32_t k0[10], k1[10];
   uint32_t c1, c2, c3;
-  uint32_t thr2;  // thr in both 16-bit halves
+  uint32_t thr2;   // thr in both 16-bit halves
+  uint32_t hthr2;  // thr / 2 in both 16-bit halves (SWAR keep test)
 };
 
 __device__ __forceinline__ PhiloxRow philox_row(const LfSegDev& s, uint32_t row) {
@@ -411,6 +412,7 @@ __device__ __forceinline__ PhiloxRow philox_row(const LfSegDev& s, uint32_t row)
   pr.c2 = s.off0;
   pr.c3 = s.off1;
   pr.thr2 = s.thr | (s.thr << 16);
+  pr.hthr2 = (s.thr >> 1) * 0x00010001u;
   return pr;
 }
 
@@ -510,6 +512,70 @@ __device__ __forceinline__ uint64_t keep_bits_philox(const PhiloxRow& pr, int co
 }
 __device__ __forceinline__ uint64_t keep_bits64_philox(const PhiloxRow& pr, int col) {
   return keep_bits_philox<8>(pr, col);
+}
+
+// SPEC.md §3 keep test of both 16-bit lanes of a Philox word at once (even threshold, so
+// u16 >= thr <=> (u16 >> 1) >= thr/2): the 15-bit halves biased by 0x8000 never borrow
+// across lanes, and lane j's verdict lands in bit 16j + 15.
+__device__ __forceinline__ uint32_t keep_sign2(uint32_t w, uint32_t hthr2) {
+  return (((w >> 1) & 0x7FFF7FFFu) | 0x80008000u) - hthr2;
+}
+// byte MSBs -> 4 bits (byte j -> bit j)
+__device__ __forceinline__ uint32_t gather_msb4(uint32_t x) { return (((x >> 7) & 0x01010101u) * 0x01020408u) >> 24; }
+
+// ① hot path: the CH Philox streams of keep_bits_philox, but the verdicts become bf16 lane
+// masks (0xFFFF per kept element, word i of chunk j in msk[j][i]) applied with a plain AND,
+// plus the packed keep bits (byte j = chunk j) that ④ and ⑤ read.
+template <int CH>
+__device__ __forceinline__ uint32_t philox_masks(const PhiloxRow& pr, int col, uint32_t (&msk)[CH][4]) {
+  uint32_t c0[CH], c1[CH], c2[CH], c3[CH];
+  const uint32_t base = (uint32_t)col >> 3;
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    c0[j] = base + j;
+    c1[j] = pr.c1;
+    c2[j] = pr.c2;
+    c3[j] = pr.c3;
+  }
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const uint64_t p0 = (uint64_t)0xD2511F53u * c0[j];
+      const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2[j];
+      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1[j] ^ pr.k0[i];
+      const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3[j] ^ pr.k1[i];
+      c1[j] = (uint32_t)p1;
+      c3[j] = (uint32_t)p0;
+      c0[j] = n0;
+      c2[j] = n2;
+    }
+  }
+  uint32_t bits = 0;
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    const uint32_t d0 = keep_sign2(c0[j], pr.hthr2), d1 = keep_sign2(c1[j], pr.hthr2);
+    const uint32_t d2 = keep_sign2(c2[j], pr.hthr2), d3 = keep_sign2(c3[j], pr.hthr2);
+    msk[j][0] = prmt(d0, 0, 0xBB99u);
+    msk[j][1] = prmt(d1, 0, 0xBB99u);
+    msk[j][2] = prmt(d2, 0, 0xBB99u);
+    msk[j][3] = prmt(d3, 0, 0xBB99u);
+    bits |= (gather_msb4(prmt(d0, d1, 0x7531u)) | (gather_msb4(prmt(d2, d3, 0x7531u)) << 4)) << (8 * j);
+  }
+  return bits;
+}
+
+// AND lane masks into chunks [c0, c0 + CH) of one 128-byte SW128 tile row
+template <int CH>
+__device__ __forceinline__ void apply_masks_sw128(uint8_t* tile, int rit, int c0, const uint32_t (&msk)[CH][4]) {
+  const uint32_t rowa = smem_u32(tile) + (uint32_t)rit * 128u;
+  uint4 v[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) v[c] = lds128(rowa + (uint32_t)(((c0 + c) ^ (rit & 7)) << 4));
+#pragma unroll
+  for (int c = 0; c < CH; ++c)
+    sts128(rowa + (uint32_t)(((c0 + c) ^ (rit & 7)) << 4),
+           make_uint4(v[c].x & msk[c][0], v[c].y & msk[c][1], v[c].z & msk[c][2], v[c].w & msk[c][3]));
 }
 
 // zero the dropped bf16 elements of chunks [c0, c0 + CH) of one 128-byte SW128 tile row

@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(kDownThreads, 2)
           // tile is still in flight, so Philox latency overlaps the TMA instead of adding to it
           const int col = kb * 64 + 32 * half;
           uint32_t bits = ~0u;
+          uint32_t msk[4][4];
           if (my_mask) {
             if (explicit_mask) {
               const uint8_t* mrow = args.segs.mask + (int64_t)row * args.segs.ld_mask;
@@ -225,13 +226,17 @@ __global__ void __launch_bounds__(kDownThreads, 2)
 #pragma unroll
               for (int c = 0; c < 4; ++c) bits |= explicit_keep8(mrow, col + 8 * c, args.k) << (8 * c);
             } else {
-              bits = (uint32_t)keep_bits_philox<4>(pr, col);
+              bits = philox_masks<4>(pr, col, msk);
             }
           }
           mbar_wait(&full[stage], phase);
           if (my_mask) {
-            if (!(args.segs.debug & 8) && bits != ~0u)
-              apply_chunks_sw128<4>(smem + stage * STAGE_BYTES, rit, 4 * half, bits);
+            if (!(args.segs.debug & 8) && bits != ~0u) {
+              if (explicit_mask)
+                apply_chunks_sw128<4>(smem + stage * STAGE_BYTES, rit, 4 * half, bits);
+              else
+                apply_masks_sw128<4>(smem + stage * STAGE_BYTES, rit, 4 * half, msk);
+            }
             // Philox runs once per step: ④ and ⑤ read these bits instead
             if (!explicit_mask && bits_row) {
               const int b0 = kb * 8 + 4 * half;

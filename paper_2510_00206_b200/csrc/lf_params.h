@@ -13,7 +13,7 @@ namespace lf {
 
 // Device-side view of one LfSegment (include/lorafusion_b200.h) with the derived
 // quantities precomputed on the host: scale = scaling / (1 - p) as fp32 and the
-// integer dropout threshold thr = floor(p * 65536) (SPEC.md §3).
+// integer dropout threshold thr = 2 * floor(p * 32768), even (SPEC.md §3).
 struct LfSegDev {
   int32_t row0, row1;  // token rows [row0, row1)
   int32_t col0, ncol;  // rank-concat columns [col0, col0 + ncol)
