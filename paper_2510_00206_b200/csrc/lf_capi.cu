@@ -335,6 +335,7 @@ int lf_base_fwd(const LfProblem* p, const uint16_t* x, const uint16_t* w, const 
   a.C = y;
   a.routes = lora ? reinterpret_cast<const lf::LfRoute*>(p->routes) : nullptr;
   a.segs = t;
+  a.group = env_int("LF_GROUP", 0);
   if (lf::gemm_launch(lf::kGemmFwd, maps, a, d.sms, (cudaStream_t)stream)) return cuda_fail("base_fwd launch");
   return LF_OK;
 }
@@ -452,6 +453,7 @@ int lf_grad_input(const LfProblem* p, const uint16_t* dy, const uint16_t* w, con
   a.C = dx;
   a.routes = lora ? reinterpret_cast<const lf::LfRoute*>(p->routes) : nullptr;
   a.segs = t;
+  a.group = env_int("LF_GROUP", 0);
   if (lf::gemm_launch(masked ? lf::kGemmDgradMasked : lf::kGemmDgrad, maps, a, d.sms, (cudaStream_t)stream))
     return cuda_fail("grad_input launch");
   return LF_OK;

@@ -42,9 +42,8 @@ struct GemmCfg {
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 512 * 16;  // + routing cache
 };
 
-// grouped raster: GROUP m-tiles share each n-column sweep so W tiles stay L2-hot
-__device__ __forceinline__ void gemm_tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
-  constexpr int G = 8;
+// grouped raster: G m-tiles share each n-column sweep so W tiles stay L2-hot
+__device__ __forceinline__ void gemm_tile_coords(int t, int tiles_m, int tiles_n, int G, int& mb, int& nb) {
   const int per_group = G * tiles_n;
   const int g = t / per_group;
   const int first_m = g * G;
@@ -70,7 +69,7 @@ __device__ __forceinline__ LfRoute route_at(const GemmArgs& a, const LfRoute* s_
 
 __device__ __forceinline__ TileInfo tile_info(const GemmArgs& a, const LfRoute* s_routes, int t) {
   TileInfo ti;
-  gemm_tile_coords(t, a.tiles_m, a.tiles_n, ti.mb, ti.nb);
+  gemm_tile_coords(t, a.tiles_m, a.tiles_n, a.group, ti.mb, ti.nb);
   ti.col_lo = ti.col_hi = 0;
   if (a.routes && !(a.segs.debug & 2048)) {
     const int tiles128 = (a.M + 127) / 128;
@@ -457,6 +456,7 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
   GemmArgs args = a;
   args.tiles_m = (args.M + 255) / 256;
   args.tiles_n = (args.N + 255) / 256;
+  if (args.group <= 0) args.group = 8;
   switch (kind) {
     case kGemmFwd:
       return launch_one<false, false, 6>(maps, args, num_sms, stream);

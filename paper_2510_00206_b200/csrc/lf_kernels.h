@@ -20,6 +20,7 @@ enum GemmKind { kGemmFwd = 0, kGemmDgrad = 1, kGemmDgradMasked = 2 };
 struct GemmArgs {
   int32_t M, N, K;
   int32_t tiles_m, tiles_n;
+  int32_t group;          // raster: m-tiles sharing each n sweep (set by gemm_launch)
   int64_t ldc;
   void* C;                // bf16 output, row-major M x N (ldc elements)
   const LfRoute* routes;  // nullptr = no LoRA chunk

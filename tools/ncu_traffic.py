@@ -1,0 +1,63 @@
+"""DRAM traffic of the lf_gemm_kernel launches of one bench step, from an ncu capture.
+
+    ncu --set full --clock-control none -k regex:lf_gemm -c 14 -o gpurun_out/gemm_step \\
+        python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline
+    python tools/ncu_traffic.py gpurun_out/gemm_step.ncu-rep > profiles/gemm_traffic.json
+
+The first 14 GEMM launches are one C2 step (② then ⑤ for each of the 7 projections).
+Algorithmic bytes per launch follow SURVEY.md §8(d): ② 2(mk+kn+mr+rn)+2mn, ⑤ 2(mn+kn+mr+kr)+2mk.
+"""
+from __future__ import annotations
+
+import csv
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"]
+
+
+def main():
+    rep = sys.argv[1]
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
+                         capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units = rows[0], rows[1]
+    launches = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        if "lf_gemm" not in d.get("Kernel Name", ""):
+            continue
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        u = dict(zip(hdr, units))
+        rd = float(d["dram__bytes_read.sum"].replace(",", "")) * scale.get(u["dram__bytes_read.sum"], 1)
+        wr = float(d["dram__bytes_write.sum"].replace(",", "")) * scale.get(u["dram__bytes_write.sum"], 1)
+        t = float(d["gpu__time_duration.sum"].replace(",", ""))
+        tu = u["gpu__time_duration.sum"]
+        t_us = {"nsecond": t / 1e3, "ns": t / 1e3, "usecond": t, "us": t, "msecond": t * 1e3, "ms": t * 1e3}[tu]
+        launches.append({"kernel": d["Kernel Name"][:60], "dram_read": rd, "dram_write": wr, "dur_us": t_us})
+    from bench import projections  # noqa: E402  (C2 shapes, bench order)
+    m, r = 8192, 16
+    alg = []  # bench.py runs each projection's forward and backward back to back
+    for name, k, n, _ in projections("c2"):
+        alg.append((name + " base_fwd", 2 * (m * k + k * n + m * r + r * n) + 2 * m * n))
+        alg.append((name + " grad_input", 2 * (m * n + k * n + m * r + k * r) + 2 * m * k))
+    n = min(len(launches), len(alg))
+    dram = sum(l["dram_read"] + l["dram_write"] for l in launches[:n])
+    algb = sum(a for _, a in alg[:n])
+    print(json.dumps({
+        "source": os.path.basename(rep) + " (ncu --set full --clock-control none, one C2 bench step)",
+        "launches": n,
+        "dram_bytes_per_launch": dram / n if n else None,
+        "algorithmic_bytes_per_launch": algb / n if n else None,
+        "dram_over_algorithmic": dram / algb if algb else None,
+        "per_launch": [dict(l, algorithmic=a[1], launcher=a[0]) for l, a in zip(launches[:n], alg[:n])],
+    }, indent=1))
+
+
+if __name__ == "__main__":
+    main()
