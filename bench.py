@@ -17,6 +17,7 @@ oracle/, numpy, all host threads) on a bounded token sample of the same workload
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import subprocess
@@ -33,7 +34,7 @@ HIDDEN_70B, KV_70B, FFN_70B = 8192, 1024, 28672
 
 def projections(config: str):
     """(name, k, n, input group) of each LoRA linear of one decoder layer."""
-    if config in ("c2", "c1"):
+    if config in ("c2", "c1", "c3"):
         h, kv, f = HIDDEN_8B, KV_8B, FFN_8B
     elif config == "c4":
         h, kv, f = HIDDEN_70B, KV_70B, FFN_70B
@@ -46,22 +47,58 @@ def projections(config: str):
 
 
 def tokens_per_gpu(config: str) -> int:
-    return {"c1": 2048, "c2": 8192, "c4": 16384}[config]
+    return {"c1": 2048, "c2": 8192, "c3": 8192, "c4": 16384}[config]
+
+
+# C3 (BASELINE.json configs[2]): FusedMultiLoRA, 4 adapters of ranks
+# 8/16/32/64 (scaling 2.0, p = 0/0.05/0.1/0.1, seeds 1..4) on uneven tile-aligned segments
+C3_RANKS = (8, 16, 32, 64)
+C3_DROPOUT = (0.0, 0.05, 0.1, 0.1)
+C3_LENGTHS = (3584, 2432, 1408, 768)
+
+
+def c3_adapters():
+    from paper_2510_00206_b200 import AdapterConfig
+
+    return [AdapterConfig(rank=r, scaling=2.0, dropout_p=p, seed=i + 1)
+            for i, (r, p) in enumerate(zip(C3_RANKS, C3_DROPOUT))]
+
+
+def c3_segments():
+    from paper_2510_00206_b200 import segments_from_lengths
+
+    return segments_from_lengths(range(len(C3_LENGTHS)), C3_LENGTHS)
+
+
+def c3_flops(m: int) -> float:
+    """4mkn + 6 Σ_seg rows·r·(k+n) over the 7 projections."""
+    return float(sum(4 * m * k * n + sum(6 * L * r * (k + n) for L, r in zip(C3_LENGTHS, C3_RANKS))
+                     for _, k, n, _ in projections("c3")))
 
 
 def step_flops(config: str, m: int, r: int) -> float:
+    if config == "c3":
+        return c3_flops(m)
     return float(sum(4 * m * k * n + 6 * m * r * (k + n) for _, k, n, _ in projections(config)))
 
 
 def gemm_flops(config: str, m: int, r: int) -> dict:
     """Algorithmic FLOPs of the two tcgen05 GEMM launchers per step."""
+    if config == "c3":
+        lr = sum(L * rr for L, rr in zip(C3_LENGTHS, C3_RANKS))
+        fwd = sum(2 * m * k * n + 2 * lr * n for _, k, n, _ in projections(config))
+        dgrad = sum(2 * m * n * k + 2 * lr * k for _, k, n, _ in projections(config))
+        return {"base_fwd": float(fwd), "grad_input": float(dgrad)}
     fwd = sum(2 * m * k * n + 2 * m * r * n for _, k, n, _ in projections(config))
     dgrad = sum(2 * m * n * k + 2 * m * r * k for _, k, n, _ in projections(config))
     return {"base_fwd": float(fwd), "grad_input": float(dgrad)}
 
 
 def lowrank_bytes(config: str, m: int, r: int) -> dict:
-    """Algorithmic HBM bytes of the memory-bound launchers per step."""
+    """Algorithmic HBM bytes of the memory-bound launchers per step (SURVEY.md §8(d));
+    C3: r = the padded rank-concat width the kernels stream (Σ padded ranks = 128)."""
+    if config == "c3":
+        r = 128
     k1 = sum(2 * m * k + 2 * k * r + 2 * m * r for _, k, n, _ in projections(config))
     k3 = sum(2 * (m * n + r * n + m * r) + 2 * m * r + 4 * r * n for _, k, n, _ in projections(config))
     k4 = sum(2 * (m * k + m * r) + 4 * k * r for _, k, n, _ in projections(config))
@@ -216,6 +253,8 @@ def workload_name(config: str) -> str:
         "c2": "LLaMa-3.1-8B layer shapes (q/k/v/o, gate/up/down) FusedLoRA r=16, 8192 tokens, bf16, 1 B200",
         "c1": "single FusedLoRA linear fwd+bwd: tokens=2048, k=n=4096, r=16, dropout=0.1",
         "c4": "LLaMa-3.1-70B layer shapes FusedLoRA r=16, 16384 tokens per GPU",
+        "c3": "FusedMultiLoRA 4 adapters, ranks {8,16,32,64}, uneven token segments {3584,2432,1408,768} "
+              "sharing one frozen W per projection (LLaMa-3.1-8B q/k/v/o/gate/up/down), 8192 tokens",
     }[config]
 
 
@@ -225,13 +264,17 @@ def workload_name(config: str) -> str:
 def build_layers(config: str, m: int, r: int, p: float, device, gen, use_fused: bool = True):
     import torch
 
-    from paper_2510_00206_b200 import FusedLoRA
+    from paper_2510_00206_b200 import FusedLoRA, FusedMultiLoRA
 
     layers, inputs, grads = {}, {}, {}
     for i, (name, k, n, grp) in enumerate(projections(config)):
         w = (torch.randn(n, k, generator=gen, device=device, dtype=torch.float32) / k**0.5).to(torch.bfloat16)
-        layer = FusedLoRA(w, rank=r, scaling=2.0, dropout_p=p, seed=1234 + i, init="gaussian",
-                          generator=gen).to(device)
+        if config == "c3":
+            adapters = [dataclasses.replace(a, seed=a.seed + 100 * i) for a in c3_adapters()]
+            layer = FusedMultiLoRA(w, adapters, init="gaussian", generator=gen).to(device)
+        else:
+            layer = FusedLoRA(w, rank=r, scaling=2.0, dropout_p=p, seed=1234 + i, init="gaussian",
+                              generator=gen).to(device)
         layers[name] = layer
         if grp not in inputs:
             # activations come from the previous layer: they need dX (⑤ runs every step)
@@ -241,19 +284,30 @@ def build_layers(config: str, m: int, r: int, p: float, device, gen, use_fused: 
     return layers, inputs, grads
 
 
+def layer_call(config: str):
+    """How a step calls one layer: FusedLoRA(x), or FusedMultiLoRA(x, segments) for C3."""
+    if config == "c3":
+        segs = c3_segments()
+        return lambda layer, x: layer(x, segs)
+    return lambda layer, x: layer(x)
+
+
+def adapter_params(layers):
+    return [p for nm in layers for p in layers[nm].parameters() if p.requires_grad]
+
+
 def fused_step(config, layers, inputs, grads, world, flat_grad=None):
     """fwd+bwd of every projection through the public module API; grads all-reduced if world>1."""
     import torch
 
+    call = layer_call(config)
     for name, k, n, grp in projections(config):
-        layer = layers[name]
-        x = inputs[grp]
-        y = layer(x)
+        y = call(layers[name], inputs[grp])
         y.backward(grads[name])
     if world > 1:
         import torch.distributed as dist
 
-        params = [p for nm in layers for p in (layers[nm].lora_A.weight, layers[nm].lora_B.weight)]
+        params = adapter_params(layers)
         flat = torch.cat([p.grad.reshape(-1) for p in params])
         dist.all_reduce(flat)
         off = 0
@@ -264,23 +318,41 @@ def fused_step(config, layers, inputs, grads, world, flat_grad=None):
 
 
 def zero_grads(layers, inputs=None):
-    for layer in layers.values():
-        layer.lora_A.weight.grad = None
-        layer.lora_B.weight.grad = None
+    for p in adapter_params(layers):
+        p.grad = None
     for t in (inputs or {}).values():
         t.grad = None
 
 
+def unfused_base(config, layers):
+    """bf16 copies of the adapter weights for the unfused torch arm: name -> (W, [A], [B])."""
+    import torch
+
+    base = {}
+    for name, k, n, grp in projections(config):
+        layer = layers[name]
+        la = layer.lora_A if config == "c3" else [layer.lora_A]
+        lb = layer.lora_B if config == "c3" else [layer.lora_B]
+        a = [m_.weight.detach().to(torch.bfloat16).clone().requires_grad_(True) for m_ in la]
+        b = [m_.weight.detach().to(torch.bfloat16).clone().requires_grad_(True) for m_ in lb]
+        base[name] = (layer.base_weight, a, b)
+    return base
+
+
 def unfused_step(config, base, inputs, grads, p):
-    """PEFT-style torch LoRA: cuBLAS F.linear + F.dropout + add/scale, autograd, W frozen."""
-    from paper_2510_00206_b200 import unfused_lora
+    """PEFT-style torch LoRA: cuBLAS F.linear + F.dropout + add/scale, autograd, W frozen
+    (C3: the per-segment multi-adapter loop)."""
+    from paper_2510_00206_b200 import unfused_lora, unfused_multi_lora
 
     for name, k, n, grp in projections(config):
         w, a, b = base[name]
-        y = unfused_lora(inputs[grp], w, a, b, 2.0, p, training=True)
+        if config == "c3":
+            y = unfused_multi_lora(inputs[grp], w, a, b, c3_adapters(), c3_segments(), training=True)
+        else:
+            y = unfused_lora(inputs[grp], w, a[0], b[0], 2.0, p, training=True)
         y.backward(grads[name])
-        a.grad = None
-        b.grad = None
+        for t in a + b:
+            t.grad = None
 
 
 def time_loop(fn, steps, warmup, sync_barrier):
@@ -396,15 +468,15 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     }
 
     # ---- unfused torch baseline (same box, same shapes) -------------------------------
-    base = {}
-    for name, k, n, grp in projections(args.config):
-        layer = layers[name]
-        a = layer.lora_A.weight.detach().to(torch.bfloat16).clone().requires_grad_(True)
-        b = layer.lora_B.weight.detach().to(torch.bfloat16).clone().requires_grad_(True)
-        base[name] = (layer.base_weight, a, b)
+    base = unfused_base(args.config, layers)
     unf_ms = time_loop(lambda: unfused_step(args.config, base, inputs, grads, p), max(2, args.steps // 2),
                        args.warmup, barrier)
     unf_ms = max_over_ranks(unf_ms)
+
+    # ---- secondary: C3 FusedMultiLoRA (BASELINE.json configs[2]) on the same box ------
+    multi = None
+    if args.config == "c2" and not args.no_multi:
+        multi = measure_c3(args, device, gen, world, barrier, max_over_ranks)
 
     # ---- end to end through the public API: pinned host inputs -> H2D, D2H of grads ---
     e2e = None
@@ -432,9 +504,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                 "projections": [[nm, k, n] for nm, k, n, _ in projections(args.config)],
                 "tokens_per_gpu": m,
                 "global_tokens": m * world,
-                "rank": r,
+                "rank": list(C3_RANKS) if args.config == "c3" else r,
                 "scaling": 2.0,
-                "dropout_p": p,
+                "dropout_p": list(C3_DROPOUT) if args.config == "c3" else p,
                 "parallelism": f"dp{world}",
                 "l2": "inputs larger than L2 (≈2 GB touched per step vs 126 MB L2)",
             },
@@ -449,6 +521,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         }
         if e2e is not None:
             line["e2e"] = e2e
+        if multi is not None:
+            line["multi_lora"] = multi
         if not args.no_cpu_baseline:
             cores = len(os.sched_getaffinity(0))
             ts = cpu_reference_step(args.config, args.cpu_sample_tokens, r, p)
@@ -457,6 +531,30 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                 "sample": f"{args.cpu_sample_tokens} tokens of each projection, fwd+bwd, numpy float64 oracle",
             }
         print(json.dumps(line), flush=True)
+
+
+def measure_c3(args, device, gen, world, barrier, max_over_ranks):
+    """C3 on the same box: 7 FusedMultiLoRA projections (4 adapters each) vs the unfused
+    per-segment torch loop, device-resident inputs, same timing rules as the headline."""
+    import torch
+
+    m = tokens_per_gpu("c3")
+    layers, inputs, grads = build_layers("c3", m, 0, 0.0, device, gen)
+
+    def step():
+        zero_grads(layers, inputs)
+        fused_step("c3", layers, inputs, grads, world)
+
+    ms = max_over_ranks(time_loop(step, args.steps, args.warmup, barrier))
+    base = unfused_base("c3", layers)
+    unf = max_over_ranks(time_loop(lambda: unfused_step("c3", base, inputs, grads, 0.0), max(2, args.steps // 2),
+                                   args.warmup, barrier))
+    del layers, inputs, grads, base
+    torch.cuda.empty_cache()
+    return {"workload": workload_name("c3"), "ranks": list(C3_RANKS), "dropout_p": list(C3_DROPOUT),
+            "segments": list(C3_LENGTHS), "ms_per_step": ms, "tokens_per_s": world * m / (ms * 1e-3),
+            "tflops": world * c3_flops(m) / (ms * 1e-3) / 1e12,
+            "unfused_torch": {"ms_per_step": unf, "tokens_per_s": world * m / (unf * 1e-3), "speedup": unf / ms}}
 
 
 def run_e2e(args, layers, inputs, grads, device, world, barrier, max_over_ranks):
@@ -468,7 +566,8 @@ def run_e2e(args, layers, inputs, grads, device, world, barrier, max_over_ranks)
     host_dy = {nm: t.cpu().pin_memory() for nm, t in grads.items()}
     dev_in = {g: torch.empty_like(t) for g, t in inputs.items()}
     dev_dy = {nm: torch.empty_like(t) for nm, t in grads.items()}
-    params = [p for nm in layers for p in (layers[nm].lora_A.weight, layers[nm].lora_B.weight)]
+    params = adapter_params(layers)
+    call = layer_call(args.config)
     host_out = torch.empty(sum(p.numel() for p in params), dtype=torch.float32).pin_memory()
     copy = torch.cuda.Stream(device)
     order = projections(args.config)
@@ -497,7 +596,7 @@ def run_e2e(args, layers, inputs, grads, device, world, barrier, max_over_ranks)
             cur.wait_event(ready[name])
             if grp not in leaves:  # activation leaf: dX is computed as in a real layer
                 leaves[grp] = dev_in[grp].detach().requires_grad_(True)
-            y = layers[name](leaves[grp])
+            y = call(layers[name], leaves[grp])
             y.backward(dev_dy[name])
         if world > 1:
             import torch.distributed as dist
@@ -515,7 +614,8 @@ def run_e2e(args, layers, inputs, grads, device, world, barrier, max_over_ranks)
     m = tokens_per_gpu(args.config)
     return {"value": world * m / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "path": "FusedLoRA modules (public API), pinned host inputs H2D on a copy stream, fp32 grads D2H"}
+            "path": ("FusedMultiLoRA" if args.config == "c3" else "FusedLoRA") +
+                    " modules (public API), pinned host inputs H2D on a copy stream, fp32 grads D2H"}
 
 
 def main() -> None:
@@ -523,7 +623,8 @@ def main() -> None:
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--no-multi", action="store_true", help="skip the secondary C3 FusedMultiLoRA measurement")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dropout", type=float, default=0.1)
     ap.add_argument("--cpu-sample-tokens", type=int, default=256)

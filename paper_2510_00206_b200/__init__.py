@@ -7,6 +7,7 @@ Public API
   dropout_keep_mask                  SPEC.md §3 mask the kernels regenerate
   traffic, GemmShape, ...            DRAM-traffic model mirroring lorasched.costmodel
   unfused_lora                       the PEFT-style torch baseline (cuBLAS + elementwise)
+  unfused_multi_lora                 its per-segment multi-adapter form
 
 The compute path is the sm_100a shared library liblorafusion_b200.so (C ABI in
 include/lorafusion_b200.h). There is no CPU fallback.
@@ -29,7 +30,7 @@ from .costmodel import (
     roundtrip_bytes,
     traffic,
 )
-from .baseline import unfused_lora
+from .baseline import unfused_lora, unfused_multi_lora
 
 __all__ = [
     "AdapterConfig",
@@ -59,4 +60,5 @@ __all__ = [
     "segments_from_lengths",
     "traffic",
     "unfused_lora",
+    "unfused_multi_lora",
 ]

@@ -141,6 +141,10 @@ __global__ void __launch_bounds__(kDownThreads, 2)
 
   UnitWalker walk(units, (int)gridDim.x, (int)blockIdx.x, nkb);
   UnitSpan sp;
+  // With any dropout in the problem EVERY stage passes through the mask warps (full ->
+  // masked), whatever its tile needs: a CTA's span may mix p = 0 and p > 0 tiles, and a
+  // per-stage choice of barrier would desynchronise `masked`'s phase from the ring's.
+  const bool gated = args.segs.mask_mode != 0;
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
@@ -169,14 +173,13 @@ __global__ void __launch_bounds__(kDownThreads, 2)
       const LfRoute rt = args.routes[sp.tile];
       const int N = rt.col_hi - rt.col_lo;
       if (N <= 0) continue;
-      const bool need_mask = tile_needs_mask(args.segs, rt);
       const int b = it & 1;
       mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d = tmem + b * args.rtot;
       const uint32_t idesc = make_idesc_bf16(128, (uint32_t)N, false, false);
       for (int kb = sp.k0; kb < sp.k1; ++kb) {
-        mbar_wait(need_mask ? &masked[stage] : &full[stage], phase);
+        mbar_wait(gated ? &masked[stage] : &full[stage], phase);
         tc_fence_after();
         const uint32_t sX = smem_u32(smem + stage * STAGE_BYTES);
         const uint64_t ax = make_sdesc(sX, 16, 1024, kLayoutSW128);
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(kDownThreads, 2)
       const int N = rt.col_hi - rt.col_lo;
       if (N <= 0) continue;
       const int row = sp.tile * 128 + rit;
-      if (tile_needs_mask(args.segs, rt)) {
+      if (gated) {
         const int seg = row < args.m ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
         const bool my_mask = seg >= 0 && (explicit_mask || args.segs.seg[seg].thr != 0);
         const PhiloxRow pr = philox_row(args.segs.seg[seg >= 0 ? seg : 0], (uint32_t)row);
@@ -254,8 +257,8 @@ __global__ void __launch_bounds__(kDownThreads, 2)
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       } else {
-        // unmasked span: the MMA consumes the stages straight from `full`; keep the ring
-        // position in step with it
+        // no dropout anywhere: the MMA consumes the stages straight from `full`; keep the
+        // ring position in step with it
         for (int kb = sp.k0; kb < sp.k1; ++kb)
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
@@ -379,6 +382,8 @@ __global__ void __launch_bounds__(kDgaThreads, 2)
   while ((int)tmem_cols < 2 * rtot) tmem_cols <<= 1;
   // profiling bit 64: stages bypass the mask warps (results invalid)
   auto needs_mask = [&](const LfRoute& rt) { return !(args.segs.debug & 64) && tile_needs_mask(args.segs, rt); };
+  // every stage passes through the mask warps when the problem has any dropout (see ①)
+  const bool gated = args.segs.mask_mode != 0 && !(args.segs.debug & 64);
   auto live = [&](int u) {  // next unit at or after u whose row tile carries adapters
     while (u < u1 && args.routes[u % tiles_m].col_hi <= args.routes[u % tiles_m].col_lo) ++u;
     return u;
@@ -445,8 +450,7 @@ __global__ void __launch_bounds__(kDgaThreads, 2)
       }
       const LfRoute rt = args.routes[mt];
       const int N = rt.col_hi - rt.col_lo;
-      const bool need_mask = needs_mask(rt);
-      mbar_wait(need_mask ? &masked[stage] : &full[stage], phase);
+      mbar_wait(gated ? &masked[stage] : &full[stage], phase);
       tc_fence_after();
       const uint32_t sX = smem_u32(smem + stage * stage_bytes);
       const uint64_t ax = make_sdesc(sX, 16384, 1024, kLayoutSW128);
@@ -492,7 +496,7 @@ __global__ void __launch_bounds__(kDgaThreads, 2)
       const int mt = cur % tiles_m, kt = cur / tiles_m;
       const LfRoute rt = args.routes[mt];
       for (int c = rt.col_lo; c < rt.col_hi; c += 16) touched |= 1u << (c >> 4);
-      if (needs_mask(rt)) {
+      if (gated) {
         const int row = mt * 128 + rit;
         const int seg = row < args.m ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
         const bool mine = seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0);

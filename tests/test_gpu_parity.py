@@ -45,6 +45,9 @@ CASES = {
                                   (0.1, 0.0, 0.1, 0.2), (5, 6, 7, 8)),
     "rows_without_adapter": H.Case(640, 256, 256, (16, 16), (100, 300), (2.0, 2.0), (0.1, 0.0), (9, 10)),
     "c1": H.Case(2048, 4096, 4096, (16,), (2048,), (2.0,), (0.1,), (1234,)),
+    # stream-K CTAs of ① / ④ wrap their stage rings while crossing from a p = 0 segment into
+    # a p > 0 one (the masked-barrier protocol must not depend on the tile)
+    "mixed_p_wrap": H.Case(4096, 4096, 128, (16, 32), (1920, 2176), (2.0, 1.0), (0.0, 0.1), (31, 32)),
 }
 
 
@@ -261,6 +264,44 @@ def test_full_size_llama8b_shapes_vs_fp32_torch(shape):
     assert rel(a.grad, dar) < 4e-3
     assert rel(b.grad, dbr) < 4e-3
     assert abs(keep.float().mean().item() - 0.9) < 2e-3
+
+
+def test_full_size_c3_multi_lora_vs_fp32_torch():
+    """BASELINE C3: 4 adapters (r 8/16/32/64 -> R = 128, p 0/0.05/0.1/0.1) on uneven segments
+    of an 8192-token microbatch at k = n = 4096, against a torch fp32 restatement of Eq. 1 per
+    segment on the kernels' own (oracle-pinned) keep mask."""
+    from paper_2510_00206_b200 import AdapterConfig, dropout_keep_mask, fused_multi_lora, segments_from_lengths
+
+    m, k, n = 8192, 4096, 4096
+    ads = [AdapterConfig(r, 2.0, p_, i + 1) for i, (r, p_) in enumerate(zip((8, 16, 32, 64), (0.0, 0.05, 0.1, 0.1)))]
+    segs = segments_from_lengths([0, 1, 2, 3], [3584, 2432, 1408, 768])
+    g = torch.Generator(device=DEV).manual_seed(5)
+    x = torch.randn(m, k, device=DEV, generator=g).to(torch.bfloat16).requires_grad_(True)
+    w = (torch.randn(n, k, device=DEV, generator=g) / k**0.5).to(torch.bfloat16)
+    a = [((torch.rand(c.rank, k, device=DEV, generator=g) * 2 - 1) / k**0.5).requires_grad_(True) for c in ads]
+    b = [(torch.randn(n, c.rank, device=DEV, generator=g) / 4).requires_grad_(True) for c in ads]
+    dy = torch.randn(m, n, device=DEV, generator=g).to(torch.bfloat16)
+    y = fused_multi_lora(x, w, a, b, ads, segs, offset=2)
+    y.backward(dy)
+    keep = dropout_keep_mask(m, k, ads, segs, offset=2, device=DEV).float()
+    xf, dyf, wf = x.detach().float(), dy.float(), w.float()
+    yr = xf @ wf.T
+    dxr = dyf @ wf
+    rel = lambda g_, r_: float((g_ - r_).norm() / r_.norm())
+    for sg in segs:
+        c = ads[sg.adapter]
+        rows = slice(sg.row_start, sg.row_end)
+        sc = c.scaling / (1.0 - c.dropout_p)
+        ab, bb = a[sg.adapter].detach().bfloat16().float(), b[sg.adapter].detach().bfloat16().float()
+        xm = xf[rows] * keep[rows]
+        s_ = ((xm @ ab.T) * sc).bfloat16().float()
+        yr[rows] += s_ @ bb.T
+        ds = ((dyf[rows] @ bb) * sc).bfloat16().float()
+        dxr[rows] += keep[rows] * (ds @ ab)
+        assert rel(a[sg.adapter].grad, ds.T @ xm) < 4e-3, f"dA{sg.adapter}"
+        assert rel(b[sg.adapter].grad, dyf[rows].T @ s_) < 4e-3, f"dB{sg.adapter}"
+    assert rel(y.detach().float(), yr) < 4e-3
+    assert rel(x.grad.float(), dxr) < 4e-3
 
 
 def test_errors_are_loud_and_typed():
