@@ -119,6 +119,10 @@ LF_API int lf_grad_input(const LfProblem* p, const uint16_t* dy, const uint16_t*
 /* Materialise the keep mask (m x k uint8) of SPEC.md §3 — for explicit-mask callers and parity tests. */
 LF_API int lf_dropout_mask(const LfProblem* p, uint8_t* keep_out, void* stream);
 
+/* Packed keep bits of the same mask (m x k/8 bytes, 16-byte aligned; bit c of byte j of a
+ * row = column 8j + c). Input-free, so callers may run it on a side stream ahead of ①. */
+LF_API int lf_keep_bits(const LfProblem* p, uint8_t* bits_out, void* stream);
+
 /* Thread-local message describing the last failure (never NULL). */
 LF_API const char* lf_last_error(void);
 

@@ -36,6 +36,7 @@ EXPORTED_SYMBOLS = (
     "lf_grad_down",
     "lf_grad_input",
     "lf_dropout_mask",
+    "lf_keep_bits",
     "lf_last_error",
     "lf_abi_version",
 )
@@ -82,6 +83,7 @@ _SIGNATURES = {
     "lf_grad_down": (ctypes.c_int, [_P, _V, _V, _V, _V]),
     "lf_grad_input": (ctypes.c_int, [_P, _V, _V, _V, _V, _V, _V]),
     "lf_dropout_mask": (ctypes.c_int, [_P, _V, _V]),
+    "lf_keep_bits": (ctypes.c_int, [_P, _V, _V]),
     "lf_last_error": (ctypes.c_char_p, []),
     "lf_abi_version": (ctypes.c_int, []),
 }

@@ -260,6 +260,17 @@ int lf_dropout_mask(const LfProblem* p, uint8_t* keep_out, void* stream) {
   return LF_OK;
 }
 
+int lf_keep_bits(const LfProblem* p, uint8_t* bits_out, void* stream) {
+  lf::LfSegTable t;
+  LF_TRY(validate(p, false, &t));
+  LF_TRY(check_ptr(bits_out, "bits_out"));
+  Dev d;
+  LF_TRY(current_device(&d));
+  if (lf::keep_bits_launch(t, p->k, bits_out, p->k / 8, d.sms, (cudaStream_t)stream))
+    return cuda_fail("keep_bits launch");
+  return LF_OK;
+}
+
 int lf_dropout_down_fwd(const LfProblem* p, const uint16_t* x, const uint16_t* a_cat, uint16_t* s_hat,
                         void* stream) {
   lf::LfSegTable t;

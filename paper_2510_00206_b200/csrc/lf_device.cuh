@@ -80,6 +80,21 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t addr, uint32_t parity
       : "memory");
   return ok;
 }
+// try_wait with a suspend-time hint: a thread whose phase is still open sleeps in the
+// barrier unit until the phase completes (or the hint, in ns, runs out) instead of
+// re-issuing try_wait — spinning waiters otherwise steal issue slots from the ALU-bound
+// mask warps sharing their scheduler.
+__device__ __forceinline__ uint32_t mbar_try_wait_sleep(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(0x100000u)
+      : "memory");
+  return ok;
+}
 // Wait for the phase with the given parity to complete. A wait that has not
 // completed after ~4e9 SM cycles traps instead of hanging the device: a protocol
 // bug becomes a launch failure the host reports, never a wedged GPU.
@@ -87,11 +102,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   if (mbar_try_wait(addr, parity)) return;
   const long long t0 = clock64();
-  uint32_t spins = 0;
-  while (!mbar_try_wait(addr, parity)) {
-    if ((++spins & 1023u) == 0 && clock64() - t0 > 4000000000LL) {
-      __trap();
-    }
+  while (!mbar_try_wait_sleep(addr, parity)) {
+    if (clock64() - t0 > 4000000000LL) __trap();
   }
 }
 
@@ -527,7 +539,7 @@ __device__ __forceinline__ uint32_t gather_msb4(uint32_t x) { return (((x >> 7) 
 // masks (0xFFFF per kept element, word i of chunk j in msk[j][i]) applied with a plain AND,
 // plus the packed keep bits (byte j = chunk j) that ④ and ⑤ read.
 template <int CH>
-__device__ __forceinline__ uint32_t philox_masks(const PhiloxRow& pr, int col, uint32_t (&msk)[CH][4]) {
+__device__ __forceinline__ uint64_t philox_masks(const PhiloxRow& pr, int col, uint32_t (&msk)[CH][4]) {
   uint32_t c0[CH], c1[CH], c2[CH], c3[CH];
   const uint32_t base = (uint32_t)col >> 3;
 #pragma unroll
@@ -551,7 +563,7 @@ __device__ __forceinline__ uint32_t philox_masks(const PhiloxRow& pr, int col, u
       c2[j] = n2;
     }
   }
-  uint32_t bits = 0;
+  uint64_t bits = 0;
 #pragma unroll
   for (int j = 0; j < CH; ++j) {
     const uint32_t d0 = keep_sign2(c0[j], pr.hthr2), d1 = keep_sign2(c1[j], pr.hthr2);
@@ -560,7 +572,7 @@ __device__ __forceinline__ uint32_t philox_masks(const PhiloxRow& pr, int col, u
     msk[j][1] = prmt(d1, 0, 0xBB99u);
     msk[j][2] = prmt(d2, 0, 0xBB99u);
     msk[j][3] = prmt(d3, 0, 0xBB99u);
-    bits |= (gather_msb4(prmt(d0, d1, 0x7531u)) | (gather_msb4(prmt(d2, d3, 0x7531u)) << 4)) << (8 * j);
+    bits |= (uint64_t)(gather_msb4(prmt(d0, d1, 0x7531u)) | (gather_msb4(prmt(d2, d3, 0x7531u)) << 4)) << (8 * j);
   }
   return bits;
 }

@@ -82,5 +82,6 @@ int finalize_launch(const LfSegTable& segs, const LfRoute* routes, float* ws, vo
 // routing table + explicit mask materialisation
 int routes_launch(const LfSegTable& segs, int32_t* routes, int ntiles, cudaStream_t stream);
 int mask_launch(const LfSegTable& segs, int32_t k, uint8_t* keep, cudaStream_t stream);
+int keep_bits_launch(const LfSegTable& segs, int32_t k, uint8_t* bits, int64_t ld, int num_sms, cudaStream_t stream);
 
 }  // namespace lf

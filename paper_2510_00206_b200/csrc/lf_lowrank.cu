@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kDownThreads, 2)
 #pragma unroll
               for (int c = 0; c < 4; ++c) bits |= explicit_keep8(mrow, col + 8 * c, args.k) << (8 * c);
             } else {
-              bits = philox_masks<4>(pr, col, msk);
+              bits = (uint32_t)philox_masks<4>(pr, col, msk);
             }
           }
           mbar_wait(&full[stage], phase);
@@ -623,6 +623,42 @@ __global__ void lf_mask_kernel(const __grid_constant__ LfSegTable segs, int32_t 
   uint8_t* out = keep + (int64_t)row * k + g * 8;
   for (int e = 0; e < 8; ++e)
     if (g * 8 + e < k) out[e] = (uint8_t)((bits >> e) & 1u);
+}
+
+// Packed keep bits (SPEC.md §3; bit c of byte j = column 8j + c) of the whole m x k mask,
+// one thread per (row, 64-column group). Input-free: it depends only on (seed, offset, row,
+// column). Rows outside every dropout segment keep everything.
+__global__ void __launch_bounds__(256) lf_keep_bits_kernel(const __grid_constant__ LfSegTable segs, int32_t k,
+                                                           uint8_t* bits, int64_t ld) {
+  const int groups = (k + 63) / 64;
+  const int64_t total = (int64_t)segs.m * groups;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / groups);
+    const int g = (int)(idx - (int64_t)row * groups);
+    const int seg = find_segment(segs, 0, segs.nseg - 1, row);
+    uint64_t b = ~0ull;
+    if (seg >= 0 && segs.seg[seg].thr) {
+      uint32_t msk[8][4];
+      b = philox_masks<8>(philox_row(segs.seg[seg], (uint32_t)row), g * 64, msk);
+    }
+    uint8_t* out = bits + (int64_t)row * ld + g * 8;
+    const int nbytes = min(8, (k - g * 64 + 7) / 8);
+    if (nbytes == 8 && ((reinterpret_cast<uintptr_t>(out) & 7u) == 0)) {
+      *reinterpret_cast<uint64_t*>(out) = b;
+    } else {
+      for (int i = 0; i < nbytes; ++i) out[i] = (uint8_t)(b >> (8 * i));
+    }
+  }
+}
+
+int keep_bits_launch(const LfSegTable& segs, int32_t k, uint8_t* bits, int64_t ld, int num_sms, cudaStream_t stream) {
+  const int64_t total = (int64_t)segs.m * ((k + 63) / 64);
+  if (total <= 0) return 0;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 4LL * num_sms) blocks = 4LL * num_sms;
+  lf_keep_bits_kernel<<<(unsigned)blocks, 256, 0, stream>>>(segs, k, bits, ld);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 int routes_launch(const LfSegTable& segs, int32_t* routes, int ntiles, cudaStream_t stream) {

@@ -77,6 +77,23 @@ def test_dropout_mask_bit_exact(name):
     assert np.array_equal(keep.cpu().numpy(), H.oracle_keep(case, segs))
 
 
+@pytest.mark.parametrize("name", ["multi4_straddle_p64", "single_r8_odd", "c1"])
+def test_keep_bits_generator_matches_oracle(name):
+    """lf_keep_bits (the input-free packed-mask generator) == packbits(oracle keep mask) on
+    every dropout row."""
+    case = CASES[name]
+    L = _lib()
+    p, routes, ws, R = H.make_problem(case, torch.device(DEV))
+    bits = torch.full((case.m, case.k // 8), 0x5A, dtype=torch.uint8, device=DEV)
+    L.check(L.load().lf_keep_bits(ctypes.byref(p), ctypes.c_void_p(bits.data_ptr()), None), "keep_bits")
+    segs, _ = H.oracle_segments(case)
+    keep = H.oracle_keep(case, segs)
+    got = np.unpackbits(bits.cpu().numpy(), axis=1, bitorder="little")[:, :case.k]
+    for s in segs:
+        rows = slice(s.row_start, s.row_end)
+        assert np.array_equal(got[rows], keep[rows]), s
+
+
 def test_packed_bits_written_by_forward_match_oracle():
     case = CASES["multi4_straddle_p64"]
     x, w, dy, a_list, b_list = H.make_inputs(case)

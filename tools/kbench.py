@@ -74,6 +74,27 @@ def main():
         "grad_input": (lambda i: lib.lf_grad_input(pp, P(DY[i]), P(W), P(DS), P(A), P(DX), st),
                        "tflops", 2 * m * n * k + 2 * m * R * k),
     }
+    BITS2 = torch.empty((m, k // 8), dtype=torch.uint8, device=dev)
+    launches["keep_bits"] = (lambda i: lib.lf_keep_bits(pp, P(BITS2), st), "gbs", m * k // 8)
+    side = torch.cuda.Stream(dev)
+    s2 = ctypes.c_void_p(side.cuda_stream)
+    fork, join = torch.cuda.Event(), torch.cuda.Event()
+
+    def gemm_with_bits(i, gemm):
+        """the input-free keep-bits generator on a side stream underneath a GEMM"""
+        main = torch.cuda.current_stream()
+        fork.record(main)
+        side.wait_event(fork)
+        rc = lib.lf_keep_bits(pp, P(BITS2), s2)
+        rc = rc or gemm(i)
+        join.record(side)
+        main.wait_event(join)
+        return rc
+
+    launches["overlap_fwd_bits"] = (lambda i: gemm_with_bits(i, launches["base_fwd"][0]), "tflops",
+                                    2 * m * k * n + 2 * m * R * n)
+    launches["overlap_dgrad_bits"] = (lambda i: gemm_with_bits(i, launches["grad_input"][0]), "tflops",
+                                      2 * m * n * k + 2 * m * R * k)
     OUT = torch.empty_like(X[0])
     launches["torch_copy_x"] = (lambda i: (OUT.copy_(X[i]), 0)[1], "gbs", 4 * m * k)
     launches["torch_sum_x"] = (lambda i: (X[i].sum(dtype=torch.float32), 0)[1], "gbs", 2 * m * k)
