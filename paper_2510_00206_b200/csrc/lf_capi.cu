@@ -18,6 +18,16 @@
 #include "lf_kernels.h"
 #include "lorafusion_b200.h"
 
+namespace lf {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("LF_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+}  // namespace lf
+
 namespace {
 
 thread_local std::string g_err = "no error";

@@ -48,6 +48,14 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
 __device__ __forceinline__ uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// Programmatic dependent launch (all lf kernels are launched with programmatic stream
+// serialization, lf_kernels.h launch_k): a kernel may start while its predecessor in the
+// stream drains, runs its prologue (mbarrier init, TMEM alloc, tensor-map prefetch), and
+// must pass pdl_wait() — full completion and memory visibility of the predecessor — before
+// its first global-memory access, read or write. No-ops without the launch attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // named barrier among a subset of warps (ids 1..15; 0 is __syncthreads)
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -650,6 +658,65 @@ __device__ __forceinline__ int find_segment(const LfSegTable& t, int lo, int hi,
     if (row >= t.seg[i].row0 && row < t.seg[i].row1) return i;
   }
   return -1;
+}
+
+// finalize one row of a split-K reduced m x R result: scale own-segment columns, zero the
+// rest, write bf16, and return the partial-sum workspace to zero.
+__device__ __forceinline__ void finalize_row(const LfSegTable& t, const LfRoute& rt, int row, float* ws,
+                                             __nv_bfloat16* out) {
+  const int rtot = t.rtot;
+  const int seg = find_segment(t, rt.seg_lo, rt.seg_hi, row);
+  const int own0 = seg >= 0 ? t.seg[seg].col0 : 0;
+  const int own1 = seg >= 0 ? t.seg[seg].col0 + t.seg[seg].ncol : 0;
+  const float scale = seg >= 0 ? t.seg[seg].scale : 0.f;
+  float* wrow = ws + (int64_t)row * rtot;
+  __nv_bfloat16* orow = out + (int64_t)row * rtot;
+  for (int c = 0; c < rtot; c += 8) {
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const bool in_range = c >= rt.col_lo && c < rt.col_hi;
+    if (in_range) {
+      const float4 a = ld_cg_f4(wrow + c), b = ld_cg_f4(wrow + c + 4);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+      *reinterpret_cast<float4*>(wrow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(wrow + c + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const bool own = c >= own0 && c < own1;
+    const float s = own ? scale : 0.f;
+    *reinterpret_cast<uint4*>(orow + c) = make_uint4(pack_bf16x2(v[0] * s, v[1] * s), pack_bf16x2(v[2] * s, v[3] * s),
+                                                     pack_bf16x2(v[4] * s, v[5] * s), pack_bf16x2(v[6] * s, v[7] * s));
+  }
+}
+
+// zero one row of an m x R bf16 result (row tiles no adapter touches)
+__device__ __forceinline__ void zero_row(int rtot, int row, __nv_bfloat16* out) {
+  __nv_bfloat16* orow = out + (int64_t)row * rtot;
+  for (int c = 0; c < rtot; c += 8) *reinterpret_cast<uint4*>(orow + c) = make_uint4(0u, 0u, 0u, 0u);
+}
+
+// Split-K completion of one 128-row tile, run by 128 epilogue threads (one row each, named
+// barrier `bar_id`) after their red.adds of this tile's partial: the partial counts `units`
+// towards `total`, and the CTA that completes the tile finalizes it (finalize_row) and
+// re-arms the counter — no separate finalize launch. Ordering: the first barrier puts every
+// thread's red.adds before thread 0's acq_rel atomic (release is cumulative over what the
+// barrier ordered before it); the second puts the atomic's acquire before all the reads.
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int32_t* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void tile_contribute(const LfSegTable& segs, const LfRoute& rt, int tile, int rit,
+                                                int units, int total, int32_t* counters, float* ws,
+                                                __nv_bfloat16* out, uint32_t bar_id, int* s_last) {
+  named_bar_sync(bar_id, 128);
+  if (rit == 0) *s_last = atom_add_acq_rel_gpu(&counters[tile], units) + units == total;
+  named_bar_sync(bar_id, 128);
+  const bool last = *s_last != 0;
+  named_bar_sync(bar_id, 128);  // s_last is reused by the next call
+  if (!last) return;
+  const int row = tile * 128 + rit;
+  if (row < segs.m && !(segs.debug & 16)) finalize_row(segs, rt, row, ws, out);
+  if (rit == 0) counters[tile] = 0;
 }
 
 }  // namespace lf

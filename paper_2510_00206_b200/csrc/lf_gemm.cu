@@ -139,10 +139,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   uint64_t* lmasked = lfull + 2;     // [2] leader: both CTAs masked their partial (8)   MASKED
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lmasked + 2);
   LfRoute* s_routes = reinterpret_cast<LfRoute*>(smem + STAGES * Cfg::STAGE_BYTES + 256);  // [kSmemRoutes]
-  if (args.routes) {
-    const int nr = min((args.M + 127) / 128, kSmemRoutes);
-    for (int i = (int)threadIdx.x; i < nr; i += (int)blockDim.x) s_routes[i] = args.routes[i];
-  }
+  pdl_launch_dependents();
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -169,6 +166,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     }
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);
+  // everything above overlaps the predecessor's tail (PDL); global memory only from here
+  pdl_wait();
+  if (args.routes) {
+    const int nr = min((args.M + 127) / 128, kSmemRoutes);
+    for (int i = (int)threadIdx.x; i < nr; i += (int)blockDim.x) s_routes[i] = args.routes[i];
+  }
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -448,7 +451,8 @@ static int launch_one(const GemmMaps& maps, const GemmArgs& args, int num_sms, c
   }
   const int tiles = args.tiles_m * args.tiles_n;
   const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  kern<<<2 * pairs, 192, Cfg::SMEM_BYTES, stream>>>(maps.a, maps.b, maps.a2, maps.b2, args);
+  if (launch_k(kern, dim3(2 * pairs), dim3(192), Cfg::SMEM_BYTES, stream, maps.a, maps.b, maps.a2, maps.b2, args))
+    return -1;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -76,10 +76,12 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmS);
   }
+  pdl_launch_dependents();
   if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();  // the prologue above overlaps the predecessor's tail; global memory only from here
   const uint32_t tmem = *tmem_slot;
   const uint32_t tm_ds = tmem;            // 2 buffers x AW columns
   const uint32_t tm_db = tmem + 2 * AW;   // nsub x AW columns
@@ -242,8 +244,6 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
-    // dŜ partials over the n-split are complete once the grid retires; lf_finalize_kernel
-    // (launched behind this grid) scales, masks, converts and re-zeroes the workspace
   }
 
   tc_fence_before();
@@ -301,8 +301,10 @@ int grad_up_launch(const CUtensorMap& tm_dy, const CUtensorMap& tm_b, const CUte
     configured = true;
   }
   dim3 grid(args.n_split, args.m_split);
-  lf_gradup_kernel<<<grid, 192, smem, stream>>>(tm_dy, tm_b, tm_s, args, stages, stage_bytes);
-  if (cudaGetLastError() != cudaSuccess) return -1;
+  if (launch_k(lf_gradup_kernel, grid, dim3(192), smem, stream, tm_dy, tm_b, tm_s, args, stages, stage_bytes))
+    return -1;
+  // a separate, fully parallel finalize: in-kernel "last contributor finalizes" leaves the
+  // finalize of a whole m-range on the tail of one CTA here (up to 13 tiles at gate/up)
   return finalize_launch(args.segs, args.routes, args.ws, args.ds, stream);
 }
 

@@ -5,16 +5,39 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "lf_params.h"
 
 namespace lf {
+
+// Programmatic dependent launch for every lf kernel (see pdl_wait in lf_device.cuh); set
+// LF_PDL=0 in the environment to launch with plain stream ordering instead.
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline int launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                    Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...) == cudaSuccess ? 0 : -1;
+}
 
 // ② / ⑤: persistent warp-specialised tcgen05 GEMM  C[M,N] = A[M,K]·B (+ LoRA K-chunk).
 //  kind FWD       : B is K-major  (N x K, nn.Linear.weight), LoRA B2 = B_cat (N x R) K-major
 //  kind DGRAD     : B is MN-major (K x N, W as stored),      LoRA B2 = A_cat (R x N) MN-major,
 //                   LoRA term concatenated into the main accumulator (no dropout)
-//  kind DGRAD_MASK: as DGRAD but the LoRA term lands in a second TMEM accumulator and is
-//                   combined as acc + keep ⊙ acc_lora in the epilogue (dropout p > 0)
+//  kind DGRAD_MASK: as DGRAD but the LoRA K-block of a tile is issued first into its empty
+//                   accumulator, the epilogue warps zero its dropped elements in TMEM, and
+//                   the dY·W main loop accumulates on top (dropout p > 0)
 enum GemmKind { kGemmFwd = 0, kGemmDgrad = 1, kGemmDgradMasked = 2 };
 
 struct GemmArgs {
@@ -72,12 +95,12 @@ struct GradDownArgs {
   const LfRoute* routes;
   LfSegTable segs;
 };
+// split-K epilogue of ③: fp32 partials (ws) -> scaled bf16 m x R, workspace re-zeroed
+int finalize_launch(const LfSegTable& segs, const LfRoute* routes, float* ws, void* out, cudaStream_t stream);
 void grad_down_config(int rtot, bool bits_tma, int* stages, int* stage_bytes);
 int grad_down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_ds, const CUtensorMap& tm_bits,
                      const GradDownArgs& args, int num_sms, cudaStream_t stream);
 
-// split-K epilogue of ① and ③: fp32 partials (ws) -> scaled bf16 m x R, workspace re-zeroed
-int finalize_launch(const LfSegTable& segs, const LfRoute* routes, float* ws, void* out, cudaStream_t stream);
 
 // routing table + explicit mask materialisation
 int routes_launch(const LfSegTable& segs, int32_t* routes, int ntiles, cudaStream_t stream);

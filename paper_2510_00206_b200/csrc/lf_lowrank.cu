@@ -30,34 +30,6 @@ __device__ __forceinline__ bool tile_needs_mask(const LfSegTable& t, const LfRou
   return false;
 }
 
-// finalize one row of a split-K reduced m x R result: scale own-segment columns, zero the
-// rest, write bf16, and return the partial-sum workspace to zero.
-__device__ __forceinline__ void finalize_row(const LfSegTable& t, const LfRoute& rt, int row, float* ws,
-                                             __nv_bfloat16* out) {
-  const int rtot = t.rtot;
-  const int seg = find_segment(t, rt.seg_lo, rt.seg_hi, row);
-  const int own0 = seg >= 0 ? t.seg[seg].col0 : 0;
-  const int own1 = seg >= 0 ? t.seg[seg].col0 + t.seg[seg].ncol : 0;
-  const float scale = seg >= 0 ? t.seg[seg].scale : 0.f;
-  float* wrow = ws + (int64_t)row * rtot;
-  __nv_bfloat16* orow = out + (int64_t)row * rtot;
-  for (int c = 0; c < rtot; c += 8) {
-    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    const bool in_range = c >= rt.col_lo && c < rt.col_hi;
-    if (in_range) {
-      const float4 a = ld_cg_f4(wrow + c), b = ld_cg_f4(wrow + c + 4);
-      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-      *reinterpret_cast<float4*>(wrow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-      *reinterpret_cast<float4*>(wrow + c + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    const bool own = c >= own0 && c < own1;
-    const float s = own ? scale : 0.f;
-    *reinterpret_cast<uint4*>(orow + c) = make_uint4(pack_bf16x2(v[0] * s, v[1] * s), pack_bf16x2(v[2] * s, v[3] * s),
-                                                     pack_bf16x2(v[4] * s, v[5] * s), pack_bf16x2(v[6] * s, v[7] * s));
-  }
-}
-
 // ------------------------------------------------------------------------------------
 // ① dropout + down projection
 // ------------------------------------------------------------------------------------
@@ -110,6 +82,7 @@ __global__ void __launch_bounds__(kDownThreads, 2)
   uint64_t* tfull = masked + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;       // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ int s_last;
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int nkb = (args.k + 63) / 64;
@@ -133,10 +106,12 @@ __global__ void __launch_bounds__(kDownThreads, 2)
   // two accumulators (R columns each): a span's flush overlaps the next span's MMAs
   uint32_t tmem_cols = 32;
   while ((int)tmem_cols < 2 * args.rtot) tmem_cols <<= 1;
+  pdl_launch_dependents();
   if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();  // the prologue above overlaps the predecessor's tail; global memory only from here
   const uint32_t tmem = *tmem_slot;
 
   UnitWalker walk(units, (int)gridDim.x, (int)blockIdx.x, nkb);
@@ -209,8 +184,11 @@ __global__ void __launch_bounds__(kDownThreads, 2)
     while (walk.next(sp)) {
       const LfRoute rt = args.routes[sp.tile];
       const int N = rt.col_hi - rt.col_lo;
-      if (N <= 0) continue;
       const int row = sp.tile * 128 + rit;
+      if (N <= 0) {  // no adapter in this row tile: its Ŝ rows are zero (written once, by the span at k = 0)
+        if (half == 0 && sp.k0 == 0 && row < args.m) zero_row(args.rtot, row, reinterpret_cast<__nv_bfloat16*>(args.s_hat));
+        continue;
+      }
       if (gated) {
         const int seg = row < args.m ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
         const bool my_mask = seg >= 0 && (explicit_mask || args.segs.seg[seg].thr != 0);
@@ -282,11 +260,12 @@ __global__ void __launch_bounds__(kDownThreads, 2)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[b]);
+        // the span's partial is in; the CTA that completes the tile finalizes it
+        tile_contribute(args.segs, rt, sp.tile, rit, sp.k1 - sp.k0, nkb, args.counters, args.ws,
+                        reinterpret_cast<__nv_bfloat16*>(args.s_hat), 1, &s_last);
       }
       ++it;
     }
-    // split-K partials are complete in the workspace once this grid retires; the
-    // lf_finalize_kernel launched behind it scales, masks and converts them
   }
 
   tc_fence_before();
@@ -297,21 +276,22 @@ __global__ void __launch_bounds__(kDownThreads, 2)
   }
 }
 
-// Split-K epilogue shared by ① and ③: per row, scale the own-segment columns of the fp32
+// Split-K epilogue of ③ (① finalizes in-kernel, see tile_contribute): per row, scale the own-segment columns of the fp32
 // partial sums by s = scaling / (1 - p), zero every other column, write bf16, and return
 // the workspace to zero. One thread per row.
 __global__ void __launch_bounds__(128) lf_finalize_kernel(const __grid_constant__ LfSegTable segs,
                                                           const LfRoute* __restrict__ routes, float* ws,
                                                           __nv_bfloat16* out) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= segs.m || (segs.debug & 16)) return;
   finalize_row(segs, routes[row / LF_TILE_M], row, ws, out);
 }
 
 int finalize_launch(const LfSegTable& segs, const LfRoute* routes, float* ws, void* out, cudaStream_t stream) {
-  lf_finalize_kernel<<<(segs.m + 127) / 128, 128, 0, stream>>>(segs, routes, ws,
-                                                                 reinterpret_cast<__nv_bfloat16*>(out));
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  return launch_k(lf_finalize_kernel, dim3((segs.m + 127) / 128), dim3(128), 0, stream, segs, routes, ws,
+                  reinterpret_cast<__nv_bfloat16*>(out));
 }
 
 int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs& args, int num_sms,
@@ -325,9 +305,8 @@ int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs
       return -1;
     configured = true;
   }
-  lf_down_kernel<<<args.ctas, kDownThreads, smem, stream>>>(tm_x, tm_a, args, stages, stage_bytes);
-  if (cudaGetLastError() != cudaSuccess) return -1;
-  return finalize_launch(args.segs, args.routes, args.ws, args.s_hat, stream);
+  return launch_k(lf_down_kernel, dim3(args.ctas), dim3(kDownThreads), smem, stream, tm_x, tm_a, args, stages,
+                  stage_bytes);
 }
 
 // ------------------------------------------------------------------------------------
@@ -405,10 +384,12 @@ __global__ void __launch_bounds__(kDgaThreads, 2)
     tma_prefetch_desc(&tmD);
     if (args.bits_tma) tma_prefetch_desc(&tmK);
   }
+  pdl_launch_dependents();
   if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();  // the prologue above overlaps the predecessor's tail; global memory only from here
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
@@ -579,14 +560,16 @@ int grad_down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_ds, const CU
       return -1;
     configured = dga::MAX_SMEM + 2048;
   }
-  lf_dgrad_a_kernel<<<args.ctas, kDgaThreads, smem, stream>>>(tm_x, tm_ds, tm_bits, args, stages, stage_bytes);
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  return launch_k(lf_dgrad_a_kernel, dim3(args.ctas), dim3(kDgaThreads), smem, stream, tm_x, tm_ds, tm_bits, args,
+                  stages, stage_bytes);
 }
 
 // ------------------------------------------------------------------------------------
 // routing table and explicit keep mask
 // ------------------------------------------------------------------------------------
 __global__ void lf_routes_kernel(const __grid_constant__ LfSegTable segs, LfRoute* routes, int ntiles) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= ntiles) return;
   const int r0 = t * LF_TILE_M;
@@ -611,6 +594,8 @@ __global__ void lf_routes_kernel(const __grid_constant__ LfSegTable segs, LfRout
 }
 
 __global__ void lf_mask_kernel(const __grid_constant__ LfSegTable segs, int32_t k, uint8_t* keep) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int groups = (k + 7) / 8;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)segs.m * groups) return;
@@ -630,6 +615,8 @@ __global__ void lf_mask_kernel(const __grid_constant__ LfSegTable segs, int32_t 
 // column). Rows outside every dropout segment keep everything.
 __global__ void __launch_bounds__(256) lf_keep_bits_kernel(const __grid_constant__ LfSegTable segs, int32_t k,
                                                            uint8_t* bits, int64_t ld) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int groups = (k + 63) / 64;
   const int64_t total = (int64_t)segs.m * groups;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -657,21 +644,19 @@ int keep_bits_launch(const LfSegTable& segs, int32_t k, uint8_t* bits, int64_t l
   if (total <= 0) return 0;
   int64_t blocks = (total + 255) / 256;
   if (blocks > 4LL * num_sms) blocks = 4LL * num_sms;
-  lf_keep_bits_kernel<<<(unsigned)blocks, 256, 0, stream>>>(segs, k, bits, ld);
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  return launch_k(lf_keep_bits_kernel, dim3((unsigned)blocks), dim3(256), 0, stream, segs, k, bits, ld);
 }
 
 int routes_launch(const LfSegTable& segs, int32_t* routes, int ntiles, cudaStream_t stream) {
   if (ntiles <= 0) return 0;
-  lf_routes_kernel<<<(ntiles + 127) / 128, 128, 0, stream>>>(segs, reinterpret_cast<LfRoute*>(routes), ntiles);
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  return launch_k(lf_routes_kernel, dim3((ntiles + 127) / 128), dim3(128), 0, stream, segs,
+                  reinterpret_cast<LfRoute*>(routes), ntiles);
 }
 
 int mask_launch(const LfSegTable& segs, int32_t k, uint8_t* keep, cudaStream_t stream) {
   const int64_t total = (int64_t)segs.m * ((k + 7) / 8);
   if (total <= 0) return 0;
-  lf_mask_kernel<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(segs, k, keep);
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  return launch_k(lf_mask_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, stream, segs, k, keep);
 }
 
 }  // namespace lf

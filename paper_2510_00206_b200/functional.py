@@ -56,7 +56,7 @@ class LaunchStats:
         self.events.setdefault(name, []).append((start, ev))
 
     # device kernels each C entry point launches (① and ③ add the split-K finalize kernel)
-    KERNELS_PER_CALL = {"dropout_down_fwd": 2, "grad_up": 2}
+    KERNELS_PER_CALL = {"grad_up": 2}  # ③ + its split-K finalize; ① finalizes in-kernel
 
     def total_launches(self) -> int:
         return sum(n * self.KERNELS_PER_CALL.get(k, 1) for k, n in self.launches.items())
