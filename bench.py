@@ -34,7 +34,7 @@ HIDDEN_70B, KV_70B, FFN_70B = 8192, 1024, 28672
 
 def projections(config: str):
     """(name, k, n, input group) of each LoRA linear of one decoder layer."""
-    if config in ("c2", "c1", "c3"):
+    if config in ("c2", "c1", "c3", "c5"):
         h, kv, f = HIDDEN_8B, KV_8B, FFN_8B
     elif config == "c4":
         h, kv, f = HIDDEN_70B, KV_70B, FFN_70B
@@ -47,7 +47,7 @@ def projections(config: str):
 
 
 def tokens_per_gpu(config: str) -> int:
-    return {"c1": 2048, "c2": 8192, "c3": 8192, "c4": 16384}[config]
+    return {"c1": 2048, "c2": 8192, "c3": 8192, "c4": 16384, "c5": 8192}[config]
 
 
 # C3 (BASELINE.json configs[2]): FusedMultiLoRA, 4 adapters of ranks
@@ -253,6 +253,7 @@ def workload_name(config: str) -> str:
         "c2": "LLaMa-3.1-8B layer shapes (q/k/v/o, gate/up/down) FusedLoRA r=16, 8192 tokens, bf16, 1 B200",
         "c1": "single FusedLoRA linear fwd+bwd: tokens=2048, k=n=4096, r=16, dropout=0.1",
         "c4": "LLaMa-3.1-70B layer shapes FusedLoRA r=16, 16384 tokens per GPU",
+        "c5": "LLaMa-3.1-8B 4 concurrent LoRA jobs, full decoder fwd+bwd step (CPU sample: the 7 LoRA linears)",
         "c3": "FusedMultiLoRA 4 adapters, ranks {8,16,32,64}, uneven token segments {3584,2432,1408,768} "
               "sharing one frozen W per projection (LLaMa-3.1-8B q/k/v/o/gate/up/down), 8192 tokens",
     }[config]
@@ -618,12 +619,142 @@ def run_e2e(args, layers, inputs, grads, device, world, barrier, max_over_ranks)
                     " modules (public API), pinned host inputs H2D on a copy stream, fp32 grads D2H"}
 
 
+# --------------------------------------------------------------------------------------
+# C5 (BASELINE.json configs[4]): full LLaMa-3.1-8B decoder, 4 concurrent LoRA jobs,
+# bin-packed microbatches from the reference planner, DP with the dA/dB all-reduce
+# --------------------------------------------------------------------------------------
+C5_SCHEDULE = os.path.join(ROOT, "tests", "golden", "schedule_c5.json")
+
+
+def c5_microbatches(world: int, per_rank: int):
+    """The first world·per_rank microbatches of the committed lorasched schedule (cycled),
+    LPT-assigned to ranks by padded rows (weak scaling: per_rank microbatches each)."""
+    from paper_2510_00206_b200 import dp
+    from paper_2510_00206_b200 import schedule as sched
+
+    with open(C5_SCHEDULE) as f:
+        doc = json.load(f)
+    _, adapters = sched.adapters_from_doc(doc)
+    mbs = sched.microbatches_from_doc(doc)
+    chosen = [mbs[i % len(mbs)] for i in range(world * per_rank)]
+    assign = dp.assign_microbatches([mb.rows for mb in chosen], world)
+    return adapters, chosen, assign
+
+
+def run_c5(args, rank: int, world: int, local_rank: int) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_00206_b200 import _lib, dp
+    from paper_2510_00206_b200 import decoder as D
+    from paper_2510_00206_b200 import functional as F_
+
+    _lib.load()
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    shape = dataclasses.replace(D.LLAMA31_8B, layers=args.layers)
+    adapters, chosen, assign = c5_microbatches(world, args.mb_per_rank)
+    mine = [chosen[i] for i in assign[rank]]
+    gen = torch.Generator(device="cpu").manual_seed(7 + rank)
+    packed = [D.pack_microbatch(mb, shape.vocab, device, gen) for mb in mine]
+    raw_all = sum(mb.raw_tokens for mb in chosen)
+    rows_all = sum(mb.rows for mb in chosen)
+    rank_rows = [(adapters[s.adapter].rank, s.rows) for mb in mine for s in mb.segments]
+    my_flops = shape.linear_flops(sum(mb.rows for mb in mine), rank_rows)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def arm(fused: bool, steps: int):
+        dgen = torch.Generator(device=device).manual_seed(1234)  # same weights on every rank
+        model = D.LoRADecoder(shape, adapters, fused=fused, device=device, generator=dgen)
+        model.train()
+        params = model.adapter_parameters()
+        reducer = dp.AdapterGradReducer(params) if world > 1 else None
+        opt = torch.optim.AdamW(params, lr=1e-4, fused=True)
+        fn = lambda: D.train_step(model, packed, reducer, opt)  # noqa: E731
+        counts = None
+        if fused:
+            for _ in range(args.warmup):
+                fn()
+            counts = F_.LaunchStats(timed=False)
+            F_.set_launch_stats(counts)
+            ms = time_loop(fn, steps, 0, barrier)
+            F_.set_launch_stats(None)
+        else:
+            ms = time_loop(fn, steps, args.warmup, barrier)
+        peak = torch.cuda.max_memory_allocated(device)
+        del model, params, reducer, opt
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats(device)
+        return max_over_ranks(ms), counts, peak
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    ms, counts, peak = arm(True, args.steps)
+    clk = clocks.stop()
+    unf_ms, _, unf_peak = arm(False, max(2, args.steps // 2))
+    flops_all = my_flops
+    if world > 1:
+        t = torch.tensor([my_flops], device=device, dtype=torch.float64)
+        dist.all_reduce(t)
+        flops_all = float(t.item())
+    peaks = measured_peaks()
+    if rank == 0:
+        line = {
+            "metric": "LoRA linear fwd+bwd tokens/s & TFLOP/s (8B/70B shapes), % of bf16 peak",
+            "value": raw_all / (ms * 1e-3),
+            "unit": "tokens/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic (random token ids, random-init LLaMa-3.1-8B weights)",
+            "config": {
+                "workload": "LLaMa-3.1-8B 4 concurrent LoRA jobs, full decoder fwd+bwd step, bin-packed microbatches "
+                            "with dA/dB allreduce",
+                "layers": shape.layers,
+                "schedule": "tests/golden/schedule_c5.json (lorasched plan_schedule, capacity 8192, S=1)",
+                "adapters": [dataclasses.asdict(a) for a in adapters],
+                "microbatches_per_rank": args.mb_per_rank,
+                "rows_per_step": rows_all,
+                "raw_tokens_per_step": raw_all,
+                "parallelism": f"dp{world}",
+                "optimizer": "AdamW (fused) on the fp32 adapter weights",
+                "l2": "inputs larger than L2",
+            },
+            "padded_rows_per_s": rows_all / (ms * 1e-3),
+            "lora_linear_tflops": flops_all / (ms * 1e-3) / 1e12,
+            "lora_linear_frac_of_bf16_peak": flops_all / (ms * 1e-3) / 1e12 / world / peaks["bf16_tflops"],
+            "unfused_torch": {"ms_per_step": unf_ms, "tokens_per_s": raw_all / (unf_ms * 1e-3),
+                              "speedup": unf_ms / ms, "peak_mem_gb": unf_peak / 1e9},
+            "peak_mem_gb": peak / 1e9,
+            "gpu_launches": counts.total_launches() if counts else None,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--layers", type=int, default=32, help="C5: decoder layers (32 = the full 8B stack)")
+    ap.add_argument("--mb-per-rank", type=int, default=4, help="C5: microbatches per rank per step")
     ap.add_argument("--no-multi", action="store_true", help="skip the secondary C3 FusedMultiLoRA measurement")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dropout", type=float, default=0.1)
@@ -646,6 +777,9 @@ def main() -> None:
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
+        if args.config == "c5":
+            run_c5(args, rank, world, local_rank)
+            return
         run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:

@@ -248,6 +248,41 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t local_addr, uint32_t ra
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// arrive (one count) + expect `bytes` of transactions on an mbarrier of CTA `rank`'s smem
+__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
+               "r"(bytes)
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------------
+// cluster launch control (dynamic persistent scheduling, sm_100)
+// ---------------------------------------------------------------------------------
+// Ask the hardware to cancel the launch of a not-yet-running cluster of this grid; the
+// 16-byte response is multicast to the same smem offset in every CTA of the cluster and
+// completes 16 transaction bytes on the mbarrier at the same offset in each of them.
+__device__ __forceinline__ void clc_try_cancel_multicast(uint32_t resp_addr, uint32_t bar_addr) {
+  asm volatile(
+      "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.multicast::cluster::all.b128 "
+      "[%0], [%1];" ::"r"(resp_addr),
+      "r"(bar_addr)
+      : "memory");
+}
+// Decode a response: the canceled cluster's first CTA x-coordinate, or -1 if none was left.
+__device__ __forceinline__ int clc_first_ctaid_x(uint32_t resp_addr) {
+  uint32_t x = 0, ok = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b128 r;\n\t"
+      "ld.shared.b128 r, [%2];\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r;\n\t"
+      "selp.u32 %1, 1, 0, p;\n\t"
+      "@p clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %0, r;\n\t}"
+      : "=r"(x), "=r"(ok)
+      : "r"(resp_addr)
+      : "memory");
+  return ok ? (int)x : -1;
+}
+
 // TMA load whose completion bytes are counted on the pair leader's mbarrier (same smem
 // offset, peer bit cleared): each CTA of a pair fills its own half of a 2-CTA MMA operand
 __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,

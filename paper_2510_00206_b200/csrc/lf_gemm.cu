@@ -23,10 +23,16 @@
 // bits → tcgen05.st), and only then is the main dY·W loop accumulated on top. The LoRA
 // block of tile i+1 is issued half-way through tile i's main loop, so its mask pass
 // runs while the tensor pipe is busy with tile i.
+#include <cstdlib>
+
 #include "lf_device.cuh"
 #include "lf_kernels.h"
 
 namespace lf {
+
+// control block after the operand ring: mbarriers, TMEM slot, tile-sequence ring
+constexpr int kGemmCtlBytes = 512;
+constexpr int kSeqDepth = 6;  // CLC responses in flight / not yet released
 
 template <bool B_MN, int STAGES>
 struct GemmCfg {
@@ -39,7 +45,7 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int ACC_COLS = BN;
   static constexpr int TMEM_COLS = 2 * ACC_COLS;  // 512
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 512 * 16;  // + routing cache
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + kGemmCtlBytes + 512 * 16;  // + routing cache
 };
 
 // grouped raster: G m-tiles share each n-column sweep so W tiles stay L2-hot
@@ -122,6 +128,55 @@ __device__ __forceinline__ uint32_t dgrad_keep32(const LfSegTable& t, int seg, i
   return dgrad_keep32_slow(t, seg, row, col, ncols);
 }
 
+// Tile sequence of one CTA pair. Dynamic (default): the grid has one cluster per tile; a
+// pair starts on its own tile (blockIdx.x / 2) and then takes over not-yet-launched
+// clusters' tiles through cluster launch control, in launch order — the tiles in flight
+// always form one contiguous window of the raster, so pairs that run slower never drift
+// onto data no other pair is reading (a static round-robin persistent schedule let them
+// drift and re-read W from DRAM: 15 GB vs 4.8 GB per C4 gate launch, ncu).
+// Response i (i >= 1) sits in slot (i-1) % kSeqDepth; every role of both CTAs reads each
+// response once, in order, and releases it on the leader's `empty` barrier (11 readers:
+// 2 producers, the MMA warp, 8 epilogue warps). Only the leader's producer requests, and
+// only after the previous response named a tile, so no request is left unread at exit.
+// Static (LF_SCHED_STATIC=1, for A/B measurements): tile i = pair + i * npairs.
+struct TileSeq {
+  uint64_t* full;   // [kSeqDepth] per CTA: response landed
+  uint64_t* empty;  // [kSeqDepth] leader: all readers done
+  uint8_t* resp;    // [kSeqDepth][16]
+  int pair, npairs, tiles;
+  bool dynamic;
+
+  static constexpr uint32_t kReaders = 11;
+
+  __device__ int first() const { return pair < tiles ? pair : -1; }
+  // leader producer only: ask for response i
+  __device__ void request(int i) const {
+    if (!dynamic) return;
+    const int slot = (i - 1) % kSeqDepth;
+    const uint32_t ph = (uint32_t)((i - 1) / kSeqDepth) & 1u;
+    mbar_wait(&empty[slot], ph ^ 1u);
+    const uint32_t fb = smem_u32(&full[slot]);
+    mbar_arrive_expect_tx_cluster(mapa_shared(fb, 0), 16);
+    mbar_arrive_expect_tx_cluster(mapa_shared(fb, 1), 16);
+    clc_try_cancel_multicast(smem_u32(resp + 16 * slot), fb);
+  }
+  // every reader: tile of response i (waits for it), or -1 when the grid is exhausted.
+  // Warp-wide readers call it with the whole warp; `arrive` = the one lane that releases.
+  __device__ int read(int i, bool arrive) const {
+    if (!dynamic) {
+      const int t = pair + i * npairs;
+      return t < tiles ? t : -1;
+    }
+    const int slot = (i - 1) % kSeqDepth;
+    const uint32_t ph = (uint32_t)((i - 1) / kSeqDepth) & 1u;
+    mbar_wait(&full[slot], ph);
+    const int x = clc_first_ctaid_x(smem_u32(resp + 16 * slot));
+    fence_proxy_async_smem();  // the next response into this slot is an async-proxy write
+    if (arrive) mbar_arrive_cluster(mapa_shared(smem_u32(&empty[slot]), 0));
+    return x < 0 ? -1 : (x >> 1);
+  }
+};
+
 template <bool B_MN, bool MASKED, int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     lf_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -138,7 +193,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   uint64_t* lfull = tempty + 2;      // [2] both CTAs: LoRA partial ready                 MASKED
   uint64_t* lmasked = lfull + 2;     // [2] leader: both CTAs masked their partial (8)   MASKED
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lmasked + 2);
-  LfRoute* s_routes = reinterpret_cast<LfRoute*>(smem + STAGES * Cfg::STAGE_BYTES + 256);  // [kSmemRoutes]
+  uint8_t* ctl = smem + STAGES * Cfg::STAGE_BYTES;
+  TileSeq seq;
+  seq.full = reinterpret_cast<uint64_t*>(ctl + 192);
+  seq.empty = seq.full + kSeqDepth;
+  seq.resp = ctl + 320;
+  LfRoute* s_routes = reinterpret_cast<LfRoute*>(ctl + kGemmCtlBytes);  // [kSmemRoutes]
   pdl_launch_dependents();
 
   const uint32_t warp = warp_id();
@@ -156,6 +216,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       mbar_init(&tempty[a], 8);
       mbar_init(&lfull[a], 1);
       mbar_init(&lmasked[a], 8);
+    }
+    for (int i = 0; i < kSeqDepth; ++i) {
+      mbar_init(&seq.full[i], 1);
+      mbar_init(&seq.empty[i], TileSeq::kReaders);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmA);
@@ -178,8 +242,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int tiles = args.tiles_m * args.tiles_n;
-  const int pair = blockIdx.x >> 1;
-  const int npairs = gridDim.x >> 1;
+  seq.pair = blockIdx.x >> 1;
+  seq.npairs = gridDim.x >> 1;
+  seq.tiles = tiles;
+  seq.dynamic = args.dynamic != 0;
   const int nkb = (args.K + Cfg::BK - 1) / Cfg::BK;
   // MASKED: where the next tile's LoRA block is interleaved (debug 256: after the main loop,
   // 512: a quarter in, 1024: three quarters in)
@@ -231,22 +297,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       };
-      for (int t = pair; t < tiles; t += npairs) {
+      int t = seq.first();
+      if (leader && t >= 0) seq.request(1);
+      for (int i = 0; t >= 0; ++i) {
         const TileInfo ti = tile_info(args, s_routes, t);
+        int tn;
         if constexpr (MASKED) {
-          if (t == pair && ti.lora()) load_lora(ti);
-          const bool has_next = t + npairs < tiles;
-          const TileInfo tn = has_next ? tile_info(args, s_routes, t + npairs) : ti;
-          const bool lora_next = has_next && tn.lora();
-          const int split = lora_next ? min(jmid, nkb) : nkb;
+          if (i == 0 && ti.lora()) load_lora(ti);
+          // the next tile's LoRA block goes in half-way through this tile's main loop
+          const int split = min(jmid, nkb);
           int kb = 0;
           for (; kb < split; ++kb) load_main(ti, kb);
-          if (lora_next) load_lora(tn);
+          tn = seq.read(i + 1, true);
+          if (leader && tn >= 0) seq.request(i + 2);
+          if (tn >= 0) {
+            const TileInfo tni = tile_info(args, s_routes, tn);
+            if (tni.lora()) load_lora(tni);
+          }
           for (; kb < nkb; ++kb) load_main(ti, kb);
         } else {
           for (int kb = 0; kb < nkb; ++kb) load_main(ti, kb);
           if (ti.lora()) load_lora(ti);
+          tn = seq.read(i + 1, true);
+          if (leader && tn >= 0) seq.request(i + 2);
         }
+        t = tn;
       }
     }
     __syncwarp();
@@ -298,11 +373,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         mma_lora(ti, tmem_base + acc * Cfg::ACC_COLS, false);
         umma_commit_pair_warp(&lfull[acc]);
       };
-      int it = 0;
-      for (int t = pair; t < tiles; t += npairs, ++it) {
+      int t = seq.first();
+      for (int it = 0; t >= 0; ++it) {
         const TileInfo ti = tile_info(args, s_routes, t);
         const int acc = it & 1;
         const uint32_t d = tmem_base + acc * Cfg::ACC_COLS;
+        int tn = -1;
+        bool have_tn = false;
         if (MASKED && (args.segs.debug & 4096)) {  // profiling: plain k-loop in the masked kernel
           mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
           tc_fence_after();
@@ -317,14 +394,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
             mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
           }
           tc_fence_after();
-          const bool has_next = t + npairs < tiles;
-          const TileInfo tn = has_next ? tile_info(args, s_routes, t + npairs) : ti;
-          const bool lora_next = has_next && tn.lora();
-          const int split = lora_next ? min(jmid, nkb) : nkb;
+          const int split = min(jmid, nkb);
           const bool acc_any = ti.lora();
           int kb = 0;
           for (; kb < split; ++kb) mma_main_block(d, kb, acc_any);
-          if (lora_next) issue_lora_first(tn, it + 1);
+          tn = seq.read(it + 1, lane_id() == 0);
+          have_tn = true;
+          if (tn >= 0) {
+            const TileInfo tni = tile_info(args, s_routes, tn);
+            if (tni.lora()) issue_lora_first(tni, it + 1);
+          }
           for (; kb < nkb; ++kb) mma_main_block(d, kb, acc_any);
         } else {
           mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
@@ -333,6 +412,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           if (ti.lora()) mma_lora(ti, d, true);
         }
         umma_commit_pair_warp(&tfull[acc]);
+        if (!have_tn) tn = seq.read(it + 1, lane_id() == 0);
+        t = tn;
       }
     }
     __syncwarp();
@@ -388,16 +469,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(lmasked_leader[acc]);
     };
-    int it = 0;
-    for (int t = pair; t < tiles; t += npairs, ++it) {
+    int t = seq.first();
+    for (int it = 0; t >= 0; ++it) {
       const TileInfo ti = tile_info(args, s_routes, t);
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
+      int tn = -1;
       if constexpr (MASKED) {
         if (it == 0 && ti.lora()) mask_pass(ti, 0);
-        if (t + npairs < tiles) {
-          const TileInfo tn = tile_info(args, s_routes, t + npairs);
-          if (tn.lora()) mask_pass(tn, it + 1);
+        tn = seq.read(it + 1, lane == 0);
+        if (tn >= 0) {
+          const TileInfo tni = tile_info(args, s_routes, tn);
+          if (tni.lora()) mask_pass(tni, it + 1);
         }
       }
       const int row = ti.mb * 256 + (int)rank * Cfg::BM + (int)(q * 32 + lane);
@@ -428,6 +511,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader[acc]);
+      if constexpr (!MASKED) tn = seq.read(it + 1, lane == 0);
+      t = tn;
     }
   }
 
@@ -450,7 +535,9 @@ static int launch_one(const GemmMaps& maps, const GemmArgs& args, int num_sms, c
     configured = true;
   }
   const int tiles = args.tiles_m * args.tiles_n;
-  const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  // dynamic: one cluster per tile (the resident pairs take over the rest through CLC);
+  // static (A/B measurements only): one persistent pair per SM pair, round-robin tiles
+  const int pairs = args.dynamic ? tiles : (tiles < num_sms / 2 ? tiles : num_sms / 2);
   if (launch_k(kern, dim3(2 * pairs), dim3(192), Cfg::SMEM_BYTES, stream, maps.a, maps.b, maps.a2, maps.b2, args))
     return -1;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
@@ -461,6 +548,8 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
   args.tiles_m = (args.M + 255) / 256;
   args.tiles_n = (args.N + 255) / 256;
   if (args.group <= 0) args.group = 8;
+  static const int sched_static = [] { const char* e = getenv("LF_SCHED_STATIC"); return e ? atoi(e) : 0; }();
+  args.dynamic = sched_static ? 0 : 1;
   switch (kind) {
     case kGemmFwd:
       return launch_one<false, false, 6>(maps, args, num_sms, stream);

@@ -44,6 +44,7 @@ struct GemmArgs {
   int32_t M, N, K;
   int32_t tiles_m, tiles_n;
   int32_t group;          // raster: m-tiles sharing each n sweep (set by gemm_launch)
+  int32_t dynamic;        // 1: CLC tile sequence (one cluster per tile), 0: static persistent
   int64_t ldc;
   void* C;                // bf16 output, row-major M x N (ldc elements)
   const LfRoute* routes;  // nullptr = no LoRA chunk

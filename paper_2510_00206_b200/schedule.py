@@ -33,13 +33,21 @@ def _need(d: Mapping, key: str, where: str):
 
 @dataclass(frozen=True)
 class MicrobatchPlan:
-    """One microbatch ready for the fused layer: its segments and total padded rows."""
+    """One microbatch ready for the fused layer: its segments and total padded rows.
+
+    ``sequences`` lists the row count of every packed sequence in row order: each sample
+    of a segment, then (when the segment was padded) one pad pseudo-sequence of
+    ``padded − raw`` rows, so varlen attention never mixes samples or attends into padding.
+    ``segment_raw`` holds each segment's raw (unpadded) token count.
+    """
 
     commit_index: int
     group_id: int
     segments: tuple
     rows: int
     raw_tokens: int
+    sequences: tuple = ()
+    segment_raw: tuple = ()
 
 
 def adapters_from_doc(doc: Mapping, seeds: Mapping[str, int] | None = None) -> tuple[list[str], list[AdapterConfig]]:
@@ -76,7 +84,7 @@ def microbatches_from_doc(doc: Mapping, adapter_ids: Sequence[str] | None = None
             continue
         if kind != KIND_MICROBATCH:
             raise ValidationError(f"{where}: unknown kind {kind!r}")
-        row, raw_total, segs = 0, 0, []
+        row, raw_total, segs, seqs, seg_raw = 0, 0, [], [], []
         for j, s in enumerate(_need(e, "segments", where)):
             sw = f"{where}.segments[{j}]"
             aid = _need(s, "adapter_id", sw)
@@ -84,8 +92,15 @@ def microbatches_from_doc(doc: Mapping, adapter_ids: Sequence[str] | None = None
                 raise ValidationError(f"{sw}: unknown adapter {aid!r}")
             mult = int(_need(s, "padding_multiple", sw))
             samples = _need(s, "samples", sw)
-            raw = sum(int(_need(r, "length", f"{sw}.samples")) for r in samples)
+            lens = [int(_need(r, "length", f"{sw}.samples")) for r in samples]
+            if any(n < 1 for n in lens):
+                raise ValidationError(f"{sw}.samples: lengths must be >= 1")
+            raw = sum(lens)
             padded = _padded(raw, mult)
+            seqs.extend(lens)
+            seg_raw.append(raw)
+            if padded > raw:
+                seqs.append(padded - raw)
             declared = s.get("padded_tokens")
             if declared is not None and int(declared) != padded:
                 raise ValidationError(f"{sw}.padded_tokens: declared {declared}, recomputed {padded}")
@@ -96,7 +111,7 @@ def microbatches_from_doc(doc: Mapping, adapter_ids: Sequence[str] | None = None
         if declared is not None and int(declared) != row:
             raise ValidationError(f"{where}.total_padded_tokens: declared {declared}, recomputed {row}")
         out.append(MicrobatchPlan(int(e.get("commit_index", i)), int(_need(e, "group_id", where)), tuple(segs), row,
-                                  raw_total))
+                                  raw_total, tuple(seqs), tuple(seg_raw)))
     return out
 
 

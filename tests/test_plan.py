@@ -103,6 +103,13 @@ def test_schedule_document_ingestion():
         assert [s.rows for s in mb.segments] == [s["padded_tokens"] for s in e["segments"]]
         assert [s.batch for s in mb.segments] == [s["global_batch_index"] for s in e["segments"]]
         assert [ids[s.adapter] for s in mb.segments] == [s["adapter_id"] for s in e["segments"]]
+        # packed sequences: every sample, then the segment's pad rows as one pseudo-sequence
+        want = []
+        for s in e["segments"]:
+            want += [r["length"] for r in s["samples"]]
+            if s["padded_tokens"] > s["raw_tokens"]:
+                want.append(s["padded_tokens"] - s["raw_tokens"])
+        assert list(mb.sequences) == want and sum(mb.sequences) == mb.rows
         plan = LayerPlan(mb.rows, 4096, 4096, cfgs, list(mb.segments))
         ref = orouting.routes([(s.row_start, s.row_end) for s in mb.segments],
                               list(zip(plan.col_starts, plan.ranks)), mb.rows)

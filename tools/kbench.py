@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--bits", action="store_true", help="① writes packed keep bits, ④/⑤ read them")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--only", default="")
+    ap.add_argument("--rounds", type=int, default=1, help="repeat the kernel list (A/B interleaving under the power cap)")
+    ap.add_argument("--power", action="store_true", help="sample SM clock and board power (NVML) per timed loop")
     args = ap.parse_args()
     import torch
 
@@ -103,22 +105,65 @@ def main():
     launches["cublas_dgrad"] = (lambda i: (torch.mm(DY[i], W, out=DX), 0)[1], "tflops", 2 * m * k * n)
     # ① once so packed bits exist for ④/⑤
     _lib.check(lib.lf_dropout_down_fwd(pp, P(X[0]), P(A), P(S), st), "down")
-    for name, (fn, unit, work) in launches.items():
-        if args.only and name not in args.only.split(","):
-            continue
+    sampler = _NvmlSampler() if args.power else None
+    order = [nm for nm in launches if not args.only or nm in args.only.split(",")]
+    if args.only:
+        order = [nm for nm in args.only.split(",") if nm in launches]
+    for rnd, name in [(rr, nm) for rr in range(args.rounds) for nm in order]:
+        fn, unit, work = launches[name]
         for i in range(3):
             _lib.check(fn(i % nbuf), name)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if sampler:
+            sampler.start()
         e0.record()
         for i in range(args.iters):
             fn(i % nbuf)
         e1.record()
         torch.cuda.synchronize()
+        extra = sampler.stop() if sampler else {}
         us = e0.elapsed_time(e1) * 1e3 / args.iters
         val = work / (us * 1e-6) / (1e9 if unit == "gbs" else 1e12)
         print(json.dumps({"kernel": name, "m": m, "k": k, "n": n, "r": R, "p": args.p, "bits": args.bits,
-                          "us": round(us, 2), unit: round(val, 1)}), flush=True)
+                          "round": rnd, "us": round(us, 2), unit: round(val, 1), **extra}), flush=True)
+
+
+class _NvmlSampler:
+    """SM clock (MHz) and board power (W) sampled every 5 ms on a thread while a loop runs."""
+
+    def __init__(self):
+        import pynvml
+
+        pynvml.nvmlInit()
+        self.nv = pynvml
+        import torch
+
+        self.h = pynvml.nvmlDeviceGetHandleByUUID("GPU-" + str(torch.cuda.get_device_properties(0).uuid))
+
+    def start(self):
+        import threading
+
+        self.samples, self.run = [], True
+        self.t = threading.Thread(target=self._loop, daemon=True)
+        self.t.start()
+
+    def _loop(self):
+        import time
+
+        while self.run:
+            self.samples.append((self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM),
+                                 self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0))
+            time.sleep(0.005)
+
+    def stop(self) -> dict:
+        self.run = False
+        self.t.join()
+        if not self.samples:
+            return {}
+        clk = sorted(c for c, _ in self.samples)
+        pw = sorted(p for _, p in self.samples)
+        return {"sm_mhz": clk[len(clk) // 2], "power_w": round(pw[len(pw) // 2], 1), "samples": len(clk)}
 
 
 if __name__ == "__main__":
