@@ -29,8 +29,9 @@
  *
  * Segments mirror lorasched's MicrobatchSegment (ls/packing.py:41-60): one
  * (adapter, global batch) group of token rows, with that adapter's AdapterSpec
- * hyper-parameters (ls/workload.py:25-48). Segments are sorted by row, disjoint,
- * and own disjoint, increasing column blocks of the concatenated rank dimension.
+ * hyper-parameters (ls/workload.py:25-48). Segments are sorted by row and disjoint;
+ * each owns a 16-aligned column block of the concatenated rank dimension, either its
+ * own (disjoint from the others) or shared with segments of the same adapter (SPEC.md §1).
  */
 #ifndef LORAFUSION_B200_H
 #define LORAFUSION_B200_H

@@ -23,11 +23,18 @@ def pad_rank(r: int) -> int:
     return -(-int(r) // 16) * 16
 
 
-def column_blocks(ranks) -> list[int]:
-    """col_start of each segment's block in the rank-concat dimension."""
-    out, c = [], 0
-    for r in ranks:
+def column_blocks(ranks, adapters=None) -> list[int]:
+    """col_start of each segment's block in the rank-concat dimension. With ``adapters``
+    (one slot per segment), segments of the same adapter share one block, assigned in
+    order of first appearance (SPEC.md §1)."""
+    out, c, seen = [], 0, {}
+    for i, r in enumerate(ranks):
+        if adapters is not None and adapters[i] in seen:
+            out.append(seen[adapters[i]])
+            continue
         out.append(c)
+        if adapters is not None:
+            seen[adapters[i]] = c
         c += pad_rank(r)
     return out
 
@@ -43,7 +50,10 @@ def routes(seg_rows, seg_cols, m: int) -> np.ndarray:
             out[t] = (0, -1, 0, 0)
         else:
             lo, hi = hit[0], hit[-1]
-            out[t] = (lo, hi, seg_cols[lo][0], seg_cols[hi][0] + seg_cols[hi][1])
+            # hull of the hit segments' column blocks (SPEC.md §4; blocks may be shared)
+            c0 = min(seg_cols[i][0] for i in hit)
+            c1 = max(seg_cols[i][0] + seg_cols[i][1] for i in hit)
+            out[t] = (lo, hi, c0, c1)
     return out
 
 

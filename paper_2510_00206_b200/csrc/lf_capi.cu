@@ -157,22 +157,29 @@ int validate(const LfProblem* p, bool need_routes, lf::LfSegTable* t) {
   t->m = p->m;
   t->rtot = p->rank_total;
   bool any_dropout = false;
-  int prev_row = 0, prev_col = 0;
+  int prev_row = 0;
   for (int i = 0; i < p->num_segments; ++i) {
     const LfSegment& s = p->segments[i];
     if (s.row_start < prev_row || s.row_end < s.row_start || s.row_end > p->m)
       return fail(LF_E_INVALID,
                   "segment %d rows [%d, %d) must be sorted, disjoint and inside [0, m=%d)", i, s.row_start, s.row_end,
                   p->m);
-    if (s.rank < 16 || s.rank % 16 || s.col_start % 16 || s.col_start < prev_col || s.col_start + s.rank > p->rank_total)
-      return fail(LF_E_INVALID,
-                  "segment %d columns [%d, %d) must be 16-aligned, increasing and inside rank_total=%d", i, s.col_start,
-                  s.col_start + s.rank, p->rank_total);
+    if (s.rank < 16 || s.rank % 16 || s.col_start % 16 || s.col_start < 0 || s.col_start + s.rank > p->rank_total)
+      return fail(LF_E_INVALID, "segment %d columns [%d, %d) must be 16-aligned and inside rank_total=%d", i,
+                  s.col_start, s.col_start + s.rank, p->rank_total);
+    // column blocks are shared (segments of one adapter, SPEC.md §1) or disjoint
+    for (int j = 0; j < i; ++j) {
+      const LfSegment& o = p->segments[j];
+      const bool same = o.col_start == s.col_start && o.rank == s.rank;
+      const bool disjoint = o.col_start + o.rank <= s.col_start || s.col_start + s.rank <= o.col_start;
+      if (!same && !disjoint)
+        return fail(LF_E_INVALID, "segment %d columns [%d, %d) partially overlap segment %d's [%d, %d)", i,
+                    s.col_start, s.col_start + s.rank, j, o.col_start, o.col_start + o.rank);
+    }
     if (!(s.dropout_p >= 0.f && s.dropout_p < 1.f))
       return fail(LF_E_INVALID, "segment %d dropout_p must be in [0, 1), got %g", i, (double)s.dropout_p);
     if (!std::isfinite(s.scaling)) return fail(LF_E_INVALID, "segment %d scaling must be finite", i);
     prev_row = s.row_end;
-    prev_col = s.col_start + s.rank;
     lf::LfSegDev& d = t->seg[i];
     d.row0 = s.row_start;
     d.row1 = s.row_end;

@@ -574,11 +574,19 @@ __global__ void lf_routes_kernel(const __grid_constant__ LfSegTable segs, LfRout
   if (t >= ntiles) return;
   const int r0 = t * LF_TILE_M;
   const int r1 = min(segs.m, r0 + LF_TILE_M);
-  int lo = -1, hi = -2;
+  int lo = -1, hi = -2, c0 = 0, c1 = 0;
   for (int i = 0; i < segs.nseg; ++i) {
     const LfSegDev& s = segs.seg[i];
     if (s.row0 < s.row1 && s.row0 < r1 && s.row1 > r0) {
-      if (lo < 0) lo = i;
+      // column blocks may be shared by segments of one adapter: take the union's hull
+      if (lo < 0) {
+        lo = i;
+        c0 = s.col0;
+        c1 = s.col0 + s.ncol;
+      } else {
+        c0 = min(c0, s.col0);
+        c1 = max(c1, s.col0 + s.ncol);
+      }
       hi = i;
     }
   }
@@ -587,8 +595,8 @@ __global__ void lf_routes_kernel(const __grid_constant__ LfSegTable segs, LfRout
     r.seg_lo = 0; r.seg_hi = -1; r.col_lo = 0; r.col_hi = 0;
   } else {
     r.seg_lo = lo; r.seg_hi = hi;
-    r.col_lo = segs.seg[lo].col0;
-    r.col_hi = segs.seg[hi].col0 + segs.seg[hi].ncol;
+    r.col_lo = c0;
+    r.col_hi = c1;
   }
   routes[t] = r;
 }

@@ -27,8 +27,10 @@ def _ptr(t: torch.Tensor | None) -> ctypes.c_void_p:
     return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
 
 
-def _stream() -> ctypes.c_void_p:
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+def _stream(device: torch.device | None = None) -> ctypes.c_void_p:
+    """The current torch stream of ``device`` as a raw cudaStream_t (cheap: no Stream object)."""
+    idx = device.index if device is not None and device.index is not None else torch._C._cuda_getDevice()
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(idx))
 
 
 class LaunchStats:
@@ -111,14 +113,15 @@ class _FusedLoRAFn(torch.autograd.Function):
         pp = ctypes.byref(plan.problem)
         y = torch.empty((m, n), dtype=_BF16, device=x.device)
         s_hat = a_cat = b_cat = None
+        st = _stream(x.device)
         if plan.has_lora:
             # bf16 operand copies: the module's cached shadows when given, else cast here
             shadows = plan.weights_bf16
             a_cat = plan.gather_a(shadows[0] if shadows else params[:n_adapters])
             b_cat = plan.gather_b(shadows[1] if shadows else params[n_adapters:])
             s_hat = torch.empty((m, R), dtype=_BF16, device=x.device)
-            _call("dropout_down_fwd", lib.lf_dropout_down_fwd, pp, _ptr(x), _ptr(a_cat), _ptr(s_hat), _stream())
-        _call("base_fwd", lib.lf_base_fwd, pp, _ptr(x), _ptr(w), _ptr(s_hat), _ptr(b_cat), _ptr(y), _stream())
+            _call("dropout_down_fwd", lib.lf_dropout_down_fwd, pp, _ptr(x), _ptr(a_cat), _ptr(s_hat), st)
+        _call("base_fwd", lib.lf_base_fwd, pp, _ptr(x), _ptr(w), _ptr(s_hat), _ptr(b_cat), _ptr(y), st)
         ctx.plan = plan
         ctx.grad_sink = grad_sink
         ctx.n_adapters = n_adapters
@@ -135,18 +138,19 @@ class _FusedLoRAFn(torch.autograd.Function):
         dy = dy.to(_BF16).contiguous()
         pp = ctypes.byref(plan.problem)
         da = db = ds = None
+        st = _stream(dy.device)
         if plan.has_lora:
             ds = torch.empty((m, R), dtype=_BF16, device=dy.device)
             # one zero-fill for both fp32 accumulators
             acc = torch.zeros(R * k + n * R, dtype=torch.float32, device=dy.device)
             da = acc[:R * k].view(R, k)
             db = acc[R * k:].view(n, R)
-            _call("grad_up", lib.lf_grad_up, pp, _ptr(dy), _ptr(b_cat), _ptr(s_hat), _ptr(ds), _ptr(db), _stream())
-            _call("grad_down", lib.lf_grad_down, pp, _ptr(x), _ptr(ds), _ptr(da), _stream())
+            _call("grad_up", lib.lf_grad_up, pp, _ptr(dy), _ptr(b_cat), _ptr(s_hat), _ptr(ds), _ptr(db), st)
+            _call("grad_down", lib.lf_grad_down, pp, _ptr(x), _ptr(ds), _ptr(da), st)
         dx = None
         if ctx.needs_input_grad[0]:
             dx = torch.empty((m, k), dtype=_BF16, device=dy.device)
-            _call("grad_input", lib.lf_grad_input, pp, _ptr(dy), _ptr(w), _ptr(ds), _ptr(a_cat), _ptr(dx), _stream())
+            _call("grad_input", lib.lf_grad_input, pp, _ptr(dy), _ptr(w), _ptr(ds), _ptr(a_cat), _ptr(dx), st)
         if ctx.grad_sink is not None and plan.has_lora:
             ctx.grad_sink(plan, da, db)
         # route the rank-concat gradients back to each adapter's parameters (summing the
@@ -155,7 +159,7 @@ class _FusedLoRAFn(torch.autograd.Function):
         ga: list = [None] * na
         gb: list = [None] * na
         if plan.has_lora:
-            for adapter, _batch, c0, r in plan.segment_grad_slices():
+            for adapter, c0, r in plan.adapter_grad_slices():
                 a_part, b_part = da[c0:c0 + r], db[:, c0:c0 + r]
                 ga[adapter] = a_part if ga[adapter] is None else ga[adapter] + a_part
                 gb[adapter] = b_part if gb[adapter] is None else gb[adapter] + b_part
@@ -238,7 +242,7 @@ def fused_multi_lora(
     if len(lora_a) != len(adapters) or len(lora_b) != len(adapters):
         raise ValidationError("lora_a, lora_b and adapters must have one entry per adapter slot")
     plan = LayerPlan(x2.shape[0], k, weight.shape[0], adapters, segments, offset=offset, training=training,
-                     keep_mask=keep_mask)
+                     keep_mask=keep_mask, share_blocks=grad_sink is None)
     if weights_bf16 is not None:
         plan.weights_bf16 = (list(weights_bf16[0]), list(weights_bf16[1]))
     return _run(x2, weight, lora_a, lora_b, plan, lead, grad_sink)

@@ -114,7 +114,7 @@ def routing_table(segments: Sequence[Segment], col_starts: Sequence[int], ranks:
             out.append((0, -1, 0, 0))
         else:
             lo, hi = hit[0], hit[-1]
-            out.append((lo, hi, col_starts[lo], col_starts[hi] + ranks[hi]))
+            out.append((lo, hi, min(col_starts[i] for i in hit), max(col_starts[i] + ranks[i] for i in hit)))
     return out
 
 
@@ -123,9 +123,10 @@ _ROUTES: dict[tuple, torch.Tensor] = {}
 _ROUTES_MAX = 256
 
 
-def workspace(device: torch.device, stream: torch.cuda.Stream, nbytes: int) -> torch.Tensor:
+def workspace(device: torch.device, stream: "torch.cuda.Stream | int", nbytes: int) -> torch.Tensor:
     """Zero-initialised scratch owned per (device, stream). Kernels return it to zero."""
-    key = (device.index if device.index is not None else torch.cuda.current_device(), stream.cuda_stream)
+    sid = stream if isinstance(stream, int) else stream.cuda_stream
+    key = (device.index if device.index is not None else torch.cuda.current_device(), sid)
     buf = _WORKSPACES.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.zeros(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
@@ -148,6 +149,7 @@ class LayerPlan:
         training: bool = True,
         keep_mask: torch.Tensor | None = None,
         device: torch.device | None = None,
+        share_blocks: bool = True,
     ):
         self.m, self.k, self.n = int(m), int(k), int(n)
         self.adapters = list(adapters)
@@ -155,10 +157,19 @@ class LayerPlan:
         self.offset = int(offset)
         self.training = bool(training)
         validate_segments(self.segments, self.m, len(self.adapters))
+        # Column blocks of the rank-concat dimension: one per adapter present (segments of
+        # the same adapter — e.g. two global batches in one microbatch — share it, their
+        # rows being disjoint), or, with share_blocks=False, one per segment so dA/dB can
+        # be split per (adapter, global batch) slot (FusedMultiLoRA(track_slot_grads=True)).
+        self.share_blocks = bool(share_blocks)
         self.ranks = [padded_rank(self.adapters[s.adapter].rank) for s in self.segments]
         self.col_starts = []
-        c = 0
-        for r in self.ranks:
+        c, first = 0, {}
+        for s, r in zip(self.segments, self.ranks):
+            if self.share_blocks and s.adapter in first:
+                self.col_starts.append(first[s.adapter])
+                continue
+            first[s.adapter] = c
             self.col_starts.append(c)
             c += r
         self.rank_total = c
@@ -214,13 +225,13 @@ class LayerPlan:
     # -- device ---------------------------------------------------------------------
     def bind(self, device: torch.device, stream: torch.cuda.Stream | None = None) -> "LayerPlan":
         """Build the routing table and attach the workspace on ``device``/``stream``."""
-        stream = stream or torch.cuda.current_stream(device)
         self.device = device
         lib = _lib.load()
+        dev_index = device.index if device.index is not None else torch._C._cuda_getDevice()
+        sid = stream.cuda_stream if stream is not None else torch._C._cuda_getCurrentRawStream(dev_index)
         # the routing table depends only on the segment table: built once per (device,
         # stream, m, segments) and reused by every later call with the same microbatch layout
-        dev_index = device.index if device.index is not None else torch.cuda.current_device()
-        key = (dev_index, stream.cuda_stream, self.m,
+        key = (dev_index, sid, self.m,
                tuple((s.row_start, s.row_end) for s in self.segments), tuple(self.col_starts), tuple(self.ranks))
         cached = _ROUTES.get(key)
         fresh = cached is None
@@ -231,7 +242,7 @@ class LayerPlan:
             _ROUTES[key] = cached
         self.routes = cached
         nbytes = _lib.workspace_bytes(self.m, self.rank_total)
-        self._ws = workspace(device, stream, nbytes)
+        self._ws = workspace(device, sid, nbytes)
         self.problem.routes = self.routes.data_ptr()
         self.problem.workspace = self._ws.data_ptr()
         self.problem.workspace_bytes = self._ws.numel()
@@ -242,30 +253,51 @@ class LayerPlan:
             from .functional import _call
 
             _call("build_routes", lib.lf_build_routes, ctypes.byref(self.problem), self.routes.data_ptr(),
-                  ctypes.c_void_p(stream.cuda_stream))
+                  ctypes.c_void_p(sid))
         return self
 
+    def column_blocks(self) -> list[tuple[int, int, int]]:
+        """(adapter, col_start, padded rank) of every distinct column block, in column order."""
+        seen, out = set(), []
+        for s, c0, r in zip(self.segments, self.col_starts, self.ranks):
+            if c0 not in seen:
+                seen.add(c0)
+                out.append((s.adapter, c0, r))
+        return sorted(out, key=lambda b: b[1])
+
     def gather_a(self, lora_a: Sequence[torch.Tensor]) -> torch.Tensor:
-        """A_cat (R x k, bf16): each segment's adapter lora_A.weight, zero-padded to its block."""
+        """A_cat (R x k, bf16): each column block's adapter lora_A.weight, zero-padded to it."""
         blocks = []
-        for s, r in zip(self.segments, self.ranks):
-            a = lora_a[s.adapter].to(torch.bfloat16)
+        for adapter, _c0, r in self.column_blocks():
+            a = lora_a[adapter].to(torch.bfloat16)
             if a.shape[0] != r:
                 a = torch.nn.functional.pad(a, (0, 0, 0, r - a.shape[0]))
             blocks.append(a)
         return torch.cat(blocks, 0).contiguous() if len(blocks) > 1 else blocks[0].contiguous()
 
     def gather_b(self, lora_b: Sequence[torch.Tensor]) -> torch.Tensor:
-        """B_cat (n x R, bf16): each segment's adapter lora_B.weight, zero-padded to its block."""
+        """B_cat (n x R, bf16): each column block's adapter lora_B.weight, zero-padded to it."""
         blocks = []
-        for s, r in zip(self.segments, self.ranks):
-            b = lora_b[s.adapter].to(torch.bfloat16)
+        for adapter, _c0, r in self.column_blocks():
+            b = lora_b[adapter].to(torch.bfloat16)
             if b.shape[1] != r:
                 b = torch.nn.functional.pad(b, (0, r - b.shape[1]))
             blocks.append(b)
         return torch.cat(blocks, 1).contiguous() if len(blocks) > 1 else blocks[0].contiguous()
 
+    def adapter_grad_slices(self) -> list[tuple[int, int, int]]:
+        """(adapter, col_start, rank) of every distinct column block: summing these into the
+        adapter's dA/dB covers each block exactly once."""
+        seen, out = set(), []
+        for s, c0 in zip(self.segments, self.col_starts):
+            if (s.adapter, c0) in seen:
+                continue
+            seen.add((s.adapter, c0))
+            out.append((s.adapter, c0, self.adapters[s.adapter].rank))
+        return out
+
     def segment_grad_slices(self) -> list[tuple[int, int, int, int]]:
-        """(adapter, batch, col_start, rank) for routing dA/dB columns to (adapter, batch) slots."""
+        """(adapter, batch, col_start, rank) for routing dA/dB columns to (adapter, batch) slots
+        (distinct per segment only when the plan was built with share_blocks=False)."""
         return [(s.adapter, s.batch, c0, self.adapters[s.adapter].rank)
                 for s, c0 in zip(self.segments, self.col_starts)]

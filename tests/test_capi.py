@@ -93,6 +93,7 @@ BAD = {
     "segment_rows_outside": dict(segs=((0, 300, 0, 16, 2.0, 0.0),)),
     "segments_unsorted": dict(R=32, segs=((128, 256, 0, 16, 2.0, 0.0), (0, 128, 16, 16, 2.0, 0.0))),
     "segments_overlap_cols": dict(R=32, segs=((0, 128, 0, 16, 2.0, 0.0), (128, 256, 8, 16, 2.0, 0.0))),
+    "segments_partial_overlap_cols": dict(R=32, segs=((0, 128, 0, 32, 2.0, 0.0), (128, 256, 16, 16, 2.0, 0.0))),
     "dropout_one": dict(segs=((0, 256, 0, 16, 2.0, 1.0),)),
     "dropout_negative": dict(segs=((0, 256, 0, 16, 2.0, -0.1),)),
     "scaling_nan": dict(segs=((0, 256, 0, 16, float("nan"), 0.0),)),

@@ -229,6 +229,52 @@ def test_same_adapter_two_batches_keeps_separate_slots():
     assert not torch.allclose(g0a, g1a)
 
 
+def test_shared_adapter_blocks_non_adjacent_vs_oracle():
+    """Default FusedMultiLoRA: segments of one adapter share its column block, also when
+    they are not adjacent (a0 | a1 | a0); checked against the oracle on that layout."""
+    from paper_2510_00206_b200 import AdapterConfig, FusedMultiLoRA, Segment
+
+    m, k, n = 640, 256, 200
+    g = torch.Generator().manual_seed(3)
+    x = torch.randn(m, k, generator=g).to(torch.bfloat16)
+    w = (torch.randn(n, k, generator=g) / k**0.5).to(torch.bfloat16)
+    dy = torch.randn(m, n, generator=g).to(torch.bfloat16)
+    ads = [AdapterConfig(16, 2.0, 0.1, 21), AdapterConfig(8, 1.0, 0.0, 22)]
+    layer = FusedMultiLoRA(w.to(DEV), ads, init="gaussian", generator=torch.Generator(device=DEV).manual_seed(4)).to(DEV)
+    with torch.no_grad():
+        for p_ in layer.parameters():
+            if p_.requires_grad:
+                p_.copy_(p_.to(torch.bfloat16).float())
+    segs = [Segment(0, 0, 200, 0), Segment(1, 200, 392, 0), Segment(0, 392, 640, 1)]
+    xd = x.to(DEV).requires_grad_(True)
+    y = layer(xd, segs)  # offset 0
+    y.backward(dy.to(DEV))
+    A = [layer.lora_A[i].weight.detach().cpu().to(torch.bfloat16) for i in range(2)]
+    B = [layer.lora_B[i].weight.detach().cpu().to(torch.bfloat16) for i in range(2)]
+    a_cat = torch.cat([A[0], torch.nn.functional.pad(A[1].float(), (0, 0, 0, 8)).to(torch.bfloat16)], 0)
+    b_cat = torch.cat([B[0], torch.nn.functional.pad(B[1].float(), (0, 8)).to(torch.bfloat16)], 1)
+    cols = [(0, 16), (16, 16), (0, 16)]
+    oseg = [olora.OracleSegment(s.row_start, s.row_end, c0, r, ads[s.adapter].scaling, ads[s.adapter].dropout_p,
+                                ads[s.adapter].seed) for s, (c0, r) in zip(segs, cols)]
+
+    class _A:
+        def __init__(self, p, seed):
+            self.dropout_p, self.seed = p, seed
+
+    keep = ophilox.keep_mask(m, k, [(i, s.row_start, s.row_end) for i, s in enumerate(oseg)],
+                             [_A(s.dropout_p, s.seed) for s in oseg], 0)
+    xf, wf, dyf = x.float().numpy(), w.float().numpy(), dy.float().numpy()
+    af, bf = a_cat.float().numpy(), b_cat.float().numpy()
+    y_ref, s_hat = olora.forward(xf, wf, af, bf, oseg, keep)
+    dx_ref, da_ref, db_ref, _ = olora.backward(dyf, xf, wf, af, bf, s_hat, oseg, keep)
+    H.assert_chain_close(y.detach().float().cpu().numpy(), y_ref, "shared:y")
+    H.assert_chain_close(xd.grad.float().cpu().numpy(), dx_ref, "shared:dx")
+    H.assert_chain_close(layer.lora_A[0].weight.grad.cpu().numpy(), da_ref[0:16], "shared:dA0")
+    H.assert_chain_close(layer.lora_B[0].weight.grad.cpu().numpy(), db_ref[:, 0:16], "shared:dB0")
+    H.assert_chain_close(layer.lora_A[1].weight.grad.cpu().numpy(), da_ref[16:24], "shared:dA1")
+    H.assert_chain_close(layer.lora_B[1].weight.grad.cpu().numpy(), db_ref[:, 16:24], "shared:dB1")
+
+
 def test_frozen_linear_no_adapter_matches_fp32_torch():
     """num_segments = 0: the tcgen05 GEMMs alone (Y = X·Wᵀ, dX = dY·W) vs a torch fp32 reference."""
     from paper_2510_00206_b200 import AdapterConfig, fused_multi_lora

@@ -6,6 +6,7 @@ import os
 
 import numpy as np
 import pytest
+import torch
 
 from oracle import routing as orouting
 from paper_2510_00206_b200 import AdapterConfig, LayerPlan, Segment, padded_rank, segments_from_lengths
@@ -37,7 +38,21 @@ def test_adapter_config_validation():
 def test_plan_columns_and_problem():
     ads = [AdapterConfig(8, 2.0, 0.0, 1), AdapterConfig(16, 1.0, 0.1, 2), AdapterConfig(64, 0.5, 0.1, 3)]
     segs = segments_from_lengths([0, 1, 2, 1], [100, 200, 300, 50], batches=[0, 0, 0, 1])
-    plan = LayerPlan(700, 256, 128, ads, segs, offset=5)
+    # default: one column block per adapter (segments 1 and 3 = adapter 1 share it)
+    shared = LayerPlan(700, 256, 128, ads, segs, offset=5)
+    assert shared.col_starts == [0, 16, 32, 16] and shared.rank_total == 96
+    assert shared.adapter_grad_slices() == [(0, 0, 8), (1, 16, 16), (2, 32, 64)]
+    assert shared.column_blocks() == [(0, 0, 16), (1, 16, 16), (2, 32, 64)]
+    a_cat = shared.gather_a([torch.full((r.rank, 256), float(i + 1)) for i, r in enumerate(ads)])
+    b_cat = shared.gather_b([torch.full((128, r.rank), float(i + 1)) for i, r in enumerate(ads)])
+    assert a_cat.shape == (96, 256) and b_cat.shape == (128, 96)
+    assert a_cat[:8].eq(1).all() and a_cat[8:16].eq(0).all() and a_cat[16:32].eq(2).all() and a_cat[32:].eq(3).all()
+    assert b_cat[:, 16:32].eq(2).all() and b_cat[:, 8:16].eq(0).all()
+    assert shared.host_routes()[5] == (3, 3, 16, 32)  # rows 640..699: segment 3 only
+    assert shared.host_routes()[4] == (2, 3, 16, 96)  # segments 2|3: hull of blocks [32,96) and [16,32)
+    assert shared.host_routes()[2] == (1, 2, 16, 96)  # rows 256..383 straddle segments 1|2
+    # per-(adapter, batch) slots: one block per segment
+    plan = LayerPlan(700, 256, 128, ads, segs, offset=5, share_blocks=False)
     assert plan.ranks == [16, 16, 64, 16]
     assert plan.col_starts == [0, 16, 32, 96]
     assert plan.rank_total == 112
@@ -51,6 +66,19 @@ def test_plan_columns_and_problem():
     # eval mode: no dropout anywhere
     ev = LayerPlan(700, 256, 128, ads, segs, training=False)
     assert not ev.needs_keep_bits and all(ev.problem.segments[i].dropout_p == 0 for i in range(4))
+
+
+def test_shared_blocks_non_adjacent_routes_hull():
+    """a0, a1, a0: the third segment reuses block 0, so a tile straddling a1|a0 spans the
+    hull [0, 32) — the device table (lf_build_routes) and the oracle agree on it."""
+    ads = [AdapterConfig(16), AdapterConfig(8)]
+    segs = [Segment(0, 0, 200), Segment(1, 200, 392), Segment(0, 392, 640, 1)]
+    plan = LayerPlan(640, 64, 64, ads, segs)
+    assert plan.col_starts == [0, 16, 0] and plan.rank_total == 32
+    ref = orouting.routes([(s.row_start, s.row_end) for s in segs], list(zip(plan.col_starts, plan.ranks)), 640)
+    assert np.array_equal(np.array(plan.host_routes(), np.int32), ref)
+    assert tuple(ref[3]) == (1, 2, 0, 32)  # rows 384..511
+    assert orouting.column_blocks([16, 8, 16], adapters=[0, 1, 0]) == [0, 16, 0]
 
 
 def test_plan_rejects_bad_tables():
