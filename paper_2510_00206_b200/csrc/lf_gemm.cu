@@ -138,7 +138,7 @@ __device__ __forceinline__ uint32_t dgrad_keep32(const LfSegTable& t, int seg, i
 // response once, in order, and releases it on the leader's `empty` barrier (11 readers:
 // 2 producers, the MMA warp, 8 epilogue warps). Only the leader's producer requests, and
 // only after the previous response named a tile, so no request is left unread at exit.
-// Static (LF_SCHED_STATIC=1, for A/B measurements): tile i = pair + i * npairs.
+// Static (operands that fit in L2 together, or LF_SCHED=1): tile i = pair + i * npairs.
 struct TileSeq {
   uint64_t* full;   // [kSeqDepth] per CTA: response landed
   uint64_t* empty;  // [kSeqDepth] leader: all readers done
@@ -548,8 +548,14 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
   args.tiles_m = (args.M + 255) / 256;
   args.tiles_n = (args.N + 255) / 256;
   if (args.group <= 0) args.group = 8;
-  static const int sched_static = [] { const char* e = getenv("LF_SCHED_STATIC"); return e ? atoi(e) : 0; }();
-  args.dynamic = sched_static ? 0 : 1;
+  // Tile schedule. While both operands fit in L2 together, the static persistent
+  // round-robin is ~5% faster (C2 q/kv, C1: no per-tile CLC round trip and the pairs'
+  // drift costs nothing); beyond that, drifting pairs re-read their operands from DRAM
+  // and the in-order CLC schedule wins (C4 q 1.49 -> 1.43 ms, gate 5.5 -> 5.08 ms; ncu,
+  // profiles/r01_sched_shapes.txt). LF_SCHED=1 forces static, 2 dynamic (A/B runs).
+  static const int sched_env = [] { const char* e = getenv("LF_SCHED"); return e ? atoi(e) : 0; }();
+  const double operand_bytes = 2.0 * ((double)args.M + (double)args.N) * (double)args.K;
+  args.dynamic = sched_env == 1 ? 0 : sched_env == 2 ? 1 : (operand_bytes > 128.0 * (1 << 20) ? 1 : 0);
   switch (kind) {
     case kGemmFwd:
       return launch_one<false, false, 6>(maps, args, num_sms, stream);
