@@ -262,7 +262,7 @@ def workload_name(config: str) -> str:
 # --------------------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------------------
-def build_layers(config: str, m: int, r: int, p: float, device, gen, use_fused: bool = True):
+def build_layers(config: str, m: int, r: int, p: float, device, gen, capturable: bool = False):
     import torch
 
     from paper_2510_00206_b200 import FusedLoRA, FusedMultiLoRA
@@ -272,10 +272,10 @@ def build_layers(config: str, m: int, r: int, p: float, device, gen, use_fused: 
         w = (torch.randn(n, k, generator=gen, device=device, dtype=torch.float32) / k**0.5).to(torch.bfloat16)
         if config == "c3":
             adapters = [dataclasses.replace(a, seed=a.seed + 100 * i) for a in c3_adapters()]
-            layer = FusedMultiLoRA(w, adapters, init="gaussian", generator=gen).to(device)
+            layer = FusedMultiLoRA(w, adapters, init="gaussian", generator=gen, capturable=capturable).to(device)
         else:
             layer = FusedLoRA(w, rank=r, scaling=2.0, dropout_p=p, seed=1234 + i, init="gaussian",
-                              generator=gen).to(device)
+                              generator=gen, capturable=capturable).to(device)
         layers[name] = layer
         if grp not in inputs:
             # activations come from the previous layer: they need dX (⑤ runs every step)
@@ -386,7 +386,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     gen = torch.Generator(device=device).manual_seed(1000 + rank)
     r, p = 16, args.dropout
     m = tokens_per_gpu(args.config)
-    layers, inputs, grads = build_layers(args.config, m, r, p, device, gen)
+    layers, inputs, grads = build_layers(args.config, m, r, p, device, gen, capturable=args.graph)
 
     def barrier():
         if world > 1:
@@ -404,27 +404,41 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         fused_step(args.config, layers, inputs, grads, world)
 
     # ---- device-resident timed region (value) ----------------------------------------
-    for _ in range(args.warmup):
-        step()
-    # launch counting is host-side only (no events): it does not perturb the timed loop
+    # launch counting is host-side only (no events): one eager step, before any capture
     counts = F_.LaunchStats(timed=False)
+    F_.set_launch_stats(counts)
+    step()
+    F_.set_launch_stats(None)
+    launches = counts.total_launches() * args.steps
+    if args.graph:
+        # the whole fwd+bwd step (all projections, and the all-reduce when world > 1) as
+        # one CUDA graph: the host leaves the loop (capturable layers: device Philox counter)
+        from paper_2510_00206_b200.graphs import GraphedStep
+
+        try:
+            run = GraphedStep(step, warmup=args.warmup).replay
+        except Exception as e:  # e.g. a collective that cannot be captured: time eagerly
+            print(f"[bench] CUDA-graph capture failed ({type(e).__name__}: {e}); timing eagerly", file=sys.stderr)
+            args.graph = False
+            run = step
+    else:
+        run = step
+    for _ in range(args.warmup):
+        run()
     clocks = ClockSampler(local_rank)
     barrier()
     torch.cuda.synchronize()
     clocks.start()
-    F_.set_launch_stats(counts)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
     for _ in range(args.steps):
-        step()
+        run()
     t1.record()
     torch.cuda.synchronize()
-    F_.set_launch_stats(None)
     clk = clocks.stop()
     barrier()
     ms = max_over_ranks(t0.elapsed_time(t1) / args.steps)
-    launches = counts.total_launches()
     # per-launcher CUDA-event timing in a separate pass over the same steps (events on the
     # launching stream bracket every launcher; kept out of the headline loop)
     stats = F_.LaunchStats(timed=True)
@@ -509,6 +523,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                 "scaling": 2.0,
                 "dropout_p": list(C3_DROPOUT) if args.config == "c3" else p,
                 "parallelism": f"dp{world}",
+                "execution": "one CUDA graph per step (capturable layers)" if args.graph else "eager",
                 "l2": "inputs larger than L2 (≈2 GB touched per step vs 126 MB L2)",
             },
             "tflops": world * flops / (ms * 1e-3) / 1e12,
@@ -540,13 +555,18 @@ def measure_c3(args, device, gen, world, barrier, max_over_ranks):
     import torch
 
     m = tokens_per_gpu("c3")
-    layers, inputs, grads = build_layers("c3", m, 0, 0.0, device, gen)
+    layers, inputs, grads = build_layers("c3", m, 0, 0.0, device, gen, capturable=args.graph)
 
     def step():
         zero_grads(layers, inputs)
         fused_step("c3", layers, inputs, grads, world)
 
-    ms = max_over_ranks(time_loop(step, args.steps, args.warmup, barrier))
+    run = step
+    if args.graph:
+        from paper_2510_00206_b200.graphs import GraphedStep
+
+        run = GraphedStep(step, warmup=args.warmup).replay
+    ms = max_over_ranks(time_loop(run, args.steps, args.warmup, barrier))
     base = unfused_base("c3", layers)
     unf = max_over_ranks(time_loop(lambda: unfused_step("c3", base, inputs, grads, 0.0), max(2, args.steps // 2),
                                    args.warmup, barrier))
@@ -761,6 +781,8 @@ def main() -> None:
     ap.add_argument("--cpu-sample-tokens", type=int, default=256)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=True,
+                    help="time the step as one captured CUDA graph (default) or eagerly")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 

@@ -49,7 +49,7 @@ extern "C" {
 #define LF_API
 #endif
 
-#define LF_ABI_VERSION 2
+#define LF_ABI_VERSION 3
 #define LF_MAX_SEGMENTS 32
 #define LF_MAX_RANK_TOTAL 128
 #define LF_ROUTE_TILE_ROWS 128 /* ls/costmodel.py:25 ROUTING_TILE_ROWS */
@@ -90,6 +90,10 @@ typedef struct LfProblem {
    * with p > 0; lf_grad_down / lf_grad_input read it instead of re-running Philox.
    * NULL: every kernel regenerates the mask. Ignored when keep_mask is set. */
   uint8_t* keep_bits;
+  /* device, optional: a uint64 step counter added to every segment's Philox offset,
+   * read by the kernels when they run — so a captured CUDA graph that advances it on
+   * the device draws a fresh mask on every replay. NULL: offsets are the host values. */
+  const uint64_t* offset_dev;
 } LfProblem;
 
 /* Bytes of zero-initialised scratch one problem needs (split-K partials + tile counters). */

@@ -13,7 +13,7 @@ from pathlib import Path
 
 from .errors import ExtensionMissingError, KernelError, ValidationError
 
-LF_ABI_VERSION = 2
+LF_ABI_VERSION = 3
 LF_MAX_SEGMENTS = 32
 LF_MAX_RANK_TOTAL = 128
 ROUTE_TILE_ROWS = 128  # ls/costmodel.py:25
@@ -69,6 +69,7 @@ class LfProblem(ctypes.Structure):
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_size_t),
         ("keep_bits", ctypes.c_void_p),
+        ("offset_dev", ctypes.c_void_p),
     ]
 
 

@@ -206,6 +206,9 @@ int validate(const LfProblem* p, bool need_routes, lf::LfSegTable* t) {
     }
   }
   if (need_routes && p->num_segments > 0 && !p->routes) return fail(LF_E_INVALID, "routes is NULL (call lf_build_routes)");
+  if (p->offset_dev && (reinterpret_cast<uintptr_t>(p->offset_dev) & 7u))
+    return fail(LF_E_INVALID, "offset_dev must be 8-byte aligned");
+  t->off_dev = p->offset_dev;
   return LF_OK;
 }
 

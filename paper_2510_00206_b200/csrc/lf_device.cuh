@@ -427,9 +427,21 @@ __host__ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t
   return c;
 }
 
+// Philox counter words 2..3 of a segment: its host offset plus the device step counter
+// (LfSegTable::off_dev, 0 when absent) — read once per thread after pdl_wait()
+__device__ __forceinline__ uint64_t table_offset(const LfSegTable& t) { return t.off_dev ? *t.off_dev : 0ull; }
+__device__ __forceinline__ void seg_offset_words(const LfSegDev& s, uint64_t extra, uint32_t& o0, uint32_t& o1) {
+  const uint64_t o = ((((uint64_t)s.off1) << 32) | (uint64_t)s.off0) + extra;
+  o0 = (uint32_t)o;
+  o1 = (uint32_t)(o >> 32);
+}
+
 // keep bits (bit e = column col8*8+e kept) for 8 consecutive columns of one row
-__device__ __forceinline__ uint32_t philox_keep8(uint32_t col8, uint32_t row, const LfSegDev& s) {
-  const U4 r = philox4x32_10(U4{col8, row, s.off0, s.off1}, s.key0, s.key1);
+__device__ __forceinline__ uint32_t philox_keep8(uint32_t col8, uint32_t row, const LfSegDev& s,
+                                                 uint64_t extra_offset = 0) {
+  uint32_t o0, o1;
+  seg_offset_words(s, extra_offset, o0, o1);
+  const U4 r = philox4x32_10(U4{col8, row, o0, o1}, s.key0, s.key1);
   const uint32_t thr = s.thr;
   uint32_t bits = 0;
   bits |= ((r.x & 0xFFFFu) >= thr) ? 0x01u : 0u;
@@ -453,7 +465,7 @@ struct PhiloxRow {
   uint32_t hthr2;  // thr / 2 in both 16-bit halves (SWAR keep test)
 };
 
-__device__ __forceinline__ PhiloxRow philox_row(const LfSegDev& s, uint32_t row) {
+__device__ __forceinline__ PhiloxRow philox_row(const LfSegDev& s, uint32_t row, uint64_t extra_offset = 0) {
   PhiloxRow pr;
   uint32_t a = s.key0, b = s.key1;
 #pragma unroll
@@ -464,8 +476,7 @@ __device__ __forceinline__ PhiloxRow philox_row(const LfSegDev& s, uint32_t row)
     b += 0xBB67AE85u;
   }
   pr.c1 = row;
-  pr.c2 = s.off0;
-  pr.c3 = s.off1;
+  seg_offset_words(s, extra_offset, pr.c2, pr.c3);
   pr.thr2 = s.thr | (s.thr << 16);
   pr.hthr2 = (s.thr >> 1) * 0x00010001u;
   return pr;

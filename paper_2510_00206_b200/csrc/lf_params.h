@@ -34,6 +34,7 @@ struct LfSegTable {
   int64_t ld_bits;      // = k / 8
   int32_t debug;        // profiling knobs (env LF_DEBUG, default 0): skip pipeline pieces, results invalid
   int32_t pad_;
+  const uint64_t* off_dev;  // device step counter added to every segment's Philox offset, or null
   LfSegDev seg[LF_MAX_SEGS];
 };
 

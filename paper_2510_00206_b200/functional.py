@@ -198,6 +198,7 @@ def fused_lora(
     keep_mask: torch.Tensor | None = None,
     training: bool = True,
     weights_bf16: tuple | None = None,
+    offset_dev: torch.Tensor | None = None,
 ) -> torch.Tensor:
     """Y = X·Wᵀ + scaling·dropout(X)·Aᵀ·Bᵀ  (Eq. 1) on one adapter.
 
@@ -206,13 +207,15 @@ def fused_lora(
     keyed by (seed, offset) unless ``keep_mask`` (uint8, m x k) is given.
     ``weights_bf16 = (a_bf16, b_bf16)``: bf16 copies of fp32 master weights kept current by
     the caller (the modules refresh them when the parameters change); default: cast here.
+    ``offset_dev``: one-element int64 CUDA tensor added to ``offset`` when the kernels run
+    (CUDA-graph capture: advance it on the device between replays).
     """
     k = weight.shape[1]
     x2, lead = _flatten_input(x, k)
     m = x2.shape[0]
     adapter = AdapterConfig(rank=lora_a.shape[0], scaling=float(scaling), dropout_p=float(dropout_p), seed=int(seed))
     plan = LayerPlan(m, k, weight.shape[0], [adapter], [Segment(0, 0, m)] if m > 0 else [], offset=offset,
-                     training=training, keep_mask=keep_mask)
+                     training=training, keep_mask=keep_mask, offset_dev=offset_dev)
     if weights_bf16 is not None:
         plan.weights_bf16 = ([weights_bf16[0]], [weights_bf16[1]])
     return _run(x2, weight, [lora_a], [lora_b], plan, lead, None)
@@ -230,6 +233,7 @@ def fused_multi_lora(
     training: bool = True,
     grad_sink: Callable | None = None,
     weights_bf16: tuple | None = None,
+    offset_dev: torch.Tensor | None = None,
 ) -> torch.Tensor:
     """Mixed-adapter microbatch: rows of ``segments`` route to their adapter's A/B, scale
     and dropout; the frozen W is streamed once for all of them.
@@ -242,7 +246,7 @@ def fused_multi_lora(
     if len(lora_a) != len(adapters) or len(lora_b) != len(adapters):
         raise ValidationError("lora_a, lora_b and adapters must have one entry per adapter slot")
     plan = LayerPlan(x2.shape[0], k, weight.shape[0], adapters, segments, offset=offset, training=training,
-                     keep_mask=keep_mask, share_blocks=grad_sink is None)
+                     keep_mask=keep_mask, share_blocks=grad_sink is None, offset_dev=offset_dev)
     if weights_bf16 is not None:
         plan.weights_bf16 = (list(weights_bf16[0]), list(weights_bf16[1]))
     return _run(x2, weight, lora_a, lora_b, plan, lead, grad_sink)

@@ -1,0 +1,45 @@
+"""CUDA-graph capture of fused LoRA training steps.
+
+A FusedLoRA forward+backward is a handful of launches plus host work (segment plan,
+C-ABI argument packing, autograd); at small token counts (C1: 2048 tokens) the host side
+takes longer than the kernels. Capturing the whole step once and replaying it removes
+the host from the loop. Layers must be built with ``capturable=True`` so the Philox step
+counter advances on the device (a fresh dropout mask per replay, SPEC.md §3) and the bf16
+operand copies are re-cast from the fp32 master weights inside the graph.
+
+    step = GraphedStep(lambda: train_step(...))   # warm-up + capture
+    for _ in range(n):
+        step.replay()
+
+Inputs/outputs of the captured region are static: refill input tensors in place (copy_)
+before a replay; gradients land in the same ``.grad`` tensors every replay.
+"""
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+
+from .errors import ValidationError
+
+
+class GraphedStep:
+    """Warm ``fn`` up on a side stream, then capture one call of it into a CUDA graph."""
+
+    def __init__(self, fn: Callable[[], object], warmup: int = 3, pool=None):
+        if not torch.cuda.is_available():
+            raise ValidationError("CUDA graphs need a CUDA device")
+        self.fn = fn
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(max(1, warmup)):
+                fn()
+        torch.cuda.current_stream().wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, pool=pool):
+            self.output = fn()
+
+    def replay(self):
+        self.graph.replay()
+        return self.output

@@ -68,6 +68,26 @@ def _frozen_base(base: nn.Linear | torch.Tensor) -> tuple[torch.Tensor, torch.Te
     return w, bias
 
 
+def _init_capturable(mod: nn.Module, capturable: bool, device) -> None:
+    """``capturable=True`` (as torch.optim's flag): the module's Philox step counter lives on
+    the device and is advanced there by every training forward, and the bf16 operand copies
+    of the fp32 adapter weights are re-cast inside each call, so a forward+backward captured
+    in a CUDA graph replays with a fresh dropout mask and the current weights."""
+    mod.capturable = bool(capturable)
+    if mod.capturable:
+        mod.register_buffer("step_counter", torch.zeros(1, dtype=torch.int64, device=device), persistent=False)
+
+
+def _step_offsets(mod: nn.Module) -> tuple[int, torch.Tensor | None]:
+    """(host offset, device counter) of this forward (SPEC.md §3)."""
+    if not mod.training:
+        return 0, None
+    if mod.capturable:
+        mod.step_counter.add_(1)  # on the device: captured into a graph with the kernels
+        return 0, mod.step_counter
+    return mod.next_offset(), None
+
+
 class FusedLoRA(nn.Module):
     """Single-adapter LoRA linear: Y = X·Wᵀ (+ bias) + scaling·dropout(X)·Aᵀ·Bᵀ."""
 
@@ -83,6 +103,7 @@ class FusedLoRA(nn.Module):
         init: str = "peft",
         dtype: torch.dtype = torch.float32,
         generator: torch.Generator | None = None,
+        capturable: bool = False,
     ):
         super().__init__()
         w, bias = _frozen_base(base)
@@ -90,6 +111,7 @@ class FusedLoRA(nn.Module):
         self.base = base if isinstance(base, nn.Linear) else None
         self.register_buffer("weight", w, persistent=False) if self.base is None else None
         self.out_features, self.in_features = w.shape
+        _init_capturable(self, capturable, w.device)
         if scaling is None:
             scaling = (alpha if alpha is not None else 32.0) / rank
         self.config = AdapterConfig(rank=rank, scaling=float(scaling), dropout_p=float(dropout_p), seed=int(seed))
@@ -115,6 +137,7 @@ class FusedLoRA(nn.Module):
 
     def forward(self, x: torch.Tensor, keep_mask: torch.Tensor | None = None) -> torch.Tensor:
         c = self.config
+        off, off_dev = _step_offsets(self)
         y = fused_lora(
             x,
             self.base_weight,
@@ -123,10 +146,12 @@ class FusedLoRA(nn.Module):
             c.scaling,
             c.dropout_p,
             seed=c.seed,
-            offset=self.next_offset() if self.training else 0,
+            offset=off,
             keep_mask=keep_mask,
             training=self.training,
-            weights_bf16=(self._shadow(self.lora_A.weight), self._shadow(self.lora_B.weight)),
+            weights_bf16=None if self.capturable else (self._shadow(self.lora_A.weight),
+                                                       self._shadow(self.lora_B.weight)),
+            offset_dev=off_dev,
         )
         if self.base_bias is not None:
             y = y + self.base_bias
@@ -151,6 +176,7 @@ class FusedMultiLoRA(nn.Module):
         dtype: torch.dtype = torch.float32,
         track_slot_grads: bool = False,
         generator: torch.Generator | None = None,
+        capturable: bool = False,
     ):
         super().__init__()
         if not adapters:
@@ -160,6 +186,7 @@ class FusedMultiLoRA(nn.Module):
         self.base = base if isinstance(base, nn.Linear) else None
         self.register_buffer("weight", w, persistent=False) if self.base is None else None
         self.out_features, self.in_features = w.shape
+        _init_capturable(self, capturable, w.device)
         self.adapters = list(adapters)
         dev = w.device
         self.lora_A = nn.ModuleList(
@@ -178,6 +205,11 @@ class FusedMultiLoRA(nn.Module):
     def base_weight(self) -> torch.Tensor:
         return self.base.weight if self.base is not None else self.weight
 
+    def next_offset(self) -> int:
+        off = self._offset
+        self._offset += 1
+        return off
+
     def _sink(self, plan: LayerPlan, da: torch.Tensor, db: torch.Tensor) -> None:
         for adapter, batch, c0, r in plan.segment_grad_slices():
             ga, gb = da[c0:c0 + r], db[:, c0:c0 + r]
@@ -190,9 +222,7 @@ class FusedMultiLoRA(nn.Module):
 
     def forward(self, x: torch.Tensor, segments: Sequence[Segment],
                 keep_mask: torch.Tensor | None = None) -> torch.Tensor:
-        off = self._offset if self.training else 0
-        if self.training:
-            self._offset += 1
+        off, off_dev = _step_offsets(self)
         y = fused_multi_lora(
             x,
             self.base_weight,
@@ -204,7 +234,9 @@ class FusedMultiLoRA(nn.Module):
             keep_mask=keep_mask,
             training=self.training,
             grad_sink=self._sink if self.track_slot_grads else None,
-            weights_bf16=([self._shadow(la.weight) for la in self.lora_A], [self._shadow(lb.weight) for lb in self.lora_B]),
+            weights_bf16=None if self.capturable else ([self._shadow(la.weight) for la in self.lora_A],
+                                                       [self._shadow(lb.weight) for lb in self.lora_B]),
+            offset_dev=off_dev,
         )
         if self.base is not None and self.base.bias is not None:
             y = y + self.base.bias

@@ -150,6 +150,7 @@ class LayerPlan:
         keep_mask: torch.Tensor | None = None,
         device: torch.device | None = None,
         share_blocks: bool = True,
+        offset_dev: torch.Tensor | None = None,
     ):
         self.m, self.k, self.n = int(m), int(k), int(n)
         self.adapters = list(adapters)
@@ -200,6 +201,13 @@ class LayerPlan:
             d.seed = int(a.seed) & (2**64 - 1)
             d.offset = self.offset & (2**64 - 1)
         p.keep_mask = keep_mask.data_ptr() if (keep_mask is not None and self.training) else None
+        # device-resident step counter added to the Philox offsets when the kernels run
+        # (CUDA-graph replays then draw fresh masks); SPEC.md §3
+        self.offset_dev = offset_dev
+        if offset_dev is not None:
+            if offset_dev.dtype != torch.int64 or offset_dev.numel() != 1 or not offset_dev.is_cuda:
+                raise ValidationError("offset_dev must be a one-element int64 CUDA tensor")
+            p.offset_dev = offset_dev.data_ptr()
         self.routes: torch.Tensor | None = None
         self._ws: torch.Tensor | None = None
         # ① writes the Philox keep mask bit-packed (m x k/8 bytes); ④/⑤ read it back

@@ -54,16 +54,17 @@ def test_struct_layout_matches_c(tmp_path):
     src = tmp_path / "layout.c"
     src.write_text(
         '#include <stdio.h>\n#include <stddef.h>\n#include "lorafusion_b200.h"\n'
-        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(LfSegment), sizeof(LfProblem),"
+        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(LfSegment), sizeof(LfProblem),"
         " offsetof(LfProblem, segments), offsetof(LfProblem, routes), offsetof(LfProblem, keep_mask),"
-        " offsetof(LfProblem, workspace), offsetof(LfProblem, workspace_bytes), offsetof(LfProblem, keep_bits));"
+        " offsetof(LfProblem, workspace), offsetof(LfProblem, workspace_bytes), offsetof(LfProblem, keep_bits),"
+        " offsetof(LfProblem, offset_dev));"
         "return 0;}\n")
     exe = tmp_path / "layout"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
     P = _lib.LfProblem
     want = [ctypes.sizeof(_lib.LfSegment), ctypes.sizeof(P), P.segments.offset, P.routes.offset, P.keep_mask.offset,
-            P.workspace.offset, P.workspace_bytes.offset, P.keep_bits.offset]
+            P.workspace.offset, P.workspace_bytes.offset, P.keep_bits.offset, P.offset_dev.offset]
     assert got == want
 
 
