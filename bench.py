@@ -299,23 +299,43 @@ def adapter_params(layers):
 
 def fused_step(config, layers, inputs, grads, world, flat_grad=None):
     """fwd+bwd of every projection through the public module API; grads all-reduced if world>1."""
-    import torch
-
     call = layer_call(config)
     for name, k, n, grp in projections(config):
         y = call(layers[name], inputs[grp])
         y.backward(grads[name])
     if world > 1:
-        import torch.distributed as dist
+        allreduce_grads(layers)
 
-        params = adapter_params(layers)
-        flat = torch.cat([p.grad.reshape(-1) for p in params])
-        dist.all_reduce(flat)
-        off = 0
-        for p in params:
-            n_ = p.numel()
-            p.grad.copy_(flat[off:off + n_].view_as(p))
-            off += n_
+
+def allreduce_grads(layers):
+    """The one data-parallel exchange: SUM all-reduce of the flat fp32 adapter gradients."""
+    import torch
+    import torch.distributed as dist
+
+    params = adapter_params(layers)
+    flat = torch.cat([p.grad.reshape(-1) for p in params])
+    dist.all_reduce(flat)
+    off = 0
+    for p in params:
+        n_ = p.numel()
+        p.grad.copy_(flat[off:off + n_].view_as(p))
+        off += n_
+
+
+def graphed_runner(step_local, world, layers, warmup):
+    """One CUDA graph for the rank-local fwd+bwd; the NCCL all-reduce (world > 1) runs
+    eagerly after each replay, so no collective is ever captured."""
+    from paper_2510_00206_b200.graphs import GraphedStep
+
+    g = GraphedStep(step_local, warmup=warmup)
+    if world == 1:
+        return g.replay
+
+    def run():
+        g.replay()
+        allreduce_grads(layers)
+
+    return run
 
 
 def zero_grads(layers, inputs=None):
@@ -403,6 +423,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         zero_grads(layers, inputs)
         fused_step(args.config, layers, inputs, grads, world)
 
+    def step_local():
+        zero_grads(layers, inputs)
+        fused_step(args.config, layers, inputs, grads, 1)
+
     # ---- device-resident timed region (value) ----------------------------------------
     # launch counting is host-side only (no events): one eager step, before any capture
     counts = F_.LaunchStats(timed=False)
@@ -413,10 +437,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     if args.graph:
         # the whole fwd+bwd step (all projections, and the all-reduce when world > 1) as
         # one CUDA graph: the host leaves the loop (capturable layers: device Philox counter)
-        from paper_2510_00206_b200.graphs import GraphedStep
-
         try:
-            run = GraphedStep(step, warmup=args.warmup).replay
+            run = graphed_runner(step_local, world, layers, args.warmup)
         except Exception as e:  # e.g. a collective that cannot be captured: time eagerly
             print(f"[bench] CUDA-graph capture failed ({type(e).__name__}: {e}); timing eagerly", file=sys.stderr)
             args.graph = False
@@ -561,11 +583,11 @@ def measure_c3(args, device, gen, world, barrier, max_over_ranks):
         zero_grads(layers, inputs)
         fused_step("c3", layers, inputs, grads, world)
 
-    run = step
-    if args.graph:
-        from paper_2510_00206_b200.graphs import GraphedStep
+    def step_local():
+        zero_grads(layers, inputs)
+        fused_step("c3", layers, inputs, grads, 1)
 
-        run = GraphedStep(step, warmup=args.warmup).replay
+    run = graphed_runner(step_local, world, layers, args.warmup) if args.graph else step
     ms = max_over_ranks(time_loop(run, args.steps, args.warmup, barrier))
     base = unfused_base("c3", layers)
     unf = max_over_ranks(time_loop(lambda: unfused_step("c3", base, inputs, grads, 0.0), max(2, args.steps // 2),
@@ -789,6 +811,10 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test knob: every rank on cuda:0 over gloo, to exercise the N > 1 code path on a 1-GPU box
+    share_gpu = os.environ.get("LF_BENCH_SHARE_GPU") == "1"
+    if share_gpu:
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -797,7 +823,10 @@ def main() -> None:
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         if args.config == "c5":
             run_c5(args, rank, world, local_rank)

@@ -1,7 +1,7 @@
-timeout 600 python -m pytest tests -m gpu -q 2>&1 | tail -3
-for c in c1 c2; do for g in --graph --no-graph; do timeout 300 python bench.py --config $c $g --steps 20 --no-multi --no-e2e --no-cpu-baseline 2>&1 | python -c "
-import sys,json
-ls=[l for l in sys.stdin if l.startswith('{')]
-if not ls: print('$c $g FAILED'); sys.exit()
-d=json.loads(ls[-1]); r=d['roofline']
-print('$c $g ms %.3f'%d['ms_per_step'], 'unf x%.3f'%d['unfused_torch']['speedup'], 'launches', d['gpu_launches'], d['clocks']['sm_mhz'], {k:round(v['ms_per_step'],3) for k,v in r['per_kernel'].items()})"; done; done
+export LF_BENCH_SHARE_GPU=1
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench_n2.log 2>&1; echo n2=$?
+tail -c 600 gpurun_out/bench_n2.log
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 2 --steps 3 --warmup 3 --impl reference > gpurun_out/bench_n2_ref.log 2>&1; echo n2ref=$?
+tail -c 300 gpurun_out/bench_n2_ref.log
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 2 --config c5 --layers 2 --mb-per-rank 1 --steps 2 --warmup 3 > gpurun_out/bench_n2_c5.log 2>&1; echo n2c5=$?
+tail -c 400 gpurun_out/bench_n2_c5.log
