@@ -383,3 +383,20 @@ def test_errors_are_loud_and_typed():
     with pytest.raises(ValidationError, match="multiples of 8"):
         xx = torch.randn(64, 60, device=DEV).to(torch.bfloat16)
         fused_lora(xx, torch.randn(64, 60, device=DEV).to(torch.bfloat16), a[:, :60].contiguous(), b, 2.0)
+
+
+@pytest.mark.parametrize("sched", ["1", "2"], ids=["static", "clc"])
+def test_every_case_under_each_gemm_schedule(sched):
+    """The GEMM launcher picks its tile schedule by operand size (static persistent vs
+    cluster-launch-control dynamic), so the small parity cases above mostly run static:
+    re-run the whole per-kernel oracle matrix with each schedule forced (LF_SCHED is read
+    once per process, hence the subprocess)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LF_SCHED=sched)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_parity.py"), "-k", "test_kernels_match_oracle",
+                        "-m", "gpu"], cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
