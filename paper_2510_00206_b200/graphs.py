@@ -38,7 +38,10 @@ class GraphedStep:
         torch.cuda.current_stream().wait_stream(side)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph, pool=pool):
-            self.output = fn()
+            out = fn()
+        # keep only the static output buffer, never the captured autograd graph (a live
+        # graph pins AccumulateGrad nodes to the capture stream)
+        self.output = out.detach() if isinstance(out, torch.Tensor) else out
 
     def replay(self):
         self.graph.replay()

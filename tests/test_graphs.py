@@ -15,7 +15,8 @@ DEV = "cuda"
 
 
 def _close(a, b, tol=2e-3):
-    return float((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-12)) <= tol
+    a, b = a.detach().float(), b.detach().float()
+    return float((a - b).norm() / b.norm().clamp_min(1e-12)) <= tol
 
 
 def test_graphed_fused_lora_matches_eager_offset_and_redraws_mask():
@@ -33,7 +34,7 @@ def test_graphed_fused_lora_matches_eager_offset_and_redraws_mask():
         cap.lora_A.weight.grad = cap.lora_B.weight.grad = x.grad = None
         y = cap(x)
         y.backward(dy)
-        return y
+        return y.detach()
 
     graphed = GraphedStep(step, warmup=3)  # warm-up runs offsets 1..3; capture runs nothing
     outs = []
@@ -74,7 +75,7 @@ def test_graphed_multi_lora_replays_track_weight_updates():
             p.grad = None
         y = layer(x, segs)
         y.backward(dy)
-        return y
+        return y.detach()
 
     graphed = GraphedStep(step)
     y0 = graphed.replay().clone()
