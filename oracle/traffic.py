@@ -54,6 +54,11 @@ def kernels(m, k, n, r, e=2, variant="unfused", pass_name="forward", mask_bytes=
         if variant == "fused_multi_lora":
             out.append(("adapter_routing_table", math.ceil(m / 128) * 16, 0))
         return out
+    if variant == "b200_built":
+        bits = m * -(-k // 8)  # bit-packed keep mask
+        rows = kernels(m, k, n, r, e, "b200_minimal", pass_name)
+        add = {"dropout_down_proj_fused": (0, bits), "grad_down_fused": (bits, 0), "grad_base_accum_fused": (bits, 0)}
+        return [(nm, rd + add.get(nm, (0, 0))[0], wr + add.get(nm, (0, 0))[1]) for nm, rd, wr in rows]
     if variant == "b200_minimal":
         f = 4  # fp32 gradient accumulators
         if fwd:

@@ -3,10 +3,12 @@ traffic API (ls/costmodel.py:21-124, 158-216, 219-306), extended with ``b200_min
 
 The reference's variants ``unfused`` / ``fused_lora`` / ``fused_multi_lora`` keep their
 kernel names and byte counts exactly (pinned by tests/golden/traffic_reference.json,
-generated from lorasched itself); ``b200_minimal`` is the traffic of the kernels this
-repo actually runs on sm_100a: the dropout mask is regenerated from Philox in ①, ④
-and ⑤ instead of being stored, ④ writes no mk-sized LoRA input-gradient (the term is
-accumulated inside ⑤'s GEMM), and dA/dB are fp32 accumulators.
+generated from lorasched itself); ``b200_minimal`` is SURVEY.md §8(d)'s floor for this
+design: the dropout mask is regenerated from Philox instead of being stored, ④ writes no
+mk-sized LoRA input-gradient (the term is accumulated inside ⑤'s GEMM), and dA/dB are
+fp32 accumulators; ``b200_built`` is what the sm_100a kernels actually move with dropout
+on — ``b200_minimal`` plus the bit-packed keep mask ① writes and ④/⑤ read (m·k/8 bytes
+each way, 1/16 of X), which replaces two of the three Philox passes.
 
 Every kernel is a table row of (name, read terms, write terms): a term is a
 (coefficient, monomial) pair over the operand sizes mk, mn, kn, mr, kr, rn, with
@@ -23,7 +25,7 @@ from .errors import ValidationError
 MASK_BYTES = 1
 ROUTING_TILE_ROWS = 128
 ROUTING_ENTRY_BYTES = 16
-VARIANTS = ("unfused", "fused_lora", "fused_multi_lora", "b200_minimal")
+VARIANTS = ("unfused", "fused_lora", "fused_multi_lora", "b200_minimal", "b200_built")
 PASSES = ("forward", "backward")
 
 
@@ -117,8 +119,9 @@ class TrafficReport:
         }
 
 
-# (name, reads, writes); unit "e" = element bytes, "mask" = 1 B, "f32" = 4 B
-_E, _M, _F = "e", "mask", "f32"
+# (name, reads, writes); unit "e" = element bytes, "mask" = 1 B, "f32" = 4 B, "byte" = 1 B
+# (with the "mk8" size: the bit-packed keep mask, m x ceil(k/8) bytes)
+_E, _M, _F, _B = "e", "mask", "f32", "byte"
 _TABLE = {
     ("frozen", "forward"): [
         ("base_gemm", [(_E, "mk"), (_E, "kn")], [(_E, "mn")]),
@@ -160,6 +163,17 @@ _TABLE = {
         ("grad_down_fused", [(_E, "mk"), (_E, "mr")], [(_F, "kr")]),
         ("grad_base_accum_fused", [(_E, "mn"), (_E, "kn"), (_E, "mr"), (_E, "kr")], [(_E, "mk")]),
     ],
+    # what the built kernels move with dropout on: ① writes the Philox keep mask
+    # bit-packed (m x k/8 bytes) so ④ and ⑤ read it instead of re-running Philox
+    ("b200_built", "forward"): [
+        ("dropout_down_proj_fused", [(_E, "mk"), (_E, "kr")], [(_E, "mr"), (_B, "mk8")]),
+        ("base_gemm_epilogue_fused", [(_E, "mk"), (_E, "kn"), (_E, "mr"), (_E, "rn")], [(_E, "mn")]),
+    ],
+    ("b200_built", "backward"): [
+        ("grad_up_fused", [(_E, "mn"), (_E, "rn"), (_E, "mr")], [(_E, "mr"), (_F, "rn")]),
+        ("grad_down_fused", [(_E, "mk"), (_E, "mr"), (_B, "mk8")], [(_F, "kr")]),
+        ("grad_base_accum_fused", [(_E, "mn"), (_E, "kn"), (_E, "mr"), (_E, "kr"), (_B, "mk8")], [(_E, "mk")]),
+    ],
 }
 
 
@@ -175,8 +189,8 @@ def traffic(shape: GemmShape, pass_name: str, variant: str) -> TrafficReport:
     if variant not in VARIANTS:
         raise ValidationError(f"variant must be one of {VARIANTS}, got {variant!r}")
     m, k, n, r = shape.m, shape.k, shape.n, shape.r
-    sizes = {"mk": m * k, "mn": m * n, "kn": k * n, "mr": m * r, "kr": k * r, "rn": r * n}
-    unit = {_E: shape.element_bytes, _M: MASK_BYTES, _F: 4}
+    sizes = {"mk": m * k, "mn": m * n, "kn": k * n, "mr": m * r, "kr": k * r, "rn": r * n, "mk8": m * -(-k // 8)}
+    unit = {_E: shape.element_bytes, _M: MASK_BYTES, _F: 4, _B: 1}
     if r == 0:
         key = "frozen"
     elif variant in ("fused_lora", "fused_multi_lora"):

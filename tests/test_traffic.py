@@ -79,6 +79,26 @@ def test_b200_minimal_formulas():
     assert abs(total / 1e6 - 186.0) < 0.5
 
 
+def test_b200_built_adds_the_packed_keep_mask():
+    """b200_built = b200_minimal + the bit-packed keep mask: written by ①, read by ④ and ⑤."""
+    m, k, n, r = 2048, 4100, 4096, 16
+    s = T.GemmShape(m, k, n, r)
+    bits = m * ((k + 7) // 8)
+    for ps in ("forward", "backward"):
+        mini = {kk.kernel: (kk.bytes_read, kk.bytes_written) for kk in T.traffic(s, ps, "b200_minimal").kernels}
+        built = {kk.kernel: (kk.bytes_read, kk.bytes_written) for kk in T.traffic(s, ps, "b200_built").kernels}
+        assert mini.keys() == built.keys()
+        for name, (rd, wr) in built.items():
+            drd, dwr = rd - mini[name][0], wr - mini[name][1]
+            want = {"dropout_down_proj_fused": (0, bits), "grad_down_fused": (bits, 0),
+                    "grad_base_accum_fused": (bits, 0)}.get(name, (0, 0))
+            assert (drd, dwr) == want, name
+    assert T.roundtrip_bytes(s, "b200_built") - T.roundtrip_bytes(s, "b200_minimal") == 3 * bits
+    for ps in ("forward", "backward"):  # the oracle's independent restatement agrees
+        ours = [(kk.kernel, kk.bytes_read, kk.bytes_written) for kk in T.traffic(s, ps, "b200_built").kernels]
+        assert ours == [tuple(x) for x in otraffic.kernels(m, k, n, r, 2, "b200_built", ps)]
+
+
 @given(m=st.integers(1, 1 << 14), k=st.integers(1, 1 << 13), n=st.integers(1, 1 << 13), r=st.integers(1, 64))
 @settings(max_examples=100, deadline=None)
 def test_b200_design_never_exceeds_reference_fused(m, k, n, r):
