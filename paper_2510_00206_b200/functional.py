@@ -98,6 +98,45 @@ def _check_operand(t: torch.Tensor, name: str, shape: tuple | None = None) -> No
         raise ValidationError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
 
 
+class OperandCache:
+    """bf16 rank-concat operands (A_cat, B_cat) of a module, keyed by the column-block
+    layout and the in-place versions of the adapter parameters: every layer call between
+    two optimizer steps that sees the same adapters reuses them instead of re-casting,
+    padding and concatenating (a dozen small launches of host work per call)."""
+
+    def __init__(self, capacity: int = 8):
+        self.capacity = capacity
+        self._d: dict = {}
+
+    def get(self, key):
+        return self._d.get(key)
+
+    def put(self, key, value) -> None:
+        if len(self._d) >= self.capacity:
+            self._d.pop(next(iter(self._d)))
+        self._d[key] = value
+
+
+def _rank_concat_operands(plan: LayerPlan, params, n_adapters: int):
+    cache: OperandCache | None = plan.operand_cache
+    key = None
+    if cache is not None:
+        blocks = plan.column_blocks()
+        used = sorted({a for a, _, _ in blocks})
+        key = (tuple((a, r) for a, _, r in blocks),
+               tuple((p.data_ptr(), p._version) for a in used for p in (params[a], params[n_adapters + a])))
+        hit = cache.get(key)
+        if hit is not None:
+            return hit
+    # bf16 operand copies: the module's cached shadows when given, else cast here
+    shadows = plan.weights_bf16
+    a_cat = plan.gather_a(shadows[0] if shadows else params[:n_adapters])
+    b_cat = plan.gather_b(shadows[1] if shadows else params[n_adapters:])
+    if cache is not None:
+        cache.put(key, (a_cat, b_cat))
+    return a_cat, b_cat
+
+
 class _FusedLoRAFn(torch.autograd.Function):
     """Autograd node over the five kernels.
 
@@ -115,10 +154,7 @@ class _FusedLoRAFn(torch.autograd.Function):
         s_hat = a_cat = b_cat = None
         st = _stream(x.device)
         if plan.has_lora:
-            # bf16 operand copies: the module's cached shadows when given, else cast here
-            shadows = plan.weights_bf16
-            a_cat = plan.gather_a(shadows[0] if shadows else params[:n_adapters])
-            b_cat = plan.gather_b(shadows[1] if shadows else params[n_adapters:])
+            a_cat, b_cat = _rank_concat_operands(plan, params, n_adapters)
             s_hat = torch.empty((m, R), dtype=_BF16, device=x.device)
             _call("dropout_down_fwd", lib.lf_dropout_down_fwd, pp, _ptr(x), _ptr(a_cat), _ptr(s_hat), st)
         _call("base_fwd", lib.lf_base_fwd, pp, _ptr(x), _ptr(w), _ptr(s_hat), _ptr(b_cat), _ptr(y), st)
@@ -199,6 +235,7 @@ def fused_lora(
     training: bool = True,
     weights_bf16: tuple | None = None,
     offset_dev: torch.Tensor | None = None,
+    operand_cache: OperandCache | None = None,
 ) -> torch.Tensor:
     """Y = X·Wᵀ + scaling·dropout(X)·Aᵀ·Bᵀ  (Eq. 1) on one adapter.
 
@@ -218,6 +255,7 @@ def fused_lora(
                      training=training, keep_mask=keep_mask, offset_dev=offset_dev)
     if weights_bf16 is not None:
         plan.weights_bf16 = ([weights_bf16[0]], [weights_bf16[1]])
+    plan.operand_cache = operand_cache
     return _run(x2, weight, [lora_a], [lora_b], plan, lead, None)
 
 
@@ -234,6 +272,7 @@ def fused_multi_lora(
     grad_sink: Callable | None = None,
     weights_bf16: tuple | None = None,
     offset_dev: torch.Tensor | None = None,
+    operand_cache: OperandCache | None = None,
 ) -> torch.Tensor:
     """Mixed-adapter microbatch: rows of ``segments`` route to their adapter's A/B, scale
     and dropout; the frozen W is streamed once for all of them.
@@ -249,6 +288,7 @@ def fused_multi_lora(
                      keep_mask=keep_mask, share_blocks=grad_sink is None, offset_dev=offset_dev)
     if weights_bf16 is not None:
         plan.weights_bf16 = (list(weights_bf16[0]), list(weights_bf16[1]))
+    plan.operand_cache = operand_cache
     return _run(x2, weight, lora_a, lora_b, plan, lead, grad_sink)
 
 

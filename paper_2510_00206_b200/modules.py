@@ -3,8 +3,10 @@
 Both wrap a frozen ``nn.Linear`` (or its weight) and keep adapter parameters under the
 PEFT names ``lora_A.weight`` (r x k) and ``lora_B.weight`` (n x r), so a PEFT/HF LoRA
 layer's state dict maps onto them directly. Adapter parameters default to fp32 master
-weights (cast to bf16 per call, gradients arrive in fp32 for the optimizer and the DP
-all-reduce); the base weight and activations are bf16.
+weights: their bf16 rank-concat operands are built once per weight update and reused
+(functional.OperandCache, keyed by the parameters' in-place versions), and gradients
+arrive in fp32 for the optimizer and the DP all-reduce; the base weight and activations
+are bf16.
 
 Dropout masks come from SPEC.md §3's counter-based Philox stream: each training forward
 uses (seed, offset) with ``offset`` advanced once per call, and backward reuses the
@@ -19,7 +21,7 @@ import torch
 from torch import nn
 
 from .errors import ValidationError
-from .functional import fused_lora, fused_multi_lora
+from .functional import OperandCache, fused_lora, fused_multi_lora
 from .plan import AdapterConfig, LayerPlan, Segment
 
 
@@ -35,25 +37,6 @@ def _init_lora(a: nn.Linear, b: nn.Linear, init: str, generator: torch.Generator
             b.weight.normal_(0.0, 1.0 / math.sqrt(b.weight.shape[1]), generator=generator)
         else:
             raise ValidationError(f"unknown init {init!r} (expected 'peft' or 'gaussian')")
-
-
-class _Bf16Shadow:
-    """bf16 operand copies of fp32 master parameters, refreshed only when a parameter
-    changes (its storage or in-place version), as a mixed-precision optimizer would keep
-    its model weights. bf16 parameters are used as they are."""
-
-    def __init__(self):
-        self._cache: dict[int, tuple] = {}
-
-    def __call__(self, p: torch.Tensor) -> torch.Tensor:
-        if p.dtype == torch.bfloat16:
-            return p.detach()
-        key = (p.data_ptr(), p._version, tuple(p.shape))
-        hit = self._cache.get(id(p))
-        if hit is None or hit[0] != key:
-            hit = (key, p.detach().to(torch.bfloat16))
-            self._cache[id(p)] = hit
-        return hit[1]
 
 
 def _frozen_base(base: nn.Linear | torch.Tensor) -> tuple[torch.Tensor, torch.Tensor | None]:
@@ -120,7 +103,7 @@ class FusedLoRA(nn.Module):
         self.lora_B = nn.Linear(rank, self.out_features, bias=False, device=dev, dtype=dtype)
         _init_lora(self.lora_A, self.lora_B, init, generator)
         self._offset = 0
-        self._shadow = _Bf16Shadow()
+        self._operands = OperandCache()
 
     @property
     def base_weight(self) -> torch.Tensor:
@@ -149,9 +132,8 @@ class FusedLoRA(nn.Module):
             offset=off,
             keep_mask=keep_mask,
             training=self.training,
-            weights_bf16=None if self.capturable else (self._shadow(self.lora_A.weight),
-                                                       self._shadow(self.lora_B.weight)),
             offset_dev=off_dev,
+            operand_cache=None if self.capturable else self._operands,
         )
         if self.base_bias is not None:
             y = y + self.base_bias
@@ -196,7 +178,7 @@ class FusedMultiLoRA(nn.Module):
         for la, lb in zip(self.lora_A, self.lora_B):
             _init_lora(la, lb, init, generator)
         self._offset = 0
-        self._shadow = _Bf16Shadow()
+        self._operands = OperandCache()
         self.track_slot_grads = track_slot_grads
         # (adapter slot, global batch) -> [dA (r x k) fp32, dB (n x r) fp32]
         self.slot_grads: dict[tuple[int, int], list[torch.Tensor]] = {}
@@ -234,9 +216,8 @@ class FusedMultiLoRA(nn.Module):
             keep_mask=keep_mask,
             training=self.training,
             grad_sink=self._sink if self.track_slot_grads else None,
-            weights_bf16=None if self.capturable else ([self._shadow(la.weight) for la in self.lora_A],
-                                                       [self._shadow(lb.weight) for lb in self.lora_B]),
             offset_dev=off_dev,
+            operand_cache=None if self.capturable else self._operands,
         )
         if self.base is not None and self.base.bias is not None:
             y = y + self.base.bias

@@ -217,6 +217,8 @@ class LayerPlan:
         # optional bf16 copies of the adapter weights (lora_A list, lora_B list) kept by a
         # module in step with its fp32 master parameters; None = cast on every call
         self.weights_bf16: tuple | None = None
+        # optional functional.OperandCache of the calling module (A_cat / B_cat reuse)
+        self.operand_cache = None
 
     # -- derived ------------------------------------------------------------------
     @property
