@@ -12,7 +12,8 @@
 // columns) — half the shared-memory operand traffic per FLOP of a single-CTA 128x256 tile.
 //   warp 0      TMA producer (one lane per CTA)
 //   warp 1      MMA issuer (one lane, leader CTA only) + TMEM allocation (both CTAs)
-//   warps 2..5  epilogue: tcgen05.ld -> bf16 -> global (and, for ⑤ with dropout, the mask pass)
+//   warps 2..9  epilogue, two per TMEM lane quadrant (half the columns each): tcgen05.ld -> bf16
+//               -> global (and, for ⑤ with dropout, the mask pass)
 // The low-rank up-projection is NOT an epilogue GEMM: [X | Ŝ]·[W | B_cat]ᵀ — the rank-R
 // LoRA operands are streamed as extra K-blocks into the same accumulator, so the output
 // tile is written exactly once and the epilogue stays a pure convert.
@@ -29,6 +30,9 @@
 #include "lf_kernels.h"
 
 namespace lf {
+
+constexpr int kEpiWarps = 8;                         // warps 2..9
+constexpr int kGemmThreads = 32 * (2 + kEpiWarps);   // producer, MMA, epilogue
 
 // control block after the operand ring: mbarriers, TMEM slot, tile-sequence ring
 constexpr int kGemmCtlBytes = 512;
@@ -135,8 +139,8 @@ __device__ __forceinline__ uint32_t dgrad_keep32(const LfSegTable& t, int seg, i
 // onto data no other pair is reading (a static round-robin persistent schedule let them
 // drift and re-read W from DRAM: 15 GB vs 4.8 GB per C4 gate launch, ncu).
 // Response i (i >= 1) sits in slot (i-1) % kSeqDepth; every role of both CTAs reads each
-// response once, in order, and releases it on the leader's `empty` barrier (11 readers:
-// 2 producers, the MMA warp, 8 epilogue warps). Only the leader's producer requests, and
+// response once, in order, and releases it on the leader's `empty` barrier (19 readers:
+// 2 producers, the MMA warp, 16 epilogue warps). Only the leader's producer requests, and
 // only after the previous response named a tile, so no request is left unread at exit.
 // Static (operands that fit in L2 together, or LF_SCHED=1): tile i = pair + i * npairs.
 struct TileSeq {
@@ -146,7 +150,7 @@ struct TileSeq {
   int pair, npairs, tiles;
   bool dynamic;
 
-  static constexpr uint32_t kReaders = 11;
+  static constexpr uint32_t kReaders = 19;  // 2 producers + the MMA warp + 2 x 8 epilogue warps
 
   __device__ int first() const { return pair < tiles ? pair : -1; }
   // leader producer only: ask for response i
@@ -178,7 +182,7 @@ struct TileSeq {
 };
 
 template <bool B_MN, bool MASKED, int STAGES>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     lf_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                    const __grid_constant__ GemmArgs args) {
@@ -189,9 +193,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);  // leader: both halves landed
   uint64_t* empty = full + STAGES;   // both CTAs: stage consumed (multicast commit)
   uint64_t* tfull = empty + STAGES;  // [2] both CTAs: main loop done
-  uint64_t* tempty = tfull + 2;      // [2] leader: both CTAs drained the accumulator (count 8)
+  uint64_t* tempty = tfull + 2;      // [2] leader: both CTAs drained the accumulator (16 warps)
   uint64_t* lfull = tempty + 2;      // [2] both CTAs: LoRA partial ready                 MASKED
-  uint64_t* lmasked = lfull + 2;     // [2] leader: both CTAs masked their partial (8)   MASKED
+  uint64_t* lmasked = lfull + 2;     // [2] leader: both CTAs masked their partial (16)  MASKED
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lmasked + 2);
   uint8_t* ctl = smem + STAGES * Cfg::STAGE_BYTES;
   TileSeq seq;
@@ -213,9 +217,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);
+      mbar_init(&tempty[a], 2 * kEpiWarps);
       mbar_init(&lfull[a], 1);
-      mbar_init(&lmasked[a], 8);
+      mbar_init(&lmasked[a], 2 * kEpiWarps);
     }
     for (int i = 0; i < kSeqDepth; ++i) {
       mbar_init(&seq.full[i], 1);
@@ -418,8 +422,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     }
     __syncwarp();
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2..5, both CTAs)
+    // ------------------------------------------------------------ epilogue (warps 2..9, both CTAs)
+    // two warps per TMEM lane quadrant, each owning half of the tile's columns: the drain and
+    // the ⑤ mask pass run at twice the width (short-K tiles were bound by them)
     const uint32_t q = warp & 3u;  // TMEM lane quadrant this warp may access
+    const int c_lo = (warp >= 6 ? 1 : 0) * (BN / 2), c_hi = c_lo + BN / 2;
     const uint32_t tempty_leader[2] = {mapa_shared(smem_u32(&tempty[0]), 0), mapa_shared(smem_u32(&tempty[1]), 0)};
     const uint32_t lmasked_leader[2] = {mapa_shared(smem_u32(&lmasked[0]), 0),
                                         mapa_shared(smem_u32(&lmasked[1]), 0)};
@@ -436,13 +443,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         seg = find_segment(args.segs, rt.seg_lo, rt.seg_hi, row);
       }
       bool active = seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0);
-      // keep bits of the row's BN columns, fetched before waiting on the LoRA partial
-      uint32_t keep[BN / 32];
+      // keep bits of the row's columns [c_lo, c_hi), fetched before waiting on the LoRA partial
+      uint32_t keep[BN / 64];
 #pragma unroll
-      for (int j = 0; j < BN / 32; ++j)
+      for (int j = 0; j < BN / 64; ++j)
         keep[j] = !active ? 0xFFFFFFFFu
                   : (args.segs.debug & 128) ? 0x7FFFFFFFu  // profiling: skip the bit loads, keep the TMEM pass
-                                            : dgrad_keep32(args.segs, seg, row, ti.nb * BN + 32 * j, args.N);
+                                            : dgrad_keep32(args.segs, seg, row, ti.nb * BN + c_lo + 32 * j, args.N);
       if (args.segs.debug & 64) active = false;
       uint32_t& lu = acc ? lora_uses1 : lora_uses0;
       mbar_wait(&lfull[acc], lu & 1);
@@ -452,8 +459,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       if (__any_sync(0xFFFFFFFFu, active)) {
         const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * Cfg::ACC_COLS;
 #pragma unroll
-        for (int c = 0; c < BN; c += 32) {
-          const uint32_t kp = keep[c / 32];
+        for (int j = 0; j < BN / 64; ++j) {
+          const int c = c_lo + 32 * j;
+          const uint32_t kp = keep[j];
           if (__all_sync(0xFFFFFFFFu, kp == 0xFFFFFFFFu)) continue;
           uint32_t v[32];
           tmem_ld32(taddr + c, v);
@@ -476,9 +484,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       const uint32_t aph = (it >> 1) & 1;
       int tn = -1;
       if constexpr (MASKED) {
-        if (it == 0 && ti.lora()) mask_pass(ti, 0);
+        const bool plain = (args.segs.debug & 4096) != 0;  // profiling: the MMA issues no LoRA-first blocks
+        if (it == 0 && ti.lora() && !plain) mask_pass(ti, 0);
         tn = seq.read(it + 1, lane == 0);
-        if (tn >= 0) {
+        if (tn >= 0 && !plain) {
           const TileInfo tni = tile_info(args, s_routes, tn);
           if (tni.lora()) mask_pass(tni, it + 1);
         }
@@ -490,7 +499,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * Cfg::ACC_COLS;
       __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(args.C) + (int64_t)row * args.ldc;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = c_lo; c < c_hi; c += 32) {
         uint32_t v[32];
         tmem_ld32(taddr + c, v);
         tmem_ld_wait();
@@ -538,7 +547,7 @@ static int launch_one(const GemmMaps& maps, const GemmArgs& args, int num_sms, c
   // dynamic: one cluster per tile (the resident pairs take over the rest through CLC);
   // static (A/B measurements only): one persistent pair per SM pair, round-robin tiles
   const int pairs = args.dynamic ? tiles : (tiles < num_sms / 2 ? tiles : num_sms / 2);
-  if (launch_k(kern, dim3(2 * pairs), dim3(192), Cfg::SMEM_BYTES, stream, maps.a, maps.b, maps.a2, maps.b2, args))
+  if (launch_k(kern, dim3(2 * pairs), dim3(kGemmThreads), Cfg::SMEM_BYTES, stream, maps.a, maps.b, maps.a2, maps.b2, args))
     return -1;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
