@@ -400,3 +400,61 @@ def test_every_case_under_each_gemm_schedule(sched):
                         os.path.join(root, "tests", "test_gpu_parity.py"), "-k", "test_kernels_match_oracle",
                         "-m", "gpu"], cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_max_segments_many_per_tile_vs_oracle():
+    """32 segments (the ABI maximum) of 4 adapters interleaved a0 a1 a2 a3 a0 ..., 24..40 rows
+    each: up to 6 segments share a 128-row tile, every adapter's block is shared by 8
+    segments (R = 16+16+32+64 = 128, the maximum), dropout on three of the adapters."""
+    from paper_2510_00206_b200 import AdapterConfig, FusedMultiLoRA, Segment
+
+    rng = np.random.default_rng(5)
+    lens = rng.integers(24, 41, size=32)
+    m, k, n = int(lens.sum()), 192, 160
+    segs, row = [], 0
+    for i, L in enumerate(lens):
+        segs.append(Segment(i % 4, row, row + int(L), i // 4))
+        row += int(L)
+    ads = [AdapterConfig(8, 2.0, 0.1, 31), AdapterConfig(16, 1.0, 0.0, 32), AdapterConfig(32, 0.5, 0.2, 33),
+           AdapterConfig(64, 2.0, 0.05, 34)]
+    g = torch.Generator().manual_seed(6)
+    x = torch.randn(m, k, generator=g).to(torch.bfloat16)
+    w = (torch.randn(n, k, generator=g) / k**0.5).to(torch.bfloat16)
+    dy = torch.randn(m, n, generator=g).to(torch.bfloat16)
+    layer = FusedMultiLoRA(w.to(DEV), ads, init="gaussian", generator=torch.Generator(device=DEV).manual_seed(7)).to(DEV)
+    with torch.no_grad():
+        for p_ in layer.parameters():
+            if p_.requires_grad:
+                p_.copy_(p_.to(torch.bfloat16).float())
+    layer._offset = 3
+    xd = x.to(DEV).requires_grad_(True)
+    y = layer(xd, segs)
+    y.backward(dy.to(DEV))
+    cols = {0: 0, 1: 16, 2: 32, 3: 64}
+    pr = {0: 16, 1: 16, 2: 32, 3: 64}
+    a_cat = torch.zeros(128, k)
+    b_cat = torch.zeros(n, 128)
+    for a in range(4):
+        A = layer.lora_A[a].weight.detach().cpu()
+        B = layer.lora_B[a].weight.detach().cpu()
+        a_cat[cols[a]:cols[a] + A.shape[0]] = A
+        b_cat[:, cols[a]:cols[a] + B.shape[1]] = B
+    oseg = [olora.OracleSegment(s.row_start, s.row_end, cols[s.adapter], pr[s.adapter], ads[s.adapter].scaling,
+                                ads[s.adapter].dropout_p, ads[s.adapter].seed) for s in segs]
+
+    class _A:
+        def __init__(self, p, seed):
+            self.dropout_p, self.seed = p, seed
+
+    keep = ophilox.keep_mask(m, k, [(i, s.row_start, s.row_end) for i, s in enumerate(oseg)],
+                             [_A(s.dropout_p, s.seed) for s in oseg], 3)
+    xf, wf, dyf = x.float().numpy(), w.float().numpy(), dy.float().numpy()
+    af, bf = a_cat.to(torch.bfloat16).float().numpy(), b_cat.to(torch.bfloat16).float().numpy()
+    y_ref, s_hat = olora.forward(xf, wf, af, bf, oseg, keep)
+    dx_ref, da_ref, db_ref, _ = olora.backward(dyf, xf, wf, af, bf, s_hat, oseg, keep)
+    H.assert_chain_close(y.detach().float().cpu().numpy(), y_ref, "seg32:y")
+    H.assert_chain_close(xd.grad.float().cpu().numpy(), dx_ref, "seg32:dx")
+    for a in range(4):
+        r = ads[a].rank
+        H.assert_chain_close(layer.lora_A[a].weight.grad.cpu().numpy(), da_ref[cols[a]:cols[a] + r], f"seg32:dA{a}")
+        H.assert_chain_close(layer.lora_B[a].weight.grad.cpu().numpy(), db_ref[:, cols[a]:cols[a] + r], f"seg32:dB{a}")
