@@ -484,6 +484,16 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         if name in lrb:
             ent["gbs"] = lrb[name] / (tot * 1e-3) / 1e9
         kernels[name] = ent
+    for name, ent in kernels.items():
+        if name in lrb:
+            ent["frac_of_hbm"] = ent["gbs"] / peaks["hbm_gbs"]
+    if p > 0 and args.config != "c3" and "dropout_down_fwd" in kernels:
+        # ① is bound by Philox4x32-10 (integer multiplies), not by HBM: its own floor is the
+        # standalone keep-mask generator (lf_keep_bits: Philox + bit packing, no X stream)
+        floor = philox_floor_ms(args.config, m, p, device)
+        kernels["dropout_down_fwd"]["bound"] = "alu (Philox4x32-10 keep mask)"
+        kernels["dropout_down_fwd"]["philox_floor_ms_per_step"] = floor
+        kernels["dropout_down_fwd"]["frac_of_philox_floor"] = floor / kernels["dropout_down_fwd"]["ms_per_step"]
     gemm_ms = sum(kernels[n]["ms_per_step"] for n in ("base_fwd", "grad_input") if n in kernels)
     gemm_tf = (gfl["base_fwd"] + gfl["grad_input"]) / (gemm_ms * 1e-3) / 1e12 if gemm_ms else 0.0
     traffic = gemm_traffic()
@@ -569,6 +579,38 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                 "sample": f"{args.cpu_sample_tokens} tokens of each projection, fwd+bwd, numpy float64 oracle",
             }
         print(json.dumps(line), flush=True)
+
+
+def philox_floor_ms(config: str, m: int, p: float, device) -> float:
+    """ms per step of the bare keep-mask generator (lf_keep_bits, C ABI) over every
+    projection's m x k dropout mask: the ALU floor of ① (CUDA events, median of 5)."""
+    import ctypes
+
+    import torch
+
+    from paper_2510_00206_b200 import AdapterConfig, LayerPlan, Segment, _lib
+    from paper_2510_00206_b200.functional import _stream
+
+    lib = _lib.load()
+    total = 0.0
+    for name, k, n, grp in projections(config):
+        plan = LayerPlan(m, k, n, [AdapterConfig(16, 2.0, p, 1234)], [Segment(0, 0, m)], offset=1)
+        plan.bind(device)
+        bits = torch.empty((m, k // 8), dtype=torch.uint8, device=device)
+        st = _stream(device)
+        fn = lambda: _lib.check(lib.lf_keep_bits(ctypes.byref(plan.problem), ctypes.c_void_p(bits.data_ptr()), st),  # noqa: E731
+                                "keep_bits")
+        fn()
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        total += sorted(ts)[2]
+    return total
 
 
 def measure_c3(args, device, gen, world, barrier, max_over_ranks):
