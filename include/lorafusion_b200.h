@@ -79,7 +79,8 @@ typedef struct LfProblem {
   int32_t m, k, n;          /* tokens, in_features, out_features */
   int32_t rank_total;       /* R: width of the rank-concat dim (multiple of 16, <= 128) */
   int32_t num_segments;     /* 0 .. LF_MAX_SEGMENTS (0 = frozen linear, no adapter) */
-  int32_t reserved;
+  int32_t row_base;         /* added to every row index of the Philox counter (SPEC.md §3): a microbatch
+                               split over several calls keeps its masks; 0 otherwise */
   LfSegment segments[LF_MAX_SEGMENTS];
   const int32_t* routes;    /* device: ceil(m/128) x 4 int32, from lf_build_routes */
   const uint8_t* keep_mask; /* device, optional explicit m x k keep mask (1 keep, 0 drop); NULL = Philox */

@@ -62,7 +62,7 @@ class LfProblem(ctypes.Structure):
         ("n", ctypes.c_int32),
         ("rank_total", ctypes.c_int32),
         ("num_segments", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("row_base", ctypes.c_int32),
         ("segments", LfSegment * LF_MAX_SEGMENTS),
         ("routes", ctypes.c_void_p),
         ("keep_mask", ctypes.c_void_p),

@@ -156,6 +156,8 @@ int validate(const LfProblem* p, bool need_routes, lf::LfSegTable* t) {
   t->nseg = p->num_segments;
   t->m = p->m;
   t->rtot = p->rank_total;
+  if (p->row_base < 0) return fail(LF_E_INVALID, "row_base must be >= 0, got %d", p->row_base);
+  t->row_base = p->row_base;
   bool any_dropout = false;
   int prev_row = 0;
   for (int i = 0; i < p->num_segments; ++i) {

@@ -109,7 +109,7 @@ __device__ __noinline__ uint32_t dgrad_keep32_slow(const LfSegTable& t, int seg,
   for (int j = 0; j < 4; ++j) {
     const int cc = col + 8 * j;
     const uint32_t b = (t.mask_mode == 2) ? explicit_keep8(t.mask + (int64_t)row * t.ld_mask, cc, ncols)
-                                           : philox_keep8((uint32_t)cc >> 3, (uint32_t)row, t.seg[seg], table_offset(t));
+                                           : philox_keep8((uint32_t)cc >> 3, (uint32_t)(row + t.row_base), t.seg[seg], table_offset(t));
     v |= b << (8 * j);
   }
   return v;

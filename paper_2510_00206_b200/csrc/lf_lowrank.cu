@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kDownThreads, 2)
       if (gated) {
         const int seg = row < args.m ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
         const bool my_mask = seg >= 0 && (explicit_mask || args.segs.seg[seg].thr != 0);
-        const PhiloxRow pr = philox_row(args.segs.seg[seg >= 0 ? seg : 0], (uint32_t)row, step_offset);
+        const PhiloxRow pr = philox_row(args.segs.seg[seg >= 0 ? seg : 0], (uint32_t)(row + args.segs.row_base), step_offset);
         uint8_t* bits_row = args.segs.bits ? args.segs.bits + (int64_t)row * args.segs.ld_bits : nullptr;
         for (int kb = sp.k0; kb < sp.k1; ++kb) {
           // the keep bits depend only on (row, column, seed, offset): generate them while the
@@ -321,7 +321,7 @@ __device__ __noinline__ void dgrad_a_keep_slow(const LfSegTable& t, int seg, int
     b0 = keep_bits64_explicit(t, row, col, ncols);
     b1 = keep_bits64_explicit(t, row, col + 64, ncols);
   } else {
-    const PhiloxRow pr = philox_row(t.seg[seg], (uint32_t)row, table_offset(t));
+    const PhiloxRow pr = philox_row(t.seg[seg], (uint32_t)(row + t.row_base), table_offset(t));
     b0 = keep_bits64_philox(pr, col);
     b1 = keep_bits64_philox(pr, col + 64);
   }
@@ -613,7 +613,7 @@ __global__ void lf_mask_kernel(const __grid_constant__ LfSegTable segs, int32_t 
   uint32_t bits = 0xFFu;
   const int seg = find_segment(segs, 0, segs.nseg - 1, row);
   if (seg >= 0 && segs.mask_mode == 1 && segs.seg[seg].thr)
-    bits = philox_keep8((uint32_t)g, (uint32_t)row, segs.seg[seg], table_offset(segs));
+    bits = philox_keep8((uint32_t)g, (uint32_t)(row + segs.row_base), segs.seg[seg], table_offset(segs));
   uint8_t* out = keep + (int64_t)row * k + g * 8;
   for (int e = 0; e < 8; ++e)
     if (g * 8 + e < k) out[e] = (uint8_t)((bits >> e) & 1u);
@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(256) lf_keep_bits_kernel(const __grid_constant
     uint64_t b = ~0ull;
     if (seg >= 0 && segs.seg[seg].thr) {
       uint32_t msk[8][4];
-      b = philox_masks<8>(philox_row(segs.seg[seg], (uint32_t)row, table_offset(segs)), g * 64, msk);
+      b = philox_masks<8>(philox_row(segs.seg[seg], (uint32_t)(row + segs.row_base), table_offset(segs)), g * 64, msk);
     }
     uint8_t* out = bits + (int64_t)row * ld + g * 8;
     const int nbytes = min(8, (k - g * 64 + 7) / 8);

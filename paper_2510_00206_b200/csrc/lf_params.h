@@ -33,7 +33,7 @@ struct LfSegTable {
   uint8_t* bits;        // bit-packed Philox keep mask (m x ld_bits bytes) when mask_mode == 1, or null
   int64_t ld_bits;      // = k / 8
   int32_t debug;        // profiling knobs (env LF_DEBUG, default 0): skip pipeline pieces, results invalid
-  int32_t pad_;
+  int32_t row_base;     // added to the row word of every Philox counter (LfProblem::row_base)
   const uint64_t* off_dev;  // device step counter added to every segment's Philox offset, or null
   LfSegDev seg[LF_MAX_SEGS];
 };

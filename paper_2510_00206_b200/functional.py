@@ -18,7 +18,7 @@ import torch
 
 from . import _lib
 from .errors import ValidationError
-from .plan import AdapterConfig, LayerPlan, Segment
+from .plan import AdapterConfig, LayerPlan, Segment, split_segments, validate_segments
 
 _BF16 = torch.bfloat16
 
@@ -284,12 +284,23 @@ def fused_multi_lora(
     x2, lead = _flatten_input(x, k)
     if len(lora_a) != len(adapters) or len(lora_b) != len(adapters):
         raise ValidationError("lora_a, lora_b and adapters must have one entry per adapter slot")
-    plan = LayerPlan(x2.shape[0], k, weight.shape[0], adapters, segments, offset=offset, training=training,
-                     keep_mask=keep_mask, share_blocks=grad_sink is None, offset_dev=offset_dev)
-    if weights_bf16 is not None:
-        plan.weights_bf16 = (list(weights_bf16[0]), list(weights_bf16[1]))
-    plan.operand_cache = operand_cache
-    return _run(x2, weight, lora_a, lora_b, plan, lead, grad_sink)
+    m = x2.shape[0]
+    validate_segments(list(segments), m, len(adapters))
+    # a microbatch beyond one launch's limits (R > 128 or > 32 segments) runs as several
+    # consecutive row ranges; Philox keeps absolute rows (row_base), so masks are unchanged
+    parts = split_segments(adapters, segments, m) if segments else [(0, m, [])]
+    ys = []
+    for r0, r1, segs in parts:
+        local = [Segment(s_.adapter, s_.row_start - r0, s_.row_end - r0, s_.batch) for s_ in segs]
+        plan = LayerPlan(r1 - r0, k, weight.shape[0], adapters, local, offset=offset, training=training,
+                         keep_mask=None if keep_mask is None else keep_mask[r0:r1],
+                         share_blocks=grad_sink is None, offset_dev=offset_dev, row_base=r0)
+        if weights_bf16 is not None:
+            plan.weights_bf16 = (list(weights_bf16[0]), list(weights_bf16[1]))
+        plan.operand_cache = operand_cache
+        ys.append(_run(x2[r0:r1] if len(parts) > 1 else x2, weight, lora_a, lora_b, plan, (r1 - r0,), grad_sink))
+    y = ys[0] if len(ys) == 1 else torch.cat(ys, 0)
+    return y.reshape(lead + (weight.shape[0],))
 
 
 def _run(x2, weight, lora_a, lora_b, plan: LayerPlan, lead, grad_sink):

@@ -89,6 +89,32 @@ def segments_from_lengths(adapters: Sequence[int], lengths: Sequence[int], batch
     return segs
 
 
+def split_segments(adapters: Sequence[AdapterConfig], segments: Sequence[Segment], m: int,
+                   max_rank_total: int | None = None, max_segments: int | None = None) -> list[tuple[int, int, list]]:
+    """Cut a microbatch whose segments exceed one launch's limits (Σ padded ranks of the
+    distinct adapters ≤ LF_MAX_RANK_TOTAL, ≤ LF_MAX_SEGMENTS segments) into consecutive row
+    ranges that each fit: [(row_start, row_end, segments)]. The ranges tile [0, m); rows in
+    no segment stay with the range before them. One range when everything fits."""
+    max_rank_total = max_rank_total or _lib.LF_MAX_RANK_TOTAL
+    max_segments = max_segments or _lib.LF_MAX_SEGMENTS
+    groups, cur, ranks = [], [], {}
+    for s in sorted(segments, key=lambda s_: s_.row_start):
+        r = padded_rank(adapters[s.adapter].rank)
+        if r > max_rank_total:
+            raise ValidationError(f"adapter {s.adapter}: rank {adapters[s.adapter].rank} exceeds {max_rank_total}")
+        total = sum(ranks.values()) + (0 if s.adapter in ranks else r)
+        if cur and (total > max_rank_total or len(cur) >= max_segments):
+            groups.append(cur)
+            cur, ranks = [], {}
+        cur.append(s)
+        ranks.setdefault(s.adapter, r)
+    if not groups:
+        return [(0, m, list(cur))]
+    groups.append(cur)
+    bounds = [0] + [g[0].row_start for g in groups[1:]] + [m]
+    return [(bounds[i], bounds[i + 1], g) for i, g in enumerate(groups)]
+
+
 def validate_segments(segments: Sequence[Segment], m: int, num_adapters: int) -> None:
     if len(segments) > _lib.LF_MAX_SEGMENTS:
         raise ValidationError(f"at most {_lib.LF_MAX_SEGMENTS} segments per microbatch, got {len(segments)}")
@@ -151,6 +177,7 @@ class LayerPlan:
         device: torch.device | None = None,
         share_blocks: bool = True,
         offset_dev: torch.Tensor | None = None,
+        row_base: int = 0,
     ):
         self.m, self.k, self.n = int(m), int(k), int(n)
         self.adapters = list(adapters)
@@ -201,6 +228,9 @@ class LayerPlan:
             d.seed = int(a.seed) & (2**64 - 1)
             d.offset = self.offset & (2**64 - 1)
         p.keep_mask = keep_mask.data_ptr() if (keep_mask is not None and self.training) else None
+        # microbatch row of this call's row 0 (Philox counters use absolute rows, SPEC.md §3)
+        self.row_base = int(row_base)
+        p.row_base = self.row_base
         # device-resident step counter added to the Philox offsets when the kernels run
         # (CUDA-graph replays then draw fresh masks); SPEC.md §3
         self.offset_dev = offset_dev

@@ -458,3 +458,49 @@ def test_max_segments_many_per_tile_vs_oracle():
         r = ads[a].rank
         H.assert_chain_close(layer.lora_A[a].weight.grad.cpu().numpy(), da_ref[cols[a]:cols[a] + r], f"seg32:dA{a}")
         H.assert_chain_close(layer.lora_B[a].weight.grad.cpu().numpy(), db_ref[:, cols[a]:cols[a] + r], f"seg32:dB{a}")
+
+
+def test_microbatch_beyond_launch_limits_is_split_with_unchanged_masks():
+    """5 adapters of rank 64 (R = 320 > 128): fused_multi_lora runs three row ranges; the
+    Philox counters keep absolute microbatch rows (row_base), so outputs and gradients equal
+    the oracle's on the unsplit microbatch."""
+    from paper_2510_00206_b200 import AdapterConfig, FusedMultiLoRA, segments_from_lengths
+
+    lens = [200, 136, 152, 96, 168]
+    m, k, n = sum(lens), 256, 192
+    ads = [AdapterConfig(64, 1.0 + 0.25 * i, 0.1 if i % 2 == 0 else 0.0, 40 + i) for i in range(5)]
+    segs = segments_from_lengths(range(5), lens)
+    g = torch.Generator().manual_seed(8)
+    x = torch.randn(m, k, generator=g).to(torch.bfloat16)
+    w = (torch.randn(n, k, generator=g) / k**0.5).to(torch.bfloat16)
+    dy = torch.randn(m, n, generator=g).to(torch.bfloat16)
+    layer = FusedMultiLoRA(w.to(DEV), ads, init="gaussian", generator=torch.Generator(device=DEV).manual_seed(9)).to(DEV)
+    with torch.no_grad():
+        for p_ in layer.parameters():
+            if p_.requires_grad:
+                p_.copy_(p_.to(torch.bfloat16).float())
+    xd = x.to(DEV).requires_grad_(True)
+    y = layer(xd, segs)  # offset 0
+    y.backward(dy.to(DEV))
+    a_cat = torch.cat([layer.lora_A[i].weight.detach().cpu() for i in range(5)], 0)
+    b_cat = torch.cat([layer.lora_B[i].weight.detach().cpu() for i in range(5)], 1)
+    oseg, row = [], 0
+    for i, L in enumerate(lens):
+        oseg.append(olora.OracleSegment(row, row + L, 64 * i, 64, ads[i].scaling, ads[i].dropout_p, ads[i].seed))
+        row += L
+
+    class _A:
+        def __init__(self, p, seed):
+            self.dropout_p, self.seed = p, seed
+
+    keep = ophilox.keep_mask(m, k, [(i, s.row_start, s.row_end) for i, s in enumerate(oseg)],
+                             [_A(s.dropout_p, s.seed) for s in oseg], 0)
+    xf, wf, dyf = x.float().numpy(), w.float().numpy(), dy.float().numpy()
+    af, bf = a_cat.to(torch.bfloat16).float().numpy(), b_cat.to(torch.bfloat16).float().numpy()
+    y_ref, s_hat = olora.forward(xf, wf, af, bf, oseg, keep)
+    dx_ref, da_ref, db_ref, _ = olora.backward(dyf, xf, wf, af, bf, s_hat, oseg, keep)
+    H.assert_chain_close(y.detach().float().cpu().numpy(), y_ref, "split:y")
+    H.assert_chain_close(xd.grad.float().cpu().numpy(), dx_ref, "split:dx")
+    for i in range(5):
+        H.assert_chain_close(layer.lora_A[i].weight.grad.cpu().numpy(), da_ref[64 * i:64 * i + 64], f"split:dA{i}")
+        H.assert_chain_close(layer.lora_B[i].weight.grad.cpu().numpy(), db_ref[:, 64 * i:64 * i + 64], f"split:dB{i}")

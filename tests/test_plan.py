@@ -173,3 +173,25 @@ def test_segments_from_microbatch_objects():
 
     segs = sched.segments_from_microbatch(MB(), ["a0", "a1", "a2"])
     assert segs == [Segment(0, 0, 128, 3), Segment(2, 128, 192, 3), Segment(2, 192, 384, 4)]
+
+
+def test_split_segments_respects_launch_limits():
+    from paper_2510_00206_b200.plan import split_segments
+
+    ads = [AdapterConfig(64) for _ in range(5)]
+    segs = segments_from_lengths([0, 1, 2, 3, 4], [100, 50, 70, 30, 60], start=10)  # rows 10..320, m = 400
+    parts = split_segments(ads, segs, 400)
+    assert [(a, b) for a, b, _ in parts] == [(0, 160), (160, 260), (260, 400)]
+    assert [[s.adapter for s in g] for _, _, g in parts] == [[0, 1], [2, 3], [4]]
+    # segments of an adapter already in the group add no columns
+    ads2 = [AdapterConfig(64), AdapterConfig(64), AdapterConfig(16)]
+    segs2 = segments_from_lengths([0, 1, 0, 1, 2], [10, 10, 10, 10, 10])
+    assert len(split_segments(ads2, segs2, 50)) == 2
+    assert [len(g) for _, _, g in split_segments(ads2, segs2, 50)] == [4, 1]
+    # everything fits: one range covering all rows
+    assert split_segments([AdapterConfig(16)], [Segment(0, 5, 9)], 20) == [(0, 20, [Segment(0, 5, 9)])]
+    # the segment-count limit
+    many = [Segment(0, i, i + 1) for i in range(40)]
+    assert [len(g) for _, _, g in split_segments([AdapterConfig(8)], many, 40)] == [32, 8]
+    with pytest.raises(ValidationError):
+        split_segments([AdapterConfig(200)], [Segment(0, 0, 4)], 4)
