@@ -772,7 +772,9 @@ def run_c5(args, rank: int, world: int, local_rank: int) -> None:
         model = D.LoRADecoder(shape, adapters, fused=fused, device=device, generator=dgen)
         model.train()
         params = model.adapter_parameters()
-        reducer = dp.AdapterGradReducer(params) if world > 1 else None
+        # bucketed fp32 all-reduce launched from post-accumulate-grad hooks during the
+        # step's last backward (overlapped, DDP-style)
+        reducer = dp.AdapterGradReducer(params).attach() if world > 1 else None
         opt = torch.optim.AdamW(params, lr=1e-4, fused=True)
         fn = lambda: D.train_step(model, packed, reducer, opt)  # noqa: E731
         counts = None
@@ -802,6 +804,7 @@ def run_c5(args, rank: int, world: int, local_rank: int) -> None:
         dist.all_reduce(t)
         flops_all = float(t.item())
     peaks = measured_peaks()
+    loads = dp.rank_loads([mb.rows for mb in chosen], assign)
     if rank == 0:
         line = {
             "metric": "LoRA linear fwd+bwd tokens/s & TFLOP/s (8B/70B shapes), % of bf16 peak",
@@ -830,6 +833,8 @@ def run_c5(args, rank: int, world: int, local_rank: int) -> None:
                 "l2": "inputs larger than L2",
             },
             "padded_rows_per_s": rows_all / (ms * 1e-3),
+            "dp": {"rows_per_rank": loads, "imbalance": dp.imbalance(loads),
+                   "note": "imbalance = 1 - mean/max of per-rank padded rows (ls/pipesim.py:275-312 simulate_dp)"},
             "lora_linear_tflops": flops_all / (ms * 1e-3) / 1e12,
             "lora_linear_frac_of_bf16_peak": flops_all / (ms * 1e-3) / 1e12 / world / peaks["bf16_tflops"],
             "unfused_torch": {"ms_per_step": unf_ms, "tokens_per_s": raw_all / (unf_ms * 1e-3),

@@ -262,12 +262,18 @@ def train_step(model: LoRADecoder, microbatches: Sequence[PackedMicrobatch], red
     adapter gradients (:class:`.dp.AdapterGradReducer`; the only cross-rank exchange,
     SURVEY.md §8(e)), then the optimizer step. Returns the summed loss (device tensor)."""
     total = None
-    for mb in microbatches:
+    overlap = reducer is not None and bool(getattr(reducer, "_hooks", None))
+    for i, mb in enumerate(microbatches):
         loss = model(mb)
+        if overlap and i == len(microbatches) - 1:
+            reducer.arm()  # buckets all-reduce as the last backward finalizes them
         loss.backward()
         total = loss.detach() if total is None else total + loss.detach()
     if reducer is not None:
-        reducer.reduce()
+        if overlap:
+            reducer.wait()
+        else:
+            reducer.reduce()
     if optimizer is not None:
         optimizer.step()
         optimizer.zero_grad(set_to_none=True)

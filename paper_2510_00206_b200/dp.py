@@ -9,8 +9,11 @@ gradients per optimizer step (NCCL over NVLink/NVSwitch on B200; gloo in CPU tes
   :func:`imbalance` reports 1 − mean/max exactly as the reference's DP model
   (``simulate_dp``, ls/pipesim.py:275-312).
 * :class:`AdapterGradReducer` — flattens every adapter gradient into fixed-size fp32
-  buckets and all-reduces them asynchronously (launch after backward, or per layer as
-  its gradients become ready), then scatters the result back into ``.grad``.
+  buckets and all-reduces them asynchronously, then scatters the result back into
+  ``.grad``. Either after backward (``reduce``), or overlapped with it: ``attach()``
+  registers post-accumulate-grad hooks, ``arm()`` before the step's last backward, and
+  each bucket's all-reduce starts the moment its last gradient is final (the backward of
+  the remaining layers runs underneath, as in DDP); ``wait()`` finishes the step.
 """
 from __future__ import annotations
 
@@ -71,17 +74,62 @@ class AdapterGradReducer:
         if cur:
             self.buckets.append(cur)
         self._pending: list[tuple[list, torch.Tensor, object]] = []
+        self._bucket_of = {id(p): b for b, bucket in enumerate(self.buckets) for p in bucket}
+        self._hooks: list = []
+        self._armed = False
+        self._ready: list[int] = []
+        self._launched: list[bool] = []
+
+    def _launch_bucket(self, b: int) -> None:
+        bucket = self.buckets[b]
+        flat = torch.cat([(p.grad if p.grad is not None else torch.zeros_like(p)).reshape(-1).float()
+                          for p in bucket])
+        work = dist.all_reduce(flat, group=self.group, async_op=True)
+        self._pending.append((bucket, flat, work))
+        self._launched[b] = True
 
     def launch(self) -> None:
-        """Flatten and start the all-reduce of every bucket (non-blocking)."""
-        for bucket in self.buckets:
-            flat = torch.cat([(p.grad if p.grad is not None else torch.zeros_like(p)).reshape(-1).float()
-                              for p in bucket])
-            work = dist.all_reduce(flat, group=self.group, async_op=True)
-            self._pending.append((bucket, flat, work))
+        """Flatten and start the all-reduce of every bucket not yet started (non-blocking)."""
+        if len(self._launched) != len(self.buckets):
+            self._launched = [False] * len(self.buckets)
+        for b in range(len(self.buckets)):
+            if not self._launched[b]:
+                self._launch_bucket(b)
+
+    # -- overlap with backward ---------------------------------------------------------
+    def attach(self) -> "AdapterGradReducer":
+        """Register the post-accumulate-grad hooks that drive ``arm()``ed steps."""
+        if not self._hooks:
+            self._hooks = [p.register_post_accumulate_grad_hook(self._on_grad) for p in self.params]
+        return self
+
+    def detach(self) -> None:
+        for h in self._hooks:
+            h.remove()
+        self._hooks = []
+
+    def arm(self) -> None:
+        """The next backward is the step's last: launch each bucket as it completes.
+        Every bucket is reduced exactly once per armed step (``wait`` launches the rest)."""
+        if not self._hooks:
+            raise ValidationError("attach() the reducer before arm()")
+        self._armed = True
+        self._ready = [0] * len(self.buckets)
+        self._launched = [False] * len(self.buckets)
+
+    def _on_grad(self, p: torch.Tensor) -> None:
+        if not self._armed:
+            return
+        b = self._bucket_of[id(p)]
+        self._ready[b] += 1
+        if self._ready[b] == len(self.buckets[b]) and not self._launched[b]:
+            self._launch_bucket(b)
 
     def wait(self) -> None:
         """Finish the reductions and write the summed (or averaged) gradients back."""
+        if self._armed:
+            self.launch()  # buckets whose parameters received no gradient this step
+            self._armed = False
         world = dist.get_world_size(self.group)
         for bucket, flat, work in self._pending:
             work.wait()
@@ -99,5 +147,6 @@ class AdapterGradReducer:
         self._pending.clear()
 
     def reduce(self) -> None:
+        self._launched = [False] * len(self.buckets)
         self.launch()
         self.wait()

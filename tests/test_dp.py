@@ -66,3 +66,64 @@ def test_adapter_grad_allreduce_world2_gloo():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}
+
+
+def _worker_overlap(rank: int, world: int, port: int, q):
+    """attach/arm: buckets launch from post-accumulate-grad hooks during the last backward."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.manual_seed(0)
+        lins = torch.nn.ModuleList(torch.nn.Linear(24, 24, bias=False) for _ in range(4))
+        params = list(lins.parameters())
+        red = dp.AdapterGradReducer(params, bucket_bytes=24 * 24 * 4 * 2).attach()  # 2 params per bucket
+        x = torch.full((3, 24), float(rank + 1))
+        launched_during_backward = []
+        orig = red._launch_bucket
+
+        def spy(b):
+            launched_during_backward.append(b)
+            orig(b)
+
+        red._launch_bucket = spy
+        for i in range(2):  # gradient accumulation: only the last backward is armed
+            h = x
+            for lin in lins:
+                h = lin(h)
+            if i == 1:
+                red.arm()
+            h.sum().backward()
+            if i == 0:
+                ok0 = not launched_during_backward
+        n_hooked = len(launched_during_backward)
+        red.wait()
+        # reference: local grads of both microbatches, summed over ranks
+        ref = [torch.zeros_like(p) for p in params]
+        for r in range(world):
+            xr = torch.full((3, 24), float(r + 1))
+            for _ in range(2):
+                ps = [p.detach().clone().requires_grad_(True) for p in params]
+                h = xr
+                for pw in ps:
+                    h = h @ pw.t()
+                h.sum().backward()
+                for acc, pw in zip(ref, ps):
+                    acc += pw.grad
+        ok = ok0 and n_hooked == len(red.buckets) and all(torch.allclose(p.grad, g, rtol=1e-5) for p, g in zip(params, ref))
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_adapter_grad_allreduce_overlapped_with_backward_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_overlap, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}
