@@ -64,7 +64,8 @@ class AdapterGradReducer:
         self.average = average
         self.buckets: list[list[torch.nn.Parameter]] = []
         cur, size = [], 0
-        for p in self.params:
+        # buckets in reverse registration order: backward finalizes the last layers first
+        for p in reversed(self.params):
             nbytes = p.numel() * 4
             if cur and size + nbytes > bucket_bytes:
                 self.buckets.append(cur)
@@ -89,12 +90,14 @@ class AdapterGradReducer:
         self._launched[b] = True
 
     def launch(self) -> None:
-        """Flatten and start the all-reduce of every bucket not yet started (non-blocking)."""
+        """Flatten and start the all-reduce of every bucket not yet started (non-blocking,
+        in bucket order)."""
         if len(self._launched) != len(self.buckets):
             self._launched = [False] * len(self.buckets)
         for b in range(len(self.buckets)):
             if not self._launched[b]:
                 self._launch_bucket(b)
+        self._next = len(self.buckets)
 
     # -- overlap with backward ---------------------------------------------------------
     def attach(self) -> "AdapterGradReducer":
@@ -109,21 +112,25 @@ class AdapterGradReducer:
         self._hooks = []
 
     def arm(self) -> None:
-        """The next backward is the step's last: launch each bucket as it completes.
-        Every bucket is reduced exactly once per armed step (``wait`` launches the rest)."""
+        """The next backward is the step's last: launch buckets as they complete. Buckets
+        start strictly in index order on every rank (collectives must match across ranks:
+        a bucket whose gradients are final waits for the ones before it), each exactly
+        once per armed step; ``wait`` launches those that never completed (parameters
+        without a gradient in this backward)."""
         if not self._hooks:
             raise ValidationError("attach() the reducer before arm()")
         self._armed = True
         self._ready = [0] * len(self.buckets)
         self._launched = [False] * len(self.buckets)
+        self._next = 0
 
     def _on_grad(self, p: torch.Tensor) -> None:
         if not self._armed:
             return
-        b = self._bucket_of[id(p)]
-        self._ready[b] += 1
-        if self._ready[b] == len(self.buckets[b]) and not self._launched[b]:
-            self._launch_bucket(b)
+        self._ready[self._bucket_of[id(p)]] += 1
+        while self._next < len(self.buckets) and self._ready[self._next] == len(self.buckets[self._next]):
+            self._launch_bucket(self._next)
+            self._next += 1
 
     def wait(self) -> None:
         """Finish the reductions and write the summed (or averaged) gradients back."""

@@ -89,28 +89,38 @@ def _worker_overlap(rank: int, world: int, port: int, q):
         red._launch_bucket = spy
         for i in range(2):  # gradient accumulation: only the last backward is armed
             h = x
-            for lin in lins:
+            for j, lin in enumerate(lins):
+                # rank 1 skips layer 1 in its last microbatch (an adapter absent from it):
+                # its bucket never completes there, yet collectives must stay matched
+                if i == 1 and rank == 1 and j == 1:
+                    continue
                 h = lin(h)
             if i == 1:
                 red.arm()
             h.sum().backward()
             if i == 0:
                 ok0 = not launched_during_backward
-        n_hooked = len(launched_during_backward)
+        during = list(launched_during_backward)
         red.wait()
         # reference: local grads of both microbatches, summed over ranks
         ref = [torch.zeros_like(p) for p in params]
         for r in range(world):
             xr = torch.full((3, 24), float(r + 1))
-            for _ in range(2):
+            for i in range(2):
                 ps = [p.detach().clone().requires_grad_(True) for p in params]
                 h = xr
-                for pw in ps:
+                for j, pw in enumerate(ps):
+                    if i == 1 and r == 1 and j == 1:
+                        continue
                     h = h @ pw.t()
                 h.sum().backward()
                 for acc, pw in zip(ref, ps):
-                    acc += pw.grad
-        ok = ok0 and n_hooked == len(red.buckets) and all(torch.allclose(p.grad, g, rtol=1e-5) for p, g in zip(params, ref))
+                    if pw.grad is not None:
+                        acc += pw.grad
+        nb = len(red.buckets)
+        ok = ok0 and launched_during_backward == list(range(nb))  # every bucket once, in order, on each rank
+        ok = ok and (len(during) == nb if rank == 0 else 0 < len(during) < nb)  # hooks launched them (rank 1: up to the gap)
+        ok = ok and all(torch.allclose(p.grad, g, rtol=1e-5) for p, g in zip(params, ref))
         q.put((rank, bool(ok)))
     finally:
         dist.destroy_process_group()
