@@ -38,17 +38,22 @@ constexpr int kGemmThreads = 32 * (2 + kEpiWarps);   // producer, MMA, epilogue
 constexpr int kGemmCtlBytes = 512;
 constexpr int kSeqDepth = 6;  // CLC responses in flight / not yet released
 
-template <bool B_MN, int STAGES>
+// WIDE: 256 x 512 pair tiles — two N = 256 MMAs per K-step share each A slice, one
+// 512-column accumulator (no double buffer): 25% less operand traffic from L2 and smem per
+// FLOP than 256 x 256, which is what the power-capped long GEMMs (C4) are bound by.
+template <bool B_MN, int STAGES, bool WIDE = false>
 struct GemmCfg {
   static constexpr int BM = 128;                  // rows per CTA (pair tile: 256)
-  static constexpr int BN = 256;                  // pair tile columns; each CTA loads BN/2 of B
+  static constexpr int BN = WIDE ? 512 : 256;     // pair tile columns; each CTA loads BN/2 of B
+  static constexpr int NH = BN / 256;             // N = 256 MMAs per K-step
+  static constexpr int NACC = WIDE ? 1 : 2;       // TMEM accumulator buffers
   static constexpr int HBN = BN / 2;
   static constexpr int BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;     // 16 KB, K-major SW128
-  static constexpr int B_BYTES = HBN * BK * 2;    // 16 KB
+  static constexpr int B_BYTES = HBN * BK * 2;    // 16 KB (WIDE: 32 KB, two 128-row pieces)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int ACC_COLS = BN;
-  static constexpr int TMEM_COLS = 2 * ACC_COLS;  // 512
+  static constexpr int TMEM_COLS = NACC * ACC_COLS;  // 512
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + kGemmCtlBytes + 512 * 16;  // + routing cache
 };
 
@@ -181,13 +186,14 @@ struct TileSeq {
   }
 };
 
-template <bool B_MN, bool MASKED, int STAGES>
+template <bool B_MN, bool MASKED, int STAGES, bool WIDE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     lf_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                    const __grid_constant__ GemmArgs args) {
-  using Cfg = GemmCfg<B_MN, STAGES>;
-  constexpr int BN = Cfg::BN, HBN = Cfg::HBN;
+  using Cfg = GemmCfg<B_MN, STAGES, WIDE>;
+  constexpr int BN = Cfg::BN, HBN = Cfg::HBN, NH = Cfg::NH, NACC = Cfg::NACC;
+  static_assert(!WIDE || (!B_MN && !MASKED), "WIDE tiles: K-major forward GEMM only");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);  // leader: both halves landed
@@ -273,7 +279,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         uint8_t* sB = sA + Cfg::A_BYTES;
         tma_load_2d_pair(sA, &tmA, &full[stage], kb * Cfg::BK, ti.mb * 256 + row_half);
         if constexpr (!B_MN) {
-          tma_load_2d_pair(sB, &tmB, &full[stage], kb * Cfg::BK, ti.nb * BN + col_half);
+          // N piece h of this CTA: rows h*256 + rank*128 of the pair tile's columns
+#pragma unroll
+          for (int h = 0; h < NH; ++h)
+            tma_load_2d_pair(sB + h * 16384, &tmB, &full[stage], kb * Cfg::BK, ti.nb * BN + h * 256 + (int)rank * 128);
         } else {
 #pragma unroll
           for (int i = 0; i < HBN / 64; ++i)
@@ -290,7 +299,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           for (int j = 0; j < nsub; ++j) {
             tma_load_2d_pair(sA + j * (Cfg::BM * 32), &tmA2, &full[stage], c + 16 * j, ti.mb * 256 + row_half);
             if constexpr (!B_MN) {
-              tma_load_2d_pair(sB + j * (HBN * 32), &tmB2, &full[stage], c + 16 * j, ti.nb * BN + col_half);
+#pragma unroll
+              for (int h = 0; h < NH; ++h)
+                tma_load_2d_pair(sB + (j * NH + h) * 4096, &tmB2, &full[stage], c + 16 * j,
+                                 ti.nb * BN + h * 256 + (int)rank * 128);
             } else {
 #pragma unroll
               for (int i = 0; i < HBN / 64; ++i)
@@ -332,7 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA, whole warp; one elected lane issues)
     if (leader) {
-      const uint32_t idesc = make_idesc_bf16(256, BN, false, B_MN);
+      const uint32_t idesc = make_idesc_bf16(256, 256, false, B_MN);  // N = 256 per instruction
       int stage = 0;
       uint32_t phase = 0;
       uint32_t lora_uses0 = 0, lora_uses1 = 0;  // MASKED: LoRA partials produced per accumulator buffer
@@ -345,8 +357,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         const uint64_t bd0 = B_MN ? make_sdesc(sB, 8192, 1024, kLayoutSW128) : make_sdesc(sB, 16, 1024, kLayoutSW128);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          umma_bf16_pair_warp(d, sdesc_add(ad0, kk * 32), sdesc_add(bd0, B_MN ? kk * 2048 : kk * 32), idesc,
-                              (acc_any || (kb | kk) != 0) ? 1u : 0u);
+#pragma unroll
+          for (int h = 0; h < NH; ++h)
+            umma_bf16_pair_warp(d + h * 256, sdesc_add(ad0, kk * 32),
+                                sdesc_add(bd0, (B_MN ? kk * 2048 : kk * 32) + h * 16384), idesc,
+                                (acc_any || (kb | kk) != 0) ? 1u : 0u);
         umma_commit_pair_warp(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       };
@@ -360,9 +375,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           const uint32_t sB = sA + Cfg::A_BYTES;
           for (int j = 0; j < nsub; ++j) {
             const uint64_t ad = make_sdesc(sA + j * (Cfg::BM * 32), 16, 256, kLayoutSW32);
-            const uint64_t bd = B_MN ? make_sdesc(sB + j * (HBN / 64) * 2048, 2048, 1024, kLayoutSW128)
-                                     : make_sdesc(sB + j * (HBN * 32), 16, 256, kLayoutSW32);
-            umma_bf16_pair_warp(d, ad, bd, idesc, accum);
+            for (int h = 0; h < NH; ++h) {
+              const uint64_t bd = B_MN ? make_sdesc(sB + j * (HBN / 64) * 2048, 2048, 1024, kLayoutSW128)
+                                       : make_sdesc(sB + (j * NH + h) * 4096, 16, 256, kLayoutSW32);
+              umma_bf16_pair_warp(d + h * 256, ad, bd, idesc, accum);
+            }
             accum = 1u;
           }
           umma_commit_pair_warp(&empty[stage]);
@@ -371,8 +388,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       };
       // MASKED: LoRA partial of local tile `it` into its (drained) buffer, then signal the mask pass
       auto issue_lora_first = [&](const TileInfo& ti, int it) {
-        const int acc = it & 1;
-        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        const int acc = it % NACC;
+        mbar_wait(&tempty[acc], ((it / NACC) & 1) ^ 1);
         tc_fence_after();
         mma_lora(ti, tmem_base + acc * Cfg::ACC_COLS, false);
         umma_commit_pair_warp(&lfull[acc]);
@@ -380,12 +397,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int t = seq.first();
       for (int it = 0; t >= 0; ++it) {
         const TileInfo ti = tile_info(args, s_routes, t);
-        const int acc = it & 1;
+        const int acc = it % NACC;
         const uint32_t d = tmem_base + acc * Cfg::ACC_COLS;
         int tn = -1;
         bool have_tn = false;
         if (MASKED && (args.segs.debug & 4096)) {  // profiling: plain k-loop in the masked kernel
-          mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+          mbar_wait(&tempty[acc], ((it / NACC) & 1) ^ 1);
           tc_fence_after();
           for (int kb = 0; kb < nkb; ++kb) mma_main_block(d, kb, false);
         } else if constexpr (MASKED) {
@@ -395,7 +412,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             mbar_wait(&lmasked[acc], lu & 1);
             ++lu;
           } else {
-            mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+            mbar_wait(&tempty[acc], ((it / NACC) & 1) ^ 1);
           }
           tc_fence_after();
           const int split = min(jmid, nkb);
@@ -410,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           }
           for (; kb < nkb; ++kb) mma_main_block(d, kb, acc_any);
         } else {
-          mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+          mbar_wait(&tempty[acc], ((it / NACC) & 1) ^ 1);
           tc_fence_after();
           for (int kb = 0; kb < nkb; ++kb) mma_main_block(d, kb, false);
           if (ti.lora()) mma_lora(ti, d, true);
@@ -433,7 +450,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint32_t lora_uses0 = 0, lora_uses1 = 0;
     // MASKED: zero the dropped elements of tile `it`'s LoRA partial in place
     auto mask_pass = [&](const TileInfo& ti, int it) {
-      const int acc = it & 1;
+      const int acc = it % NACC;
       const int row = ti.mb * 256 + (int)rank * Cfg::BM + (int)(q * 32 + lane);
       const int rt_idx = 2 * ti.mb + (int)rank;
       const bool in_m = row < args.M;
@@ -480,8 +497,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     int t = seq.first();
     for (int it = 0; t >= 0; ++it) {
       const TileInfo ti = tile_info(args, s_routes, t);
-      const int acc = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
+      const int acc = it % NACC;
+      const uint32_t aph = (it / NACC) & 1;
       int tn = -1;
       if constexpr (MASKED) {
         const bool plain = (args.segs.debug & 4096) != 0;  // profiling: the MMA issues no LoRA-first blocks
@@ -498,6 +515,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * Cfg::ACC_COLS;
       __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(args.C) + (int64_t)row * args.ldc;
+      if constexpr (NACC == 1) {
+        // single accumulator: the next tile's MMAs wait for it, so hand TMEM back as soon as
+        // this warp's 256 columns sit in registers as bf16 (128 regs), then store them while
+        // the next tile's main loop runs
+        uint32_t pk[(BN / 2) / 2];
+#pragma unroll
+        for (int c = 0; c < BN / 2; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c_lo + c, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pk[c / 2 + j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader[acc]);
+        if (row < args.M) {
+#pragma unroll
+          for (int c = 0; c < BN / 2; c += 8) {
+            const int col = n0 + c_lo + c;
+            if (col < args.N)
+              *reinterpret_cast<uint4*>(crow + col) = make_uint4(pk[c / 2], pk[c / 2 + 1], pk[c / 2 + 2], pk[c / 2 + 3]);
+          }
+        }
+        if constexpr (!MASKED) tn = seq.read(it + 1, lane == 0);
+        t = tn;
+        continue;
+      }
 #pragma unroll 1
       for (int c = c_lo; c < c_hi; c += 32) {
         uint32_t v[32];
@@ -533,10 +578,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-template <bool B_MN, bool MASKED, int STAGES>
+template <bool B_MN, bool MASKED, int STAGES, bool WIDE = false>
 static int launch_one(const GemmMaps& maps, const GemmArgs& args, int num_sms, cudaStream_t stream) {
-  using Cfg = GemmCfg<B_MN, STAGES>;
-  auto kern = lf_gemm_kernel<B_MN, MASKED, STAGES>;
+  using Cfg = GemmCfg<B_MN, STAGES, WIDE>;
+  auto kern = lf_gemm_kernel<B_MN, MASKED, STAGES, WIDE>;
   static bool configured = false;  // per instantiation; attribute set is idempotent
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) != cudaSuccess)
@@ -554,8 +599,16 @@ static int launch_one(const GemmMaps& maps, const GemmArgs& args, int num_sms, c
 
 int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_sms, cudaStream_t stream) {
   GemmArgs args = a;
+  // 256 x 512 tiles for the forward GEMM when they still fill >= 4 waves (LF_WIDE=0|1 forces):
+  // 25% fewer L2 sectors per FLOP buys clock under the power cap — C4 q/gate/down 6/5.5/12.6%
+  // faster, C2 gate 3.8%; with fewer than ~4 waves the coarser tiles quantise badly (C2 q,
+  // down: 4–14% slower). ncu, profiles/r01_wide_tiles_ab.txt
+  static const int wide_env = [] { const char* e = getenv("LF_WIDE"); return e ? atoi(e) : -1; }();
+  const bool wide_fit = (int64_t)((args.M + 255) / 256) * ((args.N + 511) / 512) >= 4 * (num_sms / 2) &&
+                        args.K >= 4096;
+  const bool wide = kind == kGemmFwd && (wide_env >= 0 ? wide_env == 1 : wide_fit);
   args.tiles_m = (args.M + 255) / 256;
-  args.tiles_n = (args.N + 255) / 256;
+  args.tiles_n = wide ? (args.N + 511) / 512 : (args.N + 255) / 256;
   if (args.group <= 0) args.group = 8;
   // Tile schedule. While both operands fit in L2 together, the static persistent
   // round-robin is ~5% faster (C2 q/kv, C1: no per-tile CLC round trip and the pairs'
@@ -567,7 +620,8 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
   args.dynamic = sched_env == 1 ? 0 : sched_env == 2 ? 1 : (operand_bytes > 128.0 * (1 << 20) ? 1 : 0);
   switch (kind) {
     case kGemmFwd:
-      return launch_one<false, false, 6>(maps, args, num_sms, stream);
+      return wide ? launch_one<false, false, 4, true>(maps, args, num_sms, stream)
+                  : launch_one<false, false, 6>(maps, args, num_sms, stream);
     case kGemmDgrad:
       return launch_one<true, false, 6>(maps, args, num_sms, stream);
     case kGemmDgradMasked:

@@ -385,17 +385,19 @@ def test_errors_are_loud_and_typed():
         fused_lora(xx, torch.randn(64, 60, device=DEV).to(torch.bfloat16), a[:, :60].contiguous(), b, 2.0)
 
 
-@pytest.mark.parametrize("sched", ["1", "2"], ids=["static", "clc"])
-def test_every_case_under_each_gemm_schedule(sched):
+@pytest.mark.parametrize("sched,wide", [("1", "0"), ("2", "0"), ("1", "1"), ("2", "1")],
+                         ids=["static", "clc", "static-wide", "clc-wide"])
+def test_every_case_under_each_gemm_schedule(sched, wide):
     """The GEMM launcher picks its tile schedule by operand size (static persistent vs
-    cluster-launch-control dynamic), so the small parity cases above mostly run static:
-    re-run the whole per-kernel oracle matrix with each schedule forced (LF_SCHED is read
+    cluster-launch-control dynamic) and the forward tile width (256 x 256 or 256 x 512) by
+    problem size, so the small parity cases above mostly run static and narrow: re-run the
+    whole per-kernel oracle matrix with each combination forced (LF_SCHED / LF_WIDE are read
     once per process, hence the subprocess)."""
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, LF_SCHED=sched)
+    env = dict(os.environ, LF_SCHED=sched, LF_WIDE=wide)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                         os.path.join(root, "tests", "test_gpu_parity.py"), "-k", "test_kernels_match_oracle",
                         "-m", "gpu"], cwd=root, env=env, capture_output=True, text=True, timeout=900)
