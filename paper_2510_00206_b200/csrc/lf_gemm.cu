@@ -193,7 +193,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                    const __grid_constant__ GemmArgs args) {
   using Cfg = GemmCfg<B_MN, STAGES, WIDE>;
   constexpr int BN = Cfg::BN, HBN = Cfg::HBN, NH = Cfg::NH, NACC = Cfg::NACC;
-  static_assert(!WIDE || (!B_MN && !MASKED), "WIDE tiles: K-major forward GEMM only");
+
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);  // leader: both halves landed
@@ -285,8 +285,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             tma_load_2d_pair(sB + h * 16384, &tmB, &full[stage], kb * Cfg::BK, ti.nb * BN + h * 256 + (int)rank * 128);
         } else {
 #pragma unroll
-          for (int i = 0; i < HBN / 64; ++i)
-            tma_load_2d_pair(sB + i * 8192, &tmB, &full[stage], ti.nb * BN + col_half + 64 * i, kb * Cfg::BK);
+          for (int h = 0; h < NH; ++h)
+#pragma unroll
+            for (int i = 0; i < 2; ++i)  // 128 MN-major columns = two 64-column SW128 boxes
+              tma_load_2d_pair(sB + h * 16384 + i * 8192, &tmB, &full[stage],
+                               ti.nb * BN + h * 256 + (int)rank * 128 + 64 * i, kb * Cfg::BK);
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       };
@@ -305,9 +308,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                                  ti.nb * BN + h * 256 + (int)rank * 128);
             } else {
 #pragma unroll
-              for (int i = 0; i < HBN / 64; ++i)
-                tma_load_2d_pair(sB + j * (HBN / 64) * 2048 + i * 2048, &tmB2, &full[stage],
-                                 ti.nb * BN + col_half + 64 * i, c + 16 * j);
+              for (int h = 0; h < NH; ++h)
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                  tma_load_2d_pair(sB + (j * NH + h) * 4096 + i * 2048, &tmB2, &full[stage],
+                                   ti.nb * BN + h * 256 + (int)rank * 128 + 64 * i, c + 16 * j);
             }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -318,7 +323,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       for (int i = 0; t >= 0; ++i) {
         const TileInfo ti = tile_info(args, s_routes, t);
         int tn;
-        if constexpr (MASKED) {
+        if constexpr (MASKED && WIDE) {
+          // one accumulator: each tile's own LoRA block first, then its main loop
+          if (ti.lora()) load_lora(ti);
+          for (int kb = 0; kb < nkb; ++kb) load_main(ti, kb);
+          tn = seq.read(i + 1, true);
+          if (leader && tn >= 0) seq.request(i + 2);
+        } else if constexpr (MASKED) {
           if (i == 0 && ti.lora()) load_lora(ti);
           // the next tile's LoRA block goes in half-way through this tile's main loop
           const int split = min(jmid, nkb);
@@ -376,7 +387,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           for (int j = 0; j < nsub; ++j) {
             const uint64_t ad = make_sdesc(sA + j * (Cfg::BM * 32), 16, 256, kLayoutSW32);
             for (int h = 0; h < NH; ++h) {
-              const uint64_t bd = B_MN ? make_sdesc(sB + j * (HBN / 64) * 2048, 2048, 1024, kLayoutSW128)
+              const uint64_t bd = B_MN ? make_sdesc(sB + (j * NH + h) * 4096, 2048, 1024, kLayoutSW128)
                                        : make_sdesc(sB + (j * NH + h) * 4096, 16, 256, kLayoutSW32);
               umma_bf16_pair_warp(d + h * 256, ad, bd, idesc, accum);
             }
@@ -405,6 +416,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           mbar_wait(&tempty[acc], ((it / NACC) & 1) ^ 1);
           tc_fence_after();
           for (int kb = 0; kb < nkb; ++kb) mma_main_block(d, kb, false);
+        } else if constexpr (MASKED && WIDE) {
+          // sequential: drained accumulator -> this tile's LoRA partial -> mask pass -> main loop
+          mbar_wait(&tempty[acc], ((it / NACC) & 1) ^ 1);
+          tc_fence_after();
+          if (ti.lora()) {
+            mma_lora(ti, d, false);
+            umma_commit_pair_warp(&lfull[acc]);
+            uint32_t& lu = lora_uses0;
+            mbar_wait(&lmasked[acc], lu & 1);
+            ++lu;
+            tc_fence_after();
+          }
+          for (int kb = 0; kb < nkb; ++kb) mma_main_block(d, kb, ti.lora());
         } else if constexpr (MASKED) {
           if (it == 0 && ti.lora()) issue_lora_first(ti, 0);
           if (ti.lora()) {
@@ -500,7 +524,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int acc = it % NACC;
       const uint32_t aph = (it / NACC) & 1;
       int tn = -1;
-      if constexpr (MASKED) {
+      if constexpr (MASKED && WIDE) {
+        if (ti.lora() && !(args.segs.debug & 4096)) mask_pass(ti, it);
+        tn = seq.read(it + 1, lane == 0);
+      } else if constexpr (MASKED) {
         const bool plain = (args.segs.debug & 4096) != 0;  // profiling: the MMA issues no LoRA-first blocks
         if (it == 0 && ti.lora() && !plain) mask_pass(ti, 0);
         tn = seq.read(it + 1, lane == 0);
@@ -603,10 +630,14 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
   // 25% fewer L2 sectors per FLOP buys clock under the power cap — C4 q/gate/down 6/5.5/12.6%
   // faster, C2 gate 3.8%; with fewer than ~4 waves the coarser tiles quantise badly (C2 q,
   // down: 4–14% slower). ncu, profiles/r01_wide_tiles_ab.txt
+  // The masked dgrad runs wide tiles sequentially (accumulator drain -> LoRA partial -> TMEM
+  // mask pass -> main loop, ~6-18% exposed at K = 4096-8192), which only long reductions
+  // amortise: C4 gate/up dgrad (K = 28672) 5.21 -> 4.90 ms, q/o and down (K = 8192) 4-5% slower.
   static const int wide_env = [] { const char* e = getenv("LF_WIDE"); return e ? atoi(e) : -1; }();
+  const int min_k = kind == kGemmDgradMasked ? 16384 : 4096;
   const bool wide_fit = (int64_t)((args.M + 255) / 256) * ((args.N + 511) / 512) >= 4 * (num_sms / 2) &&
-                        args.K >= 4096;
-  const bool wide = kind == kGemmFwd && (wide_env >= 0 ? wide_env == 1 : wide_fit);
+                        args.K >= min_k;
+  const bool wide = wide_env >= 0 ? wide_env == 1 : wide_fit;
   args.tiles_m = (args.M + 255) / 256;
   args.tiles_n = wide ? (args.N + 511) / 512 : (args.N + 255) / 256;
   if (args.group <= 0) args.group = 8;
@@ -623,9 +654,11 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
       return wide ? launch_one<false, false, 4, true>(maps, args, num_sms, stream)
                   : launch_one<false, false, 6>(maps, args, num_sms, stream);
     case kGemmDgrad:
-      return launch_one<true, false, 6>(maps, args, num_sms, stream);
+      return wide ? launch_one<true, false, 4, true>(maps, args, num_sms, stream)
+                  : launch_one<true, false, 6>(maps, args, num_sms, stream);
     case kGemmDgradMasked:
-      return launch_one<true, true, 6>(maps, args, num_sms, stream);
+      return wide ? launch_one<true, true, 4, true>(maps, args, num_sms, stream)
+                  : launch_one<true, true, 6>(maps, args, num_sms, stream);
   }
   return -1;
 }
