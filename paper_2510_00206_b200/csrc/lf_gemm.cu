@@ -473,36 +473,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                                         mapa_shared(smem_u32(&lmasked[1]), 0)};
     uint32_t lora_uses0 = 0, lora_uses1 = 0;
     // MASKED: zero the dropped elements of tile `it`'s LoRA partial in place
-    auto mask_pass = [&](const TileInfo& ti, int it) {
-      const int acc = it % NACC;
+    // keep bits of this thread's row over its columns [c_lo, c_hi) of tile `ti` (global
+    // loads, issued ahead of the LoRA partial); `active` false = nothing to mask
+    struct RowKeep {
+      bool active;
+      uint32_t bits[BN / 64];
+    };
+    auto fetch_keep = [&](const TileInfo& ti) {
+      RowKeep rk;
       const int row = ti.mb * 256 + (int)rank * Cfg::BM + (int)(q * 32 + lane);
-      const int rt_idx = 2 * ti.mb + (int)rank;
-      const bool in_m = row < args.M;
       int seg = -1;
-      if (in_m) {
-        const LfRoute rt = route_at(args, s_routes, rt_idx);
+      if (row < args.M) {
+        const LfRoute rt = route_at(args, s_routes, 2 * ti.mb + (int)rank);
         seg = find_segment(args.segs, rt.seg_lo, rt.seg_hi, row);
       }
-      bool active = seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0);
-      // keep bits of the row's columns [c_lo, c_hi), fetched before waiting on the LoRA partial
-      uint32_t keep[BN / 64];
+      rk.active = seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0);
 #pragma unroll
       for (int j = 0; j < BN / 64; ++j)
-        keep[j] = !active ? 0xFFFFFFFFu
-                  : (args.segs.debug & 128) ? 0x7FFFFFFFu  // profiling: skip the bit loads, keep the TMEM pass
-                                            : dgrad_keep32(args.segs, seg, row, ti.nb * BN + c_lo + 32 * j, args.N);
-      if (args.segs.debug & 64) active = false;
+        rk.bits[j] = !rk.active ? 0xFFFFFFFFu
+                     : (args.segs.debug & 128) ? 0x7FFFFFFFu  // profiling: skip the bit loads, keep the TMEM pass
+                                               : dgrad_keep32(args.segs, seg, row, ti.nb * BN + c_lo + 32 * j, args.N);
+      if (args.segs.debug & 64) rk.active = false;
+      return rk;
+    };
+    // MASKED: zero the dropped elements of tile `it`'s LoRA partial in place
+    auto mask_apply = [&](int it, const RowKeep& rk) {
+      const int acc = it % NACC;
       uint32_t& lu = acc ? lora_uses1 : lora_uses0;
       mbar_wait(&lfull[acc], lu & 1);
       ++lu;
       tc_fence_after();
       // tcgen05.ld/st are warp-collective (.sync.aligned): every branch around them is warp-uniform
-      if (__any_sync(0xFFFFFFFFu, active)) {
+      if (__any_sync(0xFFFFFFFFu, rk.active)) {
         const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * Cfg::ACC_COLS;
 #pragma unroll
         for (int j = 0; j < BN / 64; ++j) {
           const int c = c_lo + 32 * j;
-          const uint32_t kp = keep[j];
+          const uint32_t kp = rk.bits[j];
           if (__all_sync(0xFFFFFFFFu, kp == 0xFFFFFFFFu)) continue;
           uint32_t v[32];
           tmem_ld32(taddr + c, v);
@@ -518,16 +525,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(lmasked_leader[acc]);
     };
+    auto mask_pass = [&](const TileInfo& ti, int it) { mask_apply(it, fetch_keep(ti)); };
+    if constexpr (MASKED && WIDE) {
+      // One accumulator, so tile i+1's LoRA partial and its mask pass sit between tile i's
+      // main loop and tile i+1's: keep that gap short — tile i+1's keep bits are loaded
+      // before tile i's drain, the drain only moves TMEM into registers, and tile i's
+      // stores wait until tile i+1's mask pass has released the MMA.
+      int t = seq.first();
+      if (t >= 0) {
+        const TileInfo t0 = tile_info(args, s_routes, t);
+        if (t0.lora() && !(args.segs.debug & 4096)) mask_pass(t0, 0);
+      }
+      for (int it = 0; t >= 0; ++it) {
+        const TileInfo ti = tile_info(args, s_routes, t);
+        const int tn = seq.read(it + 1, lane == 0);
+        const bool next_lora = tn >= 0 && !(args.segs.debug & 4096) && tile_info(args, s_routes, tn).lora();
+        RowKeep nk;
+        if (next_lora) nk = fetch_keep(tile_info(args, s_routes, tn));
+        const int row = ti.mb * 256 + (int)rank * Cfg::BM + (int)(q * 32 + lane);
+        mbar_wait(&tfull[0], (uint32_t)it & 1u);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((q * 32u) << 16);
+        uint32_t pk[(BN / 2) / 2];
+#pragma unroll
+        for (int c = 0; c < BN / 2; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c_lo + c, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pk[c / 2 + j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader[0]);
+        if (next_lora) mask_apply(it + 1, nk);
+        if (row < args.M) {
+          __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(args.C) + (int64_t)row * args.ldc;
+#pragma unroll
+          for (int c = 0; c < BN / 2; c += 8) {
+            const int col = ti.nb * BN + c_lo + c;
+            if (col < args.N)
+              *reinterpret_cast<uint4*>(crow + col) = make_uint4(pk[c / 2], pk[c / 2 + 1], pk[c / 2 + 2], pk[c / 2 + 3]);
+          }
+        }
+        t = tn;
+      }
+    } else {
     int t = seq.first();
     for (int it = 0; t >= 0; ++it) {
       const TileInfo ti = tile_info(args, s_routes, t);
       const int acc = it % NACC;
       const uint32_t aph = (it / NACC) & 1;
       int tn = -1;
-      if constexpr (MASKED && WIDE) {
-        if (ti.lora() && !(args.segs.debug & 4096)) mask_pass(ti, it);
-        tn = seq.read(it + 1, lane == 0);
-      } else if constexpr (MASKED) {
+      if constexpr (MASKED) {
         const bool plain = (args.segs.debug & 4096) != 0;  // profiling: the MMA issues no LoRA-first blocks
         if (it == 0 && ti.lora() && !plain) mask_pass(ti, 0);
         tn = seq.read(it + 1, lane == 0);
@@ -595,6 +645,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       if constexpr (!MASKED) tn = seq.read(it + 1, lane == 0);
       t = tn;
     }
+    }
   }
 
   tc_fence_before();
@@ -630,11 +681,12 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
   // 25% fewer L2 sectors per FLOP buys clock under the power cap — C4 q/gate/down 6/5.5/12.6%
   // faster, C2 gate 3.8%; with fewer than ~4 waves the coarser tiles quantise badly (C2 q,
   // down: 4–14% slower). ncu, profiles/r01_wide_tiles_ab.txt
-  // The masked dgrad runs wide tiles sequentially (accumulator drain -> LoRA partial -> TMEM
-  // mask pass -> main loop, ~6-18% exposed at K = 4096-8192), which only long reductions
-  // amortise: C4 gate/up dgrad (K = 28672) 5.21 -> 4.90 ms, q/o and down (K = 8192) 4-5% slower.
+  // The masked dgrad runs wide tiles sequentially (drain to registers -> LoRA partial -> TMEM
+  // mask pass -> main loop; next tile's keep bits prefetched, stores deferred), which pays off
+  // from K = 8192: C4 q/o 1.45 -> 1.40, gate/up 5.24 -> 4.91, down 5.05 -> 4.91 ms; at K = 4096
+  // (C2 down) 2% slower.
   static const int wide_env = [] { const char* e = getenv("LF_WIDE"); return e ? atoi(e) : -1; }();
-  const int min_k = kind == kGemmDgradMasked ? 16384 : 4096;
+  const int min_k = kind == kGemmDgradMasked ? 8192 : 4096;
   const bool wide_fit = (int64_t)((args.M + 255) / 256) * ((args.N + 511) / 512) >= 4 * (num_sms / 2) &&
                         args.K >= min_k;
   const bool wide = wide_env >= 0 ? wide_env == 1 : wide_fit;
