@@ -401,9 +401,11 @@ int lf_grad_up(const LfProblem* p, const uint16_t* dy, const uint16_t* b_cat, co
   split_workspace(p, &a.ws, &a.counters);
   a.routes = reinterpret_cast<const lf::LfRoute*>(p->routes);
   a.segs = t;
-  lf::grad_up_grid(p->m, p->n, p->rank_total, d.sms, &a.n_split, &a.m_split, &a.nacc);
+  static const int gu_per_sm_env = env_int("LF_GU_PER_SM", 0);
+  const int per_sm = gu_per_sm_env > 0 ? gu_per_sm_env : 1;
+  lf::grad_up_grid(p->m, p->n, p->rank_total, d.sms, per_sm, &a.n_split, &a.m_split, &a.nacc);
   if (a.n_split <= 0) return fail(LF_E_INVALID, "rank_total=%d too large for grad_up TMEM budget", p->rank_total);
-  if (lf::grad_up_launch(tdy, tb, ts, a, d.sms, (cudaStream_t)stream)) return cuda_fail("grad_up launch");
+  if (lf::grad_up_launch(tdy, tb, ts, a, d.sms, per_sm, (cudaStream_t)stream)) return cuda_fail("grad_up launch");
   return LF_OK;
 }
 

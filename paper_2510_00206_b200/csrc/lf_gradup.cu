@@ -22,7 +22,7 @@ constexpr int DY_BYTES = 2 * 128 * 64 * 2;  // 32 KB: two 64-column SW128 boxes 
 constexpr int MAX_SMEM = 200 * 1024;
 }  // namespace gup
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, 2)
     lf_gradup_kernel(const __grid_constant__ CUtensorMap tmDy, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmS, const __grid_constant__ GradUpArgs args, int stages,
                      int stage_bytes) {
@@ -258,12 +258,14 @@ __global__ void __launch_bounds__(192, 1)
 // CTA's n-range must fit TMEM next to the two dŜ buffers: (2 + nsub) * R <= 512.
 // Among admissible splits pick the smallest critical path (max units of one 32 KB dY tile
 // per CTA), then the least partial-sum traffic R * (m_split * n + n_split * m).
-void grad_up_grid(int m, int n, int rtot, int sms, int* n_split, int* m_split, int* nacc) {
+void grad_up_grid(int m, int n, int rtot, int sms, int per_sm, int* n_split, int* m_split, int* nacc) {
   const int tiles_m = (m + 127) / 128, tiles_n = (n + 127) / 128;
   // measured on B200: rotating K-steps over several accumulators does not speed the
   // small-N chains up (the pipelines are TMA-bound), so one accumulator keeps TMEM free
   *nacc = 1;
-  const int max_nsub = 512 / (*nacc * rtot) - 2;
+  // per_sm CTAs share an SM's 512 TMEM columns (and its shared memory)
+  const int max_nsub = (512 / per_sm) / (*nacc * rtot) - 2;
+  sms *= per_sm;
   *n_split = 0;
   *m_split = 0;
   if (max_nsub < 1) return;
@@ -285,11 +287,11 @@ void grad_up_grid(int m, int n, int rtot, int sms, int* n_split, int* m_split, i
 }
 
 int grad_up_launch(const CUtensorMap& tm_dy, const CUtensorMap& tm_b, const CUtensorMap& tm_s,
-                   const GradUpArgs& args, int num_sms, cudaStream_t stream) {
+                   const GradUpArgs& args, int num_sms, int per_sm, cudaStream_t stream) {
   (void)num_sms;
   const int sh_bytes = (args.rtot / 16) * 4096;
   const int stage_bytes = gup::DY_BYTES + sh_bytes;
-  int stages = (gup::MAX_SMEM - 2 * sh_bytes) / stage_bytes;
+  int stages = (gup::MAX_SMEM / per_sm - 2 * sh_bytes) / stage_bytes;
   if (stages > 6) stages = 6;  // deep ring: ~180 KB of dY in flight per SM
   if (stages < 2) return -1;
   const int smem = stages * stage_bytes + 2 * sh_bytes + 1024 + 1024;

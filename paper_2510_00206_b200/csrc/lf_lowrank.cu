@@ -14,6 +14,8 @@
 // dropout is active four "mask" warps zero the dropped bf16 lanes of each tile in shared
 // memory (Philox4x32-10, 8 keep bits per call = one 16-byte chunk) before the single
 // MMA-issuing thread consumes it.
+#include <cstdlib>
+
 #include "lf_device.cuh"
 #include "lf_kernels.h"
 
@@ -540,11 +542,14 @@ __global__ void __launch_bounds__(kDgaThreads, 2)
   }
 }
 
-// Two layouts: without TMA'd keep bits, 2 CTAs / SM x ~110 KB rings; with them (2 KB more
-// per stage) 3 stages no longer fit twice, so 1 CTA / SM with a ~200 KB ring.
+// 2 CTAs / SM x ~110 KB rings (with TMA'd keep bits, 2 KB more per stage: 2 stages each).
 void grad_down_config(int rtot, bool bits_tma, int* stages, int* stage_bytes) {
   *stage_bytes = dga::X_BYTES + (rtot / 16) * 4096 + (bits_tma ? 2048 : 0);
-  int s = (bits_tma ? 196 * 1024 : 110 * 1024) / *stage_bytes;
+  static const int budget_kb = [] { const char* e = getenv("LF_DGA_SMEM_KB"); return e ? atoi(e) : 0; }();
+  // ~110 KB rings so two CTAs share each SM (with keep bits too: 2 x 2 stages beat one CTA
+  // with a 5-stage ring by 18-20%, kbench m = 8192/16384) unless R makes a stage too big
+  (void)bits_tma;
+  int s = (budget_kb > 0 ? budget_kb * 1024 : 112 * 1024) / *stage_bytes;
   *stages = s < 2 ? 2 : (s > 6 ? 6 : s);
 }
 
