@@ -399,7 +399,9 @@ def test_every_case_under_each_gemm_schedule(sched, wide):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, LF_SCHED=sched, LF_WIDE=wide)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
-                        os.path.join(root, "tests", "test_gpu_parity.py"), "-k", "test_kernels_match_oracle",
+                        os.path.join(root, "tests", "test_gpu_parity.py"), "-k",
+                        "test_kernels_match_oracle or test_explicit_keep_mask or test_module_api or test_shared_adapter "
+                        "or test_max_segments or test_microbatch_beyond",
                         "-m", "gpu"], cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
