@@ -61,6 +61,23 @@ def _init_capturable(mod: nn.Module, capturable: bool, device) -> None:
         mod.register_buffer("step_counter", torch.zeros(1, dtype=torch.int64, device=device), persistent=False)
 
 
+def _dropout_state(mod: nn.Module) -> dict:
+    """The Philox step counter, for checkpoints: restoring it makes a resumed run draw
+    exactly the dropout masks the uninterrupted run would have drawn (SPEC.md §3). Kept out
+    of ``state_dict`` so PEFT-style state dicts load strictly into the modules."""
+    step = int(mod.step_counter.item()) if mod.capturable else int(mod._offset)
+    return {"philox_step": step, "capturable": mod.capturable}
+
+
+def _load_dropout_state(mod: nn.Module, state: dict) -> None:
+    step = int(state.get("philox_step", 0))
+    if mod.capturable:
+        with torch.no_grad():
+            mod.step_counter.fill_(step)
+    else:
+        mod._offset = step
+
+
 def _step_offsets(mod: nn.Module) -> tuple[int, torch.Tensor | None]:
     """(host offset, device counter) of this forward (SPEC.md §3)."""
     if not mod.training:
@@ -117,6 +134,12 @@ class FusedLoRA(nn.Module):
         off = self._offset
         self._offset += 1
         return off
+
+    def dropout_state(self) -> dict:
+        return _dropout_state(self)
+
+    def load_dropout_state(self, state: dict) -> None:
+        _load_dropout_state(self, state)
 
     def forward(self, x: torch.Tensor, keep_mask: torch.Tensor | None = None) -> torch.Tensor:
         c = self.config
@@ -191,6 +214,12 @@ class FusedMultiLoRA(nn.Module):
         off = self._offset
         self._offset += 1
         return off
+
+    def dropout_state(self) -> dict:
+        return _dropout_state(self)
+
+    def load_dropout_state(self, state: dict) -> None:
+        _load_dropout_state(self, state)
 
     def _sink(self, plan: LayerPlan, da: torch.Tensor, db: torch.Tensor) -> None:
         for adapter, batch, c0, r in plan.segment_grad_slices():

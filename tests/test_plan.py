@@ -195,3 +195,25 @@ def test_split_segments_respects_launch_limits():
     assert [len(g) for _, _, g in split_segments([AdapterConfig(8)], many, 40)] == [32, 8]
     with pytest.raises(ValidationError):
         split_segments([AdapterConfig(200)], [Segment(0, 0, 4)], 4)
+
+
+def test_module_dropout_state_round_trip_and_strict_state_dict():
+    """Checkpoints: the Philox step is saved/restored explicitly (resumed runs continue the
+    dropout stream), and the state dict holds only the PEFT-named tensors, so it loads
+    strictly (CPU: no kernel runs)."""
+    from paper_2510_00206_b200 import FusedLoRA, FusedMultiLoRA
+
+    w = torch.zeros(64, 32, dtype=torch.bfloat16)
+    a = FusedLoRA(w, rank=8, dropout_p=0.1, seed=3)
+    a._offset = 17
+    b = FusedLoRA(w.clone(), rank=8, dropout_p=0.1, seed=3)
+    b.load_state_dict(a.state_dict(), strict=True)
+    assert set(a.state_dict()) == {"lora_A.weight", "lora_B.weight"}
+    b.load_dropout_state(a.dropout_state())
+    assert b._offset == 17 and b.next_offset() == 17
+    m = FusedMultiLoRA(w, [AdapterConfig(8), AdapterConfig(16)])
+    m._offset = 5
+    m2 = FusedMultiLoRA(w.clone(), [AdapterConfig(8), AdapterConfig(16)])
+    m2.load_state_dict(m.state_dict(), strict=True)
+    m2.load_dropout_state(m.dropout_state())
+    assert m2._offset == 5 and torch.equal(m2.lora_B[1].weight, m.lora_B[1].weight)
