@@ -769,14 +769,34 @@ def run_c5(args, rank: int, world: int, local_rank: int) -> None:
 
     def arm(fused: bool, steps: int):
         dgen = torch.Generator(device=device).manual_seed(1234)  # same weights on every rank
-        model = D.LoRADecoder(shape, adapters, fused=fused, device=device, generator=dgen)
+        model = D.LoRADecoder(shape, adapters, fused=fused, device=device, generator=dgen, capturable=args.graph)
         model.train()
         params = model.adapter_parameters()
-        # bucketed fp32 all-reduce launched from post-accumulate-grad hooks during the
-        # step's last backward (overlapped, DDP-style)
-        reducer = dp.AdapterGradReducer(params).attach() if world > 1 else None
         opt = torch.optim.AdamW(params, lr=1e-4, fused=True)
-        fn = lambda: D.train_step(model, packed, reducer, opt)  # noqa: E731
+        fn = None
+        graph_launches = None
+        if args.graph:
+            # both arms as per-microbatch CUDA graphs: 32 layers x (7 LoRA linears + attention
+            # + norms) of eager launches are host-bound (fused: 314 ms enqueue per 8k-token
+            # microbatch vs 323 ms on the device)
+            try:
+                reducer = dp.AdapterGradReducer(params) if world > 1 else None
+                cap_counts = F_.LaunchStats(timed=False)
+                F_.set_launch_stats(cap_counts)  # 2 warm-up passes + the capture pass
+                fn = D.GraphedTrainStep(model, packed, reducer, opt, warmup=2)
+                F_.set_launch_stats(None)
+                graph_launches = cap_counts.total_launches() // 3
+            except Exception as e:
+                F_.set_launch_stats(None)
+                print(f"[bench] C5 graph capture failed ({type(e).__name__}: {e}); timing eagerly", file=sys.stderr)
+                for p_ in params:
+                    p_.grad = None
+                fn = None
+        if fn is None:
+            # bucketed fp32 all-reduce launched from post-accumulate-grad hooks during the
+            # step's last backward (overlapped, DDP-style)
+            reducer = dp.AdapterGradReducer(params).attach() if world > 1 else None
+            fn = lambda: D.train_step(model, packed, reducer, opt)  # noqa: E731
         counts = None
         if fused:
             for _ in range(args.warmup):
@@ -785,10 +805,12 @@ def run_c5(args, rank: int, world: int, local_rank: int) -> None:
             F_.set_launch_stats(counts)
             ms = time_loop(fn, steps, 0, barrier)
             F_.set_launch_stats(None)
+            if graph_launches is not None:  # replays launch from the graph, not from Python
+                counts = graph_launches * steps
         else:
             ms = time_loop(fn, steps, args.warmup, barrier)
         peak = torch.cuda.max_memory_allocated(device)
-        del model, params, reducer, opt
+        del model, params, reducer, opt, fn
         torch.cuda.empty_cache()
         torch.cuda.reset_peak_memory_stats(device)
         return max_over_ranks(ms), counts, peak
@@ -830,6 +852,7 @@ def run_c5(args, rank: int, world: int, local_rank: int) -> None:
                 "raw_tokens_per_step": raw_all,
                 "parallelism": f"dp{world}",
                 "optimizer": "AdamW (fused) on the fp32 adapter weights",
+                "execution": "per-microbatch CUDA graphs, both arms" if args.graph else "eager",
                 "l2": "inputs larger than L2",
             },
             "padded_rows_per_s": rows_all / (ms * 1e-3),
@@ -840,7 +863,7 @@ def run_c5(args, rank: int, world: int, local_rank: int) -> None:
             "unfused_torch": {"ms_per_step": unf_ms, "tokens_per_s": raw_all / (unf_ms * 1e-3),
                               "speedup": unf_ms / ms, "peak_mem_gb": unf_peak / 1e9},
             "peak_mem_gb": peak / 1e9,
-            "gpu_launches": counts.total_launches() if counts else None,
+            "gpu_launches": (counts if isinstance(counts, int) else counts.total_launches()) if counts else None,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -180,7 +180,7 @@ def varlen_attention_sdpa(q, k, v, cu_seqlens, scale=None):
 
 class DecoderLayer(nn.Module):
     def __init__(self, shape: DecoderShape, adapters: Sequence[AdapterConfig], layer_idx: int, fused: bool,
-                 device, generator=None, dtype=torch.bfloat16, attention: str = "flash"):
+                 device, generator=None, dtype=torch.bfloat16, attention: str = "flash", capturable: bool = False):
         super().__init__()
         if fused and dtype != torch.bfloat16:
             raise ValidationError("the fused layers compute in bf16")
@@ -195,7 +195,7 @@ class DecoderLayer(nn.Module):
             ads = [AdapterConfig(a.rank, a.scaling, a.dropout_p, seed=(a.seed * 1000003 + layer_idx * 7 + i) % 2**63)
                    for a in adapters]
             if fused:
-                self.proj[name] = FusedMultiLoRA(w, ads, init="gaussian", generator=generator)
+                self.proj[name] = FusedMultiLoRA(w, ads, init="gaussian", generator=generator, capturable=capturable)
             else:
                 self.proj[name] = TorchMultiLoRA(w, ads, generator=generator)
 
@@ -227,7 +227,8 @@ class LoRADecoder(nn.Module):
     every base weight frozen, 7 multi-adapter LoRA linears per layer."""
 
     def __init__(self, shape: DecoderShape, adapters: Sequence[AdapterConfig], *, fused: bool = True, device=None,
-                 generator=None, max_pos: int = 8192, dtype=torch.bfloat16, attention: str = "flash"):
+                 generator=None, max_pos: int = 8192, dtype=torch.bfloat16, attention: str = "flash",
+                 capturable: bool = False):
         super().__init__()
         self.shape = shape
         self.adapters = list(adapters)
@@ -235,8 +236,8 @@ class LoRADecoder(nn.Module):
         self.embed.weight.requires_grad_(False)
         with torch.no_grad():
             self.embed.weight.normal_(0, 1.0, generator=generator)
-        self.layers = nn.ModuleList(DecoderLayer(shape, adapters, i, fused, device, generator, dtype, attention)
-                                    for i in range(shape.layers))
+        self.layers = nn.ModuleList(DecoderLayer(shape, adapters, i, fused, device, generator, dtype, attention,
+                                                 capturable) for i in range(shape.layers))
         self.norm = RMSNorm(shape.hidden, shape.eps, device, dtype)
         self.head = (torch.randn(shape.vocab, shape.hidden, device=device, generator=generator) /
                      math.sqrt(shape.hidden)).to(dtype)
@@ -278,3 +279,50 @@ def train_step(model: LoRADecoder, microbatches: Sequence[PackedMicrobatch], red
         optimizer.step()
         optimizer.zero_grad(set_to_none=True)
     return total
+
+
+class GraphedTrainStep:
+    """A training step whose per-microbatch forward+backward passes replay as CUDA graphs.
+
+    One graph per microbatch (its shape and segments are baked in), all drawing from one
+    memory pool — they replay in capture order, so each reuses the activation memory the
+    previous one released and the peak stays that of one microbatch. The first graph
+    writes the adapter gradients, the others accumulate into the same tensors, so the
+    optimizer (eager, after the replays) must not reset ``.grad`` to None. The gradient
+    all-reduce (``reducer.reduce()``) and the optimizer step run eagerly after the replays.
+    The fused layers must be ``capturable`` (device-side Philox counters)."""
+
+    def __init__(self, model: LoRADecoder, microbatches: Sequence[PackedMicrobatch], reducer=None, optimizer=None,
+                 warmup: int = 2):
+        self.model, self.reducer, self.optimizer = model, reducer, optimizer
+        params = model.adapter_parameters()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(max(1, warmup)):
+                for mb in microbatches:
+                    model(mb).backward()
+        torch.cuda.current_stream().wait_stream(side)
+        for p in params:
+            p.grad = None
+        pool = torch.cuda.graph_pool_handle()
+        self.graphs, self.losses = [], []
+        for mb in microbatches:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=pool):
+                loss = model(mb)
+                loss.backward()
+            self.graphs.append(g)
+            self.losses.append(loss.detach())
+
+    def __call__(self):
+        for g in self.graphs:
+            g.replay()
+        if self.reducer is not None:
+            self.reducer.reduce()
+        if self.optimizer is not None:
+            self.optimizer.step()
+        total = self.losses[0]
+        for l in self.losses[1:]:
+            total = total + l
+        return total
