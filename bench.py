@@ -524,6 +524,18 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     unf_ms = time_loop(lambda: unfused_step(args.config, base, inputs, grads, p), max(2, args.steps // 2),
                        args.warmup, barrier)
     unf_ms = max_over_ranks(unf_ms)
+    unf_graph_ms = None
+    if args.graph:
+        # the same unfused step captured as a CUDA graph too, so the comparison holds
+        # without host overhead on either side (torch dropout is graph-safe)
+        try:
+            from paper_2510_00206_b200.graphs import GraphedStep
+
+            g_unf = GraphedStep(lambda: unfused_step(args.config, base, inputs, grads, p), warmup=args.warmup)
+            unf_graph_ms = max_over_ranks(time_loop(g_unf.replay, max(2, args.steps // 2), args.warmup, barrier))
+            del g_unf
+        except Exception as e:
+            print(f"[bench] unfused graph capture failed ({type(e).__name__}: {e})", file=sys.stderr)
 
     # ---- secondary: C3 FusedMultiLoRA (BASELINE.json configs[2]) on the same box ------
     multi = None
@@ -567,7 +579,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             "tflops_per_gpu": flops / (ms * 1e-3) / 1e12,
             "frac_of_bf16_peak": flops / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
             "unfused_torch": {"ms_per_step": unf_ms, "tokens_per_s": world * m / (unf_ms * 1e-3),
-                              "speedup": unf_ms / ms},
+                              "speedup": unf_ms / ms, "execution": "eager (as PEFT runs it)",
+                              "graph_ms_per_step": unf_graph_ms,
+                              "speedup_vs_graph": (unf_graph_ms / ms) if unf_graph_ms else None},
             "roofline": roofline,
             "gpu_launches": launches,
             "clocks": clk,
