@@ -37,6 +37,11 @@ def _nvcc() -> str:
     return cand
 
 
+def _extra_flags() -> list[str]:
+    """LF_EXTRA_NVCC: extra nvcc flags for A/B experiments (e.g. -DLF_SUSPEND_NS=0)."""
+    return os.environ.get("LF_EXTRA_NVCC", "").split()
+
+
 def _sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu"))
 
@@ -47,7 +52,7 @@ def _fingerprint(debug: bool) -> str:
         if p.is_file():
             h.update(p.name.encode())
             h.update(p.read_bytes())
-    h.update(repr((ARCH_FLAGS, debug)).encode())
+    h.update(repr((ARCH_FLAGS, debug, _extra_flags())).encode())
     return h.hexdigest()[:16]
 
 
@@ -63,6 +68,7 @@ def build(force: bool = False, debug: bool = False, verbose: bool = False) -> Pa
     common = [
         *ARCH_FLAGS,
         *opt,
+        *_extra_flags(),
         "-lineinfo",
         "-std=c++17",
         "-Xcompiler",

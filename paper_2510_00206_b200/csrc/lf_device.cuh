@@ -92,14 +92,18 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t addr, uint32_t parity
 // barrier unit until the phase completes (or the hint, in ns, runs out) instead of
 // re-issuing try_wait — spinning waiters otherwise steal issue slots from the ALU-bound
 // mask warps sharing their scheduler.
+#ifndef LF_SUSPEND_NS
+#define LF_SUSPEND_NS 0x100000u
+#endif
 __device__ __forceinline__ uint32_t mbar_try_wait_sleep(uint32_t addr, uint32_t parity) {
+  if (LF_SUSPEND_NS == 0u) return mbar_try_wait(addr, parity);
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.b32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(addr), "r"(parity), "r"(0x100000u)
+      : "r"(addr), "r"(parity), "r"(LF_SUSPEND_NS)
       : "memory");
   return ok;
 }

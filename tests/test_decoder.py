@@ -142,6 +142,11 @@ def test_tiny_decoder_fused_as_accurate_as_unfused_torch():
     assert all(ef <= 2.0 * eb + 1e-2 for ef, eb in zip(e_f, e_b))
 
 
+# two runs of the same step differ in fp32 red.add order, which can flip the bf16 rounding of
+# a stored dŜ element and move whole gradient rows by one ulp: SPEC.md §5's end-to-end bound
+GRAD_RTOL = 4e-3
+
+
 @pytest.mark.gpu
 def test_graphed_train_step_matches_eager():
     """GraphedTrainStep (per-microbatch CUDA graphs sharing one pool) gives the eager step's
@@ -160,9 +165,10 @@ def test_graphed_train_step_matches_eager():
     for pe, pg in zip(eager.adapter_parameters(), graphed.adapter_parameters()):
         assert pg.grad is not None
         rel = float((pg.grad - pe.grad).norm() / pe.grad.norm().clamp_min(1e-12))
-        assert rel < 1e-3, rel
+        assert rel < GRAD_RTOL, rel
     # a second replay overwrites (first graph) and re-accumulates: same gradients again
     step()
     torch.cuda.synchronize()
     for pe, pg in zip(eager.adapter_parameters(), graphed.adapter_parameters()):
-        assert float((pg.grad - pe.grad).norm() / pe.grad.norm().clamp_min(1e-12)) < 1e-3
+        rel = float((pg.grad - pe.grad).norm() / pe.grad.norm().clamp_min(1e-12))
+        assert rel < GRAD_RTOL, rel

@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--rounds", type=int, default=1, help="repeat the kernel list (A/B interleaving under the power cap)")
     ap.add_argument("--power", action="store_true", help="sample SM clock and board power (NVML) per timed loop")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture the timed loop as one CUDA graph (GPU time without the per-call host cost)")
     args = ap.parse_args()
     import torch
 
@@ -114,12 +116,25 @@ def main():
         for i in range(3):
             _lib.check(fn(i % nbuf), name)
         torch.cuda.synchronize()
+        graph = None
+        if args.graph and not name.startswith("overlap"):
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+                for i in range(args.iters):
+                    fn(i % nbuf)
+            st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+            graph.replay()
+            torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if sampler:
             sampler.start()
         e0.record()
-        for i in range(args.iters):
-            fn(i % nbuf)
+        if graph is not None:
+            graph.replay()
+        else:
+            for i in range(args.iters):
+                fn(i % nbuf)
         e1.record()
         torch.cuda.synchronize()
         extra = sampler.stop() if sampler else {}

@@ -76,7 +76,8 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 int main(int argc, char** argv) {
-  const long rows = 8192, cols = 4096;  // 64 MB bf16; 4 rotating copies > L2
+  // rows from argv[1] (default 8192 = 64 MB bf16); 4 rotating copies > L2 at the default
+  const long rows = argc > 1 ? atol(argv[1]) : 8192, cols = 4096;
   const int NB = 4;
   void* bufs[NB];
   for (int i = 0; i < NB; ++i) {
