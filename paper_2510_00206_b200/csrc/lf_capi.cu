@@ -404,6 +404,17 @@ int lf_grad_up(const LfProblem* p, const uint16_t* dy, const uint16_t* b_cat, co
   static const int gu_per_sm_env = env_int("LF_GU_PER_SM", 0);
   const int per_sm = gu_per_sm_env > 0 ? gu_per_sm_env : 1;
   lf::grad_up_grid(p->m, p->n, p->rank_total, d.sms, per_sm, &a.n_split, &a.m_split, &a.nacc);
+  static const int gu_ns_env = env_int("LF_GU_NSPLIT", 0);  // profiling: force the n-split
+  if (gu_ns_env > 0 && a.n_split > 0) {
+    const int tiles_n = (p->n + 127) / 128, tiles_m = (p->m + 127) / 128;
+    const int max_nsub = 512 / per_sm / p->rank_total - 2;
+    int ns = gu_ns_env < tiles_n ? gu_ns_env : tiles_n;
+    if ((tiles_n + ns - 1) / ns <= max_nsub) {
+      int ms = d.sms * per_sm / ns;
+      a.n_split = ns;
+      a.m_split = ms < 1 ? 1 : (ms > tiles_m ? tiles_m : ms);
+    }
+  }
   if (a.n_split <= 0) return fail(LF_E_INVALID, "rank_total=%d too large for grad_up TMEM budget", p->rank_total);
   if (lf::grad_up_launch(tdy, tb, ts, a, d.sms, per_sm, (cudaStream_t)stream)) return cuda_fail("grad_up launch");
   return LF_OK;
