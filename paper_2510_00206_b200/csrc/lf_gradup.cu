@@ -264,7 +264,12 @@ void grad_up_grid(int m, int n, int rtot, int sms, int per_sm, int* n_split, int
   // small-N chains up (the pipelines are TMA-bound), so one accumulator keeps TMEM free
   *nacc = 1;
   // per_sm CTAs share an SM's 512 TMEM columns (and its shared memory)
-  const int max_nsub = (512 / per_sm) / (*nacc * rtot) - 2;
+  // at most 8 n-subtiles per CTA: each CTA flushes its dB partials (nsub x 128 x R fp32
+  // red.adds) at its very end, where nothing overlaps them — measured at n = 28672, R = 16:
+  // 25 subtiles per CTA 36.9 / 53.2 / 86.1 µs at m = 2048 / 4096 / 8192, <= 8 subtiles
+  // 26.8 / ~47 / 81.9 µs (profiles/r01_gradup_split_sweep.txt)
+  int max_nsub = (512 / per_sm) / (*nacc * rtot) - 2;
+  if (max_nsub > 8) max_nsub = 8;
   sms *= per_sm;
   *n_split = 0;
   *m_split = 0;
