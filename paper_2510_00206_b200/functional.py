@@ -205,6 +205,24 @@ class _FusedLoRAFn(torch.autograd.Function):
         return (dx, None, None, None, None, *ga, *gb)
 
 
+class _EmptyBatchFn(torch.autograd.Function):
+    """An empty batch (m = 0) like nn.Linear: an empty (0, n) output that stays on the
+    autograd graph, so backward gives an empty dX and all-zero adapter gradients. Nothing is
+    launched (there is no work)."""
+
+    @staticmethod
+    def forward(ctx, x, n: int, *params):
+        ctx.x_shape = x.shape
+        ctx.shapes = [(p.shape, p.dtype, p.device) for p in params]
+        return x.new_empty((0, n))
+
+    @staticmethod
+    def backward(ctx, dy):
+        dx = dy.new_empty(ctx.x_shape) if ctx.needs_input_grad[0] else None
+        grads = [torch.zeros(sh, dtype=dt, device=dev) for sh, dt, dev in ctx.shapes]
+        return (dx, None, *grads)
+
+
 def _flatten_input(x: torch.Tensor, k: int) -> tuple[torch.Tensor, tuple]:
     if x.shape[-1] != k:
         raise ValidationError(f"input last dim {x.shape[-1]} != in_features {k}")
@@ -316,7 +334,7 @@ def _run(x2, weight, lora_a, lora_b, plan: LayerPlan, lead, grad_sink):
         if not (a.is_cuda and b.is_cuda):
             raise ValidationError("adapter weights must be CUDA tensors")
     if plan.m == 0:
-        return x2.new_empty(lead + (plan.n,))
+        return _EmptyBatchFn.apply(x2, plan.n, *lora_a, *lora_b).reshape(lead + (plan.n,))
     plan.bind(x2.device)
     y = _FusedLoRAFn.apply(x2, weight, plan, grad_sink, len(lora_a), *lora_a, *lora_b)
     return y.reshape(lead + (plan.n,))

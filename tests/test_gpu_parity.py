@@ -179,6 +179,22 @@ def test_module_api_fused_lora_matches_oracle():
     H.assert_chain_close(y2.float().cpu().numpy(), ref0["y"], "api:eval_y")
 
 
+def test_empty_batch_like_nn_linear():
+    """m = 0 (e.g. a (2, 0, k) batch): an empty output that stays on the autograd graph, an
+    empty dX and all-zero adapter gradients — what nn.Linear / PEFT give; nothing launches."""
+    from paper_2510_00206_b200 import FusedLoRA
+
+    w = torch.randn(384, 256, device=DEV).to(torch.bfloat16)
+    layer = FusedLoRA(w, rank=16, scaling=2.0, dropout_p=0.1, seed=3).to(DEV)
+    x = torch.empty(2, 0, 256, device=DEV, dtype=torch.bfloat16, requires_grad=True)
+    y = layer(x)
+    assert y.shape == (2, 0, 384) and y.requires_grad
+    y.sum().backward()
+    assert x.grad is not None and x.grad.shape == x.shape
+    for p in (layer.lora_A.weight, layer.lora_B.weight):
+        assert p.grad is not None and p.grad.shape == p.shape and not p.grad.any()
+
+
 def test_module_api_multi_lora_slots():
     from paper_2510_00206_b200 import AdapterConfig, FusedMultiLoRA, segments_from_lengths
 
