@@ -711,7 +711,9 @@ __device__ __forceinline__ int find_segment(const LfSegTable& t, int lo, int hi,
 }
 
 // finalize one row of a split-K reduced m x R result: scale own-segment columns, zero the
-// rest, write bf16, and return the partial-sum workspace to zero.
+// rest, write bf16, and return the partial-sum workspace to zero. The loads of up to four
+// 8-column chunks are issued before any store (the stores alias the loaded workspace, so a
+// load-store-load loop would pay one L2 round trip per chunk: 16 at R = 128).
 __device__ __forceinline__ void finalize_row(const LfSegTable& t, const LfRoute& rt, int row, float* ws,
                                              __nv_bfloat16* out) {
   const int rtot = t.rtot;
@@ -721,21 +723,48 @@ __device__ __forceinline__ void finalize_row(const LfSegTable& t, const LfRoute&
   const float scale = seg >= 0 ? t.seg[seg].scale : 0.f;
   float* wrow = ws + (int64_t)row * rtot;
   __nv_bfloat16* orow = out + (int64_t)row * rtot;
-  for (int c = 0; c < rtot; c += 8) {
-    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    const bool in_range = c >= rt.col_lo && c < rt.col_hi;
-    if (in_range) {
-      const float4 a = ld_cg_f4(wrow + c), b = ld_cg_f4(wrow + c + 4);
-      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-      *reinterpret_cast<float4*>(wrow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-      *reinterpret_cast<float4*>(wrow + c + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int g = 0; g < rtot; g += 32) {
+    float4 v[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = g + 8 * i;
+      const bool in_range = c < rtot && c >= rt.col_lo && c < rt.col_hi;
+      v[2 * i] = in_range ? ld_cg_f4(wrow + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[2 * i + 1] = in_range ? ld_cg_f4(wrow + c + 4) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const bool own = c >= own0 && c < own1;
-    const float s = own ? scale : 0.f;
-    *reinterpret_cast<uint4*>(orow + c) = make_uint4(pack_bf16x2(v[0] * s, v[1] * s), pack_bf16x2(v[2] * s, v[3] * s),
-                                                     pack_bf16x2(v[4] * s, v[5] * s), pack_bf16x2(v[6] * s, v[7] * s));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = g + 8 * i;
+      if (c >= rtot) break;
+      if (c >= rt.col_lo && c < rt.col_hi) {
+        *reinterpret_cast<float4*>(wrow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float4*>(wrow + c + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      const float sc = (c >= own0 && c < own1) ? scale : 0.f;
+      const float4 a = v[2 * i], b = v[2 * i + 1];
+      *reinterpret_cast<uint4*>(orow + c) = make_uint4(pack_bf16x2(a.x * sc, a.y * sc), pack_bf16x2(a.z * sc, a.w * sc),
+                                                       pack_bf16x2(b.x * sc, b.y * sc), pack_bf16x2(b.z * sc, b.w * sc));
+    }
   }
+}
+
+// one 8-column chunk of finalize_row (the separate finalize launch: one thread per chunk)
+__device__ __forceinline__ void finalize_chunk(const LfSegTable& t, const LfRoute& rt, int row, int c, float* ws,
+                                               __nv_bfloat16* out) {
+  const int seg = find_segment(t, rt.seg_lo, rt.seg_hi, row);
+  const bool own = seg >= 0 && c >= t.seg[seg].col0 && c < t.seg[seg].col0 + t.seg[seg].ncol;
+  const float sc = own ? t.seg[seg].scale : 0.f;
+  float* w = ws + (int64_t)row * t.rtot + c;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+  if (c >= rt.col_lo && c < rt.col_hi) {
+    a = ld_cg_f4(w);
+    b = ld_cg_f4(w + 4);
+    *reinterpret_cast<float4*>(w) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(w + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  *reinterpret_cast<uint4*>(out + (int64_t)row * t.rtot + c) =
+      make_uint4(pack_bf16x2(a.x * sc, a.y * sc), pack_bf16x2(a.z * sc, a.w * sc), pack_bf16x2(b.x * sc, b.y * sc),
+                 pack_bf16x2(b.z * sc, b.w * sc));
 }
 
 // zero one row of an m x R bf16 result (row tiles no adapter touches)

@@ -287,13 +287,19 @@ __global__ void __launch_bounds__(128) lf_finalize_kernel(const __grid_constant_
                                                           __nv_bfloat16* out) {
   pdl_wait();
   pdl_launch_dependents();
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= segs.m || (segs.debug & 16)) return;
-  finalize_row(segs, routes[row / LF_TILE_M], row, ws, out);
+  // one thread per 8-column chunk: a single L2 round trip each (one thread per row walked
+  // its chunks serially: 60 µs per launch at R = 128, C3)
+  const int chunks = segs.rtot / 8;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)segs.m * chunks || (segs.debug & 16)) return;
+  const int row = (int)(idx / chunks);
+  const int c = (int)(idx - (int64_t)row * chunks) * 8;
+  finalize_chunk(segs, routes[row / LF_TILE_M], row, c, ws, out);
 }
 
 int finalize_launch(const LfSegTable& segs, const LfRoute* routes, float* ws, void* out, cudaStream_t stream) {
-  return launch_k(lf_finalize_kernel, dim3((segs.m + 127) / 128), dim3(128), 0, stream, segs, routes, ws,
+  const int64_t threads = (int64_t)segs.m * (segs.rtot / 8);
+  return launch_k(lf_finalize_kernel, dim3((unsigned)((threads + 127) / 128)), dim3(128), 0, stream, segs, routes, ws,
                   reinterpret_cast<__nv_bfloat16*>(out));
 }
 
