@@ -100,6 +100,13 @@ typedef struct LfProblem {
 /* Bytes of zero-initialised scratch one problem needs (split-K partials + tile counters). */
 LF_API size_t lf_workspace_bytes(int32_t m, int32_t rank_total);
 
+/* Host-only introspection (no device work, no CUDA context): the CTA grid lf_grad_up would
+   launch for an m x n problem of width rank_total on `sms` SMs — n_split CTAs along n, each
+   owning at most 8 128-column subtiles, times m_split along m, in one resident wave
+   (n_split * m_split <= sms). LF_E_INVALID for non-positive sizes or a rank_total whose
+   accumulators do not fit TMEM. */
+LF_API int lf_grad_up_grid(int32_t m, int32_t n, int32_t rank_total, int32_t sms, int32_t* n_split, int32_t* m_split);
+
 /* Routing table: per 128-row tile {seg_lo, seg_hi, col_lo, col_hi} (16 B). */
 LF_API int lf_build_routes(const LfProblem* p, int32_t* routes_out, void* stream);
 

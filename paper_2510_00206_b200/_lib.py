@@ -29,6 +29,7 @@ LIB_PATH = Path(__file__).resolve().parent / "liblorafusion_b200.so"
 # every symbol include/lorafusion_b200.h declares
 EXPORTED_SYMBOLS = (
     "lf_workspace_bytes",
+    "lf_grad_up_grid",
     "lf_build_routes",
     "lf_dropout_down_fwd",
     "lf_base_fwd",
@@ -77,6 +78,8 @@ _P = ctypes.POINTER(LfProblem)
 _V = ctypes.c_void_p
 _SIGNATURES = {
     "lf_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32]),
+    "lf_grad_up_grid": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
     "lf_build_routes": (ctypes.c_int, [_P, _V, _V]),
     "lf_dropout_down_fwd": (ctypes.c_int, [_P, _V, _V, _V, _V]),
     "lf_base_fwd": (ctypes.c_int, [_P, _V, _V, _V, _V, _V, _V]),

@@ -262,6 +262,18 @@ size_t lf_workspace_bytes(int32_t m, int32_t rank_total) {
   return align_up((size_t)m * rank_total * 4, 256) + align_up(tiles * 4, 256);
 }
 
+int lf_grad_up_grid(int32_t m, int32_t n, int32_t rank_total, int32_t sms, int32_t* n_split, int32_t* m_split) {
+  if (!n_split || !m_split) return fail(LF_E_INVALID, "n_split / m_split is NULL");
+  if (m < 1 || n < 1 || sms < 1 || rank_total < 16 || rank_total % 16 || rank_total > LF_MAX_RANK_TOTAL)
+    return fail(LF_E_INVALID, "bad grad_up grid query (m=%d n=%d rank_total=%d sms=%d)", m, n, rank_total, sms);
+  int ns = 0, ms = 0, nacc = 0;
+  lf::grad_up_grid(m, n, rank_total, sms, 1, &ns, &ms, &nacc);
+  if (ns <= 0) return fail(LF_E_INVALID, "rank_total=%d too large for grad_up TMEM budget", rank_total);
+  *n_split = ns;
+  *m_split = ms;
+  return LF_OK;
+}
+
 int lf_build_routes(const LfProblem* p, int32_t* routes_out, void* stream) {
   lf::LfSegTable t;
   LF_TRY(validate(p, false, &t));

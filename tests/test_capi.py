@@ -74,6 +74,35 @@ def test_workspace_bytes(lib):
     assert _lib.workspace_bytes(1, 16) % 256 == 0
 
 
+def _grad_up_grid(lib, m, n, R, sms=148):
+    ns, ms = ctypes.c_int32(), ctypes.c_int32()
+    rc = lib.lf_grad_up_grid(m, n, R, sms, ctypes.byref(ns), ctypes.byref(ms))
+    return rc, ns.value, ms.value
+
+
+@pytest.mark.parametrize("m,n,R", [(16384, 28672, 16), (2048, 28672, 16), (4096, 28672, 16), (8192, 14336, 16),
+                                   (8192, 4096, 16), (8192, 1024, 16), (16384, 8192, 16), (128, 1024, 16),
+                                   (8192, 4096, 128), (8192, 14336, 128), (300, 200, 64)])
+def test_grad_up_grid_one_wave_and_bounded_tail(lib, m, n, R):
+    """③'s CTA grid (host logic, no GPU): one resident wave (a grid wider than the SMs ran
+    C4 gate/up in two waves, 275 vs 152 µs), at most 8 n-subtiles per CTA (their dB partials
+    are flushed at the CTA's end), and the dB/dŜ accumulators within TMEM's 512 columns."""
+    rc, ns, ms = _grad_up_grid(lib, m, n, R)
+    assert rc == 0, _lib.last_error()
+    tiles_m, tiles_n = -(-m // 128), -(-n // 128)
+    assert 1 <= ns <= tiles_n and 1 <= ms <= tiles_m
+    assert ns * ms <= 148
+    nsub = -(-tiles_n // ns)
+    assert nsub <= 8 and (2 + nsub) * R <= 512
+
+
+def test_grad_up_grid_c4_gate_and_rejects(lib):
+    assert _grad_up_grid(lib, 16384, 28672, 16)[1:] == (28, 5)
+    assert _grad_up_grid(lib, 0, 4096, 16)[0] == _lib.LF_E_INVALID
+    assert _grad_up_grid(lib, 8192, 4096, 24)[0] == _lib.LF_E_INVALID  # not a multiple of 16
+    assert _grad_up_grid(lib, 8192, 4096, 256)[0] == _lib.LF_E_INVALID  # beyond LF_MAX_RANK_TOTAL
+
+
 def _problem(m=256, k=64, n=64, R=16, segs=((0, 256, 0, 16, 2.0, 0.1),)):
     p = _lib.LfProblem()
     p.m, p.k, p.n, p.rank_total = m, k, n, R
