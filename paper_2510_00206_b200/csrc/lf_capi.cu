@@ -195,6 +195,33 @@ int validate(const LfProblem* p, bool need_routes, lf::LfSegTable* t) {
     d.off1 = (uint32_t)(s.offset >> 32);
     if (d.thr) any_dropout = true;
   }
+  // widest per-tile hull, as lf_routes_kernel forms it: segments are sorted and disjoint, so
+  // only a segment's first and last 128-row tiles can be shared with neighbours
+  {
+    int cur = -1, c0 = 0, c1 = 0, wmax = 0;
+    for (int i = 0; i < p->num_segments; ++i) {
+      const lf::LfSegDev& d = t->seg[i];
+      if (d.row0 >= d.row1) continue;
+      const int t0 = d.row0 / 128, t1 = (d.row1 - 1) / 128;
+      if (t0 == cur) {
+        c0 = c0 < d.col0 ? c0 : d.col0;
+        c1 = c1 > d.col0 + d.ncol ? c1 : d.col0 + d.ncol;
+      } else {
+        if (cur >= 0 && c1 - c0 > wmax) wmax = c1 - c0;
+        cur = t0;
+        c0 = d.col0;
+        c1 = d.col0 + d.ncol;
+      }
+      if (t1 > t0) {  // t0 is complete; interior tiles carry this block alone
+        if (c1 - c0 > wmax) wmax = c1 - c0;
+        cur = t1;
+        c0 = d.col0;
+        c1 = d.col0 + d.ncol;
+      }
+    }
+    if (cur >= 0 && c1 - c0 > wmax) wmax = c1 - c0;
+    t->wmax = wmax > 0 ? wmax : 16;
+  }
   if (p->keep_mask) {
     t->mask_mode = 2;
     t->mask = p->keep_mask;
@@ -332,7 +359,7 @@ int lf_dropout_down_fwd(const LfProblem* p, const uint16_t* x, const uint16_t* a
   const int tiles_m = (p->m + 127) / 128;
   const int nkb = (p->k + 63) / 64;
   int stages = 0, stage_bytes = 0;
-  lf::down_config(p->rank_total, &stages, &stage_bytes);
+  lf::down_config(t.wmax, &stages, &stage_bytes);
   const int occ = occupancy_for_smem(stages * stage_bytes + 2048);
   // one resident wave sharing the units evenly (stream-K); at least 4 k-blocks per CTA so
   // the split-K partial traffic stays small next to the X stream
@@ -462,7 +489,7 @@ int lf_grad_down(const LfProblem* p, const uint16_t* x, const uint16_t* ds, floa
   a.routes = reinterpret_cast<const lf::LfRoute*>(p->routes);
   a.segs = t;
   int stages = 0, stage_bytes = 0;
-  lf::grad_down_config(p->rank_total, a.bits_tma != 0, &stages, &stage_bytes);
+  lf::grad_down_config(t.wmax, a.bits_tma != 0, &stages, &stage_bytes);
   const int occ = occupancy_for_smem(stages * stage_bytes + 2048);
   const int tiles_k = (p->k + 127) / 128;
   const int tiles_m = (p->m + 127) / 128;

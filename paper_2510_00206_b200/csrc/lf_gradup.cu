@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(192, 2)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   const int rtot = args.rtot;
-  const int sh_bytes = (rtot / 16) * 4096;
+  const int sh_bytes = (args.segs.wmax / 16) * 4096;  // Ŝ / B_cat columns of the widest routing hull
   uint8_t* sSh0 = smem + stages * stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(sSh0 + 2 * sh_bytes);
   uint64_t* empty = full + stages;
@@ -298,7 +298,7 @@ void grad_up_grid(int m, int n, int rtot, int sms, int per_sm, int* n_split, int
 int grad_up_launch(const CUtensorMap& tm_dy, const CUtensorMap& tm_b, const CUtensorMap& tm_s,
                    const GradUpArgs& args, int num_sms, int per_sm, cudaStream_t stream) {
   (void)num_sms;
-  const int sh_bytes = (args.rtot / 16) * 4096;
+  const int sh_bytes = (args.segs.wmax / 16) * 4096;
   const int stage_bytes = gup::DY_BYTES + sh_bytes;
   int stages = (gup::MAX_SMEM / per_sm - 2 * sh_bytes) / stage_bytes;
   if (stages > 6) stages = 6;  // deep ring: ~180 KB of dY in flight per SM

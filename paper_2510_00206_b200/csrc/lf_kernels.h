@@ -67,7 +67,7 @@ struct DownArgs {
   const LfRoute* routes;
   LfSegTable segs;
 };
-void down_config(int rtot, int* stages, int* stage_bytes);
+void down_config(int wmax, int* stages, int* stage_bytes);
 int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs& args, int num_sms,
                 cudaStream_t stream);
 
@@ -98,7 +98,7 @@ struct GradDownArgs {
 };
 // split-K epilogue of ③: fp32 partials (ws) -> scaled bf16 m x R, workspace re-zeroed
 int finalize_launch(const LfSegTable& segs, const LfRoute* routes, float* ws, void* out, cudaStream_t stream);
-void grad_down_config(int rtot, bool bits_tma, int* stages, int* stage_bytes);
+void grad_down_config(int wmax, bool bits_tma, int* stages, int* stage_bytes);
 int grad_down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_ds, const CUtensorMap& tm_bits,
                      const GradDownArgs& args, int num_sms, cudaStream_t stream);
 

@@ -41,8 +41,9 @@ constexpr int X_BYTES = 128 * 64 * 2;  // 16 KB
 constexpr int SMEM_BUDGET = 100 * 1024;
 }  // namespace down
 
-void down_config(int rtot, int* stages, int* stage_bytes) {
-  *stage_bytes = down::X_BYTES + rtot * 128;
+// wmax: the widest routing hull (LfSegTable::wmax), the most A_cat columns a stage holds
+void down_config(int wmax, int* stages, int* stage_bytes) {
+  *stage_bytes = down::X_BYTES + wmax * 128;
   int s = down::SMEM_BUDGET / *stage_bytes;
   *stages = s < 2 ? 2 : (s > 8 ? 8 : s);
 }
@@ -306,7 +307,7 @@ int finalize_launch(const LfSegTable& segs, const LfRoute* routes, float* ws, vo
 int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs& args, int num_sms,
                 cudaStream_t stream) {
   int stages = 0, stage_bytes = 0;
-  down_config(args.rtot, &stages, &stage_bytes);
+  down_config(args.segs.wmax, &stages, &stage_bytes);
   const int smem = stages * stage_bytes + 1024 + 256;
   static bool configured = false;
   if (!configured) {
@@ -361,7 +362,8 @@ __global__ void __launch_bounds__(kDgaThreads, 2)
   const int tiles_m = (args.m + 127) / 128;
   const int tiles_k = (args.k + 127) / 128;
   const int rtot = args.rtot;
-  const int KBITS_OFF = X_BYTES + (rtot / 16) * 4096;  // stage: X | dŜ columns | keep bits (16 B x 128 rows)
+  // stage: X | dŜ columns (up to the widest routing hull) | keep bits (16 B x 128 rows)
+  const int KBITS_OFF = X_BYTES + (args.segs.wmax / 16) * 4096;
   // stream-K over (k-tile, m-tile) units, k-tile major: a span = one k-tile's dAᵀ columns
   // summed over a run of m-tiles. Two zero-initialised accumulators (R columns each).
   const int u0 = (int)((int64_t)blockIdx.x * tiles_m * tiles_k / gridDim.x);
@@ -549,8 +551,8 @@ __global__ void __launch_bounds__(kDgaThreads, 2)
 }
 
 // 2 CTAs / SM x ~110 KB rings (with TMA'd keep bits, 2 KB more per stage: 2 stages each).
-void grad_down_config(int rtot, bool bits_tma, int* stages, int* stage_bytes) {
-  *stage_bytes = dga::X_BYTES + (rtot / 16) * 4096 + (bits_tma ? 2048 : 0);
+void grad_down_config(int wmax, bool bits_tma, int* stages, int* stage_bytes) {
+  *stage_bytes = dga::X_BYTES + (wmax / 16) * 4096 + (bits_tma ? 2048 : 0);
   static const int budget_kb = [] { const char* e = getenv("LF_DGA_SMEM_KB"); return e ? atoi(e) : 0; }();
   // ~110 KB rings so two CTAs share each SM (with keep bits too: 2 x 2 stages beat one CTA
   // with a 5-stage ring by 18-20%, kbench m = 8192/16384) unless R makes a stage too big
@@ -563,7 +565,7 @@ int grad_down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_ds, const CU
                      const GradDownArgs& args, int num_sms, cudaStream_t stream) {
   (void)num_sms;
   int stages = 0, stage_bytes = 0;
-  grad_down_config(args.rtot, args.bits_tma != 0, &stages, &stage_bytes);
+  grad_down_config(args.segs.wmax, args.bits_tma != 0, &stages, &stage_bytes);
   const int smem = stages * stage_bytes + 1024 + 256;
   static int configured = 0;
   if (configured < smem) {

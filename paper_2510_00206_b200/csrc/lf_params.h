@@ -27,6 +27,8 @@ struct LfSegTable {
   int32_t nseg;
   int32_t m;
   int32_t rtot;         // rank-concat width R
+  int32_t wmax;         // widest routing hull (col_hi - col_lo) of any 128-row tile: sizes the
+                        // per-stage R-column operand buffers of ①③④ (≤ rtot; C3: 64 of 128)
   int32_t mask_mode;    // 0 = no dropout anywhere, 1 = Philox, 2 = explicit uint8 mask
   const uint8_t* mask;  // explicit keep mask (m x ld_mask) when mask_mode == 2
   int64_t ld_mask;
