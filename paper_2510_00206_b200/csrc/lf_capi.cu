@@ -294,7 +294,7 @@ int lf_grad_up_grid(int32_t m, int32_t n, int32_t rank_total, int32_t sms, int32
   if (m < 1 || n < 1 || sms < 1 || rank_total < 16 || rank_total % 16 || rank_total > LF_MAX_RANK_TOTAL)
     return fail(LF_E_INVALID, "bad grad_up grid query (m=%d n=%d rank_total=%d sms=%d)", m, n, rank_total, sms);
   int ns = 0, ms = 0, nacc = 0;
-  lf::grad_up_grid(m, n, rank_total, sms, 1, &ns, &ms, &nacc);
+  lf::grad_up_grid(m, n, rank_total, rank_total, sms, 1, &ns, &ms, &nacc);
   if (ns <= 0) return fail(LF_E_INVALID, "rank_total=%d too large for grad_up TMEM budget", rank_total);
   *n_split = ns;
   *m_split = ms;
@@ -442,11 +442,11 @@ int lf_grad_up(const LfProblem* p, const uint16_t* dy, const uint16_t* b_cat, co
   a.segs = t;
   static const int gu_per_sm_env = env_int("LF_GU_PER_SM", 0);
   const int per_sm = gu_per_sm_env > 0 ? gu_per_sm_env : 1;
-  lf::grad_up_grid(p->m, p->n, p->rank_total, d.sms, per_sm, &a.n_split, &a.m_split, &a.nacc);
+  lf::grad_up_grid(p->m, p->n, p->rank_total, t.wmax, d.sms, per_sm, &a.n_split, &a.m_split, &a.nacc);
   static const int gu_ns_env = env_int("LF_GU_NSPLIT", 0);  // profiling: force the n-split
   if (gu_ns_env > 0 && a.n_split > 0) {
     const int tiles_n = (p->n + 127) / 128, tiles_m = (p->m + 127) / 128;
-    const int max_nsub = 512 / per_sm / p->rank_total - 2;
+    const int max_nsub = (512 / per_sm - 2 * t.wmax) / p->rank_total;
     int ns = gu_ns_env < tiles_n ? gu_ns_env : tiles_n;
     if ((tiles_n + ns - 1) / ns <= max_nsub) {
       int ms = d.sms * per_sm / ns;

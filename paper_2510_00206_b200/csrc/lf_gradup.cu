@@ -53,8 +53,12 @@ __global__ void __launch_bounds__(192, 2)
   // NA independent accumulators per chain (consecutive K-steps rotate through them): small-N
   // MMAs into a single accumulator serialise on its latency
   const int NA = args.nacc;
-  const int AW = NA * rtot;  // TMEM columns of one (multi-)accumulator
-  const uint32_t tmem_need = (uint32_t)((2 + nsub) * AW);
+  // dŜ accumulators hold one m-tile's routing hull (≤ wmax columns, tile-relative); the dB
+  // accumulators of an n-subtile collect every adapter's block (rtot columns)
+  const int wmax = args.segs.wmax;
+  const int AWs = NA * wmax;  // TMEM columns of one dŜ (multi-)accumulator
+  const int AW = NA * rtot;   // TMEM columns of one dB (multi-)accumulator
+  const uint32_t tmem_need = (uint32_t)(2 * AWs + nsub * AW);
   uint32_t tmem_cols = 32;
   while (tmem_cols < tmem_need) tmem_cols <<= 1;
 
@@ -83,8 +87,8 @@ __global__ void __launch_bounds__(192, 2)
   tc_fence_after();
   pdl_wait();  // the prologue above overlaps the predecessor's tail; global memory only from here
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tm_ds = tmem;            // 2 buffers x AW columns
-  const uint32_t tm_db = tmem + 2 * AW;   // nsub x AW columns
+  const uint32_t tm_ds = tmem;            // 2 buffers x AWs columns
+  const uint32_t tm_db = tmem + 2 * AWs;  // nsub x AW columns
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(192, 2)
         mbar_wait(&sh_full[b], bph);
         tc_fence_after();
         const uint32_t sSh = smem_u32(sSh0 + b * sh_bytes);
-        const uint32_t d_ds = tm_ds + b * AW + rt.col_lo;
+        const uint32_t d_ds = tm_ds + b * AWs;  // tile-relative: column c <-> rank-concat col_lo + c
         const uint32_t idesc_ds = make_idesc_bf16(128, (uint32_t)N, false, true);
         const uint32_t idesc_db = make_idesc_bf16(128, (uint32_t)N, true, true);
         for (int nt = nt0; nt < nt1; ++nt) {
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(192, 2)
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t a = (uint32_t)(kk % NA) * rtot;
             if (!(args.segs.debug & 1))
-              umma_bf16_warp(d_ds + a, sdesc_add(a_ds, (kk >> 2) * 16384 + (kk & 3) * 32), sdesc_add(b_ds, kk * 512),
+              umma_bf16_warp(d_ds + (uint32_t)(kk % NA) * wmax, sdesc_add(a_ds, (kk >> 2) * 16384 + (kk & 3) * 32), sdesc_add(b_ds, kk * 512),
                              idesc_ds, (nt > nt0 || kk >= NA) ? 1u : 0u);
             if (!(args.segs.debug & 32))
               umma_bf16_warp(d_db + a, sdesc_add(a_db, kk * 2048), sdesc_add(b_db, kk * 512), idesc_db, 1u);
@@ -204,7 +208,7 @@ __global__ void __launch_bounds__(192, 2)
           for (int j = 0; j < 16; ++j) s[j] = 0.f;
           for (int a = 0; a < NA; ++a) {
             uint32_t v[16];
-            tmem_ld16(tm_ds + lane_off + b * AW + a * rtot + rt.col_lo + c, v);
+            tmem_ld16(tm_ds + lane_off + b * AWs + a * wmax + c, v);
             tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 16; ++j) s[j] += __uint_as_float(v[j]);
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(192, 2)
 // CTA's n-range must fit TMEM next to the two dŜ buffers: (2 + nsub) * R <= 512.
 // Among admissible splits pick the smallest critical path (waves x max units of one 32 KB
 // dY tile per CTA), then the least partial-sum traffic R * (m_split * n + n_split * m).
-void grad_up_grid(int m, int n, int rtot, int sms, int per_sm, int* n_split, int* m_split, int* nacc) {
+void grad_up_grid(int m, int n, int rtot, int wmax, int sms, int per_sm, int* n_split, int* m_split, int* nacc) {
   const int tiles_m = (m + 127) / 128, tiles_n = (n + 127) / 128;
   // measured on B200: rotating K-steps over several accumulators does not speed the
   // small-N chains up (the pipelines are TMA-bound), so one accumulator keeps TMEM free
@@ -268,7 +272,7 @@ void grad_up_grid(int m, int n, int rtot, int sms, int per_sm, int* n_split, int
   // red.adds) at its very end, where nothing overlaps them — measured at n = 28672, R = 16:
   // 25 subtiles per CTA 36.9 / 53.2 / 86.1 µs at m = 2048 / 4096 / 8192, <= 8 subtiles
   // 26.8 / ~47 / 81.9 µs (profiles/r01_gradup_split_sweep.txt)
-  int max_nsub = (512 / per_sm) / (*nacc * rtot) - 2;
+  int max_nsub = ((512 / per_sm) - 2 * *nacc * wmax) / (*nacc * rtot);
   if (max_nsub > 8) max_nsub = 8;
   sms *= per_sm;
   *n_split = 0;

@@ -83,7 +83,7 @@ struct GradUpArgs {
   const LfRoute* routes;
   LfSegTable segs;
 };
-void grad_up_grid(int m, int n, int rtot, int sms, int per_sm, int* n_split, int* m_split, int* nacc);
+void grad_up_grid(int m, int n, int rtot, int wmax, int sms, int per_sm, int* n_split, int* m_split, int* nacc);
 int grad_up_launch(const CUtensorMap& tm_dy, const CUtensorMap& tm_b, const CUtensorMap& tm_s,
                    const GradUpArgs& args, int num_sms, int per_sm, cudaStream_t stream);
 
