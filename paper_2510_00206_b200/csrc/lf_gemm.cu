@@ -412,11 +412,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         const uint32_t d = tmem_base + acc * Cfg::ACC_COLS;
         int tn = -1;
         bool have_tn = false;
-        if (MASKED && (args.segs.debug & 4096)) {  // profiling: plain k-loop in the masked kernel
-          mbar_wait(&tempty[acc], ((it / NACC) & 1) ^ 1);
-          tc_fence_after();
-          for (int kb = 0; kb < nkb; ++kb) mma_main_block(d, kb, false);
-        } else if constexpr (MASKED && WIDE) {
+        if constexpr (MASKED && WIDE) {
           // sequential: drained accumulator -> this tile's LoRA partial -> mask pass -> main loop
           mbar_wait(&tempty[acc], ((it / NACC) & 1) ^ 1);
           tc_fence_after();
@@ -534,12 +530,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int t = seq.first();
       if (t >= 0) {
         const TileInfo t0 = tile_info(args, s_routes, t);
-        if (t0.lora() && !(args.segs.debug & 4096)) mask_pass(t0, 0);
+        if (t0.lora()) mask_pass(t0, 0);
       }
       for (int it = 0; t >= 0; ++it) {
         const TileInfo ti = tile_info(args, s_routes, t);
         const int tn = seq.read(it + 1, lane == 0);
-        const bool next_lora = tn >= 0 && !(args.segs.debug & 4096) && tile_info(args, s_routes, tn).lora();
+        const bool next_lora = tn >= 0 && tile_info(args, s_routes, tn).lora();
         RowKeep nk;
         if (next_lora) nk = fetch_keep(tile_info(args, s_routes, tn));
         const int row = ti.mb * 256 + (int)rank * Cfg::BM + (int)(q * 32 + lane);
@@ -578,10 +574,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t aph = (it / NACC) & 1;
       int tn = -1;
       if constexpr (MASKED) {
-        const bool plain = (args.segs.debug & 4096) != 0;  // profiling: the MMA issues no LoRA-first blocks
-        if (it == 0 && ti.lora() && !plain) mask_pass(ti, 0);
+        if (it == 0 && ti.lora()) mask_pass(ti, 0);
         tn = seq.read(it + 1, lane == 0);
-        if (tn >= 0 && !plain) {
+        if (tn >= 0) {
           const TileInfo tni = tile_info(args, s_routes, tn);
           if (tni.lora()) mask_pass(tni, it + 1);
         }
