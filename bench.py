@@ -224,9 +224,14 @@ def run_reference(args, rank: int, world: int) -> None:
     cores = len(os.sched_getaffinity(0))
     sample = args.cpu_sample_tokens
     r, p = 16, 0.1
-    for _ in range(max(1, min(args.warmup, 1))):
-        cpu_reference_step(args.config, 64, r, p)
-    times = [cpu_reference_step(args.config, sample, r, p, seed=i) for i in range(args.steps)]
+    # torchrun sets OMP_NUM_THREADS=1 for N > 1: rank 0 alone runs the reference here, on every
+    # host thread it may use
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=cores):
+        for _ in range(max(1, min(args.warmup, 1))):
+            cpu_reference_step(args.config, 64, r, p)
+        times = [cpu_reference_step(args.config, sample, r, p, seed=i) for i in range(args.steps)]
     t = sum(times) / len(times)
     value = sample / t
     line = {
