@@ -95,6 +95,18 @@ def main():
         main.wait_event(join)
         return rc
 
+    def dgrad_with_graddown(i):
+        """④ on a side stream concurrently with ⑤ (both only need dŜ)"""
+        main = torch.cuda.current_stream()
+        fork.record(main)
+        side.wait_event(fork)
+        rc = lib.lf_grad_down(pp, P(X[i]), P(DS), P(DA), s2)
+        rc = rc or launches["grad_input"][0](i)
+        join.record(side)
+        main.wait_event(join)
+        return rc
+
+    launches["overlap_dgrad_graddown"] = (dgrad_with_graddown, "tflops", 2 * m * n * k + 2 * m * R * k)
     launches["overlap_fwd_bits"] = (lambda i: gemm_with_bits(i, launches["base_fwd"][0]), "tflops",
                                     2 * m * k * n + 2 * m * R * n)
     launches["overlap_dgrad_bits"] = (lambda i: gemm_with_bits(i, launches["grad_input"][0]), "tflops",
