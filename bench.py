@@ -122,11 +122,13 @@ def measured_peaks() -> dict:
                 "source": "B200_PROFILING.md fallback"}
 
 
-def gemm_traffic() -> dict | None:
-    """DRAM bytes per lf_gemm_kernel launch from the committed ncu --set full capture of one
-    bench step (tools/ncu_traffic.py -> profiles/gemm_traffic.json), or None."""
+def gemm_traffic(config: str = "c2") -> dict | None:
+    """DRAM bytes per lf_gemm_kernel launch from the committed ncu capture of one bench step
+    of this config (tools/ncu_traffic.py -> profiles/gemm_traffic.json for C2,
+    profiles/gemm_traffic_<config>.json otherwise), or None when there is none."""
+    name = "gemm_traffic.json" if config == "c2" else f"gemm_traffic_{config}.json"
     try:
-        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
             return json.load(f)
     except Exception:
         return None
@@ -506,7 +508,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         kernels["dropout_down_fwd"]["frac_of_philox_floor"] = floor / kernels["dropout_down_fwd"]["ms_per_step"]
     gemm_ms = sum(kernels[n]["ms_per_step"] for n in ("base_fwd", "grad_input") if n in kernels)
     gemm_tf = (gfl["base_fwd"] + gfl["grad_input"]) / (gemm_ms * 1e-3) / 1e12 if gemm_ms else 0.0
-    traffic = gemm_traffic()
+    traffic = gemm_traffic(args.config)
     roofline = {
         "bound": "tensor",
         "kernel": "lf_gemm_kernel (② base_fwd + ⑤ grad_input)",

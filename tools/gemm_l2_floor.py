@@ -1,6 +1,6 @@
 """Per-wave L2 floor of the GEMM DRAM traffic, next to the ncu-measured bytes of one C2 step.
 
-    python tools/gemm_l2_floor.py [profiles/gemm_traffic.json]
+    python tools/gemm_l2_floor.py [profiles/gemm_traffic.json [c2|c4|c1]]
 
 SURVEY.md §8(d)'s algorithmic bytes assume every operand byte crosses HBM once. With 126 MB
 of L2 and operands of 120-350 MB that is unreachable for the long-K GEMMs: the 74 resident
@@ -50,12 +50,13 @@ def wide_rule(M: int, N: int, K: int, masked_dgrad: bool) -> bool:
 
 def main() -> None:
     path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    config = sys.argv[2] if len(sys.argv) > 2 else "c2"
     with open(path) as f:
         tr = json.load(f)
-    from bench import projections
+    from bench import projections, tokens_per_gpu
 
-    shapes = {name: (k, n) for name, k, n, _ in projections("c2")}
-    m = 8192
+    shapes = {name: (k, n) for name, k, n, _ in projections(config)}
+    m = tokens_per_gpu(config)
     rows = []
     for launch in tr["per_launch"]:
         name, kind = launch["launcher"].split()

@@ -2,9 +2,10 @@
 
     ncu --set full --clock-control none -k regex:lf_gemm -c 14 -o gpurun_out/gemm_step \\
         python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline
-    python tools/ncu_traffic.py gpurun_out/gemm_step.ncu-rep > profiles/gemm_traffic.json
+    python tools/ncu_traffic.py gpurun_out/gemm_step.ncu-rep [c2|c4] > profiles/gemm_traffic[_c4].json
 
-The first 14 GEMM launches are one C2 step (② then ⑤ for each of the 7 projections).
+The first 14 GEMM launches are one step (② then ⑤ for each of the 7 projections) of the
+config (default c2; for c4 capture `bench.py --config c4`, the --metrics of METRICS suffice).
 Algorithmic bytes per launch follow SURVEY.md §8(d): ② 2(mk+kn+mr+rn)+2mn, ⑤ 2(mn+kn+mr+kr)+2mk.
 """
 from __future__ import annotations
@@ -23,6 +24,7 @@ METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.
 
 def main():
     rep = sys.argv[1]
+    config = sys.argv[2] if len(sys.argv) > 2 else "c2"
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(out.splitlines()))
@@ -40,17 +42,17 @@ def main():
         tu = u["gpu__time_duration.sum"]
         t_us = {"nsecond": t / 1e3, "ns": t / 1e3, "usecond": t, "us": t, "msecond": t * 1e3, "ms": t * 1e3}[tu]
         launches.append({"kernel": d["Kernel Name"][:60], "dram_read": rd, "dram_write": wr, "dur_us": t_us})
-    from bench import projections  # noqa: E402  (C2 shapes, bench order)
-    m, r = 8192, 16
+    from bench import projections, tokens_per_gpu  # noqa: E402  (bench order)
+    m, r = tokens_per_gpu(config), 16
     alg = []  # bench.py runs each projection's forward and backward back to back
-    for name, k, n, _ in projections("c2"):
+    for name, k, n, _ in projections(config):
         alg.append((name + " base_fwd", 2 * (m * k + k * n + m * r + r * n) + 2 * m * n))
         alg.append((name + " grad_input", 2 * (m * n + k * n + m * r + k * r) + 2 * m * k))
     n = min(len(launches), len(alg))
     dram = sum(l["dram_read"] + l["dram_write"] for l in launches[:n])
     algb = sum(a for _, a in alg[:n])
     print(json.dumps({
-        "source": os.path.basename(rep) + " (ncu --set full --clock-control none, one C2 bench step)",
+        "source": os.path.basename(rep) + f" (ncu --clock-control none, one {config.upper()} bench step)",
         "launches": n,
         "dram_bytes_per_launch": dram / n if n else None,
         "algorithmic_bytes_per_launch": algb / n if n else None,
