@@ -49,10 +49,21 @@ def projections(config: str):
 TOKENS_OVERRIDE: int | None = None  # --tokens
 
 
-def tokens_per_gpu(config: str) -> int:
+def tokens_per_gpu(config: str, world: int = 1) -> int:
+    """Tokens each rank processes per step. C4 is strong-scaled (BASELINE configs[3], SURVEY
+    §8(d)): 16384 tokens per step in total, 16384 / N per rank; the others are weak-scaled
+    (a fixed per-GPU batch)."""
     if TOKENS_OVERRIDE:
         return TOKENS_OVERRIDE
-    return {"c1": 2048, "c2": 8192, "c3": 8192, "c4": 16384, "c5": 8192}[config]
+    if config == "c4":
+        if 16384 % world:
+            raise SystemExit(f"--config c4 strong-scales 16384 tokens: N={world} must divide it")
+        return 16384 // world
+    return {"c1": 2048, "c2": 8192, "c3": 8192, "c5": 8192}[config]
+
+
+def scaling_kind(config: str) -> str:
+    return "strong" if config == "c4" and not TOKENS_OVERRIDE else "weak"
 
 
 # C3 (BASELINE.json configs[2], SURVEY.md §8(d)): FusedMultiLoRA, 4 adapters of ranks
@@ -189,43 +200,109 @@ class ClockSampler:
 # --------------------------------------------------------------------------------------
 # reference arm: the CPU oracle (numpy port) on the host cores
 # --------------------------------------------------------------------------------------
-def cpu_reference_step(config: str, sample_tokens: int, r: int, p: float, seed: int = 0) -> float:
-    """One fwd+bwd of every projection on a `sample_tokens`-row sample with the oracle;
-    returns the wall seconds."""
+_CPU_INPUTS: dict = {}
+
+
+def _cpu_inputs(config: str, sample_tokens: int, r: int):
+    """Seeded bf16-valued inputs of every projection for the CPU leg (generated once: the
+    weight matrices take longer to draw than the sample takes to compute)."""
+    import numpy as np
+
+    from oracle import lora as olora
+
+    key = (config, sample_tokens, r)
+    if key not in _CPU_INPUTS:
+        rng = np.random.default_rng(0)
+        xs, out = {}, []
+        for name, k, n, grp in projections(config):
+            m = sample_tokens
+            if grp not in xs:
+                xs[grp] = olora.bf16_round(rng.standard_normal((m, k), dtype=np.float32))
+            w = olora.bf16_round(rng.standard_normal((n, k), dtype=np.float32) / np.sqrt(k))
+            a = olora.bf16_round((rng.random((r, k), dtype=np.float32) * 2 - 1) / np.sqrt(k))
+            b = olora.bf16_round(rng.standard_normal((n, r), dtype=np.float32) / np.sqrt(r))
+            dy = olora.bf16_round(rng.standard_normal((m, n), dtype=np.float32))
+            out.append((k, xs[grp], w, a, b, dy))
+        _CPU_INPUTS[key] = out
+    return _CPU_INPUTS[key]
+
+
+def cpu_reference_step(config: str, sample_tokens: int, r: int, p: float, step: int = 0,
+                       acc: str = "float32") -> float:
+    """One fwd+bwd of every projection on a `sample_tokens`-row sample with the oracle's
+    algorithm (oracle/lora.py: Philox keep mask, Eq. 1 at SPEC §2's rounding points) at
+    `acc` accumulation; returns the wall seconds of the compute (input generation excluded).
+    Each step draws its own dropout mask (Philox offset = step)."""
     import numpy as np
 
     from oracle import lora as olora
     from oracle import philox as ophilox
 
-    rng = np.random.default_rng(seed)
-    t0 = time.perf_counter()
+    dt = np.float32 if acc == "float32" else np.float64
     total = 0.0
-    inputs = {}
-    for name, k, n, grp in projections(config):
-        m = sample_tokens
-        if grp not in inputs:
-            inputs[grp] = olora.bf16_round(rng.standard_normal((m, k), dtype=np.float32))
-        x = inputs[grp]
-        w = olora.bf16_round(rng.standard_normal((n, k), dtype=np.float32) / np.sqrt(k))
-        a = olora.bf16_round((rng.random((r, k), dtype=np.float32) * 2 - 1) / np.sqrt(k))
-        b = olora.bf16_round(rng.standard_normal((n, r), dtype=np.float32) / np.sqrt(r))
-        dy = olora.bf16_round(rng.standard_normal((m, n), dtype=np.float32))
+    for k, x, w, a, b, dy in _cpu_inputs(config, sample_tokens, r):
+        m = x.shape[0]
         seg = [olora.OracleSegment(0, m, 0, r, 2.0, p, 1234)]
         t1 = time.perf_counter()
-        keep = ophilox.keep_mask_rows(np.arange(m), k, p, 1234, 0)
-        y, s_hat = olora.forward(x, w, a, b, seg, keep)
-        olora.backward(dy, x, w, a, b, s_hat, seg, keep)
+        keep = ophilox.keep_mask_rows(np.arange(m), k, p, 1234, step)
+        y, s_hat = olora.forward(x, w, a, b, seg, keep, acc=dt)
+        olora.backward(dy, x, w, a, b, s_hat, seg, keep, acc=dt)
         total += time.perf_counter() - t1
-    del t0
     return total
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def cpu_torch_c1(repeats: int = 3) -> dict:
+    """SURVEY §8(d) baseline 3: the unfused LoRA linear (baseline.unfused_lora) in fp32 torch
+    on the host cores at C1 (2048 tokens, k = n = 4096, r = 16, p = 0.1, W frozen), forward +
+    backward with autograd, best of `repeats` after one warm-up."""
+    import torch
+
+    from paper_2510_00206_b200.baseline import unfused_lora
+
+    g = torch.Generator().manual_seed(0)
+    m, k, n, r = 2048, 4096, 4096, 16
+    x = torch.randn(m, k, generator=g).requires_grad_(True)
+    w = torch.randn(n, k, generator=g) / k**0.5
+    a = ((torch.rand(r, k, generator=g) * 2 - 1) / k**0.5).requires_grad_(True)
+    b = (torch.randn(n, r, generator=g) / r**0.5).requires_grad_(True)
+    dy = torch.randn(m, n, generator=g)
+    best = float("inf")
+    for i in range(repeats + 1):
+        t0 = time.perf_counter()
+        unfused_lora(x, w, a, b, 2.0, 0.1, training=True).backward(dy)
+        dt_ = time.perf_counter() - t0
+        x.grad = a.grad = b.grad = None
+        if i:
+            best = min(best, dt_)
+    flops = 4 * m * k * n + 6 * m * r * (k + n)
+    return {"ms_per_step": best * 1e3, "tokens_per_s": m / best, "tflops": flops / best / 1e12,
+            "threads": torch.get_num_threads(), "cpu": cpu_model(),
+            "what": "fp32 torch-CPU unfused LoRA linear (F.linear + F.dropout + add/scale, autograd, W frozen), "
+                    "C1: 2048 tokens, k=n=4096, r=16, p=0.1; best of 3 after warm-up"}
+
+
 def run_reference(args, rank: int, world: int) -> None:
+    """--impl reference: the reference CPU path of this hot path — the oracle port
+    (oracle/lora.py, the algorithm the reference's kernel list specifies) — on the host
+    cores, on a bounded token sample of this arm's workload; same metric, unit and config."""
     if rank != 0:
         return
     cores = len(os.sched_getaffinity(0))
     sample = args.cpu_sample_tokens
-    r, p = 16, 0.1
+    r, p = 16, args.dropout
     # torchrun sets OMP_NUM_THREADS=1 for N > 1: rank 0 alone runs the reference here, on every
     # host thread it may use
     from threadpoolctl import threadpool_limits
@@ -233,7 +310,7 @@ def run_reference(args, rank: int, world: int) -> None:
     with threadpool_limits(limits=cores):
         for _ in range(max(1, min(args.warmup, 1))):
             cpu_reference_step(args.config, 64, r, p)
-        times = [cpu_reference_step(args.config, sample, r, p, seed=i) for i in range(args.steps)]
+        times = [cpu_reference_step(args.config, sample, r, p, step=i) for i in range(args.steps)]
     t = sum(times) / len(times)
     value = sample / t
     line = {
@@ -241,33 +318,53 @@ def run_reference(args, rank: int, world: int) -> None:
         "metric": "LoRA linear fwd+bwd tokens/s & TFLOP/s (8B/70B shapes), % of bf16 peak",
         "value": value,
         "unit": "tokens/s",
-        "n_gpus": args.gpus,
+        "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": t * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling_kind(args.config),
         "vs_baseline": None,
-        "dtype": "f64",
+        "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": workload_name(args.config) + f" — CPU oracle on a {sample}-token sample",
-                   "tokens_per_step": sample, "rank": r, "dropout_p": p},
+        "config": bench_config(args.config, world, r, p),
+        "execution": f"CPU, {cores} host threads (numpy BLAS), rank 0 only",
         "tflops": step_flops(args.config, sample, r) / t / 1e12,
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": f"{sample} tokens of each projection, fwd+bwd, numpy float64 oracle (oracle/lora.py)"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port", "cpu": cpu_model(),
+                         "sample": f"{sample} tokens of each projection per step, fwd+bwd, oracle/lora.py at fp32 "
+                                   "accumulation with its Philox keep mask (oracle/philox.py)"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def workload_name(config: str) -> str:
+def bench_config(config: str, world: int, r: int, p: float) -> dict:
+    """The `config` object both arms print (the driver compares them)."""
+    m = tokens_per_gpu(config, world)
     return {
-        "c2": "LLaMa-3.1-8B layer shapes (q/k/v/o, gate/up/down) FusedLoRA r=16, 8192 tokens, bf16, 1 B200",
-        "c1": "single FusedLoRA linear fwd+bwd: tokens=2048, k=n=4096, r=16, dropout=0.1",
-        "c4": "LLaMa-3.1-70B layer shapes FusedLoRA r=16, 16384 tokens per GPU",
-        "c5": "LLaMa-3.1-8B 4 concurrent LoRA jobs, full decoder fwd+bwd step (CPU sample: the 7 LoRA linears)",
-        "c3": "FusedMultiLoRA 4 adapters, ranks {8,16,32,64}, uneven token segments {3584,2432,1408,768} "
-              "sharing one frozen W per projection (LLaMa-3.1-8B q/k/v/o/gate/up/down), 8192 tokens",
+        "workload": workload_name(config, world),
+        "projections": [[nm, k, n] for nm, k, n, _ in projections(config)],
+        "tokens_per_gpu": m,
+        "global_tokens": m * world,
+        "rank": list(C3_RANKS) if config == "c3" else r,
+        "scaling": 2.0,
+        "dropout_p": list(C3_DROPOUT) if config == "c3" else p,
+        "parallelism": f"dp{world}",
+        "l2": "inputs larger than L2 (≈2 GB touched per step vs 126 MB L2)",
+    }
+
+
+def workload_name(config: str, world: int = 1) -> str:
+    m = tokens_per_gpu(config, world)
+    gpus = f"{world} B200" + ("" if world == 1 else " data-parallel")
+    return {
+        "c2": f"LLaMa-3.1-8B layer shapes (q/k/v/o, gate/up/down) FusedLoRA r=16, {m} tokens per GPU, bf16, {gpus}",
+        "c1": f"single FusedLoRA linear fwd+bwd: tokens={m} per GPU, k=n=4096, r=16, dropout=0.1, {gpus}",
+        "c4": (f"LLaMa-3.1-70B layer shapes (k=8192, n=28672) FusedLoRA r=16, {m * world} tokens per step "
+               f"({m} per GPU, {scaling_kind(config)} scaling), bf16, {gpus}"),
+        "c5": f"LLaMa-3.1-8B 4 concurrent LoRA jobs, full decoder fwd+bwd step, {gpus}",
+        "c3": f"FusedMultiLoRA 4 adapters, ranks {{8,16,32,64}}, uneven token segments {{3584,2432,1408,768}} "
+              f"sharing one frozen W per projection (LLaMa-3.1-8B q/k/v/o/gate/up/down), {m} tokens per GPU, {gpus}",
     }[config]
 
 
@@ -417,7 +514,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     torch.cuda.set_device(device)
     gen = torch.Generator(device=device).manual_seed(1000 + rank)
     r, p = 16, args.dropout
-    m = tokens_per_gpu(args.config)
+    m = tokens_per_gpu(args.config, world)
     layers, inputs, grads = build_layers(args.config, m, r, p, device, gen, capturable=args.graph)
 
     def barrier():
@@ -566,22 +663,12 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             "warmup": args.warmup,
             "ms_per_step": ms,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": scaling_kind(args.config),
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic",
-            "config": {
-                "workload": workload_name(args.config),
-                "projections": [[nm, k, n] for nm, k, n, _ in projections(args.config)],
-                "tokens_per_gpu": m,
-                "global_tokens": m * world,
-                "rank": list(C3_RANKS) if args.config == "c3" else r,
-                "scaling": 2.0,
-                "dropout_p": list(C3_DROPOUT) if args.config == "c3" else p,
-                "parallelism": f"dp{world}",
-                "execution": "one CUDA graph per step (capturable layers)" if args.graph else "eager",
-                "l2": "inputs larger than L2 (≈2 GB touched per step vs 126 MB L2)",
-            },
+            "config": bench_config(args.config, world, r, p),
+            "execution": "one CUDA graph per step (capturable layers)" if args.graph else "eager",
             "tflops": world * flops / (ms * 1e-3) / 1e12,
             "tflops_per_gpu": flops / (ms * 1e-3) / 1e12,
             "frac_of_bf16_peak": flops / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
@@ -602,7 +689,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             ts = cpu_reference_step(args.config, args.cpu_sample_tokens, r, p)
             line["cpu_baseline"] = {
                 "value": args.cpu_sample_tokens / ts, "unit": "tokens/s", "cores": cores, "kind": "port",
-                "sample": f"{args.cpu_sample_tokens} tokens of each projection, fwd+bwd, numpy float64 oracle",
+                "cpu": cpu_model(),
+                "sample": f"{args.cpu_sample_tokens} tokens of each projection, fwd+bwd, oracle/lora.py at fp32 "
+                          "accumulation with its Philox keep mask",
+                "c1_fp32_torch": cpu_torch_c1(),
             }
         print(json.dumps(line), flush=True)
 
@@ -730,7 +820,7 @@ def run_e2e(args, layers, inputs, grads, device, world, barrier, max_over_ranks)
 
     ms = time_loop(step, max(2, args.steps // 2), args.warmup, barrier)
     ms = max_over_ranks(ms)
-    m = tokens_per_gpu(args.config)
+    m = tokens_per_gpu(args.config, world)
     return {"value": world * m / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "path": ("FusedMultiLoRA" if args.config == "c3" else "FusedLoRA") +
@@ -757,6 +847,23 @@ def c5_microbatches(world: int, per_rank: int):
     chosen = [mbs[i % len(mbs)] for i in range(world * per_rank)]
     assign = dp.assign_microbatches([mb.rows for mb in chosen], world)
     return adapters, chosen, assign
+
+
+def simulate_dp_prediction(world: int, per_rank: int) -> dict | None:
+    """The reference's own DP model on this run's rank streams (committed fixture, generated
+    by importing lorasched: tests/golden/make_dp_golden.py): imbalance and predicted step
+    time under its linear and roofline (B200) time models."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "c5_simulate_dp.json")) as f:
+            gold = json.load(f)
+    except OSError:
+        return None
+    ent = gold["worlds"].get(str(world))
+    if ent is None or gold.get("microbatches_per_rank") != per_rank:
+        return None
+    return {"streams_rows": ent["streams"],
+            "imbalance_linear": ent["linear"]["imbalance"], "imbalance_roofline": ent["roofline"]["imbalance"],
+            "roofline_step_s": ent["roofline"]["total_time_s"], "source": gold["source"]}
 
 
 def run_c5(args, rank: int, world: int, local_rank: int) -> None:
@@ -881,7 +988,8 @@ def run_c5(args, rank: int, world: int, local_rank: int) -> None:
             },
             "padded_rows_per_s": rows_all / (ms * 1e-3),
             "dp": {"rows_per_rank": loads, "imbalance": dp.imbalance(loads),
-                   "note": "imbalance = 1 - mean/max of per-rank padded rows (ls/pipesim.py:275-312 simulate_dp)"},
+                   "note": "imbalance = 1 - mean/max of per-rank padded rows (ls/pipesim.py:275-312 simulate_dp)",
+                   "lorasched_simulate_dp": simulate_dp_prediction(world, args.mb_per_rank)},
             "lora_linear_tflops": flops_all / (ms * 1e-3) / 1e12,
             "lora_linear_frac_of_bf16_peak": flops_all / (ms * 1e-3) / 1e12 / world / peaks["bf16_tflops"],
             "unfused_torch": {"ms_per_step": unf_ms, "tokens_per_s": raw_all / (unf_ms * 1e-3),
@@ -920,6 +1028,10 @@ def main() -> None:
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        # keep NCCL's communicator-init lines (rank / nranks / transport) in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     # test knob: every rank on cuda:0 over gloo, to exercise the N > 1 code path on a 1-GPU box
     share_gpu = os.environ.get("LF_BENCH_SHARE_GPU") == "1"

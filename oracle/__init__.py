@@ -13,11 +13,14 @@ Contents (each module cites the reference lines it restates):
 
 Pinning status:
   * traffic bytes — pinned to the reference: tests/golden/traffic_reference.json is produced
-    by importing lorasched.costmodel itself (tests/golden/make_traffic_golden.py) and the
+    by importing lorasched.costmodel itself (tests/golden/make_reference_golden.py) and the
     frozen totals of pkg/tests/test_costmodel.py:22-27.
   * Philox — pinned to the published Random123 known-answer vectors (tests/test_oracle.py).
   * routing / segments — pinned to lorasched's own packing semantics (padded_len, segment
-    order) through tests/golden/segments_reference.json, generated with lorasched.
+    order) through tests/golden/schedule_reference.json, a schedule planned by lorasched
+    itself (tests/golden/make_reference_golden.py).
+  * DP balance — tests/golden/c5_simulate_dp.json, lorasched.pipesim.simulate_dp on the C5
+    bench's rank streams (tests/golden/make_dp_golden.py).
   * Y, dX, dA, dB numerics — PARITY UNPINNED by the reference: lorasched has no numerical
     implementation of the path (SPEC.md:8 of the reference puts the kernels out of scope).
     The oracle restates Eq. 1 and is cross-checked against an

@@ -11,7 +11,9 @@ in torch/PEFT layouts: X (m,k), W (n,k), A_cat (R,k), B_cat (n,R).
 
 Accumulation is float64 from the bf16-exact inputs; the stored intermediates Ŝ and dŜ
 and the bf16 outputs Y and dX are rounded exactly where the kernels round (fp32 first,
-then bf16 round-to-nearest-even); dA and dB are returned in fp32.
+then bf16 round-to-nearest-even); dA and dB are returned in fp32. ``acc=np.float32``
+runs the same algorithm at fp32 accumulation — used only to time the CPU baseline
+(bench.py), never as the parity reference.
 """
 from __future__ import annotations
 
@@ -60,9 +62,10 @@ def _f32(x) -> np.ndarray:
     return np.asarray(x, dtype=np.float64).astype(np.float32)
 
 
-def forward(x, w, a_cat, b_cat, segments: Sequence[OracleSegment], keep) -> tuple[np.ndarray, np.ndarray]:
+def forward(x, w, a_cat, b_cat, segments: Sequence[OracleSegment], keep,
+            acc=np.float64) -> tuple[np.ndarray, np.ndarray]:
     """Returns (y, s_hat) as bf16-valued float32 arrays. ``keep``: (m,k) uint8 (1 keep)."""
-    x = np.asarray(x, np.float64)
+    x = np.asarray(x, acc)
     m = x.shape[0]
     R = a_cat.shape[0]
     s_hat = np.zeros((m, R), np.float32)
@@ -71,19 +74,19 @@ def forward(x, w, a_cat, b_cat, segments: Sequence[OracleSegment], keep) -> tupl
             continue
         rows = slice(s.row_start, s.row_end)
         cols = slice(s.col_start, s.col_start + s.rank)
-        xm = x[rows] * np.asarray(keep[rows], np.float64)
-        acc = _f32(xm @ np.asarray(a_cat[cols], np.float64).T)
-        s_hat[rows, cols] = bf16_round(acc * segment_scale(s))
-    y = x @ np.asarray(w, np.float64).T
+        xm = x[rows] * np.asarray(keep[rows], acc)
+        part = _f32(xm @ np.asarray(a_cat[cols], acc).T)
+        s_hat[rows, cols] = bf16_round(part * segment_scale(s))
+    y = x @ np.asarray(w, acc).T
     if R:
-        y = y + np.asarray(s_hat, np.float64) @ np.asarray(b_cat, np.float64).T
+        y = y + np.asarray(s_hat, acc) @ np.asarray(b_cat, acc).T
     return bf16_round(_f32(y)), s_hat
 
 
-def backward(dy, x, w, a_cat, b_cat, s_hat, segments: Sequence[OracleSegment], keep):
+def backward(dy, x, w, a_cat, b_cat, s_hat, segments: Sequence[OracleSegment], keep, acc=np.float64):
     """Returns (dx bf16-valued, da fp32 (R,k), db fp32 (n,R), ds bf16-valued (m,R))."""
-    dy = np.asarray(dy, np.float64)
-    x = np.asarray(x, np.float64)
+    dy = np.asarray(dy, acc)
+    x = np.asarray(x, acc)
     m = dy.shape[0]
     R = a_cat.shape[0]
     ds = np.zeros((m, R), np.float32)
@@ -92,16 +95,16 @@ def backward(dy, x, w, a_cat, b_cat, s_hat, segments: Sequence[OracleSegment], k
             continue
         rows = slice(s.row_start, s.row_end)
         cols = slice(s.col_start, s.col_start + s.rank)
-        acc = _f32(dy[rows] @ np.asarray(b_cat[:, cols], np.float64))
-        ds[rows, cols] = bf16_round(acc * segment_scale(s))
-    keep64 = np.asarray(keep, np.float64)
+        part = _f32(dy[rows] @ np.asarray(b_cat[:, cols], acc))
+        ds[rows, cols] = bf16_round(part * segment_scale(s))
+    keep64 = np.asarray(keep, acc)
     xm = x * keep64
-    ds64 = np.asarray(ds, np.float64)
-    db = _f32(dy.T @ np.asarray(s_hat, np.float64)) if R else np.zeros((w.shape[0], 0), np.float32)
+    ds64 = np.asarray(ds, acc)
+    db = _f32(dy.T @ np.asarray(s_hat, acc)) if R else np.zeros((w.shape[0], 0), np.float32)
     da = _f32(ds64.T @ xm) if R else np.zeros((0, x.shape[1]), np.float32)
-    dx = dy @ np.asarray(w, np.float64)
+    dx = dy @ np.asarray(w, acc)
     if R:
-        dx = dx + keep64 * (ds64 @ np.asarray(a_cat, np.float64))
+        dx = dx + keep64 * (ds64 @ np.asarray(a_cat, acc))
     return bf16_round(_f32(dx)), da, db, ds
 
 

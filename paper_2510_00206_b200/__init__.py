@@ -2,7 +2,8 @@
 
 Public API
   FusedLoRA, FusedMultiLoRA          nn.Modules (PEFT parameter names lora_A / lora_B)
-  fused_lora, fused_multi_lora       functional forms (autograd)
+  fused_lora, fused_multi_lora       functional forms (autograd; torch.ops.lorafusion_b200.lora_fwd/_bwd)
+  invalidate_operand_caches          forget cached bf16 adapter operands after out-of-optimizer updates
   AdapterConfig, Segment, LayerPlan  adapter hyper-parameters and microbatch segment tables
   dropout_keep_mask                  SPEC.md §3 mask the kernels regenerate
   traffic, GemmShape, ...            DRAM-traffic model mirroring lorasched.costmodel
@@ -13,7 +14,7 @@ The compute path is the sm_100a shared library liblorafusion_b200.so (C ABI in
 include/lorafusion_b200.h). There is no CPU fallback.
 """
 from .errors import ExtensionMissingError, KernelError, LoRAFusionError, ValidationError
-from .functional import dropout_keep_mask, fused_lora, fused_multi_lora
+from .functional import dropout_keep_mask, fused_lora, fused_multi_lora, invalidate_operand_caches
 from .modules import FusedLoRA, FusedMultiLoRA
 from .plan import AdapterConfig, LayerPlan, Segment, padded_rank, segments_from_lengths
 from .costmodel import (
@@ -54,6 +55,7 @@ __all__ = [
     "dropout_keep_mask",
     "fused_lora",
     "fused_multi_lora",
+    "invalidate_operand_caches",
     "lora_memory_bytes",
     "padded_rank",
     "roundtrip_bytes",

@@ -308,13 +308,8 @@ int grad_up_launch(const CUtensorMap& tm_dy, const CUtensorMap& tm_b, const CUte
   if (stages > 6) stages = 6;  // deep ring: ~180 KB of dY in flight per SM
   if (stages < 2) return -1;
   const int smem = stages * stage_bytes + 2 * sh_bytes + 1024 + 1024;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(lf_gradup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gup::MAX_SMEM + 2048) !=
-        cudaSuccess)
-      return -1;
-    configured = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (ensure_smem_attr(lf_gradup_kernel, gup::MAX_SMEM + 2048, attr_done)) return -1;
   dim3 grid(args.n_split, args.m_split);
   if (launch_k(lf_gradup_kernel, grid, dim3(192), smem, stream, tm_dy, tm_b, tm_s, args, stages, stage_bytes))
     return -1;

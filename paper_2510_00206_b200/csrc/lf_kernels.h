@@ -5,11 +5,28 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <utility>
 
 #include "lf_params.h"
 
 namespace lf {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): a function
+// attribute is per-device state, and one process may drive several GPUs from several host
+// threads. `done` is the caller's static per-kernel bitmask of configured device ordinals
+// (devices >= 64 are set on every launch); the set is idempotent, so a race between two
+// threads only repeats it.
+template <typename Kern>
+inline int ensure_smem_attr(Kern kern, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return -1;
+  if (bit) done.fetch_or(bit, std::memory_order_acq_rel);
+  return 0;
+}
 
 // Programmatic dependent launch for every lf kernel (see pdl_wait in lf_device.cuh); set
 // LF_PDL=0 in the environment to launch with plain stream ordering instead.

@@ -309,12 +309,8 @@ int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs
   int stages = 0, stage_bytes = 0;
   down_config(args.segs.wmax, &stages, &stage_bytes);
   const int smem = stages * stage_bytes + 1024 + 256;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(lf_down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess)
-      return -1;
-    configured = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (ensure_smem_attr(lf_down_kernel, 200 * 1024, attr_done)) return -1;
   return launch_k(lf_down_kernel, dim3(args.ctas), dim3(kDownThreads), smem, stream, tm_x, tm_a, args, stages,
                   stage_bytes);
 }
@@ -567,13 +563,8 @@ int grad_down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_ds, const CU
   int stages = 0, stage_bytes = 0;
   grad_down_config(args.segs.wmax, args.bits_tma != 0, &stages, &stage_bytes);
   const int smem = stages * stage_bytes + 1024 + 256;
-  static int configured = 0;
-  if (configured < smem) {
-    if (cudaFuncSetAttribute(lf_dgrad_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dga::MAX_SMEM + 2048) !=
-        cudaSuccess)
-      return -1;
-    configured = dga::MAX_SMEM + 2048;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (ensure_smem_attr(lf_dgrad_a_kernel, dga::MAX_SMEM + 2048, attr_done)) return -1;
   return launch_k(lf_dgrad_a_kernel, dim3(args.ctas), dim3(kDgaThreads), smem, stream, tm_x, tm_ds, tm_bits, args,
                   stages, stage_bytes);
 }

@@ -6,25 +6,37 @@ Backward:  ③ lf_grad_up            dŜ = s·dY·B, dB += dY
                                ④ lf_grad_down          dA += dŜᵀ·(M⊙X)
                                ⑤ lf_grad_input         dX = dY·W + M⊙(dŜ·A)       (one write of dX)
 
-The base weight is frozen (LoRA fine-tuning); there is no CPU path — tensors must live on
-a B200 and the shared library must be built, otherwise the call raises.
+The two passes are registered as torch operators (``torch.ops.lorafusion_b200.lora_fwd`` /
+``lora_bwd``) with fake (meta) implementations and an autograd formula,
+so a FusedLoRA layer traces under ``torch.compile(fullgraph=True)`` without graph breaks
+and recomputes correctly under ``torch.utils.checkpoint`` (the packed keep mask and Ŝ are
+ordinary saved tensors). The operators take plain tensors and scalars: the adapter table
+(ranks, scalings, dropout p, seeds) and the segment table (adapter, row_start, row_end,
+batch) as flat lists; the host plan (LfProblem, routing table, workspace) is rebuilt from
+them inside each operator. The base weight is frozen (LoRA fine-tuning); there is no CPU
+path — tensors must live on a B200 and the shared library must be built, otherwise the call
+raises.
 """
 from __future__ import annotations
 
 import ctypes
-from typing import Callable, Sequence
+import itertools
+import weakref
+from typing import Callable, Optional, Sequence
 
 import torch
+from torch.optim.optimizer import register_optimizer_step_post_hook
 
 from . import _lib
 from .errors import ValidationError
-from .plan import AdapterConfig, LayerPlan, Segment, split_segments, validate_segments
+from .plan import AdapterConfig, LayerPlan, Segment, rank_layout, split_segments, validate_segments
 
 _BF16 = torch.bfloat16
+_NS = "lorafusion_b200"
 
 
 def _ptr(t: torch.Tensor | None) -> ctypes.c_void_p:
-    return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
+    return ctypes.c_void_p(t.data_ptr() if t is not None and t.numel() > 0 else 0)
 
 
 def _stream(device: torch.device | None = None) -> ctypes.c_void_p:
@@ -57,8 +69,8 @@ class LaunchStats:
         ev.record()
         self.events.setdefault(name, []).append((start, ev))
 
-    # device kernels each C entry point launches (① and ③ add the split-K finalize kernel)
-    KERNELS_PER_CALL = {"grad_up": 2}  # ③ + its split-K finalize; ① finalizes in-kernel
+    # device kernels each C entry point launches (③ adds its split-K finalize kernel)
+    KERNELS_PER_CALL = {"grad_up": 2}
 
     def total_launches(self) -> int:
         return sum(n * self.KERNELS_PER_CALL.get(k, 1) for k, n in self.launches.items())
@@ -98,11 +110,33 @@ def _check_operand(t: torch.Tensor, name: str, shape: tuple | None = None) -> No
         raise ValidationError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
 
 
+# --------------------------------------------------------------------------------------
+# bf16 rank-concat operand cache
+# --------------------------------------------------------------------------------------
+# Adapter weights change in place: through the optimizer (torch's fused AdamW/SGD kernels
+# leave the parameters' version counters untouched), through ``p.data`` or through external
+# updaters (apex, Megatron's main->model copy). Every optimizer step therefore bumps a
+# global weight generation (torch's global optimizer step post-hook) that is part of the
+# cache key, next to the parameters' pointers and versions; updates outside any
+# torch.optim.Optimizer must call ``invalidate_operand_caches()``.
+_GENERATION = [0]
+
+
+def invalidate_operand_caches(*_args, **_kwargs) -> None:
+    """Forget every cached bf16 A_cat/B_cat (call after updating adapter weights outside a
+    torch.optim optimizer step, e.g. through ``p.data``)."""
+    _GENERATION[0] += 1
+
+
+register_optimizer_step_post_hook(invalidate_operand_caches)
+
+
 class OperandCache:
     """bf16 rank-concat operands (A_cat, B_cat) of a module, keyed by the column-block
-    layout and the in-place versions of the adapter parameters: every layer call between
-    two optimizer steps that sees the same adapters reuses them instead of re-casting,
-    padding and concatenating (a dozen small launches of host work per call)."""
+    layout, the weight generation and the adapter parameters' pointers and in-place
+    versions: every layer call between two optimizer steps that sees the same adapters
+    reuses them instead of re-casting, padding and concatenating (a dozen small launches
+    of host work per call)."""
 
     def __init__(self, capacity: int = 8):
         self.capacity = capacity
@@ -116,95 +150,268 @@ class OperandCache:
             self._d.pop(next(iter(self._d)))
         self._d[key] = value
 
+    def clear(self) -> None:
+        self._d.clear()
 
-def _rank_concat_operands(plan: LayerPlan, params, n_adapters: int):
-    cache: OperandCache | None = plan.operand_cache
+
+# operators take an integer handle for the calling module's operand cache
+_CACHES: "weakref.WeakValueDictionary[int, OperandCache]" = weakref.WeakValueDictionary()
+_ids = itertools.count(1)
+
+
+def _cache_handle(cache: OperandCache | None) -> int:
+    if cache is None:
+        return 0
+    h = getattr(cache, "_handle", None)
+    if h is None:
+        h = next(_ids)
+        cache._handle = h
+        _CACHES[h] = cache
+    return h
+
+
+def _rank_concat_operands(plan: LayerPlan, a: Sequence[torch.Tensor], b: Sequence[torch.Tensor], cache_id: int):
+    cache = _CACHES.get(cache_id) if cache_id else None
     key = None
     if cache is not None:
         blocks = plan.column_blocks()
-        used = sorted({a for a, _, _ in blocks})
-        key = (tuple((a, r) for a, _, r in blocks),
-               tuple((p.data_ptr(), p._version) for a in used for p in (params[a], params[n_adapters + a])))
+        used = sorted({ad for ad, _, _ in blocks})
+        key = (_GENERATION[0], tuple((ad, r) for ad, _, r in blocks),
+               tuple((p.data_ptr(), p._version) for ad in used for p in (a[ad], b[ad])))
         hit = cache.get(key)
         if hit is not None:
             return hit
-    # bf16 operand copies: the module's cached shadows when given, else cast here
-    shadows = plan.weights_bf16
-    a_cat = plan.gather_a(shadows[0] if shadows else params[:n_adapters])
-    b_cat = plan.gather_b(shadows[1] if shadows else params[n_adapters:])
+    a_cat, b_cat = plan.gather_a(a), plan.gather_b(b)
     if cache is not None:
         cache.put(key, (a_cat, b_cat))
     return a_cat, b_cat
 
 
-class _FusedLoRAFn(torch.autograd.Function):
-    """Autograd node over the five kernels.
+# --------------------------------------------------------------------------------------
+# packed call description (what the operators take instead of Python objects)
+# --------------------------------------------------------------------------------------
+def _u64_to_i64(v: int) -> int:
+    v = int(v) & (2**64 - 1)
+    return v - 2**64 if v >= 2**63 else v
 
-    Inputs: x (m,k) bf16, w (n,k) bf16 frozen, the plan, an optional per-slot gradient sink,
-    then the adapter parameters lora_A[0..a) and lora_B[0..a) in their own dtype (fp32
-    master weights are cast to the bf16 rank-concat operands inside, outside autograd, so
-    their gradients come back in fp32 without a bf16 round trip)."""
+
+def pack_adapters(adapters: Sequence[AdapterConfig]) -> tuple[list[int], list[float], list[float], list[int]]:
+    return ([int(a.rank) for a in adapters], [float(a.scaling) for a in adapters],
+            [float(a.dropout_p) for a in adapters], [_u64_to_i64(a.seed) for a in adapters])
+
+
+def pack_segments(segments: Sequence[Segment]) -> list[int]:
+    return [v for s in segments for v in (int(s.adapter), int(s.row_start), int(s.row_end), int(s.batch))]
+
+
+_DESC_CACHE: dict = {}
+
+
+def _unpack(ranks, scalings, ps, seeds, segs) -> tuple[list[AdapterConfig], list[Segment]]:
+    key = (tuple(ranks), tuple(scalings), tuple(ps), tuple(seeds), tuple(segs))
+    hit = _DESC_CACHE.get(key)
+    if hit is None:
+        if len(_DESC_CACHE) >= 512:
+            _DESC_CACHE.pop(next(iter(_DESC_CACHE)))
+        adapters = [AdapterConfig(rank=r, scaling=s, dropout_p=p, seed=int(sd) & (2**64 - 1))
+                    for r, s, p, sd in zip(ranks, scalings, ps, seeds)]
+        segments = [Segment(*segs[i:i + 4]) for i in range(0, len(segs), 4)]
+        hit = _DESC_CACHE[key] = (adapters, segments)
+    return hit
+
+
+def _rank_total(ranks, segs, share_blocks) -> int:
+    segments = [Segment(*segs[i:i + 4]) for i in range(0, len(segs), 4)]
+    return rank_layout(ranks, segments, share_blocks)[2]
+
+
+def _needs_bits(ps, segs, keep_mask, training) -> bool:
+    return bool(training and keep_mask is None and any(ps[segs[i]] > 0 for i in range(0, len(segs), 4)))
+
+
+def _plan(x_rows, k, n, ranks, scalings, ps, seeds, segs, offset, offset_dev, keep_mask, training,
+          share_blocks, row_base) -> LayerPlan:
+    adapters, segments = _unpack(ranks, scalings, ps, seeds, segs)
+    return LayerPlan(x_rows, k, n, adapters, segments, offset=offset, training=training, keep_mask=keep_mask,
+                     share_blocks=share_blocks, offset_dev=offset_dev, row_base=row_base)
+
+
+# --------------------------------------------------------------------------------------
+# torch operators
+# --------------------------------------------------------------------------------------
+@torch.library.custom_op(f"{_NS}::lora_fwd", mutates_args=(), device_types="cuda")
+def lora_fwd(x: torch.Tensor, w: torch.Tensor, a: list[torch.Tensor], b: list[torch.Tensor], ranks: list[int],
+             scalings: list[float], ps: list[float], seeds: list[int], segs: list[int], offset: int,
+             offset_dev: Optional[torch.Tensor], keep_mask: Optional[torch.Tensor], training: bool,
+             share_blocks: bool, row_base: int, cache_id: int) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """① + ②: returns (Y (m,n) bf16, Ŝ (m,R) bf16, packed keep mask (m,k/8) u8 or empty)."""
+    lib = _lib.load()
+    m, k = x.shape
+    n = w.shape[0]
+    plan = _plan(m, k, n, ranks, scalings, ps, seeds, segs, offset, offset_dev, keep_mask, training,
+                 share_blocks, row_base)
+    plan.bind(x.device)
+    pp = ctypes.byref(plan.problem)
+    st = _stream(x.device)
+    y = torch.empty((m, n), dtype=_BF16, device=x.device)
+    s_hat = torch.empty((m, plan.rank_total), dtype=_BF16, device=x.device)
+    a_cat = b_cat = None
+    if plan.has_lora:
+        a_cat, b_cat = _rank_concat_operands(plan, a, b, cache_id)
+        _call("dropout_down_fwd", lib.lf_dropout_down_fwd, pp, _ptr(x), _ptr(a_cat), _ptr(s_hat), st)
+    _call("base_fwd", lib.lf_base_fwd, pp, _ptr(x), _ptr(w), _ptr(s_hat), _ptr(b_cat), _ptr(y), st)
+    bits = plan.keep_bits if plan.keep_bits is not None else torch.empty((0,), dtype=torch.uint8, device=x.device)
+    return y, s_hat, bits
+
+
+@lora_fwd.register_fake
+def _lora_fwd_fake(x, w, a, b, ranks, scalings, ps, seeds, segs, offset, offset_dev, keep_mask, training,
+                   share_blocks, row_base, cache_id):
+    m, k = x.shape
+    R = _rank_total(ranks, segs, share_blocks)
+    bits = (x.new_empty((m, k // 8), dtype=torch.uint8) if _needs_bits(ps, segs, keep_mask, training)
+            else x.new_empty((0,), dtype=torch.uint8))
+    return x.new_empty((m, w.shape[0])), x.new_empty((m, R)), bits
+
+
+@torch.library.custom_op(f"{_NS}::lora_bwd", mutates_args=(), device_types="cuda")
+def lora_bwd(dy: torch.Tensor, x: torch.Tensor, w: torch.Tensor, a: list[torch.Tensor], b: list[torch.Tensor],
+             s_hat: torch.Tensor, keep_bits: torch.Tensor, ranks: list[int], scalings: list[float], ps: list[float],
+             seeds: list[int], segs: list[int], offset: int, offset_dev: Optional[torch.Tensor],
+             keep_mask: Optional[torch.Tensor], training: bool, share_blocks: bool, row_base: int, cache_id: int,
+             need_dx: bool) -> tuple[torch.Tensor, torch.Tensor]:
+    """③ + ④ + ⑤: returns (dX (m,k) bf16 or empty, [dA_cat (R,k) | dB_cat (n,R)] fp32 flat —
+    one buffer, one zero-fill)."""
+    lib = _lib.load()
+    m, k = x.shape
+    n = w.shape[0]
+    plan = _plan(m, k, n, ranks, scalings, ps, seeds, segs, offset, offset_dev, keep_mask, training,
+                 share_blocks, row_base)
+    plan.bind(dy.device, keep_bits=keep_bits)
+    pp = ctypes.byref(plan.problem)
+    st = _stream(dy.device)
+    R = plan.rank_total
+    ds = a_cat = None
+    # one zero-fill for both fp32 accumulators
+    acc = torch.zeros(R * k + n * R, dtype=torch.float32, device=dy.device)
+    da = acc[:R * k].view(R, k)
+    db = acc[R * k:].view(n, R)
+    if plan.has_lora:
+        a_cat, b_cat = _rank_concat_operands(plan, a, b, cache_id)
+        ds = torch.empty((m, R), dtype=_BF16, device=dy.device)
+        _call("grad_up", lib.lf_grad_up, pp, _ptr(dy), _ptr(b_cat), _ptr(s_hat), _ptr(ds), _ptr(db), st)
+        _call("grad_down", lib.lf_grad_down, pp, _ptr(x), _ptr(ds), _ptr(da), st)
+    if need_dx:
+        dx = torch.empty((m, k), dtype=_BF16, device=dy.device)
+        _call("grad_input", lib.lf_grad_input, pp, _ptr(dy), _ptr(w), _ptr(ds), _ptr(a_cat), _ptr(dx), st)
+    else:
+        dx = torch.empty((0,), dtype=_BF16, device=dy.device)
+    return dx, acc
+
+
+@lora_bwd.register_fake
+def _lora_bwd_fake(dy, x, w, a, b, s_hat, keep_bits, ranks, scalings, ps, seeds, segs, offset, offset_dev,
+                   keep_mask, training, share_blocks, row_base, cache_id, need_dx):
+    m, k = x.shape
+    R = _rank_total(ranks, segs, share_blocks)
+    dx = x.new_empty((m, k)) if need_dx else x.new_empty((0,))
+    return dx, x.new_empty((R * k + w.shape[0] * R,), dtype=torch.float32)
+
+
+_PLAN_ARGS = ("ranks", "scalings", "ps", "seeds", "segs", "offset", "offset_dev", "keep_mask", "training",
+              "share_blocks", "row_base", "cache_id")
+
+
+def _setup_context(ctx, inputs, output, mark: bool = True):
+    x, w, a, b, *rest = inputs
+    y, s_hat, bits = output
+    if mark:
+        ctx.mark_non_differentiable(s_hat, bits)
+    args = dict(zip(_PLAN_ARGS, rest))
+    # the gradient of a non-tensor argument is None, except that an empty list (no segments)
+    # flattens like a list of tensors and must come back as []
+    ctx.none_grads = tuple([] if isinstance(v, list) and not v else None for v in rest)
+    ctx.n_adapters = len(a)
+    ctx.param_dtypes = [p.dtype for p in a] + [p.dtype for p in b]
+    opt = [args.pop("offset_dev"), args.pop("keep_mask")]
+    ctx.has_opt = [t is not None for t in opt]
+    ctx.args = args
+    ctx.save_for_backward(x, w, s_hat, bits, *a, *b, *[t for t in opt if t is not None])
+
+
+def _backward(ctx, dy, _ds, _dbits):
+    na = ctx.n_adapters
+    x, w, s_hat, bits, *rest = ctx.saved_tensors
+    a, b, opt = rest[:na], rest[na:2 * na], list(rest[2 * na:])
+    offset_dev = opt.pop(0) if ctx.has_opt[0] else None
+    keep_mask = opt.pop(0) if ctx.has_opt[1] else None
+    A = ctx.args
+    dy = dy.to(_BF16).contiguous()
+    need_dx = bool(ctx.needs_input_grad[0])
+    dx, dacc = torch.ops.lorafusion_b200.lora_bwd(
+        dy, x, w, list(a), list(b), s_hat, bits, A["ranks"], A["scalings"], A["ps"], A["seeds"], A["segs"],
+        A["offset"], offset_dev, keep_mask, A["training"], A["share_blocks"], A["row_base"], A["cache_id"], need_dx)
+    segs = A["segs"]
+    segments = [Segment(*segs[i:i + 4]) for i in range(0, len(segs), 4)]
+    col_starts, _, R = rank_layout(A["ranks"], segments, A["share_blocks"])
+    k, n = x.shape[1], w.shape[0]
+    da, db = dacc[:R * k].view(R, k), dacc[R * k:].view(n, R)
+    sink = getattr(ctx, "sink", None)
+    if sink is not None and segments:
+        sink(_SinkLayout(A["ranks"], segments, col_starts), da, db)
+    # route the rank-concat gradients back to each adapter's parameters (summing the
+    # blocks of one adapter when its segments do not share one, e.g. per-batch slots)
+    ga: list = [None] * na
+    gb: list = [None] * na
+    seen = set()
+    for s, c0 in zip(segments, col_starts):
+        if (s.adapter, c0) in seen:
+            continue
+        seen.add((s.adapter, c0))
+        r = A["ranks"][s.adapter]
+        a_part, b_part = da[c0:c0 + r], db[:, c0:c0 + r]
+        ga[s.adapter] = a_part if ga[s.adapter] is None else ga[s.adapter] + a_part
+        gb[s.adapter] = b_part if gb[s.adapter] is None else gb[s.adapter] + b_part
+    dts = ctx.param_dtypes
+    ga = [g.to(dts[i]) if g is not None else None for i, g in enumerate(ga)]
+    gb = [g.to(dts[na + i]) if g is not None else None for i, g in enumerate(gb)]
+    return (dx if need_dx else None, None, ga, gb) + ctx.none_grads
+
+
+torch.library.register_autograd(f"{_NS}::lora_fwd", _backward, setup_context=_setup_context)
+
+
+class _SinkLayout:
+    """What a gradient sink sees of a call: (adapter, batch, col_start, rank) per segment."""
+
+    def __init__(self, ranks, segments, col_starts):
+        self._rows = [(s.adapter, s.batch, c0, ranks[s.adapter]) for s, c0 in zip(segments, col_starts)]
+
+    def segment_grad_slices(self) -> list[tuple[int, int, int, int]]:
+        return list(self._rows)
+
+
+class _SinkFn(torch.autograd.Function):
+    """Autograd node of a call that carries a gradient sink: the same operators, with the
+    sink kept on the node for the backward (eager only; a sink is a Python side effect)."""
 
     @staticmethod
-    def forward(ctx, x, w, plan: LayerPlan, grad_sink, n_adapters: int, *params):
-        lib = _lib.load()
-        m, k, n, R = plan.m, plan.k, plan.n, plan.rank_total
-        pp = ctypes.byref(plan.problem)
-        y = torch.empty((m, n), dtype=_BF16, device=x.device)
-        s_hat = a_cat = b_cat = None
-        st = _stream(x.device)
-        if plan.has_lora:
-            a_cat, b_cat = _rank_concat_operands(plan, params, n_adapters)
-            s_hat = torch.empty((m, R), dtype=_BF16, device=x.device)
-            _call("dropout_down_fwd", lib.lf_dropout_down_fwd, pp, _ptr(x), _ptr(a_cat), _ptr(s_hat), st)
-        _call("base_fwd", lib.lf_base_fwd, pp, _ptr(x), _ptr(w), _ptr(s_hat), _ptr(b_cat), _ptr(y), st)
-        ctx.plan = plan
-        ctx.grad_sink = grad_sink
-        ctx.n_adapters = n_adapters
-        ctx.param_dtypes = [p.dtype for p in params]
-        ctx.save_for_backward(x, w, a_cat, b_cat, s_hat)
+    def forward(ctx, x, w, n_adapters, plan_args, sink, *params):
+        a, b = list(params[:n_adapters]), list(params[n_adapters:])
+        y, s_hat, bits = torch.ops.lorafusion_b200.lora_fwd(x, w, a, b, *plan_args)
+        _setup_context(ctx, (x, w, a, b, *plan_args), (y, s_hat, bits), mark=False)
+        ctx.sink = sink
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        lib = _lib.load()
-        plan: LayerPlan = ctx.plan
-        x, w, a_cat, b_cat, s_hat = ctx.saved_tensors
-        m, k, n, R = plan.m, plan.k, plan.n, plan.rank_total
-        dy = dy.to(_BF16).contiguous()
-        pp = ctypes.byref(plan.problem)
-        da = db = ds = None
-        st = _stream(dy.device)
-        if plan.has_lora:
-            ds = torch.empty((m, R), dtype=_BF16, device=dy.device)
-            # one zero-fill for both fp32 accumulators
-            acc = torch.zeros(R * k + n * R, dtype=torch.float32, device=dy.device)
-            da = acc[:R * k].view(R, k)
-            db = acc[R * k:].view(n, R)
-            _call("grad_up", lib.lf_grad_up, pp, _ptr(dy), _ptr(b_cat), _ptr(s_hat), _ptr(ds), _ptr(db), st)
-            _call("grad_down", lib.lf_grad_down, pp, _ptr(x), _ptr(ds), _ptr(da), st)
-        dx = None
-        if ctx.needs_input_grad[0]:
-            dx = torch.empty((m, k), dtype=_BF16, device=dy.device)
-            _call("grad_input", lib.lf_grad_input, pp, _ptr(dy), _ptr(w), _ptr(ds), _ptr(a_cat), _ptr(dx), st)
-        if ctx.grad_sink is not None and plan.has_lora:
-            ctx.grad_sink(plan, da, db)
-        # route the rank-concat gradients back to each adapter's parameters (summing the
-        # segments that share an adapter, e.g. two global batches in one microbatch)
-        na = ctx.n_adapters
-        ga: list = [None] * na
-        gb: list = [None] * na
-        if plan.has_lora:
-            for adapter, c0, r in plan.adapter_grad_slices():
-                a_part, b_part = da[c0:c0 + r], db[:, c0:c0 + r]
-                ga[adapter] = a_part if ga[adapter] is None else ga[adapter] + a_part
-                gb[adapter] = b_part if gb[adapter] is None else gb[adapter] + b_part
-        dts = ctx.param_dtypes
-        ga = [g.to(dts[i]) if g is not None else None for i, g in enumerate(ga)]
-        gb = [g.to(dts[na + i]) if g is not None else None for i, g in enumerate(gb)]
+        dx, _, ga, gb = _backward(ctx, dy, None, None)[:4]
         return (dx, None, None, None, None, *ga, *gb)
 
 
+# --------------------------------------------------------------------------------------
+# functional API
+# --------------------------------------------------------------------------------------
 class _EmptyBatchFn(torch.autograd.Function):
     """An empty batch (m = 0) like nn.Linear: an empty (0, n) output that stays on the
     autograd graph, so backward gives an empty dX and all-zero adapter gradients. Nothing is
@@ -240,6 +447,38 @@ def _check_frozen(weight: torch.Tensor) -> None:
         )
 
 
+def _check_call(x2, weight, lora_a, lora_b, ranks, k, n, keep_mask, offset_dev) -> None:
+    _check_operand(x2, "x")
+    _check_operand(weight, "weight", (n, k))
+    _check_frozen(weight)
+    for i, (a, b) in enumerate(zip(lora_a, lora_b)):
+        r = ranks[i]
+        if tuple(a.shape) != (r, k):
+            raise ValidationError(f"lora_a[{i}] must have shape ({r}, {k}), got {tuple(a.shape)}")
+        if tuple(b.shape) != (n, r):
+            raise ValidationError(f"lora_b[{i}] must have shape ({n}, {r}), got {tuple(b.shape)}")
+        if not (a.is_cuda and b.is_cuda):
+            raise ValidationError("adapter weights must be CUDA tensors")
+    if keep_mask is not None:
+        if keep_mask.dtype != torch.uint8 or tuple(keep_mask.shape) != (x2.shape[0], k):
+            raise ValidationError(f"keep_mask must be uint8 of shape ({x2.shape[0]}, {k})")
+        if not keep_mask.is_contiguous():
+            raise ValidationError("keep_mask must be contiguous")
+    if offset_dev is not None and (offset_dev.dtype != torch.int64 or offset_dev.numel() != 1 or not offset_dev.is_cuda):
+        raise ValidationError("offset_dev must be a one-element int64 CUDA tensor")
+
+
+def _apply(x2, weight, lora_a, lora_b, packed, segs, offset, offset_dev, keep_mask, training, share_blocks,
+           row_base, cache_id, sink=None):
+    ranks, scalings, ps, seeds = packed
+    plan_args = (ranks, scalings, ps, seeds, segs, int(offset), offset_dev, keep_mask, bool(training),
+                 bool(share_blocks), int(row_base), int(cache_id))
+    if sink is not None:
+        return _SinkFn.apply(x2, weight, len(lora_a), plan_args, sink, *lora_a, *lora_b)
+    y, _s, _bits = torch.ops.lorafusion_b200.lora_fwd(x2, weight, list(lora_a), list(lora_b), *plan_args)
+    return y
+
+
 def fused_lora(
     x: torch.Tensor,
     weight: torch.Tensor,
@@ -251,30 +490,30 @@ def fused_lora(
     offset: int = 0,
     keep_mask: torch.Tensor | None = None,
     training: bool = True,
-    weights_bf16: tuple | None = None,
     offset_dev: torch.Tensor | None = None,
     operand_cache: OperandCache | None = None,
 ) -> torch.Tensor:
     """Y = X·Wᵀ + scaling·dropout(X)·Aᵀ·Bᵀ  (Eq. 1) on one adapter.
 
     x (..., k) bf16; weight (n, k) = nn.Linear.weight (frozen); lora_a (r, k) =
-    lora_A.weight; lora_b (n, r) = lora_B.weight. Dropout uses SPEC.md §3's Philox mask
-    keyed by (seed, offset) unless ``keep_mask`` (uint8, m x k) is given.
-    ``weights_bf16 = (a_bf16, b_bf16)``: bf16 copies of fp32 master weights kept current by
-    the caller (the modules refresh them when the parameters change); default: cast here.
-    ``offset_dev``: one-element int64 CUDA tensor added to ``offset`` when the kernels run
-    (CUDA-graph capture: advance it on the device between replays).
+    lora_A.weight; lora_b (n, r) = lora_B.weight, in any float dtype (fp32 master weights
+    are cast to the bf16 operands inside, gradients come back in their dtype). Dropout uses
+    SPEC.md §3's Philox mask keyed by (seed, offset) unless ``keep_mask`` (uint8, m x k) is
+    given. ``offset_dev``: one-element int64 CUDA tensor added to ``offset`` when the kernels
+    run (CUDA graphs: a device-side step counter or an offset drawn from torch's RNG).
     """
     k = weight.shape[1]
     x2, lead = _flatten_input(x, k)
     m = x2.shape[0]
+    n = weight.shape[0]
     adapter = AdapterConfig(rank=lora_a.shape[0], scaling=float(scaling), dropout_p=float(dropout_p), seed=int(seed))
-    plan = LayerPlan(m, k, weight.shape[0], [adapter], [Segment(0, 0, m)] if m > 0 else [], offset=offset,
-                     training=training, keep_mask=keep_mask, offset_dev=offset_dev)
-    if weights_bf16 is not None:
-        plan.weights_bf16 = ([weights_bf16[0]], [weights_bf16[1]])
-    plan.operand_cache = operand_cache
-    return _run(x2, weight, [lora_a], [lora_b], plan, lead, None)
+    packed = pack_adapters([adapter])
+    _check_call(x2, weight, [lora_a], [lora_b], packed[0], k, n, keep_mask, offset_dev)
+    if m == 0:
+        return _EmptyBatchFn.apply(x2, n, lora_a, lora_b).reshape(lead + (n,))
+    y = _apply(x2, weight, [lora_a], [lora_b], packed, [0, 0, m, 0], offset, offset_dev, keep_mask, training, True,
+               0, _cache_handle(operand_cache))
+    return y.reshape(lead + (n,))
 
 
 def fused_multi_lora(
@@ -288,56 +527,42 @@ def fused_multi_lora(
     keep_mask: torch.Tensor | None = None,
     training: bool = True,
     grad_sink: Callable | None = None,
-    weights_bf16: tuple | None = None,
     offset_dev: torch.Tensor | None = None,
     operand_cache: OperandCache | None = None,
 ) -> torch.Tensor:
     """Mixed-adapter microbatch: rows of ``segments`` route to their adapter's A/B, scale
     and dropout; the frozen W is streamed once for all of them.
 
-    ``grad_sink(plan, dA_cat, dB_cat)`` (optional) receives the fp32 rank-concat gradients
-    so a caller can keep per-(adapter, global batch) slots (plan.segment_grad_slices()).
+    ``grad_sink(layout, dA_cat, dB_cat)`` (optional, eager only) receives the fp32
+    rank-concat gradients so a caller can keep per-(adapter, global batch) slots
+    (``layout.segment_grad_slices()``); segments then get one column block each.
     """
     k = weight.shape[1]
+    n = weight.shape[0]
     x2, lead = _flatten_input(x, k)
     if len(lora_a) != len(adapters) or len(lora_b) != len(adapters):
         raise ValidationError("lora_a, lora_b and adapters must have one entry per adapter slot")
     m = x2.shape[0]
-    validate_segments(list(segments), m, len(adapters))
+    segments = list(segments)
+    validate_segments(segments, m, len(adapters), max_segments=None)
+    packed = pack_adapters(adapters)
+    _check_call(x2, weight, lora_a, lora_b, packed[0], k, n, keep_mask, offset_dev)
+    if m == 0:
+        return _EmptyBatchFn.apply(x2, n, *lora_a, *lora_b).reshape(lead + (n,))
+    share = grad_sink is None
+    cache_id = _cache_handle(operand_cache)
     # a microbatch beyond one launch's limits (R > 128 or > 32 segments) runs as several
     # consecutive row ranges; Philox keeps absolute rows (row_base), so masks are unchanged
-    parts = split_segments(adapters, segments, m) if segments else [(0, m, [])]
+    parts = split_segments(adapters, segments, m, share_blocks=share) if segments else [(0, m, [])]
     ys = []
     for r0, r1, segs in parts:
         local = [Segment(s_.adapter, s_.row_start - r0, s_.row_end - r0, s_.batch) for s_ in segs]
-        plan = LayerPlan(r1 - r0, k, weight.shape[0], adapters, local, offset=offset, training=training,
-                         keep_mask=None if keep_mask is None else keep_mask[r0:r1],
-                         share_blocks=grad_sink is None, offset_dev=offset_dev, row_base=r0)
-        if weights_bf16 is not None:
-            plan.weights_bf16 = (list(weights_bf16[0]), list(weights_bf16[1]))
-        plan.operand_cache = operand_cache
-        ys.append(_run(x2[r0:r1] if len(parts) > 1 else x2, weight, lora_a, lora_b, plan, (r1 - r0,), grad_sink))
+        xp = x2[r0:r1] if len(parts) > 1 else x2
+        km = None if keep_mask is None else (keep_mask[r0:r1] if len(parts) > 1 else keep_mask)
+        ys.append(_apply(xp, weight, lora_a, lora_b, packed, pack_segments(local), offset, offset_dev, km, training,
+                         share, r0, cache_id, grad_sink))
     y = ys[0] if len(ys) == 1 else torch.cat(ys, 0)
-    return y.reshape(lead + (weight.shape[0],))
-
-
-def _run(x2, weight, lora_a, lora_b, plan: LayerPlan, lead, grad_sink):
-    _check_operand(x2, "x")
-    _check_operand(weight, "weight", (plan.n, plan.k))
-    _check_frozen(weight)
-    for i, (a, b) in enumerate(zip(lora_a, lora_b)):
-        r = plan.adapters[i].rank
-        if tuple(a.shape) != (r, plan.k):
-            raise ValidationError(f"lora_a[{i}] must have shape ({r}, {plan.k}), got {tuple(a.shape)}")
-        if tuple(b.shape) != (plan.n, r):
-            raise ValidationError(f"lora_b[{i}] must have shape ({plan.n}, {r}), got {tuple(b.shape)}")
-        if not (a.is_cuda and b.is_cuda):
-            raise ValidationError("adapter weights must be CUDA tensors")
-    if plan.m == 0:
-        return _EmptyBatchFn.apply(x2, plan.n, *lora_a, *lora_b).reshape(lead + (plan.n,))
-    plan.bind(x2.device)
-    y = _FusedLoRAFn.apply(x2, weight, plan, grad_sink, len(lora_a), *lora_a, *lora_b)
-    return y.reshape(lead + (plan.n,))
+    return y.reshape(lead + (n,))
 
 
 def dropout_keep_mask(m: int, k: int, adapters: Sequence[AdapterConfig], segments: Sequence[Segment],

@@ -8,9 +8,19 @@ weights: their bf16 rank-concat operands are built once per weight update and re
 arrive in fp32 for the optimizer and the DP all-reduce; the base weight and activations
 are bf16.
 
-Dropout masks come from SPEC.md §3's counter-based Philox stream: each training forward
-uses (seed, offset) with ``offset`` advanced once per call, and backward reuses the
-forward's pair, so no mask is ever stored.
+Dropout masks come from SPEC.md §3's counter-based Philox stream keyed by the adapter
+seed and a per-forward 64-bit offset; backward reuses the forward's pair through the
+packed keep mask, so no byte mask is ever stored. Where the offset comes from
+(``dropout_rng``):
+
+* ``"torch"`` (default): drawn from torch's CUDA generator on the device (one int64 per
+  training forward) — dropout then follows ``torch.manual_seed`` like ``nn.Dropout``,
+  replays fresh inside CUDA graphs, and ``torch.utils.checkpoint`` (which restores the RNG
+  state before recomputing) redraws the original mask.
+* ``"counter"``: a per-module step counter (on the host, or on the device with
+  ``capturable=True``), advanced once per training forward — deterministic offsets
+  0, 1, 2, ... that ``dropout_state()`` saves and restores. Not checkpoint-safe: a
+  recomputed forward would advance it again.
 """
 from __future__ import annotations
 
@@ -21,8 +31,9 @@ import torch
 from torch import nn
 
 from .errors import ValidationError
-from .functional import OperandCache, fused_lora, fused_multi_lora
-from .plan import AdapterConfig, LayerPlan, Segment
+from .functional import (OperandCache, _apply, _cache_handle, _check_call, _EmptyBatchFn, _flatten_input,
+                         fused_multi_lora, pack_adapters)
+from .plan import AdapterConfig, Segment
 
 
 def _init_lora(a: nn.Linear, b: nn.Linear, init: str, generator: torch.Generator | None = None) -> None:
@@ -40,8 +51,11 @@ def _init_lora(a: nn.Linear, b: nn.Linear, init: str, generator: torch.Generator
 
 
 def _frozen_base(base: nn.Linear | torch.Tensor) -> tuple[torch.Tensor, torch.Tensor | None]:
+    """The frozen base weight (and bias): only the adapters train, so both stop requiring grad."""
     if isinstance(base, nn.Linear):
         w, bias = base.weight, base.bias
+        if bias is not None:
+            bias.requires_grad_(False)
     elif isinstance(base, torch.Tensor):
         w, bias = base, None
     else:
@@ -51,25 +65,38 @@ def _frozen_base(base: nn.Linear | torch.Tensor) -> tuple[torch.Tensor, torch.Te
     return w, bias
 
 
-def _init_capturable(mod: nn.Module, capturable: bool, device) -> None:
-    """``capturable=True`` (as torch.optim's flag): the module's Philox step counter lives on
-    the device and is advanced there by every training forward, and the bf16 operand copies
-    of the fp32 adapter weights are re-cast inside each call, so a forward+backward captured
-    in a CUDA graph replays with a fresh dropout mask and the current weights."""
+_DROPOUT_RNGS = ("torch", "counter")
+
+
+def _init_capturable(mod: nn.Module, capturable: bool, device, dropout_rng: str) -> None:
+    """``capturable=True`` (as torch.optim's flag): the bf16 operand copies of the fp32
+    adapter weights are re-cast inside each call (no host-side cache), and in ``"counter"``
+    mode the Philox step counter lives on the device and is advanced there by every training
+    forward — so a forward+backward captured in a CUDA graph replays with a fresh dropout
+    mask and the current weights (``"torch"`` mode draws its offsets on the device anyway)."""
+    if dropout_rng not in _DROPOUT_RNGS:
+        raise ValidationError(f"dropout_rng must be one of {_DROPOUT_RNGS}, got {dropout_rng!r}")
     mod.capturable = bool(capturable)
-    if mod.capturable:
+    mod.dropout_rng = dropout_rng
+    if mod.capturable and dropout_rng == "counter":
         mod.register_buffer("step_counter", torch.zeros(1, dtype=torch.int64, device=device), persistent=False)
 
 
 def _dropout_state(mod: nn.Module) -> dict:
-    """The Philox step counter, for checkpoints: restoring it makes a resumed run draw
-    exactly the dropout masks the uninterrupted run would have drawn (SPEC.md §3). Kept out
-    of ``state_dict`` so PEFT-style state dicts load strictly into the modules."""
+    """The Philox step counter, for checkpoints (``"counter"`` mode): restoring it makes a
+    resumed run draw exactly the dropout masks the uninterrupted run would have drawn
+    (SPEC.md §3). In ``"torch"`` mode the offsets follow torch's RNG state, which training
+    checkpoints save themselves. Kept out of ``state_dict`` so PEFT-style state dicts load
+    strictly into the modules."""
+    if mod.dropout_rng == "torch":
+        return {"dropout_rng": "torch"}
     step = int(mod.step_counter.item()) if mod.capturable else int(mod._offset)
-    return {"philox_step": step, "capturable": mod.capturable}
+    return {"philox_step": step, "capturable": mod.capturable, "dropout_rng": "counter"}
 
 
 def _load_dropout_state(mod: nn.Module, state: dict) -> None:
+    if mod.dropout_rng == "torch":
+        return
     step = int(state.get("philox_step", 0))
     if mod.capturable:
         with torch.no_grad():
@@ -78,10 +105,15 @@ def _load_dropout_state(mod: nn.Module, state: dict) -> None:
         mod._offset = step
 
 
-def _step_offsets(mod: nn.Module) -> tuple[int, torch.Tensor | None]:
-    """(host offset, device counter) of this forward (SPEC.md §3)."""
-    if not mod.training:
+_OFFSET_HIGH = 2**62
+
+
+def _step_offsets(mod: nn.Module, device: torch.device, has_dropout: bool) -> tuple[int, torch.Tensor | None]:
+    """(host offset, device offset) of this forward (SPEC.md §3)."""
+    if not mod.training or not has_dropout:
         return 0, None
+    if mod.dropout_rng == "torch":
+        return 0, torch.randint(0, _OFFSET_HIGH, (1,), dtype=torch.int64, device=device)
     if mod.capturable:
         mod.step_counter.add_(1)  # on the device: captured into a graph with the kernels
         return 0, mod.step_counter
@@ -104,6 +136,7 @@ class FusedLoRA(nn.Module):
         dtype: torch.dtype = torch.float32,
         generator: torch.Generator | None = None,
         capturable: bool = False,
+        dropout_rng: str = "torch",
     ):
         super().__init__()
         w, bias = _frozen_base(base)
@@ -111,10 +144,11 @@ class FusedLoRA(nn.Module):
         self.base = base if isinstance(base, nn.Linear) else None
         self.register_buffer("weight", w, persistent=False) if self.base is None else None
         self.out_features, self.in_features = w.shape
-        _init_capturable(self, capturable, w.device)
+        _init_capturable(self, capturable, w.device, dropout_rng)
         if scaling is None:
             scaling = (alpha if alpha is not None else 32.0) / rank
         self.config = AdapterConfig(rank=rank, scaling=float(scaling), dropout_p=float(dropout_p), seed=int(seed))
+        self._packed = pack_adapters([self.config])
         dev = w.device
         self.lora_A = nn.Linear(self.in_features, rank, bias=False, device=dev, dtype=dtype)
         self.lora_B = nn.Linear(rank, self.out_features, bias=False, device=dev, dtype=dtype)
@@ -141,25 +175,26 @@ class FusedLoRA(nn.Module):
     def load_dropout_state(self, state: dict) -> None:
         _load_dropout_state(self, state)
 
+    def invalidate_operands(self) -> None:
+        """Drop the cached bf16 operands (after changing lora_A/lora_B outside an optimizer step)."""
+        self._operands.clear()
+
     def forward(self, x: torch.Tensor, keep_mask: torch.Tensor | None = None) -> torch.Tensor:
-        c = self.config
-        off, off_dev = _step_offsets(self)
-        y = fused_lora(
-            x,
-            self.base_weight,
-            self.lora_A.weight,
-            self.lora_B.weight,
-            c.scaling,
-            c.dropout_p,
-            seed=c.seed,
-            offset=off,
-            keep_mask=keep_mask,
-            training=self.training,
-            offset_dev=off_dev,
-            operand_cache=None if self.capturable else self._operands,
-        )
+        k, n = self.in_features, self.out_features
+        w = self.base_weight
+        x2, lead = _flatten_input(x, k)
+        a, b = self.lora_A.weight, self.lora_B.weight
+        _check_call(x2, w, [a], [b], self._packed[0], k, n, keep_mask, None)
+        m = x2.shape[0]
+        if m == 0:
+            y = _EmptyBatchFn.apply(x2, n, a, b)
+        else:
+            off, off_dev = _step_offsets(self, x2.device, self.config.dropout_p > 0 and keep_mask is None)
+            y = _apply(x2, w, [a], [b], self._packed, [0, 0, m, 0], off, off_dev, keep_mask, self.training, True, 0,
+                       0 if self.capturable else _cache_handle(self._operands))
+        y = y.reshape(lead + (n,))
         if self.base_bias is not None:
-            y = y + self.base_bias
+            y = y + self.base_bias.to(y.dtype)
         return y
 
     def extra_repr(self) -> str:
@@ -182,6 +217,7 @@ class FusedMultiLoRA(nn.Module):
         track_slot_grads: bool = False,
         generator: torch.Generator | None = None,
         capturable: bool = False,
+        dropout_rng: str = "torch",
     ):
         super().__init__()
         if not adapters:
@@ -191,7 +227,7 @@ class FusedMultiLoRA(nn.Module):
         self.base = base if isinstance(base, nn.Linear) else None
         self.register_buffer("weight", w, persistent=False) if self.base is None else None
         self.out_features, self.in_features = w.shape
-        _init_capturable(self, capturable, w.device)
+        _init_capturable(self, capturable, w.device, dropout_rng)
         self.adapters = list(adapters)
         dev = w.device
         self.lora_A = nn.ModuleList(
@@ -221,8 +257,12 @@ class FusedMultiLoRA(nn.Module):
     def load_dropout_state(self, state: dict) -> None:
         _load_dropout_state(self, state)
 
-    def _sink(self, plan: LayerPlan, da: torch.Tensor, db: torch.Tensor) -> None:
-        for adapter, batch, c0, r in plan.segment_grad_slices():
+    def invalidate_operands(self) -> None:
+        """Drop the cached bf16 operands (after changing lora_A/lora_B outside an optimizer step)."""
+        self._operands.clear()
+
+    def _sink(self, layout, da: torch.Tensor, db: torch.Tensor) -> None:
+        for adapter, batch, c0, r in layout.segment_grad_slices():
             ga, gb = da[c0:c0 + r], db[:, c0:c0 + r]
             slot = self.slot_grads.get((adapter, batch))
             if slot is None:
@@ -233,7 +273,9 @@ class FusedMultiLoRA(nn.Module):
 
     def forward(self, x: torch.Tensor, segments: Sequence[Segment],
                 keep_mask: torch.Tensor | None = None) -> torch.Tensor:
-        off, off_dev = _step_offsets(self)
+        has_dropout = keep_mask is None and any(
+            self.adapters[s_.adapter].dropout_p > 0 for s_ in segments)
+        off, off_dev = _step_offsets(self, self.base_weight.device, has_dropout)
         y = fused_multi_lora(
             x,
             self.base_weight,
@@ -249,5 +291,5 @@ class FusedMultiLoRA(nn.Module):
             operand_cache=None if self.capturable else self._operands,
         )
         if self.base is not None and self.base.bias is not None:
-            y = y + self.base.bias
+            y = y + self.base.bias.to(y.dtype)
         return y

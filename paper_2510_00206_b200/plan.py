@@ -90,24 +90,28 @@ def segments_from_lengths(adapters: Sequence[int], lengths: Sequence[int], batch
 
 
 def split_segments(adapters: Sequence[AdapterConfig], segments: Sequence[Segment], m: int,
-                   max_rank_total: int | None = None, max_segments: int | None = None) -> list[tuple[int, int, list]]:
-    """Cut a microbatch whose segments exceed one launch's limits (Σ padded ranks of the
-    distinct adapters ≤ LF_MAX_RANK_TOTAL, ≤ LF_MAX_SEGMENTS segments) into consecutive row
-    ranges that each fit: [(row_start, row_end, segments)]. The ranges tile [0, m); rows in
-    no segment stay with the range before them. One range when everything fits."""
+                   max_rank_total: int | None = None, max_segments: int | None = None,
+                   share_blocks: bool = True) -> list[tuple[int, int, list]]:
+    """Cut a microbatch whose segments exceed one launch's limits (rank-concat width R ≤
+    LF_MAX_RANK_TOTAL, ≤ LF_MAX_SEGMENTS segments) into consecutive row ranges that each fit:
+    [(row_start, row_end, segments)]. R counts each distinct adapter's padded rank once when
+    its segments share a column block (``share_blocks``, LayerPlan's default), else once per
+    segment (per-(adapter, batch) gradient slots). The ranges tile [0, m); rows in no segment
+    stay with the range before them. One range when everything fits."""
     max_rank_total = max_rank_total or _lib.LF_MAX_RANK_TOTAL
     max_segments = max_segments or _lib.LF_MAX_SEGMENTS
-    groups, cur, ranks = [], [], {}
+    groups, cur, ranks, width = [], [], set(), 0
     for s in sorted(segments, key=lambda s_: s_.row_start):
         r = padded_rank(adapters[s.adapter].rank)
         if r > max_rank_total:
             raise ValidationError(f"adapter {s.adapter}: rank {adapters[s.adapter].rank} exceeds {max_rank_total}")
-        total = sum(ranks.values()) + (0 if s.adapter in ranks else r)
-        if cur and (total > max_rank_total or len(cur) >= max_segments):
+        grow = 0 if (share_blocks and s.adapter in ranks) else r
+        if cur and (width + grow > max_rank_total or len(cur) >= max_segments):
             groups.append(cur)
-            cur, ranks = [], {}
+            cur, ranks, width, grow = [], set(), 0, r
         cur.append(s)
-        ranks.setdefault(s.adapter, r)
+        ranks.add(s.adapter)
+        width += grow
     if not groups:
         return [(0, m, list(cur))]
     groups.append(cur)
@@ -115,9 +119,31 @@ def split_segments(adapters: Sequence[AdapterConfig], segments: Sequence[Segment
     return [(bounds[i], bounds[i + 1], g) for i, g in enumerate(groups)]
 
 
-def validate_segments(segments: Sequence[Segment], m: int, num_adapters: int) -> None:
-    if len(segments) > _lib.LF_MAX_SEGMENTS:
-        raise ValidationError(f"at most {_lib.LF_MAX_SEGMENTS} segments per microbatch, got {len(segments)}")
+def rank_layout(adapter_ranks: Sequence[int], segments: Sequence[Segment],
+                share_blocks: bool = True) -> tuple[list[int], list[int], int]:
+    """Column blocks of the rank-concat dimension: (col_start per segment, padded rank per
+    segment, total width R). One block per adapter present — segments of the same adapter
+    (two global batches in one microbatch) share it, their rows being disjoint — or, with
+    ``share_blocks=False``, one per segment so dA/dB split per (adapter, batch) slot."""
+    padded = [padded_rank(adapter_ranks[s.adapter]) for s in segments]
+    col_starts, c, first = [], 0, {}
+    for s, r in zip(segments, padded):
+        if share_blocks and s.adapter in first:
+            col_starts.append(first[s.adapter])
+            continue
+        first[s.adapter] = c
+        col_starts.append(c)
+        c += r
+    return col_starts, padded, c
+
+
+def validate_segments(segments: Sequence[Segment], m: int, num_adapters: int,
+                      max_segments: int | None = _lib.LF_MAX_SEGMENTS) -> None:
+    """Segments must be sorted, disjoint, inside [0, m) and name a valid adapter slot; at
+    most ``max_segments`` of them per launch (None: no cap — a whole microbatch that
+    fused_multi_lora then splits into launches)."""
+    if max_segments is not None and len(segments) > max_segments:
+        raise ValidationError(f"at most {max_segments} segments per launch, got {len(segments)}")
     prev = 0
     for i, s in enumerate(segments):
         if not 0 <= s.adapter < num_adapters:
@@ -185,22 +211,9 @@ class LayerPlan:
         self.offset = int(offset)
         self.training = bool(training)
         validate_segments(self.segments, self.m, len(self.adapters))
-        # Column blocks of the rank-concat dimension: one per adapter present (segments of
-        # the same adapter — e.g. two global batches in one microbatch — share it, their
-        # rows being disjoint), or, with share_blocks=False, one per segment so dA/dB can
-        # be split per (adapter, global batch) slot (FusedMultiLoRA(track_slot_grads=True)).
         self.share_blocks = bool(share_blocks)
-        self.ranks = [padded_rank(self.adapters[s.adapter].rank) for s in self.segments]
-        self.col_starts = []
-        c, first = 0, {}
-        for s, r in zip(self.segments, self.ranks):
-            if self.share_blocks and s.adapter in first:
-                self.col_starts.append(first[s.adapter])
-                continue
-            first[s.adapter] = c
-            self.col_starts.append(c)
-            c += r
-        self.rank_total = c
+        self.col_starts, self.ranks, self.rank_total = rank_layout(
+            [a.rank for a in self.adapters], self.segments, self.share_blocks)
         if self.rank_total > _lib.LF_MAX_RANK_TOTAL:
             raise ValidationError(
                 f"sum of padded segment ranks {self.rank_total} exceeds {_lib.LF_MAX_RANK_TOTAL}; "
@@ -263,8 +276,10 @@ class LayerPlan:
         return routing_table(self.segments, self.col_starts, self.ranks, self.m)
 
     # -- device ---------------------------------------------------------------------
-    def bind(self, device: torch.device, stream: torch.cuda.Stream | None = None) -> "LayerPlan":
-        """Build the routing table and attach the workspace on ``device``/``stream``."""
+    def bind(self, device: torch.device, stream: torch.cuda.Stream | None = None,
+             keep_bits: torch.Tensor | None = None) -> "LayerPlan":
+        """Build the routing table and attach the workspace on ``device``/``stream``; the
+        packed keep mask is ``keep_bits`` (the forward's, for the backward) or a new buffer."""
         self.device = device
         lib = _lib.load()
         dev_index = device.index if device.index is not None else torch._C._cuda_getDevice()
@@ -287,7 +302,9 @@ class LayerPlan:
         self.problem.workspace = self._ws.data_ptr()
         self.problem.workspace_bytes = self._ws.numel()
         if self.needs_keep_bits:
-            self.keep_bits = torch.empty((self.m, self.k // 8), dtype=torch.uint8, device=device)
+            if keep_bits is None or keep_bits.numel() == 0:
+                keep_bits = torch.empty((self.m, self.k // 8), dtype=torch.uint8, device=device)
+            self.keep_bits = keep_bits
             self.problem.keep_bits = self.keep_bits.data_ptr()
         if self.has_lora and fresh:
             from .functional import _call

@@ -1,0 +1,174 @@
+"""The drop-in boundary under the ways PEFT/HF training drives a LoRA linear (needs a B200):
+torch operators + torch.compile, activation checkpointing, fused optimizers, biases and
+microbatches beyond one launch's limits."""
+from __future__ import annotations
+
+import pytest
+import torch
+import torch.utils.checkpoint as ckpt
+
+from paper_2510_00206_b200 import AdapterConfig, FusedLoRA, FusedMultiLoRA, Segment, segments_from_lengths
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _rel(a, b):
+    a, b = a.detach().float(), b.detach().float()
+    return float((a - b).norm() / b.norm().clamp_min(1e-12))
+
+
+def _layer(seed=0, k=512, n=384, r=16, p=0.1, **kw):
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    w = (torch.randn(n, k, device=DEV, generator=g) / k**0.5).to(torch.bfloat16)
+    return FusedLoRA(w, rank=r, scaling=2.0, dropout_p=p, seed=5, init="gaussian", generator=g, **kw)
+
+
+def _grads(layer):
+    return [p.grad.clone() for p in (layer.lora_A.weight, layer.lora_B.weight)]
+
+
+def _same_step(got, want):
+    """(Y, dX, dA, dB): Y and dX bit-identical; dA/dB within fp32 reduction-order noise
+    (④/③ accumulate split-K partials with red.global.add, whose order is not fixed)."""
+    assert torch.equal(got[0], want[0]) and torch.equal(got[1], want[1])
+    for g_, w_ in zip(got[2:], want[2:]):
+        assert _rel(g_, w_) < 1e-5
+
+
+def test_ops_are_registered_with_fake_impls():
+    """the two passes are torch operators with meta implementations."""
+    assert hasattr(torch.ops.lorafusion_b200, "lora_fwd") and hasattr(torch.ops.lorafusion_b200, "lora_bwd")
+    from torch._subclasses.fake_tensor import FakeTensorMode
+
+    with FakeTensorMode():
+        x = torch.empty(300, 256, dtype=torch.bfloat16, device=DEV)
+        w = torch.empty(128, 256, dtype=torch.bfloat16, device=DEV)
+        a = [torch.empty(8, 256, device=DEV), torch.empty(32, 256, device=DEV)]
+        b = [torch.empty(128, 8, device=DEV), torch.empty(128, 32, device=DEV)]
+        y, s, bits = torch.ops.lorafusion_b200.lora_fwd(x, w, a, b, [8, 32], [2.0, 1.0], [0.1, 0.0], [1, 2],
+                                                        [0, 0, 100, 0, 1, 100, 300, 0], 0, None, None, True, True,
+                                                        0, 0)
+        assert y.shape == (300, 128) and s.shape == (300, 48) and bits.shape == (300, 32)
+
+
+@pytest.mark.parametrize("reentrant", [False, True], ids=["non_reentrant", "reentrant"])
+def test_activation_checkpointing_redraws_the_same_mask(reentrant):
+    """torch.utils.checkpoint restores torch's RNG state before recomputing, and the default
+    dropout offsets come from torch's CUDA generator: Y and every gradient are identical
+    with and without checkpointing."""
+    layer = _layer()
+    x0 = torch.randn(640, 512, device=DEV).to(torch.bfloat16)
+    dy = torch.randn(640, 384, device=DEV).to(torch.bfloat16)
+    outs = []
+    for use_ckpt in (False, True):
+        torch.manual_seed(123)
+        x = x0.clone().requires_grad_(True)
+        layer.lora_A.weight.grad = layer.lora_B.weight.grad = None
+        if use_ckpt:
+            y = ckpt.checkpoint(lambda t: layer(t) * 1.0, x, use_reentrant=reentrant)
+        else:
+            y = layer(x) * 1.0
+        y.backward(dy)
+        outs.append((y.detach(), x.grad.clone(), *_grads(layer)))
+    _same_step(outs[1], outs[0])
+    # and a second forward draws a different mask (fresh offset per forward)
+    torch.manual_seed(123)
+    layer(x0)
+    y2 = layer(x0)
+    assert not torch.equal(y2, outs[0][0])
+
+
+def test_torch_compile_fullgraph_matches_eager():
+    """FusedLoRA traces into one graph (custom ops + fake impls + registered autograd): no
+    graph break under fullgraph=True, and the compiled fwd+bwd equals eager."""
+    layer = _layer(seed=1, capturable=True, dropout_rng="counter")
+    x0 = torch.randn(512, 512, device=DEV).to(torch.bfloat16)
+    dy = torch.randn(512, 384, device=DEV).to(torch.bfloat16)
+
+    def run(fn):
+        x = x0.clone().requires_grad_(True)
+        layer.lora_A.weight.grad = layer.lora_B.weight.grad = None
+        with torch.no_grad():
+            layer.step_counter.zero_()
+        y = fn(x)
+        y.backward(dy)
+        return (y.detach(), x.grad.clone(), *_grads(layer))
+
+    eager = run(layer)
+    compiled = torch.compile(layer, backend="aot_eager", fullgraph=True)
+    got = run(compiled)
+    _same_step(got, eager)
+
+
+def test_operand_cache_sees_fused_optimizer_updates():
+    """AdamW(fused=True) updates parameters without bumping their version counters: the
+    cached bf16 operands must still be refreshed after every optimizer step."""
+    layer = _layer(seed=2, p=0.0)
+    fresh = _layer(seed=2, p=0.0, capturable=True)  # no operand cache: re-casts every call
+    opt = torch.optim.AdamW(layer.parameters(), lr=1e-2, fused=True)
+    x = torch.randn(256, 512, device=DEV).to(torch.bfloat16)
+    for _ in range(3):
+        y = layer(x)
+        y.float().square().mean().backward()
+        v0 = layer.lora_A.weight._version
+        opt.step()
+        opt.zero_grad()
+        assert layer.lora_A.weight._version == v0  # the case the version key alone misses
+        with torch.no_grad():
+            fresh.lora_A.weight.copy_(layer.lora_A.weight)
+            fresh.lora_B.weight.copy_(layer.lora_B.weight)
+        assert torch.equal(layer(x), fresh(x))
+    # updates outside any optimizer: explicit invalidation
+    with torch.no_grad():
+        layer.lora_B.weight.data.mul_(3.0)
+        fresh.lora_B.weight.copy_(layer.lora_B.weight)
+    layer.invalidate_operands()
+    assert torch.equal(layer(x), fresh(x))
+
+
+def test_linear_bias_stays_frozen_and_keeps_bf16():
+    base = torch.nn.Linear(256, 128, bias=True, device=DEV, dtype=torch.bfloat16)
+    base.bias.data = base.bias.data.float()  # an fp32 bias must not promote the output
+    layer = FusedLoRA(base, rank=8, init="gaussian")
+    x = torch.randn(64, 256, device=DEV).to(torch.bfloat16)
+    y = layer(x)
+    assert y.dtype == torch.bfloat16 and not base.bias.requires_grad
+    ref = (x.float() @ base.weight.float().T + base.bias.float() +
+           4.0 * (x.float() @ layer.lora_A.weight.bfloat16().float().T) @ layer.lora_B.weight.bfloat16().float().T)
+    assert _rel(y, ref) < 1e-2
+
+
+def test_module_with_more_than_32_segments_splits():
+    """A microbatch of 40 segments runs as several launches (the whole-microbatch
+    check no longer rejects it); results equal the per-segment torch reference."""
+    from paper_2510_00206_b200 import unfused_multi_lora
+
+    ads = [AdapterConfig(8, 2.0, 0.0, 1), AdapterConfig(16, 1.0, 0.0, 2)]
+    segs = segments_from_lengths([i % 2 for i in range(40)], [16] * 40, batches=[i // 2 for i in range(40)])
+    g = torch.Generator(device=DEV).manual_seed(3)
+    w = (torch.randn(192, 256, device=DEV, generator=g) / 16).to(torch.bfloat16)
+    layer = FusedMultiLoRA(w, ads, init="gaussian", generator=g)
+    x = torch.randn(640, 256, device=DEV, generator=g).to(torch.bfloat16).requires_grad_(True)
+    y = layer(x, segs)
+    ref = unfused_multi_lora(x.detach(), w, [a.weight.bfloat16() for a in layer.lora_A],
+                             [b.weight.bfloat16() for b in layer.lora_B], ads, segs)
+    assert _rel(y, ref) < 1e-2
+    y.float().sum().backward()
+    assert x.grad is not None and all(p.grad is not None for p in layer.parameters() if p.requires_grad)
+
+
+def test_slot_grads_split_unshared_blocks():
+    """track_slot_grads gives each (adapter, batch) segment its own column block: three
+    rank-64 global batches (192 columns) are split into launches that fit."""
+    g = torch.Generator(device=DEV).manual_seed(4)
+    w = (torch.randn(128, 256, device=DEV, generator=g) / 16).to(torch.bfloat16)
+    ads = [AdapterConfig(64, 1.0, 0.1, 7)]
+    layer = FusedMultiLoRA(w, ads, init="gaussian", generator=g, track_slot_grads=True)
+    segs = [Segment(0, 0, 128, 0), Segment(0, 128, 256, 1), Segment(0, 256, 384, 2)]
+    x = torch.randn(384, 256, device=DEV, generator=g).to(torch.bfloat16)
+    layer(x, segs).float().square().mean().backward()
+    total_a = sum(layer.slot_grads[(0, bt)][0] for bt in range(3))
+    total_b = sum(layer.slot_grads[(0, bt)][1] for bt in range(3))
+    torch.testing.assert_close(total_a, layer.lora_A[0].weight.grad, rtol=1e-5, atol=1e-6)
+    torch.testing.assert_close(total_b, layer.lora_B[0].weight.grad, rtol=1e-5, atol=1e-6)

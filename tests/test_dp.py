@@ -137,3 +137,25 @@ def test_adapter_grad_allreduce_overlapped_with_backward_world2_gloo():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}
+
+
+def test_c5_imbalance_matches_reference_simulate_dp():
+    """The C5 bench leg's DP balance, restated by dp.imbalance over the LPT-assigned rank
+    loads, equals lorasched's own simulate_dp on the same rank streams (linear time model;
+    fixture generated from the reference by tests/golden/make_dp_golden.py)."""
+    import json
+    import os
+
+    import bench
+    from paper_2510_00206_b200 import dp as dp_
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "c5_simulate_dp.json")) as f:
+        gold = json.load(f)
+    for world, ent in gold["worlds"].items():
+        _, chosen, assign = bench.c5_microbatches(int(world), gold["microbatches_per_rank"])
+        assert assign == ent["assignment"]
+        loads = dp_.rank_loads([mb.rows for mb in chosen], assign)
+        assert abs(dp_.imbalance(loads) - ent["linear"]["imbalance"]) < 1e-12
+        # per-step max over ranks (simulate_dp's step cost) in rows, linear model: 1e-6 s/row x 3
+        steps = [max(s[i] for s in ent["streams"]) for i in range(len(ent["streams"][0]))]
+        assert abs(sum(steps) * 3e-6 - ent["linear"]["total_time_s"]) < 1e-9

@@ -25,9 +25,9 @@ def test_graphed_fused_lora_matches_eager_offset_and_redraws_mask():
     w = (torch.randn(n, k, device=DEV, generator=g) / k**0.5).to(torch.bfloat16)
     x = torch.randn(m, k, device=DEV, generator=g).to(torch.bfloat16).requires_grad_(True)
     dy = torch.randn(m, n, device=DEV, generator=g).to(torch.bfloat16)
-    cap = FusedLoRA(w, rank=r, scaling=2.0, dropout_p=0.1, seed=9, init="gaussian", capturable=True,
+    cap = FusedLoRA(w, rank=r, scaling=2.0, dropout_p=0.1, seed=9, init="gaussian", capturable=True, dropout_rng="counter",
                     generator=torch.Generator(device=DEV).manual_seed(1))
-    ref = FusedLoRA(w, rank=r, scaling=2.0, dropout_p=0.1, seed=9, init="gaussian",
+    ref = FusedLoRA(w, rank=r, scaling=2.0, dropout_p=0.1, seed=9, init="gaussian", dropout_rng="counter",
                     generator=torch.Generator(device=DEV).manual_seed(1))
 
     def step():

@@ -12,6 +12,7 @@ from oracle import routing as orouting
 from paper_2510_00206_b200 import AdapterConfig, LayerPlan, Segment, padded_rank, segments_from_lengths
 from paper_2510_00206_b200 import schedule as sched
 from paper_2510_00206_b200.errors import ValidationError
+from paper_2510_00206_b200.plan import split_segments, validate_segments
 
 GOLD_SCHED = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "schedule_reference.json")))
 
@@ -204,16 +205,52 @@ def test_module_dropout_state_round_trip_and_strict_state_dict():
     from paper_2510_00206_b200 import FusedLoRA, FusedMultiLoRA
 
     w = torch.zeros(64, 32, dtype=torch.bfloat16)
-    a = FusedLoRA(w, rank=8, dropout_p=0.1, seed=3)
+    a = FusedLoRA(w, rank=8, dropout_p=0.1, seed=3, dropout_rng="counter")
     a._offset = 17
-    b = FusedLoRA(w.clone(), rank=8, dropout_p=0.1, seed=3)
+    b = FusedLoRA(w.clone(), rank=8, dropout_p=0.1, seed=3, dropout_rng="counter")
     b.load_state_dict(a.state_dict(), strict=True)
     assert set(a.state_dict()) == {"lora_A.weight", "lora_B.weight"}
     b.load_dropout_state(a.dropout_state())
     assert b._offset == 17 and b.next_offset() == 17
-    m = FusedMultiLoRA(w, [AdapterConfig(8), AdapterConfig(16)])
+    m = FusedMultiLoRA(w, [AdapterConfig(8), AdapterConfig(16)], dropout_rng="counter")
     m._offset = 5
-    m2 = FusedMultiLoRA(w.clone(), [AdapterConfig(8), AdapterConfig(16)])
+    m2 = FusedMultiLoRA(w.clone(), [AdapterConfig(8), AdapterConfig(16)], dropout_rng="counter")
     m2.load_state_dict(m.state_dict(), strict=True)
     m2.load_dropout_state(m.dropout_state())
     assert m2._offset == 5 and torch.equal(m2.lora_B[1].weight, m.lora_B[1].weight)
+    # torch-RNG offsets (the default) follow torch's RNG state instead: nothing to restore
+    t = FusedLoRA(w.clone(), rank=8, dropout_p=0.1)
+    assert t.dropout_rng == "torch" and t.dropout_state() == {"dropout_rng": "torch"}
+    t.load_dropout_state({"philox_step": 3})
+    with pytest.raises(ValidationError):
+        FusedLoRA(w.clone(), rank=8, dropout_rng="numpy")
+
+
+def test_frozen_base_bias_does_not_train():
+    from paper_2510_00206_b200 import FusedLoRA
+
+    base = torch.nn.Linear(32, 64, bias=True)
+    layer = FusedLoRA(base, rank=8)
+    assert not base.weight.requires_grad and not base.bias.requires_grad
+    assert {n for n, p in layer.named_parameters() if p.requires_grad} == {"lora_A.weight", "lora_B.weight"}
+
+
+def test_split_segments_counts_unshared_blocks_per_segment():
+    """FusedMultiLoRA(track_slot_grads=True) gives every segment its own column block: the
+    split must count a rank-64 adapter's three global batches as 192 columns."""
+    segs = [Segment(0, 0, 100, 0), Segment(0, 100, 200, 1), Segment(0, 200, 300, 2)]
+    assert len(split_segments([AdapterConfig(64)], segs, 300)) == 1
+    parts = split_segments([AdapterConfig(64)], segs, 300, share_blocks=False)
+    assert [(r0, r1, len(g)) for r0, r1, g in parts] == [(0, 200, 2), (200, 300, 1)]
+    for r0, r1, g in parts:
+        local = [Segment(s.adapter, s.row_start - r0, s.row_end - r0, s.batch) for s in g]
+        LayerPlan(r1 - r0, 64, 64, [AdapterConfig(64)], local, share_blocks=False)  # fits one launch
+
+
+def test_whole_microbatch_validation_has_no_segment_cap():
+    """More than 32 segments are valid for a microbatch (fused_multi_lora splits it into
+    launches); one launch's plan still enforces the cap."""
+    segs = segments_from_lengths([0] * 40, [1] * 40)
+    validate_segments(segs, 40, 1, max_segments=None)
+    with pytest.raises(ValidationError):
+        validate_segments(segs, 40, 1)

@@ -18,6 +18,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
     ap.add_argument("--unfused", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="profile one replay of the step captured as a CUDA graph")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -27,7 +28,7 @@ def main():
     dev = torch.device("cuda")
     gen = torch.Generator(device=dev).manual_seed(0)
     m = bench.tokens_per_gpu(args.config)
-    layers, inputs, grads = bench.build_layers(args.config, m, 16, 0.1, dev, gen)
+    layers, inputs, grads = bench.build_layers(args.config, m, 16, 0.1, dev, gen, capturable=args.graph)
     if args.unfused:
         base = {}
         for name, k, n, grp in bench.projections(args.config):
@@ -40,6 +41,10 @@ def main():
         def step():
             bench.zero_grads(layers, inputs)
             bench.fused_step(args.config, layers, inputs, grads, 1)
+    if args.graph:
+        from paper_2510_00206_b200.graphs import GraphedStep
+
+        step = GraphedStep(step, warmup=3).replay
     for _ in range(3):
         step()
     torch.cuda.synchronize()
