@@ -69,8 +69,9 @@ __device__ __forceinline__ void gemm_tile_coords(int t, int tiles_m, int tiles_n
 }
 
 struct TileInfo {
-  int mb, nb;          // 256 x 256 pair-tile coordinates
-  int col_lo, col_hi;  // LoRA K-range: union over the tile's two 128-row routes
+  int mb, nb;          // cluster-tile coordinates: rows [mb * NP * 256, +NP * 256), columns [nb * BN, +BN)
+  int col_lo, col_hi;  // LoRA K-range: union over the cluster tile's 128-row routes (every pair of
+                       // the cluster streams the same stages: the multicast operand is shared)
   __device__ bool lora() const { return col_hi > col_lo; }
 };
 
@@ -82,14 +83,15 @@ __device__ __forceinline__ LfRoute route_at(const GemmArgs& a, const LfRoute* s_
   return r < kSmemRoutes ? s_routes[r] : a.routes[r];
 }
 
+template <int NP>
 __device__ __forceinline__ TileInfo tile_info(const GemmArgs& a, const LfRoute* s_routes, int t) {
   TileInfo ti;
   gemm_tile_coords(t, a.tiles_m, a.tiles_n, a.group, ti.mb, ti.nb);
   ti.col_lo = ti.col_hi = 0;
   if (a.routes && !(a.segs.debug & 2048)) {
     const int tiles128 = (a.M + 127) / 128;
-    for (int h = 0; h < 2; ++h) {
-      const int r = 2 * ti.mb + h;
+    for (int h = 0; h < 2 * NP; ++h) {
+      const int r = 2 * NP * ti.mb + h;
       if (r >= tiles128) break;
       const LfRoute rt = route_at(a, s_routes, r);
       if (rt.col_hi <= rt.col_lo) continue;
@@ -148,32 +150,34 @@ __device__ __forceinline__ uint32_t dgrad_keep32(const LfSegTable& t, int seg, i
 // 2 producers, the MMA warp, 16 epilogue warps). Only the leader's producer requests, and
 // only after the previous response named a tile, so no request is left unread at exit.
 // Static (operands that fit in L2 together, or LF_SCHED=1): tile i = pair + i * npairs.
+template <int CL>
 struct TileSeq {
   uint64_t* full;   // [kSeqDepth] per CTA: response landed
-  uint64_t* empty;  // [kSeqDepth] leader: all readers done
+  uint64_t* empty;  // [kSeqDepth] cluster rank 0: all readers done
   uint8_t* resp;    // [kSeqDepth][16]
-  int pair, npairs, tiles;
+  int cluster, nclusters, tiles;
   bool dynamic;
 
-  static constexpr uint32_t kReaders = 19;  // 2 producers + the MMA warp + 2 x 8 epilogue warps
+  // every CTA's producer, each pair leader's MMA warp, every CTA's 8 epilogue warps
+  static constexpr uint32_t kReaders = CL * (1 + kEpiWarps) + CL / 2;
 
-  __device__ int first() const { return pair < tiles ? pair : -1; }
-  // leader producer only: ask for response i
+  __device__ int first() const { return cluster < tiles ? cluster : -1; }
+  // cluster rank 0's producer only: ask for response i
   __device__ void request(int i) const {
     if (!dynamic) return;
     const int slot = (i - 1) % kSeqDepth;
     const uint32_t ph = (uint32_t)((i - 1) / kSeqDepth) & 1u;
     mbar_wait(&empty[slot], ph ^ 1u);
     const uint32_t fb = smem_u32(&full[slot]);
-    mbar_arrive_expect_tx_cluster(mapa_shared(fb, 0), 16);
-    mbar_arrive_expect_tx_cluster(mapa_shared(fb, 1), 16);
+#pragma unroll
+    for (int c = 0; c < CL; ++c) mbar_arrive_expect_tx_cluster(mapa_shared(fb, c), 16);
     clc_try_cancel_multicast(smem_u32(resp + 16 * slot), fb);
   }
   // every reader: tile of response i (waits for it), or -1 when the grid is exhausted.
   // Warp-wide readers call it with the whole warp; `arrive` = the one lane that releases.
   __device__ int read(int i, bool arrive) const {
     if (!dynamic) {
-      const int t = pair + i * npairs;
+      const int t = cluster + i * nclusters;
       return t < tiles ? t : -1;
     }
     const int slot = (i - 1) % kSeqDepth;
@@ -182,29 +186,35 @@ struct TileSeq {
     const int x = clc_first_ctaid_x(smem_u32(resp + 16 * slot));
     fence_proxy_async_smem();  // the next response into this slot is an async-proxy write
     if (arrive) mbar_arrive_cluster(mapa_shared(smem_u32(&empty[slot]), 0));
-    return x < 0 ? -1 : (x >> 1);
+    return x < 0 ? -1 : (x / CL);
   }
 };
 
-template <bool B_MN, bool MASKED, int STAGES, bool WIDE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+// CL = CTAs per cluster: 2 = one CTA pair; 4 = two pairs stacked along M (cluster tile
+// 512 x BN) that share the B operand — the pair-0 CTAs TMA-load each B tile once and
+// multicast it into both pairs' shared memory (half the B reads from L2 per FLOP), and every
+// pair leader's MMA commit releases the stage in all four CTAs.
+template <bool B_MN, bool MASKED, int STAGES, bool WIDE, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
     lf_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                    const __grid_constant__ GemmArgs args) {
   using Cfg = GemmCfg<B_MN, STAGES, WIDE>;
   constexpr int BN = Cfg::BN, HBN = Cfg::HBN, NH = Cfg::NH, NACC = Cfg::NACC;
+  constexpr int NP = CL / 2;                                    // CTA pairs per cluster
+  constexpr uint16_t kAllCtas = (uint16_t)((1u << CL) - 1u);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);  // leader: both halves landed
-  uint64_t* empty = full + STAGES;   // both CTAs: stage consumed (multicast commit)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);  // pair leader: both halves landed
+  uint64_t* empty = full + STAGES;   // every CTA: stage consumed by every pair (multicast commits)
   uint64_t* tfull = empty + STAGES;  // [2] both CTAs: main loop done
   uint64_t* tempty = tfull + 2;      // [2] leader: both CTAs drained the accumulator (16 warps)
   uint64_t* lfull = tempty + 2;      // [2] both CTAs: LoRA partial ready                 MASKED
   uint64_t* lmasked = lfull + 2;     // [2] leader: both CTAs masked their partial (16)  MASKED
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lmasked + 2);
   uint8_t* ctl = smem + STAGES * Cfg::STAGE_BYTES;
-  TileSeq seq;
+  TileSeq<CL> seq;
   seq.full = reinterpret_cast<uint64_t*>(ctl + 192);
   seq.empty = seq.full + kSeqDepth;
   seq.resp = ctl + 320;
@@ -213,13 +223,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1u;        // rank within the CTA pair
+  const uint32_t pid = crank >> 1;         // pair index within the cluster
+  const uint32_t lrank = crank & ~1u;      // cluster rank of this pair's leader
+  const bool leader = rank == 0;           // pair leader: issues the pair's MMAs
+  const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pid));
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], NP);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -229,7 +243,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
     for (int i = 0; i < kSeqDepth; ++i) {
       mbar_init(&seq.full[i], 1);
-      mbar_init(&seq.empty[i], TileSeq::kReaders);
+      mbar_init(&seq.empty[i], TileSeq<CL>::kReaders);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmA);
@@ -252,8 +266,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int tiles = args.tiles_m * args.tiles_n;
-  seq.pair = blockIdx.x >> 1;
-  seq.npairs = gridDim.x >> 1;
+  seq.cluster = blockIdx.x / CL;
+  seq.nclusters = gridDim.x / CL;
   seq.tiles = tiles;
   seq.dynamic = args.dynamic != 0;
   const int nkb = (args.K + Cfg::BK - 1) / Cfg::BK;
@@ -267,8 +281,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      const int row_half = (int)rank * Cfg::BM;  // this CTA's rows of the 256-row tile
-      const int col_half = (int)rank * HBN;      // this CTA's columns of the 256-column tile
+      const int row_half = (int)rank * Cfg::BM;  // this CTA's rows of its pair's 256-row tile
+      // B (the operand every pair of the cluster shares): loaded by the pair-0 CTAs only, into
+      // the same-rank CTA of every pair
+      const bool loads_b = pid == 0;
+      const uint16_t b_mask = (uint16_t)(((1u << CL) - 1u) & (0x5555u << rank));
+      auto load_b = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
+        if constexpr (CL == 2) {
+          tma_load_2d_pair(dst, map, &full[stage], c0, c1);
+        } else {
+          if (loads_b) tma_load_2d_pair_mc(dst, map, &full[stage], c0, c1, b_mask);
+        }
+      };
       auto begin_stage = [&](uint32_t bytes) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (leader) mbar_arrive_expect_tx(&full[stage], 2 * bytes);
@@ -277,19 +301,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         begin_stage(Cfg::STAGE_BYTES);
         uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
         uint8_t* sB = sA + Cfg::A_BYTES;
-        tma_load_2d_pair(sA, &tmA, &full[stage], kb * Cfg::BK, ti.mb * 256 + row_half);
+        tma_load_2d_pair(sA, &tmA, &full[stage], kb * Cfg::BK, (ti.mb * NP + (int)pid) * 256 + row_half);
         if constexpr (!B_MN) {
           // N piece h of this CTA: rows h*256 + rank*128 of the pair tile's columns
 #pragma unroll
           for (int h = 0; h < NH; ++h)
-            tma_load_2d_pair(sB + h * 16384, &tmB, &full[stage], kb * Cfg::BK, ti.nb * BN + h * 256 + (int)rank * 128);
+            load_b(sB + h * 16384, &tmB, kb * Cfg::BK, ti.nb * BN + h * 256 + (int)rank * 128);
         } else {
 #pragma unroll
           for (int h = 0; h < NH; ++h)
 #pragma unroll
             for (int i = 0; i < 2; ++i)  // 128 MN-major columns = two 64-column SW128 boxes
-              tma_load_2d_pair(sB + h * 16384 + i * 8192, &tmB, &full[stage],
-                               ti.nb * BN + h * 256 + (int)rank * 128 + 64 * i, kb * Cfg::BK);
+              load_b(sB + h * 16384 + i * 8192, &tmB, ti.nb * BN + h * 256 + (int)rank * 128 + 64 * i,
+                     kb * Cfg::BK);
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       };
@@ -300,35 +324,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sB = sA + Cfg::A_BYTES;
           for (int j = 0; j < nsub; ++j) {
-            tma_load_2d_pair(sA + j * (Cfg::BM * 32), &tmA2, &full[stage], c + 16 * j, ti.mb * 256 + row_half);
+            tma_load_2d_pair(sA + j * (Cfg::BM * 32), &tmA2, &full[stage], c + 16 * j,
+                             (ti.mb * NP + (int)pid) * 256 + row_half);
             if constexpr (!B_MN) {
 #pragma unroll
               for (int h = 0; h < NH; ++h)
-                tma_load_2d_pair(sB + (j * NH + h) * 4096, &tmB2, &full[stage], c + 16 * j,
-                                 ti.nb * BN + h * 256 + (int)rank * 128);
+                load_b(sB + (j * NH + h) * 4096, &tmB2, c + 16 * j, ti.nb * BN + h * 256 + (int)rank * 128);
             } else {
 #pragma unroll
               for (int h = 0; h < NH; ++h)
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
-                  tma_load_2d_pair(sB + (j * NH + h) * 4096 + i * 2048, &tmB2, &full[stage],
-                                   ti.nb * BN + h * 256 + (int)rank * 128 + 64 * i, c + 16 * j);
+                  load_b(sB + (j * NH + h) * 4096 + i * 2048, &tmB2, ti.nb * BN + h * 256 + (int)rank * 128 + 64 * i,
+                         c + 16 * j);
             }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       };
       int t = seq.first();
-      if (leader && t >= 0) seq.request(1);
+      if (crank == 0 && t >= 0) seq.request(1);
       for (int i = 0; t >= 0; ++i) {
-        const TileInfo ti = tile_info(args, s_routes, t);
+        const TileInfo ti = tile_info<NP>(args, s_routes, t);
         int tn;
         if constexpr (MASKED && WIDE) {
           // one accumulator: each tile's own LoRA block first, then its main loop
           if (ti.lora()) load_lora(ti);
           for (int kb = 0; kb < nkb; ++kb) load_main(ti, kb);
           tn = seq.read(i + 1, true);
-          if (leader && tn >= 0) seq.request(i + 2);
+          if (crank == 0 && tn >= 0) seq.request(i + 2);
         } else if constexpr (MASKED) {
           if (i == 0 && ti.lora()) load_lora(ti);
           // the next tile's LoRA block goes in half-way through this tile's main loop
@@ -336,9 +360,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           int kb = 0;
           for (; kb < split; ++kb) load_main(ti, kb);
           tn = seq.read(i + 1, true);
-          if (leader && tn >= 0) seq.request(i + 2);
+          if (crank == 0 && tn >= 0) seq.request(i + 2);
           if (tn >= 0) {
-            const TileInfo tni = tile_info(args, s_routes, tn);
+            const TileInfo tni = tile_info<NP>(args, s_routes, tn);
             if (tni.lora()) load_lora(tni);
           }
           for (; kb < nkb; ++kb) load_main(ti, kb);
@@ -346,7 +370,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           for (int kb = 0; kb < nkb; ++kb) load_main(ti, kb);
           if (ti.lora()) load_lora(ti);
           tn = seq.read(i + 1, true);
-          if (leader && tn >= 0) seq.request(i + 2);
+          if (crank == 0 && tn >= 0) seq.request(i + 2);
         }
         t = tn;
       }
@@ -373,7 +397,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             umma_bf16_pair_warp(d + h * 256, sdesc_add(ad0, kk * 32),
                                 sdesc_add(bd0, (B_MN ? kk * 2048 : kk * 32) + h * 16384), idesc,
                                 (acc_any || (kb | kk) != 0) ? 1u : 0u);
-        umma_commit_pair_warp(&empty[stage]);
+        umma_commit_pair_warp_mask(&empty[stage], kAllCtas);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       };
       auto mma_lora = [&](const TileInfo& ti, uint32_t d, bool acc_any) {
@@ -393,7 +417,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             }
             accum = 1u;
           }
-          umma_commit_pair_warp(&empty[stage]);
+          umma_commit_pair_warp_mask(&empty[stage], kAllCtas);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       };
@@ -403,11 +427,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&tempty[acc], ((it / NACC) & 1) ^ 1);
         tc_fence_after();
         mma_lora(ti, tmem_base + acc * Cfg::ACC_COLS, false);
-        umma_commit_pair_warp(&lfull[acc]);
+        umma_commit_pair_warp_mask(&lfull[acc], pair_mask);
       };
       int t = seq.first();
       for (int it = 0; t >= 0; ++it) {
-        const TileInfo ti = tile_info(args, s_routes, t);
+        const TileInfo ti = tile_info<NP>(args, s_routes, t);
         const int acc = it % NACC;
         const uint32_t d = tmem_base + acc * Cfg::ACC_COLS;
         int tn = -1;
@@ -418,7 +442,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           tc_fence_after();
           if (ti.lora()) {
             mma_lora(ti, d, false);
-            umma_commit_pair_warp(&lfull[acc]);
+            umma_commit_pair_warp_mask(&lfull[acc], pair_mask);
             uint32_t& lu = lora_uses0;
             mbar_wait(&lmasked[acc], lu & 1);
             ++lu;
@@ -442,7 +466,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           tn = seq.read(it + 1, lane_id() == 0);
           have_tn = true;
           if (tn >= 0) {
-            const TileInfo tni = tile_info(args, s_routes, tn);
+            const TileInfo tni = tile_info<NP>(args, s_routes, tn);
             if (tni.lora()) issue_lora_first(tni, it + 1);
           }
           for (; kb < nkb; ++kb) mma_main_block(d, kb, acc_any);
@@ -452,7 +476,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           for (int kb = 0; kb < nkb; ++kb) mma_main_block(d, kb, false);
           if (ti.lora()) mma_lora(ti, d, true);
         }
-        umma_commit_pair_warp(&tfull[acc]);
+        umma_commit_pair_warp_mask(&tfull[acc], pair_mask);
         if (!have_tn) tn = seq.read(it + 1, lane_id() == 0);
         t = tn;
       }
@@ -464,9 +488,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     // the ⑤ mask pass run at twice the width (short-K tiles were bound by them)
     const uint32_t q = warp & 3u;  // TMEM lane quadrant this warp may access
     const int c_lo = (warp >= 6 ? 1 : 0) * (BN / 2), c_hi = c_lo + BN / 2;
-    const uint32_t tempty_leader[2] = {mapa_shared(smem_u32(&tempty[0]), 0), mapa_shared(smem_u32(&tempty[1]), 0)};
-    const uint32_t lmasked_leader[2] = {mapa_shared(smem_u32(&lmasked[0]), 0),
-                                        mapa_shared(smem_u32(&lmasked[1]), 0)};
+    const uint32_t tempty_leader[2] = {mapa_shared(smem_u32(&tempty[0]), lrank),
+                                       mapa_shared(smem_u32(&tempty[1]), lrank)};
+    const uint32_t lmasked_leader[2] = {mapa_shared(smem_u32(&lmasked[0]), lrank),
+                                        mapa_shared(smem_u32(&lmasked[1]), lrank)};
+    // first row of this CTA's 128 rows of cluster tile `ti`
+    auto cta_row0 = [&](const TileInfo& ti) { return (ti.mb * NP + (int)pid) * 256 + (int)rank * Cfg::BM; };
     uint32_t lora_uses0 = 0, lora_uses1 = 0;
     // MASKED: zero the dropped elements of tile `it`'s LoRA partial in place
     // keep bits of this thread's row over its columns [c_lo, c_hi) of tile `ti` (global
@@ -477,10 +504,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     };
     auto fetch_keep = [&](const TileInfo& ti) {
       RowKeep rk;
-      const int row = ti.mb * 256 + (int)rank * Cfg::BM + (int)(q * 32 + lane);
+      const int row = cta_row0(ti) + (int)(q * 32 + lane);
       int seg = -1;
       if (row < args.M) {
-        const LfRoute rt = route_at(args, s_routes, 2 * ti.mb + (int)rank);
+        const LfRoute rt = route_at(args, s_routes, 2 * (ti.mb * NP + (int)pid) + (int)rank);
         seg = find_segment(args.segs, rt.seg_lo, rt.seg_hi, row);
       }
       rk.active = seg >= 0 && (args.segs.mask_mode == 2 || args.segs.seg[seg].thr != 0);
@@ -529,16 +556,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       // stores wait until tile i+1's mask pass has released the MMA.
       int t = seq.first();
       if (t >= 0) {
-        const TileInfo t0 = tile_info(args, s_routes, t);
+        const TileInfo t0 = tile_info<NP>(args, s_routes, t);
         if (t0.lora()) mask_pass(t0, 0);
       }
       for (int it = 0; t >= 0; ++it) {
-        const TileInfo ti = tile_info(args, s_routes, t);
+        const TileInfo ti = tile_info<NP>(args, s_routes, t);
         const int tn = seq.read(it + 1, lane == 0);
-        const bool next_lora = tn >= 0 && tile_info(args, s_routes, tn).lora();
+        const bool next_lora = tn >= 0 && tile_info<NP>(args, s_routes, tn).lora();
         RowKeep nk;
-        if (next_lora) nk = fetch_keep(tile_info(args, s_routes, tn));
-        const int row = ti.mb * 256 + (int)rank * Cfg::BM + (int)(q * 32 + lane);
+        if (next_lora) nk = fetch_keep(tile_info<NP>(args, s_routes, tn));
+        const int row = cta_row0(ti) + (int)(q * 32 + lane);
         mbar_wait(&tfull[0], (uint32_t)it & 1u);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((q * 32u) << 16);
@@ -569,7 +596,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     } else {
     int t = seq.first();
     for (int it = 0; t >= 0; ++it) {
-      const TileInfo ti = tile_info(args, s_routes, t);
+      const TileInfo ti = tile_info<NP>(args, s_routes, t);
       const int acc = it % NACC;
       const uint32_t aph = (it / NACC) & 1;
       int tn = -1;
@@ -577,11 +604,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if (it == 0 && ti.lora()) mask_pass(ti, 0);
         tn = seq.read(it + 1, lane == 0);
         if (tn >= 0) {
-          const TileInfo tni = tile_info(args, s_routes, tn);
+          const TileInfo tni = tile_info<NP>(args, s_routes, tn);
           if (tni.lora()) mask_pass(tni, it + 1);
         }
       }
-      const int row = ti.mb * 256 + (int)rank * Cfg::BM + (int)(q * 32 + lane);
+      const int row = cta_row0(ti) + (int)(q * 32 + lane);
       const int n0 = ti.nb * BN;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
@@ -651,21 +678,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-template <bool B_MN, bool MASKED, int STAGES, bool WIDE = false>
+template <bool B_MN, bool MASKED, int STAGES, bool WIDE, int CL>
 static int launch_one(const GemmMaps& maps, const GemmArgs& args, int num_sms, cudaStream_t stream) {
   using Cfg = GemmCfg<B_MN, STAGES, WIDE>;
-  auto kern = lf_gemm_kernel<B_MN, MASKED, STAGES, WIDE>;
-  static bool configured = false;  // per instantiation; attribute set is idempotent
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) != cudaSuccess)
-      return -1;
-    configured = true;
-  }
+  auto kern = lf_gemm_kernel<B_MN, MASKED, STAGES, WIDE, CL>;
+  static std::atomic<uint64_t> attr_done{0};  // per instantiation, per device
+  if (ensure_smem_attr(kern, Cfg::SMEM_BYTES, attr_done)) return -1;
   const int tiles = args.tiles_m * args.tiles_n;
-  // dynamic: one cluster per tile (the resident pairs take over the rest through CLC);
-  // static (A/B measurements only): one persistent pair per SM pair, round-robin tiles
-  const int pairs = args.dynamic ? tiles : (tiles < num_sms / 2 ? tiles : num_sms / 2);
-  if (launch_k(kern, dim3(2 * pairs), dim3(kGemmThreads), Cfg::SMEM_BYTES, stream, maps.a, maps.b, maps.a2, maps.b2, args))
+  // dynamic: one cluster per tile (the resident clusters take over the rest through CLC);
+  // static: one persistent cluster per CL SMs, round-robin tiles
+  const int clusters = args.dynamic ? tiles : (tiles < num_sms / CL ? tiles : num_sms / CL);
+  if (launch_k(kern, dim3(CL * clusters), dim3(kGemmThreads), Cfg::SMEM_BYTES, stream, maps.a, maps.b, maps.a2,
+               maps.b2, args))
     return -1;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
@@ -685,9 +709,6 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
   const bool wide_fit = (int64_t)((args.M + 255) / 256) * ((args.N + 511) / 512) >= 4 * (num_sms / 2) &&
                         args.K >= min_k;
   const bool wide = wide_env >= 0 ? wide_env == 1 : wide_fit;
-  args.tiles_m = (args.M + 255) / 256;
-  args.tiles_n = wide ? (args.N + 511) / 512 : (args.N + 255) / 256;
-  if (args.group <= 0) args.group = 8;
   // Tile schedule. While both operands fit in L2 together, the static persistent
   // round-robin is ~5% faster (C2 q/kv, C1: no per-tile CLC round trip and the pairs'
   // drift costs nothing); beyond that, drifting pairs re-read their operands from DRAM
@@ -696,17 +717,28 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
   static const int sched_env = [] { const char* e = getenv("LF_SCHED"); return e ? atoi(e) : 0; }();
   const double operand_bytes = 2.0 * ((double)args.M + (double)args.N) * (double)args.K;
   args.dynamic = sched_env == 1 ? 0 : sched_env == 2 ? 1 : (operand_bytes > 128.0 * (1 << 20) ? 1 : 0);
+  // Two CTA pairs per cluster sharing B by TMA multicast (LF_CL=4; parity-green, off by
+  // default): it cuts the power drawn per FLOP (C4 gate: 1.37 -> 1.47 GHz under the cap) but
+  // a B200 holds only 33 four-CTA clusters at one CTA per SM — 132 of 148 SMs; pairs use
+  // all 148 (tools/cluster_occupancy.cu) — so every shape measured slower end to end
+  // (C4 step 42.0 -> 46.4 ms, C2 5.67 -> 6.56 ms; profiles/r02_cluster_multicast_ab.txt)
+  static const int cl_env = [] { const char* e = getenv("LF_CL"); return e ? atoi(e) : 0; }();
+  const bool cl4 = cl_env == 4;
+  args.tiles_m = cl4 ? (args.M + 511) / 512 : (args.M + 255) / 256;
+  args.tiles_n = wide ? (args.N + 511) / 512 : (args.N + 255) / 256;
+  if (args.group <= 0) args.group = cl4 ? 4 : 8;
+#define LF_GEMM_LAUNCH(BMN, MSK, ST, WD)                                                        \
+  (cl4 ? launch_one<BMN, MSK, ST, WD, 4>(maps, args, num_sms, stream)                          \
+       : launch_one<BMN, MSK, ST, WD, 2>(maps, args, num_sms, stream))
   switch (kind) {
     case kGemmFwd:
-      return wide ? launch_one<false, false, 4, true>(maps, args, num_sms, stream)
-                  : launch_one<false, false, 6>(maps, args, num_sms, stream);
+      return wide ? LF_GEMM_LAUNCH(false, false, 4, true) : LF_GEMM_LAUNCH(false, false, 6, false);
     case kGemmDgrad:
-      return wide ? launch_one<true, false, 4, true>(maps, args, num_sms, stream)
-                  : launch_one<true, false, 6>(maps, args, num_sms, stream);
+      return wide ? LF_GEMM_LAUNCH(true, false, 4, true) : LF_GEMM_LAUNCH(true, false, 6, false);
     case kGemmDgradMasked:
-      return wide ? launch_one<true, true, 4, true>(maps, args, num_sms, stream)
-                  : launch_one<true, true, 6>(maps, args, num_sms, stream);
+      return wide ? LF_GEMM_LAUNCH(true, true, 4, true) : LF_GEMM_LAUNCH(true, true, 6, false);
   }
+#undef LF_GEMM_LAUNCH
   return -1;
 }
 

@@ -13,7 +13,12 @@ import sys
 METRICS = {
     "dur_us": ("gpu__time_duration.sum", {"ns": 1e-3, "nsecond": 1e-3, "us": 1, "usecond": 1, "ms": 1e3, "msecond": 1e3}),
     "sm_clock_ghz": ("sm__cycles_elapsed.avg.per_second", {"Ghz": 1, "GHz": 1, "Mhz": 1e-3, "MHz": 1e-3}),
-    "tensor_pipe_active_pct": ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", {}),
+    # the tensor-pipe utilisation (B200_PROFILING.md): cycles the tcgen05 pipe is busy over elapsed cycles
+    "tensor_pipe_active_pct": ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", {}),
+    # kept for reference only: the TPC triage section's realtime counter (reads ~half of the
+    # above on the 2-CTA MMAs — it is not the utilisation figure)
+    "tpc_triage_tensor_realtime_pct": ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", {}),
+    "mem_tensor_active_pct": ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", {}),
     "sm_throughput_pct": ("sm__throughput.avg.pct_of_peak_sustained_elapsed", {}),
     "dram_throughput_pct": ("dram__throughput.avg.pct_of_peak_sustained_elapsed", {}),
     "l2_throughput_pct": ("lts__throughput.avg.pct_of_peak_sustained_elapsed", {}),
