@@ -406,12 +406,44 @@ def adapter_params(layers):
     return [p for nm in layers for p in layers[nm].parameters() if p.requires_grad]
 
 
+# projections that read the same input in a decoder layer: run as one FusedLoRAGroup
+# (SURVEY §8(f)#4 — the input gradient is summed inside the ⑤ GEMM epilogues)
+SHARED_INPUT_GROUPS = ("attn", "mlp")
+GROUPED = True  # --no-group: every projection as its own FusedLoRA call
+_UNITS: dict = {}
+
+
+def step_units(config: str, layers: dict):
+    """How one step calls the layers: [(group input, [names], module or FusedLoRAGroup)]."""
+    from paper_2510_00206_b200 import FusedLoRAGroup
+
+    cache = _UNITS
+    key = (id(layers), config, GROUPED)
+    if key not in cache:
+        units, by_grp = [], {}
+        for name, k, n, grp in projections(config):
+            by_grp.setdefault(grp, []).append(name)
+        for grp, names in by_grp.items():
+            if GROUPED and config != "c3" and grp in SHARED_INPUT_GROUPS and len(names) > 1:
+                units.append((grp, names, FusedLoRAGroup.from_layers({nm: layers[nm] for nm in names})))
+            else:
+                units.extend((grp, [nm], layers[nm]) for nm in names)
+        cache[key] = units
+    return cache[key]
+
+
 def fused_step(config, layers, inputs, grads, world, flat_grad=None):
     """fwd+bwd of every projection through the public module API; grads all-reduced if world>1."""
+    import torch
+
     call = layer_call(config)
-    for name, k, n, grp in projections(config):
-        y = call(layers[name], inputs[grp])
-        y.backward(grads[name])
+    for grp, names, mod in step_units(config, layers):
+        if len(names) > 1:
+            ys = mod(inputs[grp])
+            torch.autograd.backward(ys, [grads[nm] for nm in names])
+        else:
+            y = call(mod, inputs[grp])
+            y.backward(grads[names[0]])
     if world > 1:
         allreduce_grads(layers)
 
@@ -768,55 +800,62 @@ def measure_c3(args, device, gen, world, barrier, max_over_ranks):
 
 def run_e2e(args, layers, inputs, grads, device, world, barrier, max_over_ranks):
     """Same step through the module API, with every input copied H2D from pinned host
-    memory (copy stream, overlapped with compute) and all adapter grads read back D2H."""
+    memory and all adapter grads read back D2H. The copies run on a copy stream into two
+    alternating sets of device buffers, so step i+1's inputs cross PCIe while step i
+    computes (the copy engine, not the SMs, bounds this leg: ~1.1 GB per C2 step)."""
     import torch
 
     host_in = {g: t.detach().cpu().pin_memory() for g, t in inputs.items()}
     host_dy = {nm: t.cpu().pin_memory() for nm, t in grads.items()}
-    dev_in = {g: torch.empty_like(t) for g, t in inputs.items()}
-    dev_dy = {nm: torch.empty_like(t) for nm, t in grads.items()}
+    bufs = [({g: torch.empty_like(t) for g, t in inputs.items()}, {nm: torch.empty_like(t) for nm, t in grads.items()})
+            for _ in range(2)]
+    done = [torch.cuda.Event(), torch.cuda.Event()]  # compute finished with buffer set i
     params = adapter_params(layers)
     call = layer_call(args.config)
     host_out = torch.empty(sum(p.numel() for p in params), dtype=torch.float32).pin_memory()
     copy = torch.cuda.Stream(device)
-    order = projections(args.config)
+    units = step_units(args.config, layers)
     h2d = sum(t.numel() * t.element_size() for t in host_in.values()) + \
         sum(t.numel() * t.element_size() for t in host_dy.values())
     d2h = host_out.numel() * 4
+    it = [0]
 
     def step():
+        b = it[0] & 1
+        it[0] += 1
+        dev_in, dev_dy = bufs[b]
         zero_grads(layers)
         ready = {}
+        cur = torch.cuda.current_stream(device)
         with torch.cuda.stream(copy):
-            for name, k, n, grp in order:
+            copy.wait_event(done[b])  # the step that last read this buffer set is done with it
+            for grp, names, _mod in units:
                 if grp not in ready:
                     dev_in[grp].copy_(host_in[grp], non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record(copy)
-                    ready[grp] = ev
-                dev_dy[name].copy_(host_dy[name], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(copy)
-                ready[name] = ev
-        cur = torch.cuda.current_stream(device)
+                    ready[grp] = torch.cuda.Event()
+                    ready[grp].record(copy)
+                for nm in names:
+                    dev_dy[nm].copy_(host_dy[nm], non_blocking=True)
+                    ready[nm] = torch.cuda.Event()
+                    ready[nm].record(copy)
         leaves = {}
-        for name, k, n, grp in order:
+        for grp, names, mod in units:
             cur.wait_event(ready[grp])
-            cur.wait_event(ready[name])
+            for nm in names:
+                cur.wait_event(ready[nm])
             if grp not in leaves:  # activation leaf: dX is computed as in a real layer
                 leaves[grp] = dev_in[grp].detach().requires_grad_(True)
-            y = call(layers[name], leaves[grp])
-            y.backward(dev_dy[name])
+            if len(names) > 1:
+                torch.autograd.backward(mod(leaves[grp]), [dev_dy[nm] for nm in names])
+            else:
+                call(mod, leaves[grp]).backward(dev_dy[names[0]])
+        done[b].record(cur)
+        flat = torch.cat([p.grad.reshape(-1) for p in params])
         if world > 1:
             import torch.distributed as dist
 
-            flat = torch.cat([p.grad.reshape(-1) for p in params])
             dist.all_reduce(flat)
-        else:
-            flat = torch.cat([p.grad.reshape(-1) for p in params])
         host_out.copy_(flat, non_blocking=True)
-        # the copy stream must not overwrite inputs of this step before compute used them
-        copy.wait_stream(cur)
 
     ms = time_loop(step, max(2, args.steps // 2), args.warmup, barrier)
     ms = max_over_ranks(ms)
@@ -1013,6 +1052,8 @@ def main() -> None:
                     help="tokens per GPU (default: the config's; e.g. --config c4 --tokens 2048 = the per-rank "
                          "load of C4's 16384-token strong scaling at 8 GPUs)")
     ap.add_argument("--no-multi", action="store_true", help="skip the secondary C3 FusedMultiLoRA measurement")
+    ap.add_argument("--group", action=argparse.BooleanOptionalAction, default=True,
+                    help="q/k/v and gate/up as FusedLoRAGroup calls (shared input; default) or separate layers")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dropout", type=float, default=0.1)
     ap.add_argument("--cpu-sample-tokens", type=int, default=256)
@@ -1022,6 +1063,8 @@ def main() -> None:
                     help="time the step as one captured CUDA graph (default) or eagerly")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    global GROUPED
+    GROUPED = args.group
     if args.tokens:
         global TOKENS_OVERRIDE
         TOKENS_OVERRIDE = args.tokens

@@ -49,7 +49,7 @@ extern "C" {
 #define LF_API
 #endif
 
-#define LF_ABI_VERSION 3
+#define LF_ABI_VERSION 4
 #define LF_MAX_SEGMENTS 32
 #define LF_MAX_RANK_TOTAL 128
 #define LF_ROUTE_TILE_ROWS 128 /* ls/costmodel.py:25 ROUTING_TILE_ROWS */
@@ -128,6 +128,14 @@ LF_API int lf_grad_down(const LfProblem* p, const uint16_t* x, const uint16_t* d
 /* ⑤ dx = dY·W + M ⊙ (dŜ·A_cat), written once. */
 LF_API int lf_grad_input(const LfProblem* p, const uint16_t* dy, const uint16_t* w, const uint16_t* ds,
                   const uint16_t* a_cat, uint16_t* dx, void* stream);
+
+/* ⑤ accumulating: dx += dY·W + M ⊙ (dŜ·A_cat) — dx (bf16, m x k) is read and written once in
+ * the GEMM epilogue (fp32 sum, one bf16 rounding: what torch's add of the two bf16 tensors
+ * gives). Several projections that read the same input (q/k/v, gate/up: SURVEY §8(f)#4)
+ * sum their input gradients this way instead of through separate elementwise adds.
+ * ABI 4. */
+LF_API int lf_grad_input_accum(const LfProblem* p, const uint16_t* dy, const uint16_t* w, const uint16_t* ds,
+                        const uint16_t* a_cat, uint16_t* dx, void* stream);
 
 /* Materialise the keep mask (m x k uint8) of SPEC.md §3 — for explicit-mask callers and parity tests. */
 LF_API int lf_dropout_mask(const LfProblem* p, uint8_t* keep_out, void* stream);

@@ -2,6 +2,7 @@
 
 Public API
   FusedLoRA, FusedMultiLoRA          nn.Modules (PEFT parameter names lora_A / lora_B)
+  FusedLoRAGroup                     projections sharing one input (q/k/v, gate/up), dX summed in-GEMM
   fused_lora, fused_multi_lora       functional forms (autograd; torch.ops.lorafusion_b200.lora_fwd/_bwd)
   invalidate_operand_caches          forget cached bf16 adapter operands after out-of-optimizer updates
   AdapterConfig, Segment, LayerPlan  adapter hyper-parameters and microbatch segment tables
@@ -14,8 +15,8 @@ The compute path is the sm_100a shared library liblorafusion_b200.so (C ABI in
 include/lorafusion_b200.h). There is no CPU fallback.
 """
 from .errors import ExtensionMissingError, KernelError, LoRAFusionError, ValidationError
-from .functional import dropout_keep_mask, fused_lora, fused_multi_lora, invalidate_operand_caches
-from .modules import FusedLoRA, FusedMultiLoRA
+from .functional import dropout_keep_mask, fused_lora, fused_lora_group, fused_multi_lora, invalidate_operand_caches
+from .modules import FusedLoRA, FusedLoRAGroup, FusedMultiLoRA
 from .plan import AdapterConfig, LayerPlan, Segment, padded_rank, segments_from_lengths
 from .costmodel import (
     B200,
@@ -38,6 +39,7 @@ __all__ = [
     "B200",
     "ExtensionMissingError",
     "FusedLoRA",
+    "FusedLoRAGroup",
     "FusedMultiLoRA",
     "GemmShape",
     "H100_SXM",
@@ -54,6 +56,7 @@ __all__ = [
     "down_projection_intensity",
     "dropout_keep_mask",
     "fused_lora",
+    "fused_lora_group",
     "fused_multi_lora",
     "invalidate_operand_caches",
     "lora_memory_bytes",

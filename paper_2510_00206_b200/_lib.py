@@ -13,7 +13,7 @@ from pathlib import Path
 
 from .errors import ExtensionMissingError, KernelError, ValidationError
 
-LF_ABI_VERSION = 3
+LF_ABI_VERSION = 4
 LF_MAX_SEGMENTS = 32
 LF_MAX_RANK_TOTAL = 128
 ROUTE_TILE_ROWS = 128  # ls/costmodel.py:25
@@ -36,6 +36,7 @@ EXPORTED_SYMBOLS = (
     "lf_grad_up",
     "lf_grad_down",
     "lf_grad_input",
+    "lf_grad_input_accum",
     "lf_dropout_mask",
     "lf_keep_bits",
     "lf_last_error",
@@ -86,6 +87,7 @@ _SIGNATURES = {
     "lf_grad_up": (ctypes.c_int, [_P, _V, _V, _V, _V, _V, _V]),
     "lf_grad_down": (ctypes.c_int, [_P, _V, _V, _V, _V]),
     "lf_grad_input": (ctypes.c_int, [_P, _V, _V, _V, _V, _V, _V]),
+    "lf_grad_input_accum": (ctypes.c_int, [_P, _V, _V, _V, _V, _V, _V]),
     "lf_dropout_mask": (ctypes.c_int, [_P, _V, _V]),
     "lf_keep_bits": (ctypes.c_int, [_P, _V, _V]),
     "lf_last_error": (ctypes.c_char_p, []),

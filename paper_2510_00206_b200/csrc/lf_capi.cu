@@ -501,8 +501,8 @@ int lf_grad_down(const LfProblem* p, const uint16_t* x, const uint16_t* ds, floa
   return LF_OK;
 }
 
-int lf_grad_input(const LfProblem* p, const uint16_t* dy, const uint16_t* w, const uint16_t* ds,
-                  const uint16_t* a_cat, uint16_t* dx, void* stream) {
+static int grad_input_impl(const LfProblem* p, const uint16_t* dy, const uint16_t* w, const uint16_t* ds,
+                           const uint16_t* a_cat, uint16_t* dx, int accumulate, void* stream) {
   lf::LfSegTable t;
   LF_TRY(validate(p, true, &t));
   LF_TRY(check_ptr(dy, "dy"));
@@ -536,12 +536,23 @@ int lf_grad_input(const LfProblem* p, const uint16_t* dy, const uint16_t* w, con
   a.K = p->n;
   a.ldc = p->k;
   a.C = dx;
+  a.accumulate = accumulate;
   a.routes = lora ? reinterpret_cast<const lf::LfRoute*>(p->routes) : nullptr;
   a.segs = t;
   a.group = env_int("LF_GROUP", 0);
   if (lf::gemm_launch(masked ? lf::kGemmDgradMasked : lf::kGemmDgrad, maps, a, d.sms, (cudaStream_t)stream))
     return cuda_fail("grad_input launch");
   return LF_OK;
+}
+
+int lf_grad_input(const LfProblem* p, const uint16_t* dy, const uint16_t* w, const uint16_t* ds,
+                  const uint16_t* a_cat, uint16_t* dx, void* stream) {
+  return grad_input_impl(p, dy, w, ds, a_cat, dx, 0, stream);
+}
+
+int lf_grad_input_accum(const LfProblem* p, const uint16_t* dy, const uint16_t* w, const uint16_t* ds,
+                        const uint16_t* a_cat, uint16_t* dx, void* stream) {
+  return grad_input_impl(p, dy, w, ds, a_cat, dx, 1, stream);
 }
 
 }  // extern "C"

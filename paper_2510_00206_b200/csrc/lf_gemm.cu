@@ -139,6 +139,42 @@ __device__ __forceinline__ uint32_t dgrad_keep32(const LfSegTable& t, int seg, i
   return dgrad_keep32_slow(t, seg, row, col, ncols);
 }
 
+// `accumulate` (lf_grad_input_accum): C += result — the old bf16 values and the new ones are
+// summed in fp32 and rounded once, as torch adds two bf16 tensors (the input gradient of
+// projections that share X is summed by the GEMMs instead of separate elementwise adds).
+// The epilogue prefetches its rows of C into L2 before it waits for the accumulator, then
+// loads them in batches, so the read-modify-write costs no DRAM round trip per chunk.
+__device__ __forceinline__ uint4 add_bf16x8(uint4 v, uint4 o) {
+  const uint32_t a[4] = {v.x, v.y, v.z, v.w}, b[4] = {o.x, o.y, o.z, o.w};
+  uint32_t r[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a[i]));
+    const float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b[i]));
+    r[i] = pack_bf16x2(fa.x + fb.x, fa.y + fb.y);
+  }
+  return make_uint4(r[0], r[1], r[2], r[3]);
+}
+__device__ __forceinline__ uint4 ld_c8(const __nv_bfloat16* src) {
+  uint4 v;
+  asm volatile("ld.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src));
+  return v;
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+// L2 prefetch of `ncols` bf16 of one C row starting at `col` (128-byte lines)
+__device__ __forceinline__ void prefetch_c_row(const __nv_bfloat16* crow, int col, int ncols, int N) {
+  for (int c = col; c < col + ncols && c < N; c += 64) prefetch_l2(crow + c);
+}
+// one 16-byte chunk of C (the wide tiles' deferred stores hold 128 words of the tile in
+// registers already: one chunk at a time keeps the read-modify-write out of local memory;
+// the row is L2-hot from the prefetch)
+__device__ __forceinline__ void store_c8(__nv_bfloat16* dst, uint4 v, int accumulate) {
+  if (accumulate) v = add_bf16x8(v, ld_c8(dst));
+  *reinterpret_cast<uint4*>(dst) = v;
+}
+
 // Tile sequence of one CTA pair. Dynamic (default): the grid has one cluster per tile; a
 // pair starts on its own tile (blockIdx.x / 2) and then takes over not-yet-launched
 // clusters' tiles through cluster launch control, in launch order — the tiles in flight
@@ -194,7 +230,7 @@ struct TileSeq {
 // 512 x BN) that share the B operand — the pair-0 CTAs TMA-load each B tile once and
 // multicast it into both pairs' shared memory (half the B reads from L2 per FLOP), and every
 // pair leader's MMA commit releases the stage in all four CTAs.
-template <bool B_MN, bool MASKED, int STAGES, bool WIDE, int CL>
+template <bool B_MN, bool MASKED, int STAGES, bool WIDE, int CL, bool ACC>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
     lf_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
@@ -566,6 +602,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
         RowKeep nk;
         if (next_lora) nk = fetch_keep(tile_info<NP>(args, s_routes, tn));
         const int row = cta_row0(ti) + (int)(q * 32 + lane);
+        if (ACC && row < args.M)  // prefetch the rows this tile accumulates into
+          prefetch_c_row(reinterpret_cast<const __nv_bfloat16*>(args.C) + (int64_t)row * args.ldc, ti.nb * BN + c_lo,
+                         BN / 2, args.N);
         mbar_wait(&tfull[0], (uint32_t)it & 1u);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((q * 32u) << 16);
@@ -588,7 +627,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
           for (int c = 0; c < BN / 2; c += 8) {
             const int col = ti.nb * BN + c_lo + c;
             if (col < args.N)
-              *reinterpret_cast<uint4*>(crow + col) = make_uint4(pk[c / 2], pk[c / 2 + 1], pk[c / 2 + 2], pk[c / 2 + 3]);
+              store_c8(crow + col, make_uint4(pk[c / 2], pk[c / 2 + 1], pk[c / 2 + 2], pk[c / 2 + 3]), ACC);
           }
         }
         t = tn;
@@ -610,10 +649,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
       }
       const int row = cta_row0(ti) + (int)(q * 32 + lane);
       const int n0 = ti.nb * BN;
+      __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(args.C) + (int64_t)row * args.ldc;
+      if constexpr (ACC) if (row < args.M) prefetch_c_row(crow, n0 + c_lo, BN / 2, args.N);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * Cfg::ACC_COLS;
-      __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(args.C) + (int64_t)row * args.ldc;
       if constexpr (NACC == 1) {
         // single accumulator: the next tile's MMAs wait for it, so hand TMEM back as soon as
         // this warp's 256 columns sit in registers as bf16 (128 regs), then store them while
@@ -635,7 +675,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
           for (int c = 0; c < BN / 2; c += 8) {
             const int col = n0 + c_lo + c;
             if (col < args.N)
-              *reinterpret_cast<uint4*>(crow + col) = make_uint4(pk[c / 2], pk[c / 2 + 1], pk[c / 2 + 2], pk[c / 2 + 3]);
+              store_c8(crow + col, make_uint4(pk[c / 2], pk[c / 2 + 1], pk[c / 2 + 2], pk[c / 2 + 3]), ACC);
           }
         }
         if constexpr (!MASKED) tn = seq.read(it + 1, lane == 0);
@@ -644,11 +684,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
       }
 #pragma unroll 1
       for (int c = c_lo; c < c_hi; c += 32) {
+        const int col0 = n0 + c;
+        uint4 old[4];
+        if (ACC && row < args.M) {  // loads first (L2-hot: prefetched above)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (col0 + 8 * j < args.N) old[j] = ld_c8(crow + col0 + 8 * j);
+        }
         uint32_t v[32];
         tmem_ld32(taddr + c, v);
         tmem_ld_wait();
         if (row < args.M) {
-          const int col0 = n0 + c;
           uint4 pk[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j)
@@ -658,7 +704,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
                                pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (col0 + 8 * j < args.N) *reinterpret_cast<uint4*>(crow + col0 + 8 * j) = pk[j];
+            if (col0 + 8 * j < args.N)
+              *reinterpret_cast<uint4*>(crow + col0 + 8 * j) = ACC ? add_bf16x8(pk[j], old[j]) : pk[j];
         }
       }
       tc_fence_before();
@@ -678,10 +725,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-template <bool B_MN, bool MASKED, int STAGES, bool WIDE, int CL>
+template <bool B_MN, bool MASKED, int STAGES, bool WIDE, int CL, bool ACC = false>
 static int launch_one(const GemmMaps& maps, const GemmArgs& args, int num_sms, cudaStream_t stream) {
   using Cfg = GemmCfg<B_MN, STAGES, WIDE>;
-  auto kern = lf_gemm_kernel<B_MN, MASKED, STAGES, WIDE, CL>;
+  auto kern = lf_gemm_kernel<B_MN, MASKED, STAGES, WIDE, CL, ACC>;
   static std::atomic<uint64_t> attr_done{0};  // per instantiation, per device
   if (ensure_smem_attr(kern, Cfg::SMEM_BYTES, attr_done)) return -1;
   const int tiles = args.tiles_m * args.tiles_n;
@@ -730,6 +777,16 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
 #define LF_GEMM_LAUNCH(BMN, MSK, ST, WD)                                                        \
   (cl4 ? launch_one<BMN, MSK, ST, WD, 4>(maps, args, num_sms, stream)                          \
        : launch_one<BMN, MSK, ST, WD, 2>(maps, args, num_sms, stream))
+  // accumulating dgrads (lf_grad_input_accum) are their own instantiations: the C
+  // read-modify-write would otherwise cost the plain epilogues registers (the 256 x 512
+  // tiles hold 128 words of output per thread)
+#define LF_GEMM_LAUNCH_ACC(BMN, MSK, ST, WD) launch_one<BMN, MSK, ST, WD, 2, true>(maps, args, num_sms, stream)
+  if (args.accumulate) {
+    if (kind == kGemmFwd) return -1;
+    const bool masked = kind == kGemmDgradMasked;
+    return wide ? (masked ? LF_GEMM_LAUNCH_ACC(true, true, 4, true) : LF_GEMM_LAUNCH_ACC(true, false, 4, true))
+                : (masked ? LF_GEMM_LAUNCH_ACC(true, true, 6, false) : LF_GEMM_LAUNCH_ACC(true, false, 6, false));
+  }
   switch (kind) {
     case kGemmFwd:
       return wide ? LF_GEMM_LAUNCH(false, false, 4, true) : LF_GEMM_LAUNCH(false, false, 6, false);
@@ -738,6 +795,7 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
     case kGemmDgradMasked:
       return wide ? LF_GEMM_LAUNCH(true, true, 4, true) : LF_GEMM_LAUNCH(true, true, 6, false);
   }
+#undef LF_GEMM_LAUNCH_ACC
 #undef LF_GEMM_LAUNCH
   return -1;
 }

@@ -64,6 +64,7 @@ struct GemmArgs {
   int32_t dynamic;        // 1: CLC tile sequence (one cluster per tile), 0: static persistent
   int64_t ldc;
   void* C;                // bf16 output, row-major M x N (ldc elements)
+  int32_t accumulate;     // 1: C += result (bf16 read-modify-write in the epilogue)
   const LfRoute* routes;  // nullptr = no LoRA chunk
   LfSegTable segs;        // keep-mask source for kGemmDgradMasked
 };

@@ -381,6 +381,163 @@ def _backward(ctx, dy, _ds, _dbits):
 torch.library.register_autograd(f"{_NS}::lora_fwd", _backward, setup_context=_setup_context)
 
 
+# --------------------------------------------------------------------------------------
+# shared-input groups (SURVEY §8(f)#4): several LoRA linears reading the same X
+# --------------------------------------------------------------------------------------
+def _group_plan(j, x_rows, k, n, ranks, scalings, ps, seeds, offset, offset_dev, training) -> LayerPlan:
+    return _plan(x_rows, k, n, [ranks[j]], [scalings[j]], [ps[j]], [seeds[j]], [0, 0, x_rows, 0], offset, offset_dev,
+                 None, training, True, 0)
+
+
+@torch.library.custom_op(f"{_NS}::lora_group_fwd", mutates_args=(), device_types="cuda")
+def lora_group_fwd(x: torch.Tensor, ws: list[torch.Tensor], a: list[torch.Tensor], b: list[torch.Tensor],
+                   ranks: list[int], scalings: list[float], ps: list[float], seeds: list[int], offset: int,
+                   offset_dev: Optional[torch.Tensor], training: bool,
+                   cache_id: int) -> tuple[list[torch.Tensor], list[torch.Tensor], list[torch.Tensor]]:
+    """① + ② of every projection j (own adapter, seed and dropout mask, one shared Philox
+    offset): returns ([Y_j], [Ŝ_j], [packed keep mask_j or empty])."""
+    lib = _lib.load()
+    m, k = x.shape
+    st = _stream(x.device)
+    ys, shats, bits = [], [], []
+    for j, w in enumerate(ws):
+        plan = _group_plan(j, m, k, w.shape[0], ranks, scalings, ps, seeds, offset, offset_dev, training)
+        plan.bind(x.device)
+        pp = ctypes.byref(plan.problem)
+        a_cat, b_cat = _rank_concat_operands(plan, [a[j]], [b[j]], cache_id)
+        s_hat = torch.empty((m, plan.rank_total), dtype=_BF16, device=x.device)
+        y = torch.empty((m, w.shape[0]), dtype=_BF16, device=x.device)
+        _call("dropout_down_fwd", lib.lf_dropout_down_fwd, pp, _ptr(x), _ptr(a_cat), _ptr(s_hat), st)
+        _call("base_fwd", lib.lf_base_fwd, pp, _ptr(x), _ptr(w), _ptr(s_hat), _ptr(b_cat), _ptr(y), st)
+        ys.append(y)
+        shats.append(s_hat)
+        bits.append(plan.keep_bits if plan.keep_bits is not None
+                    else torch.empty((0,), dtype=torch.uint8, device=x.device))
+    return ys, shats, bits
+
+
+@lora_group_fwd.register_fake
+def _lora_group_fwd_fake(x, ws, a, b, ranks, scalings, ps, seeds, offset, offset_dev, training, cache_id):
+    m, k = x.shape
+    ys = [x.new_empty((m, w.shape[0])) for w in ws]
+    shats = [x.new_empty((m, -(-r // 16) * 16)) for r in ranks]
+    bits = [x.new_empty((m, k // 8), dtype=torch.uint8) if (training and p_ > 0) else
+            x.new_empty((0,), dtype=torch.uint8) for p_ in ps]
+    return ys, shats, bits
+
+
+@torch.library.custom_op(f"{_NS}::lora_group_bwd", mutates_args=(), device_types="cuda")
+def lora_group_bwd(dys: list[torch.Tensor], x: torch.Tensor, ws: list[torch.Tensor], a: list[torch.Tensor],
+                   b: list[torch.Tensor], shats: list[torch.Tensor], bits: list[torch.Tensor], ranks: list[int],
+                   scalings: list[float], ps: list[float], seeds: list[int], offset: int,
+                   offset_dev: Optional[torch.Tensor], training: bool, cache_id: int,
+                   need_dx: bool) -> tuple[torch.Tensor, list[torch.Tensor]]:
+    """③ + ④ + ⑤ of every projection: returns (dX = Σ_j dX_j, [dA_j | dB_j] fp32 flat per j).
+    The first ⑤ writes dX, the others add into it in their epilogues (lf_grad_input_accum):
+    no separate gradient-sum kernels."""
+    lib = _lib.load()
+    m, k = x.shape
+    st = _stream(x.device)
+    dx = torch.empty((m, k) if need_dx else (0,), dtype=_BF16, device=x.device)
+    daccs = []
+    for j, w in enumerate(ws):
+        n = w.shape[0]
+        plan = _group_plan(j, m, k, n, ranks, scalings, ps, seeds, offset, offset_dev, training)
+        plan.bind(x.device, keep_bits=bits[j])
+        pp = ctypes.byref(plan.problem)
+        R = plan.rank_total
+        a_cat, b_cat = _rank_concat_operands(plan, [a[j]], [b[j]], cache_id)
+        acc = torch.zeros(R * k + n * R, dtype=torch.float32, device=x.device)
+        ds = torch.empty((m, R), dtype=_BF16, device=x.device)
+        dy = dys[j]
+        _call("grad_up", lib.lf_grad_up, pp, _ptr(dy), _ptr(b_cat), _ptr(shats[j]), _ptr(ds), _ptr(acc[R * k:]), st)
+        _call("grad_down", lib.lf_grad_down, pp, _ptr(x), _ptr(ds), _ptr(acc[:R * k]), st)
+        if need_dx:
+            fn = lib.lf_grad_input if j == 0 else lib.lf_grad_input_accum
+            _call("grad_input", fn, pp, _ptr(dy), _ptr(w), _ptr(ds), _ptr(a_cat), _ptr(dx), st)
+        daccs.append(acc)
+    return dx, daccs
+
+
+@lora_group_bwd.register_fake
+def _lora_group_bwd_fake(dys, x, ws, a, b, shats, bits, ranks, scalings, ps, seeds, offset, offset_dev, training,
+                         cache_id, need_dx):
+    m, k = x.shape
+    dx = x.new_empty((m, k) if need_dx else (0,))
+    daccs = []
+    for r, w in zip(ranks, ws):
+        R = -(-r // 16) * 16
+        daccs.append(x.new_empty((R * k + w.shape[0] * R,), dtype=torch.float32))
+    return dx, daccs
+
+
+_GROUP_ARGS = ("ranks", "scalings", "ps", "seeds", "offset", "offset_dev", "training", "cache_id")
+
+
+def _group_setup_context(ctx, inputs, output):
+    x, ws, a, b, *rest = inputs
+    ys, shats, bits = output
+    ctx.mark_non_differentiable(*shats, *bits)
+    args = dict(zip(_GROUP_ARGS, rest))
+    offset_dev = args.pop("offset_dev")
+    ctx.has_off = offset_dev is not None
+    ctx.J = len(ws)
+    ctx.param_dtypes = [p.dtype for p in a] + [p.dtype for p in b]
+    ctx.args = args
+    ctx.save_for_backward(x, *ws, *a, *b, *shats, *bits, *([offset_dev] if ctx.has_off else []))
+
+
+def _group_backward(ctx, gys, _gs, _gbits):
+    J = ctx.J
+    x, *rest = ctx.saved_tensors
+    ws, a, b = rest[:J], rest[J:2 * J], rest[2 * J:3 * J]
+    shats, bits = rest[3 * J:4 * J], rest[4 * J:5 * J]
+    offset_dev = rest[5 * J] if ctx.has_off else None
+    A = ctx.args
+    need_dx = bool(ctx.needs_input_grad[0])
+    dys = [(g if g is not None else torch.zeros((x.shape[0], w.shape[0]), dtype=_BF16, device=x.device))
+           .to(_BF16).contiguous() for g, w in zip(gys, ws)]
+    dx, daccs = torch.ops.lorafusion_b200.lora_group_bwd(
+        dys, x, list(ws), list(a), list(b), list(shats), list(bits), A["ranks"], A["scalings"], A["ps"], A["seeds"],
+        A["offset"], offset_dev, A["training"], A["cache_id"], need_dx)
+    k = x.shape[1]
+    ga, gb = [], []
+    for j, (r, w, acc) in enumerate(zip(A["ranks"], ws, daccs)):
+        R = -(-r // 16) * 16
+        ga.append(acc[:R * k].view(R, k)[:r].to(ctx.param_dtypes[j]))
+        gb.append(acc[R * k:].view(w.shape[0], R)[:, :r].to(ctx.param_dtypes[J + j]))
+    return (dx if need_dx else None, [None] * J, ga, gb) + (None,) * len(_GROUP_ARGS)
+
+
+torch.library.register_autograd(f"{_NS}::lora_group_fwd", _group_backward, setup_context=_group_setup_context)
+
+
+def fused_lora_group(x: torch.Tensor, weights: Sequence[torch.Tensor], lora_a: Sequence[torch.Tensor],
+                     lora_b: Sequence[torch.Tensor], adapters: Sequence[AdapterConfig], offset: int = 0,
+                     training: bool = True, offset_dev: torch.Tensor | None = None,
+                     operand_cache: OperandCache | None = None) -> list[torch.Tensor]:
+    """Several LoRA linears that read the same input (q/k/v, gate/up): Y_j = X·W_jᵀ +
+    s_j·dropout_j(X)·A_jᵀ·B_jᵀ, each with its own adapter, seed and mask (one Philox offset
+    for the call). Same results as separate fused_lora calls, but the input gradient
+    Σ_j dX_j is summed inside the ⑤ GEMM epilogues (SURVEY §8(f)#4)."""
+    if not weights or len(weights) != len(lora_a) or len(weights) != len(lora_b) or len(weights) != len(adapters):
+        raise ValidationError("fused_lora_group needs one weight, lora_a, lora_b and adapter per projection")
+    k = weights[0].shape[1]
+    x2, lead = _flatten_input(x, k)
+    packed = pack_adapters(adapters)
+    for j, w in enumerate(weights):
+        if w.shape[1] != k:
+            raise ValidationError(f"weights[{j}] has in_features {w.shape[1]}, expected {k} (one shared input)")
+        _check_call(x2, w, [lora_a[j]], [lora_b[j]], [packed[0][j]], k, w.shape[0], None, offset_dev)
+    if x2.shape[0] == 0:
+        return [_EmptyBatchFn.apply(x2, w.shape[0], a_, b_).reshape(lead + (w.shape[0],))
+                for w, a_, b_ in zip(weights, lora_a, lora_b)]
+    ys, _s, _bits = torch.ops.lorafusion_b200.lora_group_fwd(
+        x2, list(weights), list(lora_a), list(lora_b), *packed, int(offset), offset_dev, bool(training),
+        _cache_handle(operand_cache))
+    return [y.reshape(lead + (y.shape[1],)) for y in ys]
+
+
 class _SinkLayout:
     """What a gradient sink sees of a call: (adapter, batch, col_start, rank) per segment."""
 

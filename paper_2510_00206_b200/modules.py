@@ -293,3 +293,130 @@ class FusedMultiLoRA(nn.Module):
         if self.base is not None and self.base.bias is not None:
             y = y + self.base.bias.to(y.dtype)
         return y
+
+
+class FusedLoRAGroup(nn.Module):
+    """Several LoRA linears that read the same input — q/k/v of an attention block, gate/up
+    of a SwiGLU MLP — as one module (shared-input fusion).
+
+    ``projections`` maps names (e.g. "q_proj") to frozen bases (nn.Linear or weight); every
+    projection is a :class:`FusedLoRA` child with its own adapter (PEFT names
+    ``<name>.lora_A.weight`` / ``<name>.lora_B.weight``), seed and dropout mask, so
+    ``group.q_proj(x)`` alone still works. ``forward(x)`` returns the projections' outputs in
+    order. What the group adds: one Philox offset per call (one offset draw instead of one
+    per projection), and backward sums the input gradient Σ_j dX_j inside the ⑤ GEMM
+    epilogues (lf_grad_input_accum) instead of the per-projection elementwise adds autograd
+    would run for an input read several times.
+    """
+
+    def __init__(
+        self,
+        projections: "dict[str, nn.Linear | torch.Tensor]",
+        rank: int | Sequence[int],
+        scaling: float | Sequence[float] | None = None,
+        dropout_p: float | Sequence[float] = 0.0,
+        *,
+        alpha: float | None = None,
+        seeds: Sequence[int] | None = None,
+        init: str = "peft",
+        dtype: torch.dtype = torch.float32,
+        generator: torch.Generator | None = None,
+        capturable: bool = False,
+        dropout_rng: str = "torch",
+    ):
+        super().__init__()
+        names = list(projections)
+        if not names:
+            raise ValidationError("FusedLoRAGroup needs at least one projection")
+        J = len(names)
+
+        def per(v, what):
+            vs = list(v) if isinstance(v, (list, tuple)) else [v] * J
+            if len(vs) != J:
+                raise ValidationError(f"{what}: one value per projection ({J}), got {len(vs)}")
+            return vs
+
+        ranks, scalings, ps = per(rank, "rank"), per(scaling, "scaling"), per(dropout_p, "dropout_p")
+        seeds = per(list(seeds) if seeds is not None else list(range(J)), "seeds")
+        layers = {}
+        for j, nm in enumerate(names):
+            layers[nm] = FusedLoRA(projections[nm], ranks[j], scalings[j], ps[j], alpha=alpha, seed=seeds[j], init=init,
+                                   dtype=dtype, generator=generator, capturable=capturable, dropout_rng=dropout_rng)
+        self._adopt(layers, capturable, dropout_rng)
+
+    @classmethod
+    def from_layers(cls, layers: "dict[str, FusedLoRA]", capturable: bool | None = None,
+                    dropout_rng: str | None = None) -> "FusedLoRAGroup":
+        """Group existing FusedLoRA layers that read the same input (their parameters are
+        shared, not copied)."""
+        if not layers:
+            raise ValidationError("FusedLoRAGroup needs at least one projection")
+        first = next(iter(layers.values()))
+        obj = cls.__new__(cls)
+        nn.Module.__init__(obj)
+        obj._adopt(dict(layers), first.capturable if capturable is None else capturable,
+                   first.dropout_rng if dropout_rng is None else dropout_rng)
+        return obj
+
+    def _adopt(self, layers: "dict[str, FusedLoRA]", capturable: bool, dropout_rng: str) -> None:
+        names = list(layers)
+        self.names = names
+        for nm in names:  # children under their own names: PEFT keys "<name>.lora_A.weight"
+            if not nm.isidentifier():
+                raise ValidationError(f"projection name {nm!r} must be a Python identifier")
+            if not isinstance(layers[nm], FusedLoRA):
+                raise ValidationError(f"projection {nm!r} must be a FusedLoRA layer")
+            self.add_module(nm, layers[nm])
+        ks = {self.proj(nm).in_features for nm in names}
+        if len(ks) != 1:
+            raise ValidationError(f"all projections of a group read the same input: in_features {sorted(ks)}")
+        self.in_features = ks.pop()
+        _init_capturable(self, capturable, self.proj(names[0]).base_weight.device, dropout_rng)
+        self._offset = 0
+        self._operands = OperandCache(capacity=2 * len(names))
+        cfgs = [self.proj(nm).config for nm in names]
+        self._packed = pack_adapters(cfgs)
+        self._has_dropout = any(c.dropout_p > 0 for c in cfgs)
+
+    def proj(self, name: str) -> FusedLoRA:
+        return self._modules[name]
+
+    def next_offset(self) -> int:
+        off = self._offset
+        self._offset += 1
+        return off
+
+    def dropout_state(self) -> dict:
+        return _dropout_state(self)
+
+    def load_dropout_state(self, state: dict) -> None:
+        _load_dropout_state(self, state)
+
+    def invalidate_operands(self) -> None:
+        self._operands.clear()
+
+    def forward(self, x: torch.Tensor) -> tuple[torch.Tensor, ...]:
+        from .functional import lora_group_fwd  # noqa: F401  (registers the operator)
+
+        projs = [self._modules[nm] for nm in self.names]
+        ws = [p.base_weight for p in projs]
+        a = [p.lora_A.weight for p in projs]
+        b = [p.lora_B.weight for p in projs]
+        k = self.in_features
+        x2, lead = _flatten_input(x, k)
+        for j, p in enumerate(projs):
+            _check_call(x2, ws[j], [a[j]], [b[j]], [self._packed[0][j]], k, p.out_features, None, None)
+        if x2.shape[0] == 0:
+            ys = [_EmptyBatchFn.apply(x2, w.shape[0], a_, b_) for w, a_, b_ in zip(ws, a, b)]
+        else:
+            off, off_dev = _step_offsets(self, x2.device, self._has_dropout)
+            ys, _s, _bits = torch.ops.lorafusion_b200.lora_group_fwd(
+                x2, ws, a, b, *self._packed, off, off_dev, self.training,
+                0 if self.capturable else _cache_handle(self._operands))
+        out = []
+        for p, y in zip(projs, ys):
+            y = y.reshape(lead + (p.out_features,))
+            if p.base_bias is not None:
+                y = y + p.base_bias.to(y.dtype)
+            out.append(y)
+        return tuple(out)

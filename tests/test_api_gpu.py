@@ -172,3 +172,62 @@ def test_slot_grads_split_unshared_blocks():
     total_b = sum(layer.slot_grads[(0, bt)][1] for bt in range(3))
     torch.testing.assert_close(total_a, layer.lora_A[0].weight.grad, rtol=1e-5, atol=1e-6)
     torch.testing.assert_close(total_b, layer.lora_B[0].weight.grad, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("p", [0.0, 0.1])
+def test_group_matches_separate_projections(p):
+    """FusedLoRAGroup (q/k/v sharing X) = three FusedLoRA layers at the same Philox offset:
+    identical outputs, identical dX to autograd's sequential sum of the three input
+    gradients (the ⑤ epilogues add in the same order and rounding), same dA/dB."""
+    from paper_2510_00206_b200 import FusedLoRAGroup
+
+    g = torch.Generator(device=DEV).manual_seed(11)
+    k = 512
+    bases = {nm: (torch.randn(n, k, device=DEV, generator=g) / k**0.5).to(torch.bfloat16)
+             for nm, n in (("q_proj", 512), ("k_proj", 128), ("v_proj", 128))}
+    grp = FusedLoRAGroup(bases, rank=[16, 8, 16], scaling=[2.0, 1.0, 0.5], dropout_p=[p, p, 0.0], seeds=[3, 4, 5],
+                         init="gaussian", generator=g, dropout_rng="counter")
+    x0 = torch.randn(640, k, device=DEV, generator=g).to(torch.bfloat16)
+    dys = [torch.randn(640, n.shape[0], device=DEV, generator=g).to(torch.bfloat16) for n in bases.values()]
+    grp._offset = 7
+    x = x0.clone().requires_grad_(True)
+    ys = grp(x)
+    torch.autograd.backward(ys, dys)
+    got = [(y.detach(), grp.proj(nm).lora_A.weight.grad.clone(), grp.proj(nm).lora_B.weight.grad.clone())
+           for y, nm in zip(ys, grp.names)]
+    dx_group = x.grad.clone()
+    xs = x0.clone().requires_grad_(True)
+    for j, nm in enumerate(grp.names):
+        layer = grp.proj(nm)
+        layer.lora_A.weight.grad = layer.lora_B.weight.grad = None
+        layer.dropout_rng = "counter"
+        layer._offset = 7
+        y = layer(xs)
+        y.backward(dys[j])
+        assert torch.equal(y, got[j][0])
+        assert _rel(layer.lora_A.weight.grad, got[j][1]) < 1e-5 and _rel(layer.lora_B.weight.grad, got[j][2]) < 1e-5
+    assert torch.equal(dx_group, xs.grad)
+
+
+def test_group_compiles_fullgraph():
+    from paper_2510_00206_b200 import FusedLoRAGroup
+
+    g = torch.Generator(device=DEV).manual_seed(12)
+    bases = {nm: (torch.randn(256, 256, device=DEV, generator=g) / 16).to(torch.bfloat16) for nm in ("gate", "up")}
+    grp = FusedLoRAGroup(bases, rank=16, dropout_p=0.1, init="gaussian", generator=g, capturable=True,
+                         dropout_rng="counter")
+    x0 = torch.randn(384, 256, device=DEV, generator=g).to(torch.bfloat16)
+
+    def run(fn):
+        x = x0.clone().requires_grad_(True)
+        for p_ in grp.parameters():
+            p_.grad = None
+        with torch.no_grad():
+            grp.step_counter.zero_()
+        y1, y2 = fn(x)
+        (y1.float() * y2.float()).sum().backward()
+        return y1.detach(), x.grad.clone(), grp.gate.lora_A.weight.grad.clone()
+
+    eager = run(grp)
+    got = run(torch.compile(grp, backend="aot_eager", fullgraph=True))
+    assert torch.equal(got[0], eager[0]) and torch.equal(got[1], eager[1]) and _rel(got[2], eager[2]) < 1e-5

@@ -254,3 +254,17 @@ def test_whole_microbatch_validation_has_no_segment_cap():
     validate_segments(segs, 40, 1, max_segments=None)
     with pytest.raises(ValidationError):
         validate_segments(segs, 40, 1)
+
+
+def test_group_module_names_and_validation():
+    from paper_2510_00206_b200 import FusedLoRAGroup
+
+    w = lambda n, k: torch.zeros(n, k, dtype=torch.bfloat16)  # noqa: E731
+    g = FusedLoRAGroup({"q_proj": w(64, 32), "k_proj": w(16, 32), "v_proj": w(16, 32)}, rank=[16, 8, 8])
+    assert [n for n, _ in g.named_parameters()] == [f"{p}.lora_{ab}.weight" for p in ("q_proj", "k_proj", "v_proj")
+                                                    for ab in ("A", "B")]
+    assert g.k_proj.config.rank == 8 and g.q_proj.config.seed == 0 and g.v_proj.config.seed == 2
+    with pytest.raises(ValidationError):
+        FusedLoRAGroup({"a": w(64, 32), "b": w(64, 16)}, rank=8)  # different inputs
+    with pytest.raises(ValidationError):
+        FusedLoRAGroup({"a": w(64, 32)}, rank=[8, 16])
