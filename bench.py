@@ -517,6 +517,59 @@ def unfused_step(config, base, inputs, grads, p):
             t.grad = None
 
 
+_KERNEL_CLASSES = (
+    ("lf_gemm_kernel<false", "② base_fwd (lf_gemm_kernel, K-major W)"),
+    ("lf_gemm_kernel<true", "⑤ grad_input (lf_gemm_kernel, MN-major W)"),
+    ("lf_down_kernel", "① dropout_down_fwd (lf_down_kernel)"),
+    ("lf_gradup_kernel", "③ grad_up (lf_gradup_kernel)"),
+    ("lf_finalize_kernel", "③ grad_up dŜ finalize (lf_finalize_kernel)"),
+    ("lf_dgrad_a_kernel", "④ grad_down (lf_dgrad_a_kernel)"),
+    ("lf_routes_kernel", "routing table (lf_routes_kernel)"),
+    ("distribution", "torch: dropout offset draw (randint)"),
+    ("fill", "torch: zero-fill of the fp32 dA/dB accumulators"),
+    ("elementwise", "torch: elementwise (fp32->bf16 operand casts, gradient sums, counters)"),
+)
+
+
+def step_breakdown(run, steps: int = 1) -> dict:
+    """Where one step's device time goes: CUPTI kernel records of `steps` replays, each
+    kernel credited with the time it extends the covered part of the timeline (programmatic
+    dependent launch overlaps neighbours), gaps as `idle` — the parts sum to the span."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(steps):
+            run()
+        torch.cuda.synchronize()
+    evs = sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
+                  and not e.name.startswith(("Memcpy", "Memset"))), key=lambda e: e.time_range.start)
+    if not evs:
+        return {}
+    parts: dict = {}
+    t0 = evs[0].time_range.start
+    covered = t0
+    idle = 0.0
+    for e in evs:
+        a, b = e.time_range.start, e.time_range.end
+        if a > covered:
+            idle += a - covered
+        gain = max(0.0, b - max(a, covered))
+        covered = max(covered, b)
+        name = next((lbl for key, lbl in _KERNEL_CLASSES if key in e.name), "other: " + e.name[:48])
+        ent = parts.setdefault(name, [0, 0.0])
+        ent[0] += 1
+        ent[1] += gain
+    span = covered - t0
+    out = {nm: {"ms_per_step": v[1] / 1e3 / steps, "kernels_per_step": v[0] / steps}
+           for nm, v in sorted(parts.items(), key=lambda kv: -kv[1][1])}
+    out["idle (gaps between kernels)"] = {"ms_per_step": idle / 1e3 / steps}
+    return {"span_ms_per_step": span / 1e3 / steps, "parts": out,
+            "method": "torch.profiler (CUPTI) over one graph replay after the timed loop; overlapping kernels "
+                      "(PDL) credited with the time each extends the timeline, so parts + idle = span"}
+
+
 def time_loop(fn, steps, warmup, sync_barrier):
     import torch
 
@@ -612,6 +665,13 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     F_.set_launch_stats(None)
     durs = stats.durations_ms()
 
+    breakdown = None
+    if True:  # every rank replays (the replay may hold a collective)
+        try:
+            breakdown = step_breakdown(run)
+        except Exception as e:  # profiler unavailable: the line still stands without it
+            print(f"[bench] step breakdown failed ({type(e).__name__}: {e})", file=sys.stderr)
+
     # ---- per-kernel roofline ----------------------------------------------------------
     peaks = measured_peaks()
     gfl = gemm_flops(args.config, m, r)
@@ -651,8 +711,6 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "frac_of_sustained": gemm_tf / peaks["bf16_tflops_sustained"],
         "share_of_step": gemm_ms / ms,
         "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-        "traffic_detail": traffic,
-        "per_kernel": kernels,
     }
 
     # ---- unfused torch baseline (same box, same shapes) -------------------------------
@@ -714,8 +772,6 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         }
         if e2e is not None:
             line["e2e"] = e2e
-        if multi is not None:
-            line["multi_lora"] = multi
         if not args.no_cpu_baseline:
             cores = len(os.sched_getaffinity(0))
             ts = cpu_reference_step(args.config, args.cpu_sample_tokens, r, p)
@@ -726,6 +782,12 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                           "accumulation with its Philox keep mask",
                 "c1_fp32_torch": cpu_torch_c1(),
             }
+        # the bulky parts last, so a truncated tail of the line keeps the headline keys
+        line["per_kernel"] = kernels
+        if multi is not None:
+            line["multi_lora"] = multi
+        line["step_breakdown"] = breakdown
+        line["gemm_traffic_detail"] = traffic
         print(json.dumps(line), flush=True)
 
 
@@ -1052,7 +1114,8 @@ def main() -> None:
                     help="tokens per GPU (default: the config's; e.g. --config c4 --tokens 2048 = the per-rank "
                          "load of C4's 16384-token strong scaling at 8 GPUs)")
     ap.add_argument("--no-multi", action="store_true", help="skip the secondary C3 FusedMultiLoRA measurement")
-    ap.add_argument("--group", action=argparse.BooleanOptionalAction, default=True,
+    ap.add_argument("--group", action=argparse.BooleanOptionalAction,
+                    default=os.environ.get("LF_BENCH_GROUP", "1") != "0",
                     help="q/k/v and gate/up as FusedLoRAGroup calls (shared input; default) or separate layers")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dropout", type=float, default=0.1)

@@ -59,7 +59,7 @@ enum {
   LF_OK = 0,
   LF_E_INVALID = -1,     /* bad argument: maps to ValueError (ls/errors.py:12) */
   LF_E_CUDA = -2,        /* CUDA runtime / driver failure: maps to RuntimeError */
-  LF_E_UNSUPPORTED = -3, /* device is not sm_100 */
+  LF_E_UNSUPPORTED = -3, /* device is not sm_100, or a variant this build does not provide */
 };
 
 /* One (adapter, global batch) segment of token rows. */
@@ -125,6 +125,14 @@ LF_API int lf_grad_up(const LfProblem* p, const uint16_t* dy, const uint16_t* b_
 /* ④ da_accum (R x k, fp32) += dŜᵀ·(M⊙X). */
 LF_API int lf_grad_down(const LfProblem* p, const uint16_t* x, const uint16_t* ds, float* da_accum, void* stream);
 
+/* ④ for projections that read the same input X (q/k/v, gate/up):
+ * da_accum[j] (R_j x k, fp32) += dŜ_jᵀ·(M_j⊙X) for j < nproj (<= 3), one launch that reads
+ * each X tile from DRAM once (projection j's copy is masked with its own keep bits).
+ * probs[j] is projection j's problem (same m, k; one segment over all rows). Falls back to
+ * per-projection lf_grad_down when a problem does not have that shape. ABI 4. */
+LF_API int lf_grad_down_group(const LfProblem* const* probs, int32_t nproj, const uint16_t* x,
+                              const uint16_t* const* ds, float* const* da_accum, void* stream);
+
 /* ⑤ dx = dY·W + M ⊙ (dŜ·A_cat), written once. */
 LF_API int lf_grad_input(const LfProblem* p, const uint16_t* dy, const uint16_t* w, const uint16_t* ds,
                   const uint16_t* a_cat, uint16_t* dx, void* stream);
@@ -133,6 +141,7 @@ LF_API int lf_grad_input(const LfProblem* p, const uint16_t* dy, const uint16_t*
  * the GEMM epilogue (fp32 sum, one bf16 rounding: what torch's add of the two bf16 tensors
  * gives). Several projections that read the same input (q/k/v, gate/up: SURVEY §8(f)#4)
  * sum their input gradients this way instead of through separate elementwise adds.
+ * LF_E_UNSUPPORTED (nothing launched) for shapes that run on 256x512 tiles: add instead.
  * ABI 4. */
 LF_API int lf_grad_input_accum(const LfProblem* p, const uint16_t* dy, const uint16_t* w, const uint16_t* ds,
                         const uint16_t* a_cat, uint16_t* dx, void* stream);

@@ -35,6 +35,7 @@ EXPORTED_SYMBOLS = (
     "lf_base_fwd",
     "lf_grad_up",
     "lf_grad_down",
+    "lf_grad_down_group",
     "lf_grad_input",
     "lf_grad_input_accum",
     "lf_dropout_mask",
@@ -86,6 +87,8 @@ _SIGNATURES = {
     "lf_base_fwd": (ctypes.c_int, [_P, _V, _V, _V, _V, _V, _V]),
     "lf_grad_up": (ctypes.c_int, [_P, _V, _V, _V, _V, _V, _V]),
     "lf_grad_down": (ctypes.c_int, [_P, _V, _V, _V, _V]),
+    "lf_grad_down_group": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int32, _V, ctypes.POINTER(_V),
+                                          ctypes.POINTER(_V), _V]),
     "lf_grad_input": (ctypes.c_int, [_P, _V, _V, _V, _V, _V, _V]),
     "lf_grad_input_accum": (ctypes.c_int, [_P, _V, _V, _V, _V, _V, _V]),
     "lf_dropout_mask": (ctypes.c_int, [_P, _V, _V]),

@@ -501,6 +501,77 @@ int lf_grad_down(const LfProblem* p, const uint16_t* x, const uint16_t* ds, floa
   return LF_OK;
 }
 
+// ④ over a shared-input group: one launch when every projection is a single segment over
+// all rows whose keep bits (if any) ①'s launch left 16-byte pitched; otherwise (and for
+// J = 1) the per-projection lf_grad_down.
+int lf_grad_down_group(const LfProblem* const* probs, int32_t nproj, const uint16_t* x, const uint16_t* const* ds,
+                       float* const* da_accum, void* stream) {
+  if (!probs || nproj < 1 || nproj > lf::kMaxGroup || !ds || !da_accum)
+    return fail(LF_E_INVALID, "lf_grad_down_group: 1..%d projections with ds / da_accum arrays", lf::kMaxGroup);
+  LF_TRY(check_ptr(x, "x"));
+  bool fused = nproj > 1;
+  lf::LfSegTable t[lf::kMaxGroup];
+  int rsum = 0, rmax = 0;
+  for (int j = 0; j < nproj; ++j) {
+    const LfProblem* p = probs[j];
+    if (!p) return fail(LF_E_INVALID, "lf_grad_down_group: projection %d has no problem", j);
+    LF_TRY(validate(p, true, &t[j]));
+    LF_TRY(check_ptr(ds[j], "ds"));
+    LF_TRY(check_ptr(da_accum[j], "da_accum"));
+    if (p->m != probs[0]->m || p->k != probs[0]->k)
+      return fail(LF_E_INVALID, "lf_grad_down_group: projections must share the input (m, k)");
+    const bool single = p->num_segments == 1 && p->segments[0].row_start == 0 && p->segments[0].row_end == p->m &&
+                        p->segments[0].col_start == 0 && p->segments[0].rank == p->rank_total && p->row_base == 0;
+    const bool bits_ok = t[j].mask_mode == 0 || (t[j].mask_mode == 1 && t[j].bits && t[j].ld_bits % 16 == 0);
+    if (!single || !bits_ok) fused = false;
+    rsum += p->rank_total;
+    if (p->rank_total > rmax) rmax = p->rank_total;
+  }
+  static const int group_env = env_int("LF_GROUP_DOWN", 1);
+  if (2 * rsum > 512 || !group_env) fused = false;
+  if (!fused) {
+    for (int j = 0; j < nproj; ++j) LF_TRY(lf_grad_down(probs[j], x, ds[j], da_accum[j], stream));
+    return LF_OK;
+  }
+  Dev d;
+  LF_TRY(current_device(&d));
+  lf::GroupDownMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  lf::GroupDownArgs a;
+  memset(&a, 0, sizeof(a));
+  const LfProblem* p0 = probs[0];
+  if (!make_map(&maps.x, x, p0->m, p0->k, p0->k, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+    return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (x)");
+  int off = 0;
+  for (int j = 0; j < nproj; ++j) {
+    const LfProblem* p = probs[j];
+    if (!make_map(&maps.d[j], ds[j], p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B))
+      return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (ds)");
+    a.masked[j] = t[j].mask_mode == 1 && t[j].seg[0].thr != 0;
+    if (a.masked[j] && !make_map_u8(&maps.bits[j], t[j].bits, p->m, t[j].ld_bits, t[j].ld_bits, 16, 128))
+      return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (keep bits)");
+    a.R[j] = p->rank_total;
+    a.off[j] = off;
+    off += p->rank_total;
+    a.da[j] = da_accum[j];
+  }
+  a.m = p0->m;
+  a.k = p0->k;
+  a.J = nproj;
+  a.rsum = rsum;
+  a.rmax = rmax;
+  a.debug = t[0].debug;
+  int stages = 0, stage_bytes = 0;
+  lf::grad_down_group_config(rmax, &stages, &stage_bytes);
+  const int occ = occupancy_for_smem(stages * stage_bytes + 2048);
+  const long units = (long)((p0->k + 127) / 128) * ((p0->m + 127) / 128) * nproj;
+  long ctas = (long)occ * d.sms;
+  if (ctas > units) ctas = units;
+  a.ctas = (int)ctas;
+  if (lf::grad_down_group_launch(maps, a, (cudaStream_t)stream)) return cuda_fail("grad_down_group launch");
+  return LF_OK;
+}
+
 static int grad_input_impl(const LfProblem* p, const uint16_t* dy, const uint16_t* w, const uint16_t* ds,
                            const uint16_t* a_cat, uint16_t* dx, int accumulate, void* stream) {
   lf::LfSegTable t;
@@ -540,8 +611,10 @@ static int grad_input_impl(const LfProblem* p, const uint16_t* dy, const uint16_
   a.routes = lora ? reinterpret_cast<const lf::LfRoute*>(p->routes) : nullptr;
   a.segs = t;
   a.group = env_int("LF_GROUP", 0);
-  if (lf::gemm_launch(masked ? lf::kGemmDgradMasked : lf::kGemmDgrad, maps, a, d.sms, (cudaStream_t)stream))
-    return cuda_fail("grad_input launch");
+  const int rc = lf::gemm_launch(masked ? lf::kGemmDgradMasked : lf::kGemmDgrad, maps, a, d.sms, (cudaStream_t)stream);
+  if (rc == lf::kGemmUnsupported)
+    return fail(LF_E_UNSUPPORTED, "grad_input: accumulation is not built for the 256x512 tiles this shape uses");
+  if (rc) return cuda_fail("grad_input launch");
   return LF_OK;
 }
 

@@ -778,14 +778,14 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
   (cl4 ? launch_one<BMN, MSK, ST, WD, 4>(maps, args, num_sms, stream)                          \
        : launch_one<BMN, MSK, ST, WD, 2>(maps, args, num_sms, stream))
   // accumulating dgrads (lf_grad_input_accum) are their own instantiations: the C
-  // read-modify-write would otherwise cost the plain epilogues registers (the 256 x 512
-  // tiles hold 128 words of output per thread)
-#define LF_GEMM_LAUNCH_ACC(BMN, MSK, ST, WD) launch_one<BMN, MSK, ST, WD, 2, true>(maps, args, num_sms, stream)
+  // read-modify-write would otherwise cost the plain epilogues registers. Only the 256 x 256
+  // tiles accumulate: the 256 x 512 epilogue already holds 128 words of output per thread and
+  // spills with it (the caller sums those with a separate add instead: kGemmUnsupported)
   if (args.accumulate) {
     if (kind == kGemmFwd) return -1;
-    const bool masked = kind == kGemmDgradMasked;
-    return wide ? (masked ? LF_GEMM_LAUNCH_ACC(true, true, 4, true) : LF_GEMM_LAUNCH_ACC(true, false, 4, true))
-                : (masked ? LF_GEMM_LAUNCH_ACC(true, true, 6, false) : LF_GEMM_LAUNCH_ACC(true, false, 6, false));
+    if (wide) return kGemmUnsupported;
+    return kind == kGemmDgradMasked ? launch_one<true, true, 6, false, 2, true>(maps, args, num_sms, stream)
+                                    : launch_one<true, false, 6, false, 2, true>(maps, args, num_sms, stream);
   }
   switch (kind) {
     case kGemmFwd:

@@ -56,6 +56,7 @@ inline int launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, 
 //                   accumulator, the epilogue warps zero its dropped elements in TMEM, and
 //                   the dY·W main loop accumulates on top (dropout p > 0)
 enum GemmKind { kGemmFwd = 0, kGemmDgrad = 1, kGemmDgradMasked = 2 };
+constexpr int kGemmUnsupported = -3;  // gemm_launch: valid request this build does not run (nothing launched)
 
 struct GemmArgs {
   int32_t M, N, K;
@@ -114,6 +115,29 @@ struct GradDownArgs {
   const LfRoute* routes;
   LfSegTable segs;
 };
+// ④ for a shared-input group: dA_j += dŜ_jᵀ·(M_j⊙X) for the J projections
+// that read the same X (q/k/v, gate/up), one launch. Each unit loads the X tile once per
+// projection, back to back, so only the first load of a tile comes from DRAM (the
+// projection-major layout of separate launches reads X J times from DRAM); each projection
+// has its own keep bits (TMA'd per stage), dŜ and accumulators.
+constexpr int kMaxGroup = 3;
+struct GroupDownArgs {
+  int32_t m, k, J;
+  int32_t ctas;
+  int32_t rsum;                   // Σ_j R_j: one TMEM accumulator buffer
+  int32_t rmax;                   // widest R_j: sizes the dŜ part of a stage
+  int32_t R[kMaxGroup];           // padded rank of projection j
+  int32_t off[kMaxGroup];         // its accumulator's first TMEM column in a buffer
+  int32_t masked[kMaxGroup];      // its keep bits ride in each stage (p > 0)
+  int32_t debug;
+  float* da[kMaxGroup];           // fp32 R_j x k accumulators
+};
+struct GroupDownMaps {
+  CUtensorMap x, d[kMaxGroup], bits[kMaxGroup];
+};
+void grad_down_group_config(int rmax, int* stages, int* stage_bytes);
+int grad_down_group_launch(const GroupDownMaps& maps, const GroupDownArgs& args, cudaStream_t stream);
+
 // split-K epilogue of ③: fp32 partials (ws) -> scaled bf16 m x R, workspace re-zeroed
 int finalize_launch(const LfSegTable& segs, const LfRoute* routes, float* ws, void* out, cudaStream_t stream);
 void grad_down_config(int wmax, bool bits_tma, int* stages, int* stage_bytes);

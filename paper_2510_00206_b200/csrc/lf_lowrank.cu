@@ -570,6 +570,212 @@ int grad_down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_ds, const CU
 }
 
 // ------------------------------------------------------------------------------------
+// ④ for a shared-input group: dA_j += dŜ_jᵀ·(M_j⊙X), j = 0..J-1, one launch
+// ------------------------------------------------------------------------------------
+// Units (k-tile, m-tile, projection), projection fastest: the X tile of (k-tile, m-tile) is
+// TMA-loaded J times in a row — the first load streams it from DRAM, the others hit L2 —
+// and each copy is masked in place with its own projection's keep bits (mask warps), so the
+// MMA of projection j reads M_j⊙X. Stream-K as ④: every CTA takes an equal contiguous share
+// of the units; a span is one k-tile's run, flushed per projection with red.global.add.
+__global__ void __launch_bounds__(kDgaThreads, 2)
+    lf_dgrad_a_group_kernel(const __grid_constant__ GroupDownMaps maps, const __grid_constant__ GroupDownArgs args,
+                            int stages, int stage_bytes) {
+  using namespace dga;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+  uint64_t* empty = full + stages;
+  uint64_t* masked = empty + stages;
+  uint64_t* tfull = masked + stages;  // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint64_t* tzero = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tzero + 1);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int J = args.J;
+  const int tiles_m = (args.m + 127) / 128;
+  const int tiles_k = (args.k + 127) / 128;
+  const int per_k = tiles_m * J;  // units per k-tile
+  const int units = tiles_k * per_k;
+  const int KBITS_OFF = X_BYTES + (args.rmax / 16) * 4096;
+  const int u0 = (int)((int64_t)blockIdx.x * units / gridDim.x);
+  const int u1 = (int)((int64_t)(blockIdx.x + 1) * units / gridDim.x);
+  uint32_t tmem_cols = 32;
+  while ((int)tmem_cols < 2 * args.rsum) tmem_cols <<= 1;
+  bool gated = false;
+  for (int j = 0; j < J; ++j) gated |= args.masked[j] != 0;
+  if (args.debug & 64) gated = false;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&masked[s], 8);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    mbar_init(tzero, 4);
+    fence_barrier_init();
+    tma_prefetch_desc(&maps.x);
+    for (int j = 0; j < J; ++j) {
+      tma_prefetch_desc(&maps.d[j]);
+      if (args.masked[j]) tma_prefetch_desc(&maps.bits[j]);
+    }
+  }
+  pdl_launch_dependents();
+  if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = u0; u < u1; ++u) {
+        const int kt = u / per_k, r = u - kt * per_k, mt = r / J, j = r - mt * J;
+        const int R = args.R[j];
+        const bool kb = args.masked[j] && gated;
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sX = smem + stage * stage_bytes;
+        mbar_arrive_expect_tx(&full[stage], X_BYTES + (R / 16) * 4096 + (kb ? 2048 : 0));
+        tma_load_2d(sX, &maps.x, &full[stage], kt * 128, mt * 128);
+        tma_load_2d(sX + 16384, &maps.x, &full[stage], kt * 128 + 64, mt * 128);
+        for (int g = 0; g < R / 16; ++g) tma_load_2d(sX + X_BYTES + g * 4096, &maps.d[j], &full[stage], 16 * g, mt * 128);
+        if (kb) tma_load_2d(sX + KBITS_OFF, &maps.bits[j], &full[stage], kt * 16, mt * 128);
+        if (++stage == stages) { stage = 0; phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    mbar_wait(tzero, 0);
+    tc_fence_after();
+    int stage = 0, it = 0;
+    uint32_t phase = 0;
+    bool open = false;
+    for (int u = u0; u < u1; ++u) {
+      const int kt = u / per_k, r = u - kt * per_k, mt = r / J, j = r - mt * J;
+      (void)mt;
+      const int b = it & 1;
+      if (!open) {
+        mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        open = true;
+      }
+      const int R = args.R[j];
+      mbar_wait(gated ? &masked[stage] : &full[stage], phase);
+      tc_fence_after();
+      const uint32_t sX = smem_u32(smem + stage * stage_bytes);
+      const uint64_t ax = make_sdesc(sX, 16384, 1024, kLayoutSW128);
+      const uint64_t bd = make_sdesc(sX + X_BYTES, 4096, 256, kLayoutSW32);
+      const uint32_t idesc = make_idesc_bf16(128, (uint32_t)R, true, true);
+      const uint32_t d = tmem + b * args.rsum + args.off[j];
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        if (!(args.debug & 1)) umma_bf16_warp(d, sdesc_add(ax, kk * 2048), sdesc_add(bd, kk * 512), idesc, 1u);
+      }
+      umma_commit_warp(&empty[stage]);
+      if (++stage == stages) { stage = 0; phase ^= 1; }
+      if (u + 1 >= u1 || (u + 1) / per_k != kt) {  // span ends: hand the accumulators to the flush
+        umma_commit_warp(&tfull[b]);
+        ++it;
+        open = false;
+      }
+    }
+    __syncwarp();
+  } else {
+    const uint32_t q = warp & 3u;
+    const uint32_t taddr = tmem + ((q * 32u) << 16);
+    uint32_t z[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) z[i] = 0u;
+    if (warp < 6) {
+      for (int c = 0; c < 2 * args.rsum; c += 16) tmem_st16(taddr + c, z);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tzero);
+    }
+    const int rit = (int)(q * 32 + lane);
+    const int half = warp >= 6 ? 1 : 0;
+    int stage = 0, it = 0;
+    uint32_t phase = 0;
+    uint32_t touched = 0;  // projections with contributions in the open span
+    for (int u = u0; u < u1; ++u) {
+      const int kt = u / per_k, r = u - kt * per_k, mt = r / J, j = r - mt * J;
+      touched |= 1u << j;
+      if (gated) {
+        const int row = mt * 128 + rit;
+        mbar_wait(&full[stage], phase);
+        if (args.masked[j] && row < args.m) {
+          uint8_t* sX = smem + stage * stage_bytes;
+          const uint64_t bits = lds64(smem_u32(sX + KBITS_OFF) + (uint32_t)(rit * 16 + half * 8));
+          if (!(args.debug & 8)) apply_row_sw128(sX + half * 16384, rit, bits);
+        }
+        if (!(args.debug & 4)) fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&masked[stage]);
+      }
+      if (++stage == stages) { stage = 0; phase ^= 1; }
+      if (half == 0 && (u + 1 >= u1 || (u + 1) / per_k != kt)) {
+        const int b = it & 1;
+        mbar_wait(&tfull[b], (it >> 1) & 1);
+        tc_fence_after();
+        const int kcol = kt * 128 + rit;
+        for (int jj = 0; jj < J; ++jj) {
+          if (!((touched >> jj) & 1u)) continue;
+          for (int g = 0; g < args.R[jj] / 16; ++g) {
+            uint32_t v[16];
+            const uint32_t a = taddr + b * args.rsum + args.off[jj] + g * 16;
+            tmem_ld16(a, v);
+            tmem_ld_wait();
+            if (kcol < args.k && !(args.debug & 2)) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                red_add_f32(args.da[jj] + (int64_t)(g * 16 + i) * args.k + kcol, __uint_as_float(v[i]));
+            }
+            tmem_st16(a, z);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[b]);
+        ++it;
+        touched = 0;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, tmem_cols);
+  }
+}
+
+void grad_down_group_config(int rmax, int* stages, int* stage_bytes) {
+  *stage_bytes = dga::X_BYTES + (rmax / 16) * 4096 + 2048;
+  const int s = (112 * 1024) / *stage_bytes;
+  *stages = s < 2 ? 2 : (s > 6 ? 6 : s);
+}
+
+int grad_down_group_launch(const GroupDownMaps& maps, const GroupDownArgs& args, cudaStream_t stream) {
+  int stages = 0, stage_bytes = 0;
+  grad_down_group_config(args.rmax, &stages, &stage_bytes);
+  const int smem = stages * stage_bytes + 1024 + 256;
+  static std::atomic<uint64_t> attr_done{0};
+  if (ensure_smem_attr(lf_dgrad_a_group_kernel, dga::MAX_SMEM + 2048, attr_done)) return -1;
+  return launch_k(lf_dgrad_a_group_kernel, dim3(args.ctas), dim3(kDgaThreads), smem, stream, maps, args, stages,
+                  stage_bytes);
+}
+
+// ------------------------------------------------------------------------------------
 // routing table and explicit keep mask
 // ------------------------------------------------------------------------------------
 __global__ void lf_routes_kernel(const __grid_constant__ LfSegTable segs, LfRoute* routes, int ntiles) {

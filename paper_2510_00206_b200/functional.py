@@ -170,6 +170,16 @@ def _cache_handle(cache: OperandCache | None) -> int:
     return h
 
 
+def _own(t: torch.Tensor | None, inputs: Sequence[torch.Tensor], empty_shape, like: torch.Tensor) -> torch.Tensor:
+    """An operator output that never aliases an input (gather_* returns a bf16 adapter weight
+    itself when no cast or padding is needed)."""
+    if t is None:
+        return like.new_empty(empty_shape)
+    if any(t.data_ptr() == i.data_ptr() for i in inputs):
+        return t.clone()
+    return t
+
+
 def _rank_concat_operands(plan: LayerPlan, a: Sequence[torch.Tensor], b: Sequence[torch.Tensor], cache_id: int):
     cache = _CACHES.get(cache_id) if cache_id else None
     key = None
@@ -243,8 +253,11 @@ def _plan(x_rows, k, n, ranks, scalings, ps, seeds, segs, offset, offset_dev, ke
 def lora_fwd(x: torch.Tensor, w: torch.Tensor, a: list[torch.Tensor], b: list[torch.Tensor], ranks: list[int],
              scalings: list[float], ps: list[float], seeds: list[int], segs: list[int], offset: int,
              offset_dev: Optional[torch.Tensor], keep_mask: Optional[torch.Tensor], training: bool,
-             share_blocks: bool, row_base: int, cache_id: int) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
-    """① + ②: returns (Y (m,n) bf16, Ŝ (m,R) bf16, packed keep mask (m,k/8) u8 or empty)."""
+             share_blocks: bool, row_base: int,
+             cache_id: int) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
+    """① + ②: returns (Y (m,n) bf16, Ŝ (m,R) bf16, packed keep mask (m,k/8) u8 or empty,
+    A_cat (R,k) bf16, B_cat (n,R) bf16) — the rank-concat operands are saved for the
+    backward, so it never re-casts the adapter weights."""
     lib = _lib.load()
     m, k = x.shape
     n = w.shape[0]
@@ -261,7 +274,8 @@ def lora_fwd(x: torch.Tensor, w: torch.Tensor, a: list[torch.Tensor], b: list[to
         _call("dropout_down_fwd", lib.lf_dropout_down_fwd, pp, _ptr(x), _ptr(a_cat), _ptr(s_hat), st)
     _call("base_fwd", lib.lf_base_fwd, pp, _ptr(x), _ptr(w), _ptr(s_hat), _ptr(b_cat), _ptr(y), st)
     bits = plan.keep_bits if plan.keep_bits is not None else torch.empty((0,), dtype=torch.uint8, device=x.device)
-    return y, s_hat, bits
+    a_cat, b_cat = _own(a_cat, a, (0, k), x), _own(b_cat, b, (n, 0), x)
+    return y, s_hat, bits, a_cat, b_cat
 
 
 @lora_fwd.register_fake
@@ -271,11 +285,13 @@ def _lora_fwd_fake(x, w, a, b, ranks, scalings, ps, seeds, segs, offset, offset_
     R = _rank_total(ranks, segs, share_blocks)
     bits = (x.new_empty((m, k // 8), dtype=torch.uint8) if _needs_bits(ps, segs, keep_mask, training)
             else x.new_empty((0,), dtype=torch.uint8))
-    return x.new_empty((m, w.shape[0])), x.new_empty((m, R)), bits
+    n = w.shape[0]
+    ops = (x.new_empty((R, k)), x.new_empty((n, R))) if segs else (x.new_empty((0, k)), x.new_empty((n, 0)))
+    return x.new_empty((m, n)), x.new_empty((m, R)), bits, *ops
 
 
 @torch.library.custom_op(f"{_NS}::lora_bwd", mutates_args=(), device_types="cuda")
-def lora_bwd(dy: torch.Tensor, x: torch.Tensor, w: torch.Tensor, a: list[torch.Tensor], b: list[torch.Tensor],
+def lora_bwd(dy: torch.Tensor, x: torch.Tensor, w: torch.Tensor, a_cat: torch.Tensor, b_cat: torch.Tensor,
              s_hat: torch.Tensor, keep_bits: torch.Tensor, ranks: list[int], scalings: list[float], ps: list[float],
              seeds: list[int], segs: list[int], offset: int, offset_dev: Optional[torch.Tensor],
              keep_mask: Optional[torch.Tensor], training: bool, share_blocks: bool, row_base: int, cache_id: int,
@@ -291,13 +307,12 @@ def lora_bwd(dy: torch.Tensor, x: torch.Tensor, w: torch.Tensor, a: list[torch.T
     pp = ctypes.byref(plan.problem)
     st = _stream(dy.device)
     R = plan.rank_total
-    ds = a_cat = None
+    ds = None
     # one zero-fill for both fp32 accumulators
     acc = torch.zeros(R * k + n * R, dtype=torch.float32, device=dy.device)
     da = acc[:R * k].view(R, k)
     db = acc[R * k:].view(n, R)
     if plan.has_lora:
-        a_cat, b_cat = _rank_concat_operands(plan, a, b, cache_id)
         ds = torch.empty((m, R), dtype=_BF16, device=dy.device)
         _call("grad_up", lib.lf_grad_up, pp, _ptr(dy), _ptr(b_cat), _ptr(s_hat), _ptr(ds), _ptr(db), st)
         _call("grad_down", lib.lf_grad_down, pp, _ptr(x), _ptr(ds), _ptr(da), st)
@@ -310,7 +325,7 @@ def lora_bwd(dy: torch.Tensor, x: torch.Tensor, w: torch.Tensor, a: list[torch.T
 
 
 @lora_bwd.register_fake
-def _lora_bwd_fake(dy, x, w, a, b, s_hat, keep_bits, ranks, scalings, ps, seeds, segs, offset, offset_dev,
+def _lora_bwd_fake(dy, x, w, a_cat, b_cat, s_hat, keep_bits, ranks, scalings, ps, seeds, segs, offset, offset_dev,
                    keep_mask, training, share_blocks, row_base, cache_id, need_dx):
     m, k = x.shape
     R = _rank_total(ranks, segs, share_blocks)
@@ -324,9 +339,9 @@ _PLAN_ARGS = ("ranks", "scalings", "ps", "seeds", "segs", "offset", "offset_dev"
 
 def _setup_context(ctx, inputs, output, mark: bool = True):
     x, w, a, b, *rest = inputs
-    y, s_hat, bits = output
+    y, s_hat, bits, a_cat, b_cat = output
     if mark:
-        ctx.mark_non_differentiable(s_hat, bits)
+        ctx.mark_non_differentiable(s_hat, bits, a_cat, b_cat)
     args = dict(zip(_PLAN_ARGS, rest))
     # the gradient of a non-tensor argument is None, except that an empty list (no segments)
     # flattens like a list of tensors and must come back as []
@@ -336,20 +351,19 @@ def _setup_context(ctx, inputs, output, mark: bool = True):
     opt = [args.pop("offset_dev"), args.pop("keep_mask")]
     ctx.has_opt = [t is not None for t in opt]
     ctx.args = args
-    ctx.save_for_backward(x, w, s_hat, bits, *a, *b, *[t for t in opt if t is not None])
+    ctx.save_for_backward(x, w, s_hat, bits, a_cat, b_cat, *[t for t in opt if t is not None])
 
 
-def _backward(ctx, dy, _ds, _dbits):
+def _backward(ctx, dy, _ds=None, _dbits=None, _da=None, _db=None):
     na = ctx.n_adapters
-    x, w, s_hat, bits, *rest = ctx.saved_tensors
-    a, b, opt = rest[:na], rest[na:2 * na], list(rest[2 * na:])
+    x, w, s_hat, bits, a_cat, b_cat, *opt = ctx.saved_tensors
     offset_dev = opt.pop(0) if ctx.has_opt[0] else None
     keep_mask = opt.pop(0) if ctx.has_opt[1] else None
     A = ctx.args
     dy = dy.to(_BF16).contiguous()
     need_dx = bool(ctx.needs_input_grad[0])
     dx, dacc = torch.ops.lorafusion_b200.lora_bwd(
-        dy, x, w, list(a), list(b), s_hat, bits, A["ranks"], A["scalings"], A["ps"], A["seeds"], A["segs"],
+        dy, x, w, a_cat, b_cat, s_hat, bits, A["ranks"], A["scalings"], A["ps"], A["seeds"], A["segs"],
         A["offset"], offset_dev, keep_mask, A["training"], A["share_blocks"], A["row_base"], A["cache_id"], need_dx)
     segs = A["segs"]
     segments = [Segment(*segs[i:i + 4]) for i in range(0, len(segs), 4)]
@@ -393,13 +407,14 @@ def _group_plan(j, x_rows, k, n, ranks, scalings, ps, seeds, offset, offset_dev,
 def lora_group_fwd(x: torch.Tensor, ws: list[torch.Tensor], a: list[torch.Tensor], b: list[torch.Tensor],
                    ranks: list[int], scalings: list[float], ps: list[float], seeds: list[int], offset: int,
                    offset_dev: Optional[torch.Tensor], training: bool,
-                   cache_id: int) -> tuple[list[torch.Tensor], list[torch.Tensor], list[torch.Tensor]]:
+                   cache_id: int) -> tuple[list[torch.Tensor], list[torch.Tensor], list[torch.Tensor],
+                                           list[torch.Tensor], list[torch.Tensor]]:
     """① + ② of every projection j (own adapter, seed and dropout mask, one shared Philox
-    offset): returns ([Y_j], [Ŝ_j], [packed keep mask_j or empty])."""
+    offset): returns ([Y_j], [Ŝ_j], [packed keep mask_j or empty], [A_j bf16], [B_j bf16])."""
     lib = _lib.load()
     m, k = x.shape
     st = _stream(x.device)
-    ys, shats, bits = [], [], []
+    ys, shats, bits, acs, bcs = [], [], [], [], []
     for j, w in enumerate(ws):
         plan = _group_plan(j, m, k, w.shape[0], ranks, scalings, ps, seeds, offset, offset_dev, training)
         plan.bind(x.device)
@@ -413,7 +428,9 @@ def lora_group_fwd(x: torch.Tensor, ws: list[torch.Tensor], a: list[torch.Tensor
         shats.append(s_hat)
         bits.append(plan.keep_bits if plan.keep_bits is not None
                     else torch.empty((0,), dtype=torch.uint8, device=x.device))
-    return ys, shats, bits
+        acs.append(_own(a_cat, a, None, x))
+        bcs.append(_own(b_cat, b, None, x))
+    return ys, shats, bits, acs, bcs
 
 
 @lora_group_fwd.register_fake
@@ -423,12 +440,14 @@ def _lora_group_fwd_fake(x, ws, a, b, ranks, scalings, ps, seeds, offset, offset
     shats = [x.new_empty((m, -(-r // 16) * 16)) for r in ranks]
     bits = [x.new_empty((m, k // 8), dtype=torch.uint8) if (training and p_ > 0) else
             x.new_empty((0,), dtype=torch.uint8) for p_ in ps]
-    return ys, shats, bits
+    acs = [x.new_empty((-(-r // 16) * 16, k)) for r in ranks]
+    bcs = [x.new_empty((w.shape[0], -(-r // 16) * 16)) for r, w in zip(ranks, ws)]
+    return ys, shats, bits, acs, bcs
 
 
 @torch.library.custom_op(f"{_NS}::lora_group_bwd", mutates_args=(), device_types="cuda")
-def lora_group_bwd(dys: list[torch.Tensor], x: torch.Tensor, ws: list[torch.Tensor], a: list[torch.Tensor],
-                   b: list[torch.Tensor], shats: list[torch.Tensor], bits: list[torch.Tensor], ranks: list[int],
+def lora_group_bwd(dys: list[torch.Tensor], x: torch.Tensor, ws: list[torch.Tensor], acs: list[torch.Tensor],
+                   bcs: list[torch.Tensor], shats: list[torch.Tensor], bits: list[torch.Tensor], ranks: list[int],
                    scalings: list[float], ps: list[float], seeds: list[int], offset: int,
                    offset_dev: Optional[torch.Tensor], training: bool, cache_id: int,
                    need_dx: bool) -> tuple[torch.Tensor, list[torch.Tensor]]:
@@ -439,28 +458,46 @@ def lora_group_bwd(dys: list[torch.Tensor], x: torch.Tensor, ws: list[torch.Tens
     m, k = x.shape
     st = _stream(x.device)
     dx = torch.empty((m, k) if need_dx else (0,), dtype=_BF16, device=x.device)
-    daccs = []
-    for j, w in enumerate(ws):
+    plans, daccs, dss = [], [], []
+    for j, w in enumerate(ws):  # ③ per projection (each reads its own dY)
         n = w.shape[0]
         plan = _group_plan(j, m, k, n, ranks, scalings, ps, seeds, offset, offset_dev, training)
         plan.bind(x.device, keep_bits=bits[j])
-        pp = ctypes.byref(plan.problem)
         R = plan.rank_total
-        a_cat, b_cat = _rank_concat_operands(plan, [a[j]], [b[j]], cache_id)
         acc = torch.zeros(R * k + n * R, dtype=torch.float32, device=x.device)
         ds = torch.empty((m, R), dtype=_BF16, device=x.device)
-        dy = dys[j]
-        _call("grad_up", lib.lf_grad_up, pp, _ptr(dy), _ptr(b_cat), _ptr(shats[j]), _ptr(ds), _ptr(acc[R * k:]), st)
-        _call("grad_down", lib.lf_grad_down, pp, _ptr(x), _ptr(ds), _ptr(acc[:R * k]), st)
-        if need_dx:
-            fn = lib.lf_grad_input if j == 0 else lib.lf_grad_input_accum
-            _call("grad_input", fn, pp, _ptr(dy), _ptr(w), _ptr(ds), _ptr(a_cat), _ptr(dx), st)
+        _call("grad_up", lib.lf_grad_up, ctypes.byref(plan.problem), _ptr(dys[j]), _ptr(bcs[j]), _ptr(shats[j]),
+              _ptr(ds), _ptr(acc[R * k:]), st)
+        plans.append(plan)
         daccs.append(acc)
+        dss.append(ds)
+    # ④ for all projections in one launch: each X tile leaves DRAM once
+    J = len(ws)
+    probs = (ctypes.POINTER(_lib.LfProblem) * J)(*[ctypes.pointer(pl.problem) for pl in plans])
+    ds_ptrs = (ctypes.c_void_p * J)(*[d_.data_ptr() for d_ in dss])
+    da_ptrs = (ctypes.c_void_p * J)(*[a_.data_ptr() for a_ in daccs])
+    _call("grad_down", lib.lf_grad_down_group, probs, J, _ptr(x), ds_ptrs, da_ptrs, st)
+    if need_dx:  # ⑤: the first writes dX, the others add into it in their epilogues
+        for j, w in enumerate(ws):
+            args = (ctypes.byref(plans[j].problem), _ptr(dys[j]), _ptr(w), _ptr(dss[j]), _ptr(acs[j]))
+            if j == 0:
+                _call("grad_input", lib.lf_grad_input, *args, _ptr(dx), st)
+                continue
+            st_ = _STATS
+            tok = st_.begin("grad_input") if st_ is not None else None
+            rc = lib.lf_grad_input_accum(*args, _ptr(dx), st)
+            if rc == _lib.LF_E_UNSUPPORTED:  # 256x512-tile shapes: their own output, then one add
+                tmp = torch.empty_like(dx)
+                rc = lib.lf_grad_input(*args, _ptr(tmp), st)
+                dx.add_(tmp)
+            if st_ is not None:
+                st_.end("grad_input", tok)
+            _lib.check(rc, "grad_input")
     return dx, daccs
 
 
 @lora_group_bwd.register_fake
-def _lora_group_bwd_fake(dys, x, ws, a, b, shats, bits, ranks, scalings, ps, seeds, offset, offset_dev, training,
+def _lora_group_bwd_fake(dys, x, ws, acs, bcs, shats, bits, ranks, scalings, ps, seeds, offset, offset_dev, training,
                          cache_id, need_dx):
     m, k = x.shape
     dx = x.new_empty((m, k) if need_dx else (0,))
@@ -476,18 +513,18 @@ _GROUP_ARGS = ("ranks", "scalings", "ps", "seeds", "offset", "offset_dev", "trai
 
 def _group_setup_context(ctx, inputs, output):
     x, ws, a, b, *rest = inputs
-    ys, shats, bits = output
-    ctx.mark_non_differentiable(*shats, *bits)
+    ys, shats, bits, acs, bcs = output
+    ctx.mark_non_differentiable(*shats, *bits, *acs, *bcs)
     args = dict(zip(_GROUP_ARGS, rest))
     offset_dev = args.pop("offset_dev")
     ctx.has_off = offset_dev is not None
     ctx.J = len(ws)
     ctx.param_dtypes = [p.dtype for p in a] + [p.dtype for p in b]
     ctx.args = args
-    ctx.save_for_backward(x, *ws, *a, *b, *shats, *bits, *([offset_dev] if ctx.has_off else []))
+    ctx.save_for_backward(x, *ws, *acs, *bcs, *shats, *bits, *([offset_dev] if ctx.has_off else []))
 
 
-def _group_backward(ctx, gys, _gs, _gbits):
+def _group_backward(ctx, gys, _gs=None, _gbits=None, _ga=None, _gb=None):
     J = ctx.J
     x, *rest = ctx.saved_tensors
     ws, a, b = rest[:J], rest[J:2 * J], rest[2 * J:3 * J]
@@ -532,9 +569,9 @@ def fused_lora_group(x: torch.Tensor, weights: Sequence[torch.Tensor], lora_a: S
     if x2.shape[0] == 0:
         return [_EmptyBatchFn.apply(x2, w.shape[0], a_, b_).reshape(lead + (w.shape[0],))
                 for w, a_, b_ in zip(weights, lora_a, lora_b)]
-    ys, _s, _bits = torch.ops.lorafusion_b200.lora_group_fwd(
+    ys = torch.ops.lorafusion_b200.lora_group_fwd(
         x2, list(weights), list(lora_a), list(lora_b), *packed, int(offset), offset_dev, bool(training),
-        _cache_handle(operand_cache))
+        _cache_handle(operand_cache))[0]
     return [y.reshape(lead + (y.shape[1],)) for y in ys]
 
 
@@ -555,14 +592,15 @@ class _SinkFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, n_adapters, plan_args, sink, *params):
         a, b = list(params[:n_adapters]), list(params[n_adapters:])
-        y, s_hat, bits = torch.ops.lorafusion_b200.lora_fwd(x, w, a, b, *plan_args)
-        _setup_context(ctx, (x, w, a, b, *plan_args), (y, s_hat, bits), mark=False)
+        out = torch.ops.lorafusion_b200.lora_fwd(x, w, a, b, *plan_args)
+        _setup_context(ctx, (x, w, a, b, *plan_args), out, mark=False)
+        y = out[0]
         ctx.sink = sink
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        dx, _, ga, gb = _backward(ctx, dy, None, None)[:4]
+        dx, _, ga, gb = _backward(ctx, dy)[:4]
         return (dx, None, None, None, None, *ga, *gb)
 
 
@@ -632,8 +670,7 @@ def _apply(x2, weight, lora_a, lora_b, packed, segs, offset, offset_dev, keep_ma
                  bool(share_blocks), int(row_base), int(cache_id))
     if sink is not None:
         return _SinkFn.apply(x2, weight, len(lora_a), plan_args, sink, *lora_a, *lora_b)
-    y, _s, _bits = torch.ops.lorafusion_b200.lora_fwd(x2, weight, list(lora_a), list(lora_b), *plan_args)
-    return y
+    return torch.ops.lorafusion_b200.lora_fwd(x2, weight, list(lora_a), list(lora_b), *plan_args)[0]
 
 
 def fused_lora(

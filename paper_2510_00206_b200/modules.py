@@ -410,9 +410,9 @@ class FusedLoRAGroup(nn.Module):
             ys = [_EmptyBatchFn.apply(x2, w.shape[0], a_, b_) for w, a_, b_ in zip(ws, a, b)]
         else:
             off, off_dev = _step_offsets(self, x2.device, self._has_dropout)
-            ys, _s, _bits = torch.ops.lorafusion_b200.lora_group_fwd(
+            ys = torch.ops.lorafusion_b200.lora_group_fwd(
                 x2, ws, a, b, *self._packed, off, off_dev, self.training,
-                0 if self.capturable else _cache_handle(self._operands))
+                0 if self.capturable else _cache_handle(self._operands))[0]
         out = []
         for p, y in zip(projs, ys):
             y = y.reshape(lead + (p.out_features,))
