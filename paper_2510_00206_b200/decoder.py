@@ -27,6 +27,7 @@ from torch import nn
 
 from .baseline import unfused_multi_lora
 from .errors import ValidationError
+from .functional import refresh_stale_operand_shadows
 from .modules import FusedMultiLoRA
 from .plan import AdapterConfig, Segment
 
@@ -316,6 +317,7 @@ class GraphedTrainStep:
             self.losses.append(loss.detach())
 
     def __call__(self):
+        refresh_stale_operand_shadows()
         for g in self.graphs:
             g.replay()
         if self.reducer is not None:

@@ -123,12 +123,84 @@ _GENERATION = [0]
 
 
 def invalidate_operand_caches(*_args, **_kwargs) -> None:
-    """Forget every cached bf16 A_cat/B_cat (call after updating adapter weights outside a
-    torch.optim optimizer step, e.g. through ``p.data``)."""
+    """Forget every cached bf16 A_cat/B_cat and refresh every persistent bf16 operand copy
+    (call after updating adapter weights outside a torch.optim optimizer step, e.g. through
+    ``p.data``). Runs automatically after every optimizer step."""
     _GENERATION[0] += 1
+    for sh in list(_SHADOW_SETS):
+        sh.refresh_all()
 
 
+_SHADOW_SETS: "weakref.WeakSet" = weakref.WeakSet()
 register_optimizer_step_post_hook(invalidate_operand_caches)
+
+
+class ShadowOperands:
+    """Persistent bf16 operand copies (A (R,k), B (n,R), zero-padded to R = rank rounded up
+    to 16) of single-adapter projections, for ``capturable`` modules: a CUDA graph reads them
+    at fixed addresses, so no cast runs inside the graph. They are refreshed in place — all
+    of them in one multi-tensor copy per device — after every optimizer step (the global
+    post-hook above), and by a lookup that sees a parameter's in-place version change; an
+    update through ``p.data`` needs ``invalidate_operand_caches()`` (or the module's
+    ``invalidate_operands()``)."""
+
+    def __init__(self):
+        self._d: dict = {}
+        _SHADOW_SETS.add(self)
+
+    def lookup(self, a: torch.Tensor, b: torch.Tensor, R: int) -> tuple[torch.Tensor, torch.Tensor]:
+        key = (a.data_ptr(), b.data_ptr(), R)
+        ent = self._d.get(key)
+        if ent is None:
+            if len(self._d) >= 16:  # parameters moved (module.to): drop the stale copies
+                self._d.clear()
+            ent = [torch.zeros((R, a.shape[1]), dtype=_BF16, device=a.device),
+                   torch.zeros((b.shape[0], R), dtype=_BF16, device=b.device), -1, -1,
+                   weakref.ref(a), weakref.ref(b)]
+            self._d[key] = ent
+        if ent[2] != a._version or ent[3] != b._version:
+            self._copy([ent])
+        return ent[0], ent[1]
+
+    @staticmethod
+    def _copy(ents) -> None:
+        by_dev: dict = {}
+        for ent in ents:
+            a, b = ent[4](), ent[5]()
+            if a is None or b is None:
+                continue
+            r = a.shape[0]
+            dst, src = by_dev.setdefault(a.device, ([], []))
+            dst += [ent[0][:r], ent[1][:, :r]]
+            src += [a.detach(), b.detach()]
+            ent[2], ent[3] = a._version, b._version
+        with torch.no_grad():
+            for dst, src in by_dev.values():
+                torch._foreach_copy_(dst, src)
+
+    def refresh_all(self) -> None:
+        self._copy(list(self._d.values()))
+
+    def stale(self) -> list:
+        """Entries whose parameters changed in place since their last copy (host check)."""
+        out = []
+        for ent in self._d.values():
+            a, b = ent[4](), ent[5]()
+            if a is not None and b is not None and (ent[2] != a._version or ent[3] != b._version):
+                out.append(ent)
+        return out
+
+
+def refresh_stale_operand_shadows() -> None:
+    """Re-copy the persistent bf16 operands whose fp32 parameters changed in place (version
+    counter) since their last copy — a host-side check, one multi-tensor copy only when
+    something changed. GraphedStep.replay() calls it before every replay."""
+    ents = [e for sh in list(_SHADOW_SETS) for e in sh.stale()]
+    if ents:
+        ShadowOperands._copy(ents)
+
+    def clear(self) -> None:
+        self.refresh_all()
 
 
 class OperandCache:
@@ -155,11 +227,11 @@ class OperandCache:
 
 
 # operators take an integer handle for the calling module's operand cache
-_CACHES: "weakref.WeakValueDictionary[int, OperandCache]" = weakref.WeakValueDictionary()
+_CACHES: "weakref.WeakValueDictionary[int, OperandCache | ShadowOperands]" = weakref.WeakValueDictionary()
 _ids = itertools.count(1)
 
 
-def _cache_handle(cache: OperandCache | None) -> int:
+def _cache_handle(cache: "OperandCache | ShadowOperands | None") -> int:
     if cache is None:
         return 0
     h = getattr(cache, "_handle", None)
@@ -182,6 +254,12 @@ def _own(t: torch.Tensor | None, inputs: Sequence[torch.Tensor], empty_shape, li
 
 def _rank_concat_operands(plan: LayerPlan, a: Sequence[torch.Tensor], b: Sequence[torch.Tensor], cache_id: int):
     cache = _CACHES.get(cache_id) if cache_id else None
+    if isinstance(cache, ShadowOperands):
+        blocks = plan.column_blocks()
+        if len(blocks) == 1:
+            ad = blocks[0][0]
+            return cache.lookup(a[ad], b[ad], blocks[0][2])
+        cache = None  # several adapters in one call: gather per call
     key = None
     if cache is not None:
         blocks = plan.column_blocks()
@@ -191,10 +269,29 @@ def _rank_concat_operands(plan: LayerPlan, a: Sequence[torch.Tensor], b: Sequenc
         hit = cache.get(key)
         if hit is not None:
             return hit
-    a_cat, b_cat = plan.gather_a(a), plan.gather_b(b)
+    blocks = plan.column_blocks()
+    if len(blocks) == 1 and blocks[0][2] == a[blocks[0][0]].shape[0]:
+        # one adapter, rank a multiple of 16: both casts in one multi-tensor launch
+        ad = blocks[0][0]
+        a_cat = torch.empty(a[ad].shape, dtype=_BF16, device=a[ad].device)
+        b_cat = torch.empty(b[ad].shape, dtype=_BF16, device=b[ad].device)
+        torch._foreach_copy_([a_cat, b_cat], [a[ad].detach(), b[ad].detach()])
+    else:
+        a_cat, b_cat = plan.gather_a(a), plan.gather_b(b)
     if cache is not None:
         cache.put(key, (a_cat, b_cat))
     return a_cat, b_cat
+
+
+def _group_operands(a: Sequence[torch.Tensor], b: Sequence[torch.Tensor], ranks) -> tuple[list, list] | None:
+    """bf16 copies of every projection's A and B in one multi-tensor cast (ranks multiples of
+    16, no padding needed), or None."""
+    if any(_padr(r) != r for r in ranks):
+        return None
+    acs = [torch.empty(t.shape, dtype=_BF16, device=t.device) for t in a]
+    bcs = [torch.empty(t.shape, dtype=_BF16, device=t.device) for t in b]
+    torch._foreach_copy_(acs + bcs, [t.detach() for t in a] + [t.detach() for t in b])
+    return acs, bcs
 
 
 # --------------------------------------------------------------------------------------
@@ -342,6 +439,8 @@ def _setup_context(ctx, inputs, output, mark: bool = True):
     y, s_hat, bits, a_cat, b_cat = output
     if mark:
         ctx.mark_non_differentiable(s_hat, bits, a_cat, b_cat)
+    # no zero tensors for the outputs nothing differentiates (Ŝ, keep bits, operands)
+    ctx.set_materialize_grads(False)
     args = dict(zip(_PLAN_ARGS, rest))
     # the gradient of a non-tensor argument is None, except that an empty list (no segments)
     # flattens like a list of tensors and must come back as []
@@ -360,6 +459,8 @@ def _backward(ctx, dy, _ds=None, _dbits=None, _da=None, _db=None):
     offset_dev = opt.pop(0) if ctx.has_opt[0] else None
     keep_mask = opt.pop(0) if ctx.has_opt[1] else None
     A = ctx.args
+    if dy is None:  # Y unused downstream (materialize_grads is off)
+        dy = torch.zeros((x.shape[0], w.shape[0]), dtype=_BF16, device=x.device)
     dy = dy.to(_BF16).contiguous()
     need_dx = bool(ctx.needs_input_grad[0])
     dx, dacc = torch.ops.lorafusion_b200.lora_bwd(
@@ -398,6 +499,10 @@ torch.library.register_autograd(f"{_NS}::lora_fwd", _backward, setup_context=_se
 # --------------------------------------------------------------------------------------
 # shared-input groups: several LoRA linears reading the same X
 # --------------------------------------------------------------------------------------
+def _padr(r: int) -> int:
+    return -(-int(r) // 16) * 16
+
+
 def _group_plan(j, x_rows, k, n, ranks, scalings, ps, seeds, offset, offset_dev, training) -> LayerPlan:
     return _plan(x_rows, k, n, [ranks[j]], [scalings[j]], [ps[j]], [seeds[j]], [0, 0, x_rows, 0], offset, offset_dev,
                  None, training, True, 0)
@@ -415,11 +520,15 @@ def lora_group_fwd(x: torch.Tensor, ws: list[torch.Tensor], a: list[torch.Tensor
     m, k = x.shape
     st = _stream(x.device)
     ys, shats, bits, acs, bcs = [], [], [], [], []
+    pre = _group_operands(a, b, ranks) if not cache_id else None  # shadows / cache: per projection below
     for j, w in enumerate(ws):
         plan = _group_plan(j, m, k, w.shape[0], ranks, scalings, ps, seeds, offset, offset_dev, training)
         plan.bind(x.device)
         pp = ctypes.byref(plan.problem)
-        a_cat, b_cat = _rank_concat_operands(plan, [a[j]], [b[j]], cache_id)
+        if pre is not None:
+            a_cat, b_cat = pre[0][j], pre[1][j]
+        else:
+            a_cat, b_cat = _rank_concat_operands(plan, [a[j]], [b[j]], cache_id)
         s_hat = torch.empty((m, plan.rank_total), dtype=_BF16, device=x.device)
         y = torch.empty((m, w.shape[0]), dtype=_BF16, device=x.device)
         _call("dropout_down_fwd", lib.lf_dropout_down_fwd, pp, _ptr(x), _ptr(a_cat), _ptr(s_hat), st)
@@ -450,21 +559,26 @@ def lora_group_bwd(dys: list[torch.Tensor], x: torch.Tensor, ws: list[torch.Tens
                    bcs: list[torch.Tensor], shats: list[torch.Tensor], bits: list[torch.Tensor], ranks: list[int],
                    scalings: list[float], ps: list[float], seeds: list[int], offset: int,
                    offset_dev: Optional[torch.Tensor], training: bool, cache_id: int,
-                   need_dx: bool) -> tuple[torch.Tensor, list[torch.Tensor]]:
-    """③ + ④ + ⑤ of every projection: returns (dX = Σ_j dX_j, [dA_j | dB_j] fp32 flat per j).
+                   need_dx: bool) -> tuple[torch.Tensor, torch.Tensor]:
+    """③ + ④ + ⑤ of every projection: returns (dX = Σ_j dX_j, [dA_0 | dB_0 | dA_1 | dB_1 ...]
+    fp32 flat, one zero-fill for the whole group).
     The first ⑤ writes dX, the others add into it in their epilogues (lf_grad_input_accum):
     no separate gradient-sum kernels."""
     lib = _lib.load()
     m, k = x.shape
     st = _stream(x.device)
     dx = torch.empty((m, k) if need_dx else (0,), dtype=_BF16, device=x.device)
+    sizes = [_padr(r) * (k + w.shape[0]) for r, w in zip(ranks, ws)]
+    dacc = torch.zeros(sum(sizes), dtype=torch.float32, device=x.device)
     plans, daccs, dss = [], [], []
+    pos = 0
     for j, w in enumerate(ws):  # ③ per projection (each reads its own dY)
         n = w.shape[0]
         plan = _group_plan(j, m, k, n, ranks, scalings, ps, seeds, offset, offset_dev, training)
         plan.bind(x.device, keep_bits=bits[j])
         R = plan.rank_total
-        acc = torch.zeros(R * k + n * R, dtype=torch.float32, device=x.device)
+        acc = dacc[pos:pos + sizes[j]]
+        pos += sizes[j]
         ds = torch.empty((m, R), dtype=_BF16, device=x.device)
         _call("grad_up", lib.lf_grad_up, ctypes.byref(plan.problem), _ptr(dys[j]), _ptr(bcs[j]), _ptr(shats[j]),
               _ptr(ds), _ptr(acc[R * k:]), st)
@@ -493,7 +607,7 @@ def lora_group_bwd(dys: list[torch.Tensor], x: torch.Tensor, ws: list[torch.Tens
             if st_ is not None:
                 st_.end("grad_input", tok)
             _lib.check(rc, "grad_input")
-    return dx, daccs
+    return dx, dacc
 
 
 @lora_group_bwd.register_fake
@@ -501,11 +615,7 @@ def _lora_group_bwd_fake(dys, x, ws, acs, bcs, shats, bits, ranks, scalings, ps,
                          cache_id, need_dx):
     m, k = x.shape
     dx = x.new_empty((m, k) if need_dx else (0,))
-    daccs = []
-    for r, w in zip(ranks, ws):
-        R = -(-r // 16) * 16
-        daccs.append(x.new_empty((R * k + w.shape[0] * R,), dtype=torch.float32))
-    return dx, daccs
+    return dx, x.new_empty((sum(_padr(r) * (k + w.shape[0]) for r, w in zip(ranks, ws)),), dtype=torch.float32)
 
 
 _GROUP_ARGS = ("ranks", "scalings", "ps", "seeds", "offset", "offset_dev", "training", "cache_id")
@@ -515,6 +625,7 @@ def _group_setup_context(ctx, inputs, output):
     x, ws, a, b, *rest = inputs
     ys, shats, bits, acs, bcs = output
     ctx.mark_non_differentiable(*shats, *bits, *acs, *bcs)
+    ctx.set_materialize_grads(False)
     args = dict(zip(_GROUP_ARGS, rest))
     offset_dev = args.pop("offset_dev")
     ctx.has_off = offset_dev is not None
@@ -534,13 +645,16 @@ def _group_backward(ctx, gys, _gs=None, _gbits=None, _ga=None, _gb=None):
     need_dx = bool(ctx.needs_input_grad[0])
     dys = [(g if g is not None else torch.zeros((x.shape[0], w.shape[0]), dtype=_BF16, device=x.device))
            .to(_BF16).contiguous() for g, w in zip(gys, ws)]
-    dx, daccs = torch.ops.lorafusion_b200.lora_group_bwd(
+    dx, dacc = torch.ops.lorafusion_b200.lora_group_bwd(
         dys, x, list(ws), list(a), list(b), list(shats), list(bits), A["ranks"], A["scalings"], A["ps"], A["seeds"],
         A["offset"], offset_dev, A["training"], A["cache_id"], need_dx)
     k = x.shape[1]
     ga, gb = [], []
-    for j, (r, w, acc) in enumerate(zip(A["ranks"], ws, daccs)):
-        R = -(-r // 16) * 16
+    pos = 0
+    for j, (r, w) in enumerate(zip(A["ranks"], ws)):
+        R = _padr(r)
+        acc = dacc[pos:pos + R * (k + w.shape[0])]
+        pos += R * (k + w.shape[0])
         ga.append(acc[:R * k].view(R, k)[:r].to(ctx.param_dtypes[j]))
         gb.append(acc[R * k:].view(w.shape[0], R)[:, :r].to(ctx.param_dtypes[J + j]))
     return (dx if need_dx else None, [None] * J, ga, gb) + (None,) * len(_GROUP_ARGS)

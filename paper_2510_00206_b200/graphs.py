@@ -5,7 +5,9 @@ C-ABI argument packing, autograd); at small token counts (C1: 2048 tokens) the h
 takes longer than the kernels. Capturing the whole step once and replaying it removes
 the host from the loop. Layers must be built with ``capturable=True`` so the Philox step
 counter advances on the device (a fresh dropout mask per replay, SPEC.md §3) and the bf16
-operand copies are re-cast from the fp32 master weights inside the graph.
+operands are persistent copies the graph reads at fixed addresses (functional.ShadowOperands):
+refreshed after every optimizer step and, before each replay, for any adapter weight whose
+in-place version changed (updates through ``p.data`` need invalidate_operand_caches()).
 
     step = GraphedStep(lambda: train_step(...))   # warm-up + capture
     for _ in range(n):
@@ -21,6 +23,7 @@ from typing import Callable
 import torch
 
 from .errors import ValidationError
+from .functional import refresh_stale_operand_shadows
 
 
 class GraphedStep:
@@ -44,5 +47,6 @@ class GraphedStep:
         self.output = out.detach() if isinstance(out, torch.Tensor) else out
 
     def replay(self):
+        refresh_stale_operand_shadows()  # adapter weights changed in place since the last replay
         self.graph.replay()
         return self.output

@@ -13,14 +13,16 @@ seed and a per-forward 64-bit offset; backward reuses the forward's pair through
 packed keep mask, so no byte mask is ever stored. Where the offset comes from
 (``dropout_rng``):
 
-* ``"torch"`` (default): drawn from torch's CUDA generator on the device (one int64 per
-  training forward) — dropout then follows ``torch.manual_seed`` like ``nn.Dropout``,
-  replays fresh inside CUDA graphs, and ``torch.utils.checkpoint`` (which restores the RNG
-  state before recomputing) redraws the original mask.
-* ``"counter"``: a per-module step counter (on the host, or on the device with
-  ``capturable=True``), advanced once per training forward — deterministic offsets
-  0, 1, 2, ... that ``dropout_state()`` saves and restores. Not checkpoint-safe: a
-  recomputed forward would advance it again.
+* ``"torch"`` (default without ``capturable``): drawn from torch's CUDA generator on the
+  device (one int64 per training forward) — dropout then follows ``torch.manual_seed`` like
+  ``nn.Dropout`` and ``torch.utils.checkpoint`` (which restores the RNG state before
+  recomputing) redraws the original mask.
+* ``"counter"`` (default with ``capturable=True``): a per-module step counter (on the host,
+  or on the device for capturable modules), advanced once per training forward —
+  deterministic offsets 0, 1, 2, ... that ``dropout_state()`` saves and restores. A CUDA
+  graph replays it with one tiny add per forward; a random draw inside a graph costs a
+  launch gap of ~30 µs per forward on B200 (profiles/r02_step_breakdown.txt). Not
+  checkpoint-safe: a recomputed forward would advance it again.
 """
 from __future__ import annotations
 
@@ -31,8 +33,8 @@ import torch
 from torch import nn
 
 from .errors import ValidationError
-from .functional import (OperandCache, _apply, _cache_handle, _check_call, _EmptyBatchFn, _flatten_input,
-                         fused_multi_lora, pack_adapters)
+from .functional import (OperandCache, ShadowOperands, _apply, _cache_handle, _check_call, _EmptyBatchFn,
+                         _flatten_input, fused_multi_lora, pack_adapters)
 from .plan import AdapterConfig, Segment
 
 
@@ -68,12 +70,14 @@ def _frozen_base(base: nn.Linear | torch.Tensor) -> tuple[torch.Tensor, torch.Te
 _DROPOUT_RNGS = ("torch", "counter")
 
 
-def _init_capturable(mod: nn.Module, capturable: bool, device, dropout_rng: str) -> None:
+def _init_capturable(mod: nn.Module, capturable: bool, device, dropout_rng: str | None) -> None:
     """``capturable=True`` (as torch.optim's flag): the bf16 operand copies of the fp32
     adapter weights are re-cast inside each call (no host-side cache), and in ``"counter"``
     mode the Philox step counter lives on the device and is advanced there by every training
     forward — so a forward+backward captured in a CUDA graph replays with a fresh dropout
     mask and the current weights (``"torch"`` mode draws its offsets on the device anyway)."""
+    if dropout_rng is None:
+        dropout_rng = "counter" if capturable else "torch"
     if dropout_rng not in _DROPOUT_RNGS:
         raise ValidationError(f"dropout_rng must be one of {_DROPOUT_RNGS}, got {dropout_rng!r}")
     mod.capturable = bool(capturable)
@@ -136,7 +140,7 @@ class FusedLoRA(nn.Module):
         dtype: torch.dtype = torch.float32,
         generator: torch.Generator | None = None,
         capturable: bool = False,
-        dropout_rng: str = "torch",
+        dropout_rng: str | None = None,
     ):
         super().__init__()
         w, bias = _frozen_base(base)
@@ -154,7 +158,9 @@ class FusedLoRA(nn.Module):
         self.lora_B = nn.Linear(rank, self.out_features, bias=False, device=dev, dtype=dtype)
         _init_lora(self.lora_A, self.lora_B, init, generator)
         self._offset = 0
-        self._operands = OperandCache()
+        # bf16 operands: a version-keyed cache (eager), or persistent copies a CUDA graph can
+        # read at fixed addresses, refreshed after every optimizer step (capturable)
+        self._operands = ShadowOperands() if capturable else OperandCache()
 
     @property
     def base_weight(self) -> torch.Tensor:
@@ -191,7 +197,7 @@ class FusedLoRA(nn.Module):
         else:
             off, off_dev = _step_offsets(self, x2.device, self.config.dropout_p > 0 and keep_mask is None)
             y = _apply(x2, w, [a], [b], self._packed, [0, 0, m, 0], off, off_dev, keep_mask, self.training, True, 0,
-                       0 if self.capturable else _cache_handle(self._operands))
+                       _cache_handle(self._operands))
         y = y.reshape(lead + (n,))
         if self.base_bias is not None:
             y = y + self.base_bias.to(y.dtype)
@@ -217,7 +223,7 @@ class FusedMultiLoRA(nn.Module):
         track_slot_grads: bool = False,
         generator: torch.Generator | None = None,
         capturable: bool = False,
-        dropout_rng: str = "torch",
+        dropout_rng: str | None = None,
     ):
         super().__init__()
         if not adapters:
@@ -237,7 +243,9 @@ class FusedMultiLoRA(nn.Module):
         for la, lb in zip(self.lora_A, self.lora_B):
             _init_lora(la, lb, init, generator)
         self._offset = 0
-        self._operands = OperandCache()
+        # bf16 operands: a version-keyed cache (eager), or persistent copies a CUDA graph can
+        # read at fixed addresses, refreshed after every optimizer step (capturable)
+        self._operands = ShadowOperands() if capturable else OperandCache()
         self.track_slot_grads = track_slot_grads
         # (adapter slot, global batch) -> [dA (r x k) fp32, dB (n x r) fp32]
         self.slot_grads: dict[tuple[int, int], list[torch.Tensor]] = {}
@@ -288,7 +296,7 @@ class FusedMultiLoRA(nn.Module):
             training=self.training,
             grad_sink=self._sink if self.track_slot_grads else None,
             offset_dev=off_dev,
-            operand_cache=None if self.capturable else self._operands,
+            operand_cache=self._operands,
         )
         if self.base is not None and self.base.bias is not None:
             y = y + self.base.bias.to(y.dtype)
@@ -322,7 +330,7 @@ class FusedLoRAGroup(nn.Module):
         dtype: torch.dtype = torch.float32,
         generator: torch.Generator | None = None,
         capturable: bool = False,
-        dropout_rng: str = "torch",
+        dropout_rng: str | None = None,
     ):
         super().__init__()
         names = list(projections)
@@ -373,7 +381,7 @@ class FusedLoRAGroup(nn.Module):
         self.in_features = ks.pop()
         _init_capturable(self, capturable, self.proj(names[0]).base_weight.device, dropout_rng)
         self._offset = 0
-        self._operands = OperandCache(capacity=2 * len(names))
+        self._operands = ShadowOperands() if capturable else OperandCache(capacity=2 * len(names))
         cfgs = [self.proj(nm).config for nm in names]
         self._packed = pack_adapters(cfgs)
         self._has_dropout = any(c.dropout_p > 0 for c in cfgs)
@@ -411,8 +419,7 @@ class FusedLoRAGroup(nn.Module):
         else:
             off, off_dev = _step_offsets(self, x2.device, self._has_dropout)
             ys = torch.ops.lorafusion_b200.lora_group_fwd(
-                x2, ws, a, b, *self._packed, off, off_dev, self.training,
-                0 if self.capturable else _cache_handle(self._operands))[0]
+                x2, ws, a, b, *self._packed, off, off_dev, self.training, _cache_handle(self._operands))[0]
         out = []
         for p, y in zip(projs, ys):
             y = y.reshape(lead + (p.out_features,))

@@ -86,3 +86,40 @@ def test_graphed_multi_lora_replays_track_weight_updates():
     torch.cuda.synchronize()
     assert not _close(y1, y0, tol=1e-2)
     assert _close(y1, eager)
+
+
+def test_graphed_fused_lora_sees_optimizer_and_inplace_updates():
+    """Capturable FusedLoRA reads persistent bf16 operand copies inside the graph; they are
+    refreshed by every optimizer step (fused AdamW included: no version bump) and, before a
+    replay, for parameters changed in place."""
+    g = torch.Generator(device=DEV).manual_seed(5)
+    m, k, n = 512, 256, 384
+    w = (torch.randn(n, k, device=DEV, generator=g) / 16).to(torch.bfloat16)
+    cap = FusedLoRA(w, rank=16, dropout_p=0.0, init="gaussian", capturable=True, generator=g)
+    ref = FusedLoRA(w, rank=16, dropout_p=0.0, init="gaussian")
+    x = torch.randn(m, k, device=DEV, generator=g).to(torch.bfloat16)
+    opt = torch.optim.AdamW(cap.parameters(), lr=1e-2, fused=True)
+
+    def step():
+        y = cap(x)
+        y.float().square().mean().backward()
+        return y.detach()
+
+    graphed = GraphedStep(step, warmup=2)
+
+    def check():
+        y = graphed.replay()
+        with torch.no_grad():
+            ref.lora_A.weight.copy_(cap.lora_A.weight)
+            ref.lora_B.weight.copy_(cap.lora_B.weight)
+            ref.invalidate_operands()
+            assert torch.equal(y, ref(x))
+
+    check()
+    for _ in range(2):
+        opt.step()  # post-hook refreshes the copies
+        opt.zero_grad(set_to_none=False)
+        check()
+    with torch.no_grad():
+        cap.lora_B.weight.mul_(2.0)  # in place: version bump, refreshed before the replay
+    check()

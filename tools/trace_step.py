@@ -30,13 +30,8 @@ def main():
     m = bench.tokens_per_gpu(args.config)
     layers, inputs, grads = bench.build_layers(args.config, m, 16, 0.1, dev, gen, capturable=args.graph)
     if args.unfused:
-        base = {}
-        for name, k, n, grp in bench.projections(args.config):
-            layer = layers[name]
-            a = layer.lora_A.weight.detach().to(torch.bfloat16).clone().requires_grad_(True)
-            b = layer.lora_B.weight.detach().to(torch.bfloat16).clone().requires_grad_(True)
-            base[name] = (layer.base_weight, a, b)
-        step = lambda: bench.unfused_step(args.config, base, inputs, grads, 0.1)
+        base = bench.unfused_base(args.config, layers)
+        step = lambda: bench.unfused_step(args.config, base, inputs, grads, 0.1)  # noqa: E731
     else:
         def step():
             bench.zero_grads(layers, inputs)
@@ -81,7 +76,7 @@ def main():
     prev_end = t0
     for e in kern:
         gap = max(0.0, e.time_range.start - prev_end)
-        a = agg[e.name[:60]]
+        a = agg[e.name[:60] if "elementwise" not in e.name else e.name[e.name.find("<"):][:150]]
         a[0] += 1
         a[1] += e.time_range.end - e.time_range.start
         a[2] += gap
