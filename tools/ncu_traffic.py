@@ -4,8 +4,9 @@
         python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline
     python tools/ncu_traffic.py gpurun_out/gemm_step.ncu-rep [c2|c4] > profiles/gemm_traffic[_c4].json
 
-The first 14 GEMM launches are one step (② then ⑤ for each of the 7 projections) of the
-config (default c2; for c4 capture `bench.py --config c4`, the --metrics of METRICS suffice).
+The first 14 GEMM launches are one step of the config in bench.py's order (a shared-input
+group's ② launches, then its ⑤ launches; single projections ② then ⑤), default c2; for c4
+capture `bench.py --config c4` (the --metrics of METRICS suffice).
 Algorithmic bytes per launch follow SURVEY.md §8(d): ② 2(mk+kn+mr+rn)+2mn, ⑤ 2(mn+kn+mr+kr)+2mk.
 """
 from __future__ import annotations
@@ -42,12 +43,27 @@ def main():
         tu = u["gpu__time_duration.sum"]
         t_us = {"nsecond": t / 1e3, "ns": t / 1e3, "usecond": t, "us": t, "msecond": t * 1e3, "ms": t * 1e3}[tu]
         launches.append({"kernel": d["Kernel Name"][:60], "dram_read": rd, "dram_write": wr, "dur_us": t_us})
-    from bench import projections, tokens_per_gpu  # noqa: E402  (bench order)
-    m, r = tokens_per_gpu(config), 16
-    alg = []  # bench.py runs each projection's forward and backward back to back
-    for name, k, n, _ in projections(config):
-        alg.append((name + " base_fwd", 2 * (m * k + k * n + m * r + r * n) + 2 * m * n))
-        alg.append((name + " grad_input", 2 * (m * n + k * n + m * r + k * r) + 2 * m * k))
+    import bench  # noqa: E402  (bench order)
+
+    m, r = bench.tokens_per_gpu(config), 16
+    shapes = {name: (k, n) for name, k, n, _ in bench.projections(config)}
+    grouped = os.environ.get("LF_BENCH_GROUP", "1") != "0"
+    order = []  # bench.fused_step: a shared-input group runs all forwards, then all backwards
+    by_grp: dict = {}
+    for name, k, n, grp in bench.projections(config):
+        by_grp.setdefault(grp, []).append(name)
+    for grp, names in by_grp.items():
+        if grouped and config != "c3" and grp in bench.SHARED_INPUT_GROUPS and len(names) > 1:
+            order += [(nm, "base_fwd") for nm in names] + [(nm, "grad_input") for nm in names]
+        else:
+            for nm in names:
+                order += [(nm, "base_fwd"), (nm, "grad_input")]
+    alg = []
+    for name, kind in order:
+        k, n = shapes[name]
+        b = (2 * (m * k + k * n + m * r + r * n) + 2 * m * n if kind == "base_fwd"
+             else 2 * (m * n + k * n + m * r + k * r) + 2 * m * k)
+        alg.append((f"{name} {kind}", b))
     n = min(len(launches), len(alg))
     dram = sum(l["dram_read"] + l["dram_write"] for l in launches[:n])
     algb = sum(a for _, a in alg[:n])
