@@ -137,12 +137,12 @@ LF_API int lf_grad_down_group(const LfProblem* const* probs, int32_t nproj, cons
 LF_API int lf_grad_input(const LfProblem* p, const uint16_t* dy, const uint16_t* w, const uint16_t* ds,
                   const uint16_t* a_cat, uint16_t* dx, void* stream);
 
-/* ⑤ accumulating: dx += dY·W + M ⊙ (dŜ·A_cat) — dx (bf16, m x k) is read and written once in
- * the GEMM epilogue (fp32 sum, one bf16 rounding: what torch's add of the two bf16 tensors
- * gives). Several projections that read the same input (q/k/v, gate/up: SURVEY §8(f)#4)
- * sum their input gradients this way instead of through separate elementwise adds.
- * LF_E_UNSUPPORTED (nothing launched) for shapes that run on 256x512 tiles: add instead.
- * ABI 4. */
+/* ⑤ accumulating: dx += dY·W + M ⊙ (dŜ·A_cat) — the GEMM epilogue adds its bf16 result into
+ * dx (bf16, m x k) in L2 (red.add of bf16 pairs, one rounding per element; each element is
+ * added once per call, so the sum is deterministic). Several projections that read the
+ * same input (q/k/v, gate/up: SURVEY §8(f)#4) sum their input gradients this way instead of
+ * through separate elementwise adds. Every tile shape is supported (LF_E_UNSUPPORTED is
+ * kept for ABI 4 callers). ABI 4. */
 LF_API int lf_grad_input_accum(const LfProblem* p, const uint16_t* dy, const uint16_t* w, const uint16_t* ds,
                         const uint16_t* a_cat, uint16_t* dx, void* stream);
 

@@ -139,40 +139,22 @@ __device__ __forceinline__ uint32_t dgrad_keep32(const LfSegTable& t, int seg, i
   return dgrad_keep32_slow(t, seg, row, col, ncols);
 }
 
-// `accumulate` (lf_grad_input_accum): C += result — the old bf16 values and the new ones are
-// summed in fp32 and rounded once, as torch adds two bf16 tensors (the input gradient of
-// projections that share X is summed by the GEMMs instead of separate elementwise adds).
-// The epilogue prefetches its rows of C into L2 before it waits for the accumulator, then
-// loads them in batches, so the read-modify-write costs no DRAM round trip per chunk.
-__device__ __forceinline__ uint4 add_bf16x8(uint4 v, uint4 o) {
-  const uint32_t a[4] = {v.x, v.y, v.z, v.w}, b[4] = {o.x, o.y, o.z, o.w};
-  uint32_t r[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a[i]));
-    const float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b[i]));
-    r[i] = pack_bf16x2(fa.x + fb.x, fa.y + fb.y);
-  }
-  return make_uint4(r[0], r[1], r[2], r[3]);
+// `accumulate` (lf_grad_input_accum): C += result, the input gradient of projections that
+// share X summed by the GEMMs instead of separate elementwise adds. The epilogue hands the
+// addition to L2 (red.global.add.noftz.v4.bf16x2: 8 bf16 per lane, each element added once
+// per launch, so the sum is deterministic): no load of the old C, no round trip in the
+// epilogue — a register read-modify-write cost short-K tiles 30% (k/v dgrad) and did not fit
+// the 256 x 512 tiles' registers at all.
+__device__ __forceinline__ void red_add_bf16x8(__nv_bfloat16* dst, uint4 v) {
+  asm volatile("red.global.add.noftz.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
 }
-__device__ __forceinline__ uint4 ld_c8(const __nv_bfloat16* src) {
-  uint4 v;
-  asm volatile("ld.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src));
-  return v;
-}
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-// L2 prefetch of `ncols` bf16 of one C row starting at `col` (128-byte lines)
-__device__ __forceinline__ void prefetch_c_row(const __nv_bfloat16* crow, int col, int ncols, int N) {
-  for (int c = col; c < col + ncols && c < N; c += 64) prefetch_l2(crow + c);
-}
-// one 16-byte chunk of C (the wide tiles' deferred stores hold 128 words of the tile in
-// registers already: one chunk at a time keeps the read-modify-write out of local memory;
-// the row is L2-hot from the prefetch)
 __device__ __forceinline__ void store_c8(__nv_bfloat16* dst, uint4 v, int accumulate) {
-  if (accumulate) v = add_bf16x8(v, ld_c8(dst));
-  *reinterpret_cast<uint4*>(dst) = v;
+  if (accumulate)
+    red_add_bf16x8(dst, v);
+  else
+    *reinterpret_cast<uint4*>(dst) = v;
 }
 
 // Tile sequence of one CTA pair. Dynamic (default): the grid has one cluster per tile; a
@@ -602,9 +584,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
         RowKeep nk;
         if (next_lora) nk = fetch_keep(tile_info<NP>(args, s_routes, tn));
         const int row = cta_row0(ti) + (int)(q * 32 + lane);
-        if (ACC && row < args.M)  // prefetch the rows this tile accumulates into
-          prefetch_c_row(reinterpret_cast<const __nv_bfloat16*>(args.C) + (int64_t)row * args.ldc, ti.nb * BN + c_lo,
-                         BN / 2, args.N);
         mbar_wait(&tfull[0], (uint32_t)it & 1u);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((q * 32u) << 16);
@@ -650,7 +629,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int row = cta_row0(ti) + (int)(q * 32 + lane);
       const int n0 = ti.nb * BN;
       __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(args.C) + (int64_t)row * args.ldc;
-      if constexpr (ACC) if (row < args.M) prefetch_c_row(crow, n0 + c_lo, BN / 2, args.N);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * Cfg::ACC_COLS;
@@ -685,12 +663,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #pragma unroll 1
       for (int c = c_lo; c < c_hi; c += 32) {
         const int col0 = n0 + c;
-        uint4 old[4];
-        if (ACC && row < args.M) {  // loads first (L2-hot: prefetched above)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (col0 + 8 * j < args.N) old[j] = ld_c8(crow + col0 + 8 * j);
-        }
         uint32_t v[32];
         tmem_ld32(taddr + c, v);
         tmem_ld_wait();
@@ -704,8 +676,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
                                pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (col0 + 8 * j < args.N)
-              *reinterpret_cast<uint4*>(crow + col0 + 8 * j) = ACC ? add_bf16x8(pk[j], old[j]) : pk[j];
+            if (col0 + 8 * j < args.N) store_c8(crow + col0 + 8 * j, pk[j], ACC);
         }
       }
       tc_fence_before();
@@ -777,15 +748,14 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
 #define LF_GEMM_LAUNCH(BMN, MSK, ST, WD)                                                        \
   (cl4 ? launch_one<BMN, MSK, ST, WD, 4>(maps, args, num_sms, stream)                          \
        : launch_one<BMN, MSK, ST, WD, 2>(maps, args, num_sms, stream))
-  // accumulating dgrads (lf_grad_input_accum) are their own instantiations: the C
-  // read-modify-write would otherwise cost the plain epilogues registers. Only the 256 x 256
-  // tiles accumulate: the 256 x 512 epilogue already holds 128 words of output per thread and
-  // spills with it (the caller sums those with a separate add instead: kGemmUnsupported)
+  // accumulating dgrads (lf_grad_input_accum) are their own instantiations (pairs only)
   if (args.accumulate) {
     if (kind == kGemmFwd) return -1;
-    if (wide) return kGemmUnsupported;
-    return kind == kGemmDgradMasked ? launch_one<true, true, 6, false, 2, true>(maps, args, num_sms, stream)
-                                    : launch_one<true, false, 6, false, 2, true>(maps, args, num_sms, stream);
+    if (kind == kGemmDgradMasked)
+      return wide ? launch_one<true, true, 4, true, 2, true>(maps, args, num_sms, stream)
+                  : launch_one<true, true, 6, false, 2, true>(maps, args, num_sms, stream);
+    return wide ? launch_one<true, false, 4, true, 2, true>(maps, args, num_sms, stream)
+                : launch_one<true, false, 6, false, 2, true>(maps, args, num_sms, stream);
   }
   switch (kind) {
     case kGemmFwd:

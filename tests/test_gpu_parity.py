@@ -547,3 +547,35 @@ def test_microbatch_beyond_launch_limits_is_split_with_unchanged_masks():
     for i in range(5):
         H.assert_chain_close(layer.lora_A[i].weight.grad.cpu().numpy(), da_ref[64 * i:64 * i + 64], f"split:dA{i}")
         H.assert_chain_close(layer.lora_B[i].weight.grad.cpu().numpy(), db_ref[:, 64 * i:64 * i + 64], f"split:dB{i}")
+
+
+@pytest.mark.parametrize("m,k,n,p", [(8192, 4096, 1024, 0.1), (1000, 520, 264, 0.1), (8192, 5120, 4096, 0.0),
+                                     (8192, 5120, 8192, 0.1)],
+                         ids=["kv_short_k", "ragged", "wide", "wide_masked"])
+def test_grad_input_accum_adds_in_l2(m, k, n, p):
+    """lf_grad_input_accum: dx += ⑤ is the bf16 sum of the old dx and what lf_grad_input writes
+    for the same problem (one rounding per element: torch's add of the two bf16 tensors),
+    including the 256 x 512 tiles (wide / wide_masked) that previously needed a separate add."""
+    lib = _lib().load()
+    case = H.Case(m, k, n, (16,), (m,), (2.0,), (p,), (21,))
+    prob, routes, ws, R = H.make_problem(case, torch.device(DEV), use_bits=True)
+    g = torch.Generator(device=DEV).manual_seed(5)
+    x = torch.randn(m, k, device=DEV, generator=g).to(torch.bfloat16)
+    dy = torch.randn(m, n, device=DEV, generator=g).to(torch.bfloat16)
+    w = (torch.randn(n, k, device=DEV, generator=g) / k**0.5).to(torch.bfloat16)
+    a = (torch.randn(R, k, device=DEV, generator=g) / k**0.5).to(torch.bfloat16)
+    ds = torch.randn(m, R, device=DEV, generator=g).to(torch.bfloat16)
+    s_hat = torch.empty(m, R, device=DEV, dtype=torch.bfloat16)
+    dx0 = torch.randn(m, k, device=DEV, generator=g).to(torch.bfloat16)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    pp = ctypes.byref(prob)
+    _lib().check(lib.lf_build_routes(pp, P(routes), st), "routes")
+    _lib().check(lib.lf_dropout_down_fwd(pp, P(x), P(a), P(s_hat), st), "down")  # writes the keep bits
+    plain = torch.empty(m, k, device=DEV, dtype=torch.bfloat16)
+    _lib().check(lib.lf_grad_input(pp, P(dy), P(w), P(ds), P(a), P(plain), st), "grad_input")
+    acc = dx0.clone()
+    _lib().check(lib.lf_grad_input_accum(pp, P(dy), P(w), P(ds), P(a), P(acc), st), "grad_input_accum")
+    torch.cuda.synchronize()
+    want = (dx0.float() + plain.float()).to(torch.bfloat16)
+    assert torch.equal(acc, want), int((acc != want).sum())

@@ -19,4 +19,11 @@ ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum 
   python bench.py --config c4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > /dev/null 2>&1
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:lf_gemm -c 2 -o $OUT/gemm_step_c1 \
   python bench.py --config c1 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > /dev/null 2>&1
+# summarise on the box (the .ncu-rep files exceed gpurun's 64 MiB copy-back)
+python tools/ncu_summary.py $OUT/gemm_step.ncu-rep > $OUT/gemm_ncu_summary.json
+python tools/ncu_summary.py $OUT/lowrank_step.ncu-rep > $OUT/lowrank_ncu_summary.json
+python tools/ncu_traffic.py $OUT/gemm_step.ncu-rep c2 > $OUT/gemm_traffic.json
+python tools/ncu_traffic.py $OUT/gemm_step_c4.ncu-rep c4 > $OUT/gemm_traffic_c4.json
+python tools/ncu_traffic.py $OUT/gemm_step_c1.ncu-rep c1 > $OUT/gemm_traffic_c1.json
+rm -f $OUT/*.ncu-rep
 ls -la $OUT
