@@ -25,6 +25,10 @@ LF_E_CUDA = -2
 LF_E_UNSUPPORTED = -3
 
 LIB_PATH = Path(__file__).resolve().parent / "liblorafusion_b200.so"
+# LF_LIB: load another build of the same library instead (interleaved A/B runs of two builds
+# on one box: tools/ab.sh "LF_LIB=_variants/a.so" "LF_LIB=_variants/b.so")
+if os.environ.get("LF_LIB"):
+    LIB_PATH = Path(os.environ["LF_LIB"]).resolve()
 
 # every symbol include/lorafusion_b200.h declares
 EXPORTED_SYMBOLS = (

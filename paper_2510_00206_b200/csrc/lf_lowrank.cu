@@ -73,6 +73,9 @@ struct UnitWalker {
   }
 };
 
+// EXPLICIT: the keep mask comes from a caller's uint8 mask (mask_mode 2) instead of Philox —
+// a separate instantiation, so the Philox hot loop carries no per-k-block mode test
+template <bool EXPLICIT>
 __global__ void __launch_bounds__(kDownThreads, 2)
     lf_down_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ DownArgs args, int STAGES, int STAGE_BYTES) {
@@ -178,11 +181,19 @@ __global__ void __launch_bounds__(kDownThreads, 2)
   } else {
     // mask warps 2..9: thread <-> tile row 32*(warp&3) + lane, half = which 4 of the row's 8
     // 16-byte chunks it masks; warps 2..5 (half 0) also flush each span's partial sums
+    // (measured: whole rows of alternate stages per thread — 8 Philox streams, half the
+    // barrier round trips — ran 1-2% slower than this split)
     const uint32_t q = warp & 3u;
     const int half = warp >= 6 ? 1 : 0;
     const int rit = (int)(q * 32 + lane);
-    const bool explicit_mask = args.segs.mask_mode == 2;
     const uint64_t step_offset = table_offset(args.segs);
+    // shared addresses of this thread's four chunks in stage 0 (SW128: chunk c of row r at
+    // ((c ^ (r & 7)) * 16); the stage offset is added per k-block
+    const uint32_t row0 = smem_u32(smem) + (uint32_t)rit * 128u;
+    uint32_t coff[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) coff[c] = row0 + (uint32_t)(((4 * half + c) ^ (rit & 7)) << 4);
+    const int nbytes = (int)args.segs.ld_bits;
     int stage = 0, it = 0;
     uint32_t phase = 0;
     while (walk.next(sp)) {
@@ -195,9 +206,12 @@ __global__ void __launch_bounds__(kDownThreads, 2)
       }
       if (gated) {
         const int seg = row < args.m ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
-        const bool my_mask = seg >= 0 && (explicit_mask || args.segs.seg[seg].thr != 0);
+        const bool my_mask = seg >= 0 && (EXPLICIT || args.segs.seg[seg].thr != 0);
         const PhiloxRow pr = philox_row(args.segs.seg[seg >= 0 ? seg : 0], (uint32_t)(row + args.segs.row_base), step_offset);
-        uint8_t* bits_row = args.segs.bits ? args.segs.bits + (int64_t)row * args.segs.ld_bits : nullptr;
+        // Philox runs once per step: ④ and ⑤ read the packed bits written here (4 bytes per
+        // k-block and thread; word stores when the row pitch keeps them aligned)
+        uint8_t* bits_row = (!EXPLICIT && my_mask && args.segs.bits) ? args.segs.bits + (int64_t)row * nbytes : nullptr;
+        const bool bits_words = (nbytes & 3) == 0 && ((reinterpret_cast<uintptr_t>(args.segs.bits) & 3u) == 0);
         for (int kb = sp.k0; kb < sp.k1; ++kb) {
           // the keep bits depend only on (row, column, seed, offset): generate them while the
           // tile is still in flight, so Philox latency overlaps the TMA instead of adding to it
@@ -205,7 +219,7 @@ __global__ void __launch_bounds__(kDownThreads, 2)
           uint32_t bits = ~0u;
           uint32_t msk[4][4];
           if (my_mask) {
-            if (explicit_mask) {
+            if constexpr (EXPLICIT) {
               const uint8_t* mrow = args.segs.mask + (int64_t)row * args.segs.ld_mask;
               bits = 0;
 #pragma unroll
@@ -215,25 +229,30 @@ __global__ void __launch_bounds__(kDownThreads, 2)
             }
           }
           mbar_wait(&full[stage], phase);
-          if (my_mask) {
-            if (!(args.segs.debug & 8) && bits != ~0u) {
-              if (explicit_mask)
-                apply_chunks_sw128<4>(smem + stage * STAGE_BYTES, rit, 4 * half, bits);
+          if (my_mask && bits != ~0u) {
+            const uint32_t so = (uint32_t)(stage * STAGE_BYTES);
+            uint4 v[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[c] = lds128(coff[c] + so);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              if constexpr (EXPLICIT)
+                sts128(coff[c] + so, apply_keep8(v[c], (bits >> (8 * c)) & 0xFFu));
               else
-                apply_masks_sw128<4>(smem + stage * STAGE_BYTES, rit, 4 * half, msk);
-            }
-            // Philox runs once per step: ④ and ⑤ read these bits instead
-            if (!explicit_mask && bits_row) {
-              const int b0 = kb * 8 + 4 * half;
-              if (b0 + 4 <= (int)args.segs.ld_bits && ((reinterpret_cast<uintptr_t>(bits_row + b0) & 3u) == 0)) {
-                *reinterpret_cast<uint32_t*>(bits_row + b0) = bits;
-              } else {
-                for (int i = 0; i < 4; ++i)
-                  if (b0 + i < (int)args.segs.ld_bits) bits_row[b0 + i] = (uint8_t)(bits >> (8 * i));
-              }
+                sts128(coff[c] + so, make_uint4(v[c].x & msk[c][0], v[c].y & msk[c][1], v[c].z & msk[c][2],
+                                                v[c].w & msk[c][3]));
             }
           }
-          if (!(args.segs.debug & 4)) fence_proxy_async_smem();
+          if (bits_row) {
+            const int b0 = kb * 8 + 4 * half;
+            if (bits_words && b0 + 4 <= nbytes) {
+              *reinterpret_cast<uint32_t*>(bits_row + b0) = bits;
+            } else {
+              for (int i = 0; i < 4; ++i)
+                if (b0 + i < nbytes) bits_row[b0 + i] = (uint8_t)(bits >> (8 * i));
+            }
+          }
+          fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) mbar_arrive(&masked[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -309,10 +328,11 @@ int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs
   int stages = 0, stage_bytes = 0;
   down_config(args.segs.wmax, &stages, &stage_bytes);
   const int smem = stages * stage_bytes + 1024 + 256;
-  static std::atomic<uint64_t> attr_done{0};
-  if (ensure_smem_attr(lf_down_kernel, 200 * 1024, attr_done)) return -1;
-  return launch_k(lf_down_kernel, dim3(args.ctas), dim3(kDownThreads), smem, stream, tm_x, tm_a, args, stages,
-                  stage_bytes);
+  const bool expl = args.segs.mask_mode == 2;
+  auto kern = expl ? lf_down_kernel<true> : lf_down_kernel<false>;
+  static std::atomic<uint64_t> attr_done[2] = {0, 0};
+  if (ensure_smem_attr(kern, 200 * 1024, attr_done[expl ? 1 : 0])) return -1;
+  return launch_k(kern, dim3(args.ctas), dim3(kDownThreads), smem, stream, tm_x, tm_a, args, stages, stage_bytes);
 }
 
 // ------------------------------------------------------------------------------------
