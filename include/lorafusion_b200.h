@@ -49,7 +49,7 @@ extern "C" {
 #define LF_API
 #endif
 
-#define LF_ABI_VERSION 4
+#define LF_ABI_VERSION 5
 #define LF_MAX_SEGMENTS 32
 #define LF_MAX_RANK_TOTAL 128
 #define LF_ROUTE_TILE_ROWS 128 /* ls/costmodel.py:25 ROUTING_TILE_ROWS */
@@ -132,6 +132,23 @@ LF_API int lf_grad_down(const LfProblem* p, const uint16_t* x, const uint16_t* d
  * per-projection lf_grad_down when a problem does not have that shape. ABI 4. */
 LF_API int lf_grad_down_group(const LfProblem* const* probs, int32_t nproj, const uint16_t* x,
                               const uint16_t* const* ds, float* const* da_accum, void* stream);
+
+/* ② for a shared-input group (q/k/v): y[j] = X·W_jᵀ + Ŝ_j·B_jᵀ for j < nproj (<= 3) as ONE
+ * GEMM over the concatenated output columns (k/v's narrow N no longer runs as its own
+ * under-filled launch). probs[j]: projection j's problem (same m, k; one segment over all
+ * rows); w / s_hat / b_cat / y: per-projection arrays as for lf_base_fwd. Falls back to
+ * per-projection lf_base_fwd for other shapes. ABI 5. */
+LF_API int lf_base_fwd_group(const LfProblem* const* probs, int32_t nproj, const uint16_t* x,
+                             const uint16_t* const* w, const uint16_t* const* s_hat, const uint16_t* const* b_cat,
+                             uint16_t* const* y, void* stream);
+
+/* ⑤ for a shared-input group: dx = Σ_j dY_j·W_j + M_j ⊙ (dŜ_j·A_cat_j) as ONE GEMM over the
+ * concatenated reduction dims, written once (each projection's masked LoRA term enters the
+ * accumulator before the main loop; masks from the packed keep bits ① wrote). Falls back to
+ * lf_grad_input + lf_grad_input_accum per projection for other shapes. ABI 5. */
+LF_API int lf_grad_input_group(const LfProblem* const* probs, int32_t nproj, const uint16_t* const* dy,
+                               const uint16_t* const* w, const uint16_t* const* ds, const uint16_t* const* a_cat,
+                               uint16_t* dx, void* stream);
 
 /* ⑤ dx = dY·W + M ⊙ (dŜ·A_cat), written once. */
 LF_API int lf_grad_input(const LfProblem* p, const uint16_t* dy, const uint16_t* w, const uint16_t* ds,

@@ -13,7 +13,7 @@ from pathlib import Path
 
 from .errors import ExtensionMissingError, KernelError, ValidationError
 
-LF_ABI_VERSION = 4
+LF_ABI_VERSION = 5
 LF_MAX_SEGMENTS = 32
 LF_MAX_RANK_TOTAL = 128
 ROUTE_TILE_ROWS = 128  # ls/costmodel.py:25
@@ -42,6 +42,8 @@ EXPORTED_SYMBOLS = (
     "lf_grad_down_group",
     "lf_grad_input",
     "lf_grad_input_accum",
+    "lf_base_fwd_group",
+    "lf_grad_input_group",
     "lf_dropout_mask",
     "lf_keep_bits",
     "lf_last_error",
@@ -95,6 +97,10 @@ _SIGNATURES = {
                                           ctypes.POINTER(_V), _V]),
     "lf_grad_input": (ctypes.c_int, [_P, _V, _V, _V, _V, _V, _V]),
     "lf_grad_input_accum": (ctypes.c_int, [_P, _V, _V, _V, _V, _V, _V]),
+    "lf_base_fwd_group": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int32, _V, ctypes.POINTER(_V),
+                                         ctypes.POINTER(_V), ctypes.POINTER(_V), ctypes.POINTER(_V), _V]),
+    "lf_grad_input_group": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int32, ctypes.POINTER(_V),
+                                           ctypes.POINTER(_V), ctypes.POINTER(_V), ctypes.POINTER(_V), _V, _V]),
     "lf_dropout_mask": (ctypes.c_int, [_P, _V, _V]),
     "lf_keep_bits": (ctypes.c_int, [_P, _V, _V]),
     "lf_last_error": (ctypes.c_char_p, []),

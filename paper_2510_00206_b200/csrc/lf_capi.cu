@@ -387,16 +387,17 @@ int lf_base_fwd(const LfProblem* p, const uint16_t* x, const uint16_t* w, const 
   Dev d;
   LF_TRY(current_device(&d));
   lf::GemmMaps maps;
-  if (!make_map(&maps.a, x, p->m, p->k, p->k, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&maps.b, w, p->n, p->k, p->k, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+  memset(&maps, 0, sizeof(maps));
+  if (!make_map(&maps.a[0], x, p->m, p->k, p->k, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&maps.b[0], w, p->n, p->k, p->k, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))
     return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (x / w)");
   if (lora) {
-    if (!make_map(&maps.a2, s_hat, p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
-        !make_map(&maps.b2, b_cat, p->n, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B))
+    if (!make_map(&maps.a2[0], s_hat, p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
+        !make_map(&maps.b2[0], b_cat, p->n, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B))
       return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (s_hat / b_cat)");
   } else {
-    maps.a2 = maps.a;
-    maps.b2 = maps.b;
+    maps.a2[0] = maps.a[0];
+    maps.b2[0] = maps.b[0];
   }
   lf::GemmArgs a;
   memset(&a, 0, sizeof(a));
@@ -588,17 +589,18 @@ static int grad_input_impl(const LfProblem* p, const uint16_t* dy, const uint16_
   LF_TRY(current_device(&d));
   const bool masked = lora && t.mask_mode != 0;
   lf::GemmMaps maps;
+  memset(&maps, 0, sizeof(maps));
   // dX[m, k] = dY[m, n] · W[n, k]: A = dY (K-major), B = W (MN-major), K = n
-  if (!make_map(&maps.a, dy, p->m, p->n, p->n, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&maps.b, w, p->n, p->k, p->k, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))
+  if (!make_map(&maps.a[0], dy, p->m, p->n, p->n, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&maps.b[0], w, p->n, p->k, p->k, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))
     return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (dy / w)");
   if (lora) {
-    if (!make_map(&maps.a2, ds, p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
-        !make_map(&maps.b2, a_cat, p->rank_total, p->k, p->k, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B))
+    if (!make_map(&maps.a2[0], ds, p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
+        !make_map(&maps.b2[0], a_cat, p->rank_total, p->k, p->k, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B))
       return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (ds / a_cat)");
   } else {
-    maps.a2 = maps.a;
-    maps.b2 = maps.b;
+    maps.a2[0] = maps.a[0];
+    maps.b2[0] = maps.b[0];
   }
   lf::GemmArgs a;
   memset(&a, 0, sizeof(a));
@@ -615,6 +617,139 @@ static int grad_input_impl(const LfProblem* p, const uint16_t* dy, const uint16_
   if (rc == lf::kGemmUnsupported)
     return fail(LF_E_UNSUPPORTED, "grad_input: accumulation is not built for the 256x512 tiles this shape uses");
   if (rc) return cuda_fail("grad_input launch");
+  return LF_OK;
+}
+
+// shared-input groups (② / ⑤ over J projections that read the same input): one GEMM when
+// every projection is a single adapter segment over all rows (the FusedLoRAGroup case) and
+// its width fits the group tiling; otherwise the projections run one by one (⑤: the first
+// writes dX, the others add into it). LF_GROUP_GEMM=0 forces the per-projection path.
+static bool group_single(const LfProblem* p) {
+  return p->num_segments == 1 && p->segments[0].row_start == 0 && p->segments[0].row_end == p->m &&
+         p->segments[0].col_start == 0 && p->segments[0].rank == p->rank_total && p->row_base == 0 &&
+         p->rank_total >= 16;
+}
+
+int lf_base_fwd_group(const LfProblem* const* probs, int32_t nproj, const uint16_t* x, const uint16_t* const* w,
+                      const uint16_t* const* s_hat, const uint16_t* const* b_cat, uint16_t* const* y, void* stream) {
+  if (!probs || nproj < 1 || nproj > lf::kMaxGroup || !w || !s_hat || !b_cat || !y)
+    return fail(LF_E_INVALID, "lf_base_fwd_group: 1..%d projections with w / s_hat / b_cat / y arrays", lf::kMaxGroup);
+  LF_TRY(check_ptr(x, "x"));
+  bool fused = nproj > 1;
+  lf::LfSegTable t[lf::kMaxGroup];
+  for (int j = 0; j < nproj; ++j) {
+    const LfProblem* p = probs[j];
+    if (!p) return fail(LF_E_INVALID, "lf_base_fwd_group: projection %d has no problem", j);
+    LF_TRY(validate(p, true, &t[j]));
+    if (p->m != probs[0]->m || p->k != probs[0]->k)
+      return fail(LF_E_INVALID, "lf_base_fwd_group: projections must share the input (m, k)");
+    LF_TRY(check_ptr(w[j], "w"));
+    LF_TRY(check_ptr(y[j], "y"));
+    if (!group_single(p)) fused = false;
+  }
+  static const int group_env = env_int("LF_GROUP_GEMM", 1);
+  if (fused && group_env) {
+    Dev d;
+    LF_TRY(current_device(&d));
+    lf::GemmMaps maps;
+    memset(&maps, 0, sizeof(maps));
+    lf::GemmArgs a;
+    memset(&a, 0, sizeof(a));
+    const LfProblem* p0 = probs[0];
+    if (!make_map(&maps.a[0], x, p0->m, p0->k, p0->k, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+      return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (x)");
+    int n = 0;
+    for (int j = 0; j < nproj; ++j) {
+      const LfProblem* p = probs[j];
+      LF_TRY(check_ptr(s_hat[j], "s_hat"));
+      LF_TRY(check_ptr(b_cat[j], "b_cat"));
+      if (!make_map(&maps.b[j], w[j], p->n, p->k, p->k, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+          !make_map(&maps.a2[j], s_hat[j], p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
+          !make_map(&maps.b2[j], b_cat[j], p->n, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B))
+        return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (w / s_hat / b_cat)");
+      n += p->n;
+      a.send[j] = n;
+      a.lcols[j] = p->rank_total;
+      a.Cs[j] = y[j];
+      a.ldcs[j] = p->n;
+    }
+    a.nseg = nproj;
+    a.M = p0->m;
+    a.N = n;
+    a.K = p0->k;
+    a.segs = t[0];
+    a.group = env_int("LF_GROUP", 0);
+    const int rc = lf::gemm_launch_group(lf::kGemmFwd, maps, a, d.sms, (cudaStream_t)stream);
+    if (rc == 0) return LF_OK;
+    if (rc != lf::kGemmUnsupported) return cuda_fail("base_fwd_group launch");
+  }
+  for (int j = 0; j < nproj; ++j) LF_TRY(lf_base_fwd(probs[j], x, w[j], s_hat[j], b_cat[j], y[j], stream));
+  return LF_OK;
+}
+
+int lf_grad_input_group(const LfProblem* const* probs, int32_t nproj, const uint16_t* const* dy,
+                        const uint16_t* const* w, const uint16_t* const* ds, const uint16_t* const* a_cat, uint16_t* dx,
+                        void* stream) {
+  if (!probs || nproj < 1 || nproj > lf::kMaxGroup || !dy || !w || !ds || !a_cat)
+    return fail(LF_E_INVALID, "lf_grad_input_group: 1..%d projections with dy / w / ds / a_cat arrays", lf::kMaxGroup);
+  LF_TRY(check_ptr(dx, "dx"));
+  bool fused = nproj > 1;
+  bool masked = false;
+  lf::LfSegTable t[lf::kMaxGroup];
+  for (int j = 0; j < nproj; ++j) {
+    const LfProblem* p = probs[j];
+    if (!p) return fail(LF_E_INVALID, "lf_grad_input_group: projection %d has no problem", j);
+    LF_TRY(validate(p, true, &t[j]));
+    if (p->m != probs[0]->m || p->k != probs[0]->k)
+      return fail(LF_E_INVALID, "lf_grad_input_group: projections must share the input (m, k)");
+    LF_TRY(check_ptr(dy[j], "dy"));
+    LF_TRY(check_ptr(w[j], "w"));
+    if (!group_single(p)) fused = false;
+    const bool m_j = t[j].mask_mode != 0 && t[j].seg[0].thr != 0;
+    if (m_j && !(t[j].mask_mode == 1 && t[j].bits)) fused = false;  // packed bits from ① only
+    masked = masked || m_j;
+  }
+  static const int group_env = env_int("LF_GROUP_GEMM", 1);
+  if (fused && group_env) {
+    Dev d;
+    LF_TRY(current_device(&d));
+    lf::GemmMaps maps;
+    memset(&maps, 0, sizeof(maps));
+    lf::GemmArgs a;
+    memset(&a, 0, sizeof(a));
+    const LfProblem* p0 = probs[0];
+    int kk = 0;
+    for (int j = 0; j < nproj; ++j) {
+      const LfProblem* p = probs[j];
+      LF_TRY(check_ptr(ds[j], "ds"));
+      LF_TRY(check_ptr(a_cat[j], "a_cat"));
+      // dX[m, k] = Σ_j dY_j[m, n_j] · W_j[n_j, k]: A = dY_j (K-major), B = W_j (MN-major)
+      if (!make_map(&maps.a[j], dy[j], p->m, p->n, p->n, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+          !make_map(&maps.b[j], w[j], p->n, p->k, p->k, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+          !make_map(&maps.a2[j], ds[j], p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
+          !make_map(&maps.b2[j], a_cat[j], p->rank_total, p->k, p->k, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B))
+        return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (dy / w / ds / a_cat)");
+      kk += p->n;
+      a.send[j] = kk;
+      a.lcols[j] = p->rank_total;
+      a.gbits[j] = (t[j].mask_mode == 1 && t[j].seg[0].thr != 0) ? t[j].bits : nullptr;
+    }
+    a.ld_gbits = t[0].ld_bits;
+    a.nseg = nproj;
+    a.M = p0->m;
+    a.N = p0->k;
+    a.K = kk;
+    a.ldc = p0->k;
+    a.C = dx;
+    a.segs = t[0];
+    a.group = env_int("LF_GROUP", 0);
+    const int rc = lf::gemm_launch_group(masked ? lf::kGemmDgradMasked : lf::kGemmDgrad, maps, a, d.sms,
+                                         (cudaStream_t)stream);
+    if (rc == 0) return LF_OK;
+    if (rc != lf::kGemmUnsupported) return cuda_fail("grad_input_group launch");
+  }
+  for (int j = 0; j < nproj; ++j)
+    LF_TRY(grad_input_impl(probs[j], dy[j], w[j], ds[j], a_cat[j], dx, j > 0 ? 1 : 0, stream));
   return LF_OK;
 }
 

@@ -72,6 +72,7 @@ struct TileInfo {
   int mb, nb;          // cluster-tile coordinates: rows [mb * NP * 256, +NP * 256), columns [nb * BN, +BN)
   int col_lo, col_hi;  // LoRA K-range: union over the cluster tile's 128-row routes (every pair of
                        // the cluster streams the same stages: the multicast operand is shared)
+  int proj, noff;      // GRP forward: projection owning the tile's columns, its first column
   __device__ bool lora() const { return col_hi > col_lo; }
 };
 
@@ -212,11 +213,17 @@ struct TileSeq {
 // 512 x BN) that share the B operand — the pair-0 CTAs TMA-load each B tile once and
 // multicast it into both pairs' shared memory (half the B reads from L2 per FLOP), and every
 // pair leader's MMA commit releases the stage in all four CTAs.
-template <bool B_MN, bool MASKED, int STAGES, bool WIDE, int CL, bool ACC>
+// GRP (shared-input groups, lf_base_fwd_group / lf_grad_input_group): J = args.nseg
+// projections that read the same input in ONE launch. Forward: the projections' output
+// columns are concatenated (N segments) — a tile belongs to one projection, takes W_j's rows,
+// the LoRA K-block of Ŝ_j / B_j and writes Y_j. Input gradient: their reduction dims are
+// concatenated (K segments: dY_j·W_j summed in the accumulator, dX written once) and each
+// projection's masked LoRA term M_j ⊙ (dŜ_j·A_j) enters the drained accumulator first: the
+// J partials take turns in it (MMA → epilogue masks into registers → next partial), the
+// masked sum goes back to TMEM, and the main loop accumulates on top.
+template <bool B_MN, bool MASKED, int STAGES, bool WIDE, int CL, bool ACC, bool GRP>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
-    lf_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
-                   const __grid_constant__ GemmArgs args) {
+    lf_gemm_kernel(const __grid_constant__ GemmMaps maps, const __grid_constant__ GemmArgs args) {
   using Cfg = GemmCfg<B_MN, STAGES, WIDE>;
   constexpr int BN = Cfg::BN, HBN = Cfg::HBN, NH = Cfg::NH, NACC = Cfg::NACC;
   constexpr int NP = CL / 2;                                    // CTA pairs per cluster
@@ -230,7 +237,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
   uint64_t* tempty = tfull + 2;      // [2] leader: both CTAs drained the accumulator (16 warps)
   uint64_t* lfull = tempty + 2;      // [2] both CTAs: LoRA partial ready                 MASKED
   uint64_t* lmasked = lfull + 2;     // [2] leader: both CTAs masked their partial (16)  MASKED
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lmasked + 2);
+  uint64_t* lnext = lmasked + 2;     // [2] leader: both CTAs read partial j < J-1 (16)  MASKED GRP
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lnext + 2);
   uint8_t* ctl = smem + STAGES * Cfg::STAGE_BYTES;
   TileSeq<CL> seq;
   seq.full = reinterpret_cast<uint64_t*>(ctl + 192);
@@ -258,17 +266,21 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tempty[a], 2 * kEpiWarps);
       mbar_init(&lfull[a], 1);
       mbar_init(&lmasked[a], 2 * kEpiWarps);
+      mbar_init(&lnext[a], 2 * kEpiWarps);
     }
     for (int i = 0; i < kSeqDepth; ++i) {
       mbar_init(&seq.full[i], 1);
       mbar_init(&seq.empty[i], TileSeq<CL>::kReaders);
     }
     fence_barrier_init();
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-    if (args.routes) {
-      tma_prefetch_desc(&tmA2);
-      tma_prefetch_desc(&tmB2);
+    const int nmaps = GRP ? args.nseg : 1;
+    for (int j = 0; j < nmaps; ++j) {
+      tma_prefetch_desc(&maps.a[GRP && B_MN ? j : 0]);
+      tma_prefetch_desc(&maps.b[j]);
+      if (args.routes || GRP) {
+        tma_prefetch_desc(&maps.a2[j]);
+        tma_prefetch_desc(&maps.b2[j]);
+      }
     }
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);
@@ -293,6 +305,36 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
   // 512: a quarter in, 1024: three quarters in)
   const int jmid = (args.segs.debug & 256) ? nkb : (args.segs.debug & 512) ? nkb / 4
                    : (args.segs.debug & 1024) ? (3 * nkb) / 4 : nkb / 2;
+  // GRP: J projections (1 otherwise); the masked dgrad issues partial j of the next tile at
+  // k-block split(j) of the current one (J = 1: jmid)
+  const int J = GRP ? args.nseg : 1;
+  auto split_at = [&](int j) { return min(nkb, jmid + (j * (nkb - jmid)) / J); };
+  // GRP input gradient: K segment of k-block kb (projection j, its first k-block)
+  auto kseg = [&](int kb, int& j, int& kb0) {
+    j = 0;
+    kb0 = 0;
+    if constexpr (GRP && B_MN) {
+      while (j + 1 < args.nseg && kb * Cfg::BK >= args.send[j]) {
+        kb0 = args.send[j] / Cfg::BK;
+        ++j;
+      }
+    }
+  };
+  auto tinfo = [&](int t) {
+    TileInfo ti = tile_info<NP>(args, s_routes, t);
+    ti.proj = 0;
+    ti.noff = 0;
+    if constexpr (GRP) {
+      if constexpr (!B_MN) {
+        const int n0 = ti.nb * BN;
+        while (ti.proj + 1 < args.nseg && n0 >= args.send[ti.proj]) ++ti.proj;
+        ti.noff = ti.proj ? args.send[ti.proj - 1] : 0;
+      }
+      ti.col_lo = 0;
+      ti.col_hi = args.lcols[ti.proj];
+    }
+    return ti;
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -319,51 +361,63 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
         begin_stage(Cfg::STAGE_BYTES);
         uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
         uint8_t* sB = sA + Cfg::A_BYTES;
-        tma_load_2d_pair(sA, &tmA, &full[stage], kb * Cfg::BK, (ti.mb * NP + (int)pid) * 256 + row_half);
+        int j, kb0;
+        kseg(kb, j, kb0);  // GRP dgrad: dY_j / W_j hold k-blocks [kb0, ...) of the concatenated K
+        const int kl = (kb - kb0) * Cfg::BK;
+        tma_load_2d_pair(sA, &maps.a[j], &full[stage], kl, (ti.mb * NP + (int)pid) * 256 + row_half);
         if constexpr (!B_MN) {
-          // N piece h of this CTA: rows h*256 + rank*128 of the pair tile's columns
+          // N piece h of this CTA: rows h*256 + rank*128 of the pair tile's columns (GRP: of W_proj)
+          const CUtensorMap* mb = &maps.b[ti.proj];
 #pragma unroll
           for (int h = 0; h < NH; ++h)
-            load_b(sB + h * 16384, &tmB, kb * Cfg::BK, ti.nb * BN + h * 256 + (int)rank * 128);
+            load_b(sB + h * 16384, mb, kl, ti.nb * BN - ti.noff + h * 256 + (int)rank * 128);
         } else {
 #pragma unroll
           for (int h = 0; h < NH; ++h)
 #pragma unroll
             for (int i = 0; i < 2; ++i)  // 128 MN-major columns = two 64-column SW128 boxes
-              load_b(sB + h * 16384 + i * 8192, &tmB, ti.nb * BN + h * 256 + (int)rank * 128 + 64 * i,
-                     kb * Cfg::BK);
+              load_b(sB + h * 16384 + i * 8192, &maps.b[j], ti.nb * BN + h * 256 + (int)rank * 128 + 64 * i, kl);
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       };
-      auto load_lora = [&](const TileInfo& ti) {
-        for (int c = ti.col_lo; c < ti.col_hi; c += 64) {
-          const int nsub = min(4, (ti.col_hi - c) >> 4);
+      // LoRA K-blocks [c_lo, c_hi) of operand pair j (Ŝ_j / B_j forward, dŜ_j / A_j dgrad)
+      auto load_lora_j = [&](const TileInfo& ti, int j, int c_lo, int c_hi) {
+        for (int c = c_lo; c < c_hi; c += 64) {
+          const int nsub = min(4, (c_hi - c) >> 4);
           begin_stage(nsub * (Cfg::BM * 32 + HBN * 32));
           uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sB = sA + Cfg::A_BYTES;
-          for (int j = 0; j < nsub; ++j) {
-            tma_load_2d_pair(sA + j * (Cfg::BM * 32), &tmA2, &full[stage], c + 16 * j,
+          for (int u = 0; u < nsub; ++u) {
+            tma_load_2d_pair(sA + u * (Cfg::BM * 32), &maps.a2[j], &full[stage], c + 16 * u,
                              (ti.mb * NP + (int)pid) * 256 + row_half);
             if constexpr (!B_MN) {
 #pragma unroll
               for (int h = 0; h < NH; ++h)
-                load_b(sB + (j * NH + h) * 4096, &tmB2, c + 16 * j, ti.nb * BN + h * 256 + (int)rank * 128);
+                load_b(sB + (u * NH + h) * 4096, &maps.b2[j], c + 16 * u,
+                       ti.nb * BN - ti.noff + h * 256 + (int)rank * 128);
             } else {
 #pragma unroll
               for (int h = 0; h < NH; ++h)
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
-                  load_b(sB + (j * NH + h) * 4096 + i * 2048, &tmB2, ti.nb * BN + h * 256 + (int)rank * 128 + 64 * i,
-                         c + 16 * j);
+                  load_b(sB + (u * NH + h) * 4096 + i * 2048, &maps.b2[j],
+                         ti.nb * BN + h * 256 + (int)rank * 128 + 64 * i, c + 16 * u);
             }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       };
+      auto load_lora = [&](const TileInfo& ti) {
+        if constexpr (GRP && B_MN) {  // every projection's block (p = 0: they all accumulate)
+          for (int j = 0; j < J; ++j) load_lora_j(ti, j, 0, args.lcols[j]);
+        } else {
+          load_lora_j(ti, ti.proj, ti.col_lo, ti.col_hi);
+        }
+      };
       int t = seq.first();
       if (crank == 0 && t >= 0) seq.request(1);
       for (int i = 0; t >= 0; ++i) {
-        const TileInfo ti = tile_info<NP>(args, s_routes, t);
+        const TileInfo ti = tinfo(t);
         int tn;
         if constexpr (MASKED && WIDE) {
           // one accumulator: each tile's own LoRA block first, then its main loop
@@ -372,16 +426,25 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
           tn = seq.read(i + 1, true);
           if (crank == 0 && tn >= 0) seq.request(i + 2);
         } else if constexpr (MASKED) {
-          if (i == 0 && ti.lora()) load_lora(ti);
-          // the next tile's LoRA block goes in half-way through this tile's main loop
-          const int split = min(jmid, nkb);
+          // partial j of the next tile's LoRA term goes in at k-block split_at(j) of this
+          // tile's main loop (J = 1: half-way); GRP: projection j's dŜ_j / A_j
+          auto lora_part = [&](const TileInfo& tx, int j) {
+            if constexpr (GRP) load_lora_j(tx, j, 0, args.lcols[j]);
+            else load_lora(tx);
+          };
+          if (i == 0 && ti.lora())
+            for (int j = 0; j < J; ++j) lora_part(ti, j);
           int kb = 0;
-          for (; kb < split; ++kb) load_main(ti, kb);
-          tn = seq.read(i + 1, true);
-          if (crank == 0 && tn >= 0) seq.request(i + 2);
-          if (tn >= 0) {
-            const TileInfo tni = tile_info<NP>(args, s_routes, tn);
-            if (tni.lora()) load_lora(tni);
+          tn = -1;
+          TileInfo tni;
+          for (int j = 0; j < J; ++j) {
+            for (const int split = split_at(j); kb < split; ++kb) load_main(ti, kb);
+            if (j == 0) {
+              tn = seq.read(i + 1, true);
+              if (crank == 0 && tn >= 0) seq.request(i + 2);
+              if (tn >= 0) tni = tinfo(tn);
+            }
+            if (tn >= 0 && tni.lora()) lora_part(tni, j);
           }
           for (; kb < nkb; ++kb) load_main(ti, kb);
         } else {
@@ -418,10 +481,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
         umma_commit_pair_warp_mask(&empty[stage], kAllCtas);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       };
-      auto mma_lora = [&](const TileInfo& ti, uint32_t d, bool acc_any) {
+      auto mma_lora_cols = [&](int c_lo, int c_hi, uint32_t d, bool acc_any) {
         uint32_t accum = acc_any ? 1u : 0u;
-        for (int c = ti.col_lo; c < ti.col_hi; c += 64) {
-          const int nsub = min(4, (ti.col_hi - c) >> 4);
+        for (int c = c_lo; c < c_hi; c += 64) {
+          const int nsub = min(4, (c_hi - c) >> 4);
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t sA = smem_u32(smem + stage * Cfg::STAGE_BYTES);
@@ -439,17 +502,33 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       };
-      // MASKED: LoRA partial of local tile `it` into its (drained) buffer, then signal the mask pass
-      auto issue_lora_first = [&](const TileInfo& ti, int it) {
+      auto mma_lora = [&](const TileInfo& ti, uint32_t d, bool acc_any) {
+        if constexpr (GRP && B_MN) {
+          for (int j = 0; j < J; ++j) mma_lora_cols(0, args.lcols[j], d, acc_any || j > 0);
+        } else {
+          mma_lora_cols(ti.col_lo, ti.col_hi, d, acc_any);
+        }
+      };
+      uint32_t next_uses0 = 0, next_uses1 = 0;  // MASKED GRP: partials handed over per buffer
+      // MASKED: LoRA partial j of local tile `it` into its (drained) buffer, then signal the
+      // mask pass (GRP: partial j > 0 waits until the epilogue has read partial j - 1)
+      auto issue_lora_first = [&](const TileInfo& ti, int it, int j) {
         const int acc = it % NACC;
-        mbar_wait(&tempty[acc], ((it / NACC) & 1) ^ 1);
+        if (j == 0) {
+          mbar_wait(&tempty[acc], ((it / NACC) & 1) ^ 1);
+        } else {
+          uint32_t& nu = acc ? next_uses1 : next_uses0;
+          mbar_wait(&lnext[acc], nu & 1);
+          ++nu;
+        }
         tc_fence_after();
-        mma_lora(ti, tmem_base + acc * Cfg::ACC_COLS, false);
+        if constexpr (GRP) mma_lora_cols(0, args.lcols[j], tmem_base + acc * Cfg::ACC_COLS, false);
+        else mma_lora(ti, tmem_base + acc * Cfg::ACC_COLS, false);
         umma_commit_pair_warp_mask(&lfull[acc], pair_mask);
       };
       int t = seq.first();
       for (int it = 0; t >= 0; ++it) {
-        const TileInfo ti = tile_info<NP>(args, s_routes, t);
+        const TileInfo ti = tinfo(t);
         const int acc = it % NACC;
         const uint32_t d = tmem_base + acc * Cfg::ACC_COLS;
         int tn = -1;
@@ -468,7 +547,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
           }
           for (int kb = 0; kb < nkb; ++kb) mma_main_block(d, kb, ti.lora());
         } else if constexpr (MASKED) {
-          if (it == 0 && ti.lora()) issue_lora_first(ti, 0);
+          if (it == 0 && ti.lora())
+            for (int j = 0; j < J; ++j) issue_lora_first(ti, 0, j);
           if (ti.lora()) {
             uint32_t& lu = acc ? lora_uses1 : lora_uses0;
             mbar_wait(&lmasked[acc], lu & 1);
@@ -477,15 +557,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
             mbar_wait(&tempty[acc], ((it / NACC) & 1) ^ 1);
           }
           tc_fence_after();
-          const int split = min(jmid, nkb);
           const bool acc_any = ti.lora();
           int kb = 0;
-          for (; kb < split; ++kb) mma_main_block(d, kb, acc_any);
-          tn = seq.read(it + 1, lane_id() == 0);
-          have_tn = true;
-          if (tn >= 0) {
-            const TileInfo tni = tile_info<NP>(args, s_routes, tn);
-            if (tni.lora()) issue_lora_first(tni, it + 1);
+          TileInfo tni;
+          for (int j = 0; j < J; ++j) {
+            for (const int split = split_at(j); kb < split; ++kb) mma_main_block(d, kb, acc_any);
+            if (j == 0) {
+              tn = seq.read(it + 1, lane_id() == 0);
+              have_tn = true;
+              if (tn >= 0) tni = tinfo(tn);
+            }
+            if (tn >= 0 && tni.lora()) issue_lora_first(tni, it + 1, j);
           }
           for (; kb < nkb; ++kb) mma_main_block(d, kb, acc_any);
         } else {
@@ -566,7 +648,103 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(lmasked_leader[acc]);
     };
-    auto mask_pass = [&](const TileInfo& ti, int it) { mask_apply(it, fetch_keep(ti)); };
+    const uint32_t lnext_leader[2] = {mapa_shared(smem_u32(&lnext[0]), lrank), mapa_shared(smem_u32(&lnext[1]), lrank)};
+    // GRP: the J masked LoRA partials of tile `it` arrive one after another in its drained
+    // buffer; each is read, masked with its projection's keep bits and added to a running sum
+    // in registers, and the sum goes back to TMEM for the main loop to accumulate on top. The
+    // running sum of a thread's 128 columns is held as bf16 pairs between partials (fp32
+    // would not fit next to the rest of the kernel in 168 registers: 3 warps share an SMSP's
+    // register file): each partial is added in fp32 and the sum rounded once per partial —
+    // the per-projection path rounds each projection's whole dX_j to bf16 before summing.
+    auto mask_pass_grp = [&](const TileInfo& ti, int it) {
+      const int acc = it % NACC;
+      uint32_t& lu = acc ? lora_uses1 : lora_uses0;
+      const int row = cta_row0(ti) + (int)(q * 32 + lane);
+      const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * Cfg::ACC_COLS;
+      const int nbytes = (int)args.ld_gbits;
+      const int b0 = (ti.nb * BN + c_lo) >> 3;
+      uint32_t r[BN / 4];  // 128 columns as bf16 pairs
+#pragma unroll
+      for (int j = 0; j < kMaxGroup; ++j) {
+        if (j >= J) break;
+        uint32_t kb4[BN / 64];
+        const uint8_t* gb = args.gbits[j];
+#pragma unroll
+        for (int c = 0; c < BN / 64; ++c) {
+          kb4[c] = 0xFFFFFFFFu;
+          if (gb && row < args.M) {
+            const uint8_t* rb = gb + (int64_t)row * nbytes;
+            const int bb = b0 + 4 * c;
+            if (bb + 4 <= nbytes && ((reinterpret_cast<uintptr_t>(rb + bb) & 3u) == 0)) {
+              kb4[c] = *reinterpret_cast<const uint32_t*>(rb + bb);
+            } else {
+              uint32_t w = 0;
+              for (int i = 0; i < 4; ++i)
+                if (bb + i < nbytes) w |= (uint32_t)rb[bb + i] << (8 * i);
+              kb4[c] = w;
+            }
+          }
+        }
+        mbar_wait(&lfull[acc], lu & 1);
+        ++lu;
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {  // 16 columns per TMEM load (register pressure)
+          uint32_t v[16];
+          tmem_ld16(taddr + c_lo + 16 * c, v);
+          tmem_ld_wait();
+          const uint32_t kp = kb4[c >> 1] >> (16 * (c & 1));
+#pragma unroll
+          for (int e = 0; e < 16; e += 2) {
+            float x0 = ((kp >> e) & 1u) ? __uint_as_float(v[e]) : 0.f;
+            float x1 = ((kp >> (e + 1)) & 1u) ? __uint_as_float(v[e + 1]) : 0.f;
+            uint32_t& w = r[8 * c + e / 2];
+            if (j > 0) {
+              x0 += __uint_as_float(w << 16);
+              x1 += __uint_as_float(w & 0xFFFF0000u);
+            }
+            w = pack_bf16x2(x0, x1);
+          }
+        }
+        if (j + 1 < J) {  // the MMA may overwrite the buffer with partial j + 1
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(lnext_leader[acc]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[16];
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          const uint32_t w = r[8 * c + e / 2];
+          v[e] = w << 16;
+          v[e + 1] = w & 0xFFFF0000u;
+        }
+        tmem_st16(taddr + c_lo + 16 * c, v);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(lmasked_leader[acc]);
+    };
+    auto mask_pass = [&](const TileInfo& ti, int it) {
+      if constexpr (GRP) mask_pass_grp(ti, it);
+      else mask_apply(it, fetch_keep(ti));
+    };
+    // output of tile `ti`: base, row pitch, first column and column limit (GRP forward: the
+    // projection's own Y_j)
+    auto out_base = [&](const TileInfo& ti, int row, int& col0, int& lim) {
+      if constexpr (GRP && !B_MN) {
+        col0 = ti.nb * BN - ti.noff;
+        lim = args.send[ti.proj] - ti.noff;
+        return reinterpret_cast<__nv_bfloat16*>(args.Cs[ti.proj]) + (int64_t)row * args.ldcs[ti.proj];
+      } else {
+        col0 = ti.nb * BN;
+        lim = args.N;
+        return reinterpret_cast<__nv_bfloat16*>(args.C) + (int64_t)row * args.ldc;
+      }
+    };
     if constexpr (MASKED && WIDE) {
       // One accumulator, so tile i+1's LoRA partial and its mask pass sit between tile i's
       // main loop and tile i+1's: keep that gap short — tile i+1's keep bits are loaded
@@ -574,15 +752,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
       // stores wait until tile i+1's mask pass has released the MMA.
       int t = seq.first();
       if (t >= 0) {
-        const TileInfo t0 = tile_info<NP>(args, s_routes, t);
+        const TileInfo t0 = tinfo(t);
         if (t0.lora()) mask_pass(t0, 0);
       }
       for (int it = 0; t >= 0; ++it) {
-        const TileInfo ti = tile_info<NP>(args, s_routes, t);
+        const TileInfo ti = tinfo(t);
         const int tn = seq.read(it + 1, lane == 0);
-        const bool next_lora = tn >= 0 && tile_info<NP>(args, s_routes, tn).lora();
+        const bool next_lora = tn >= 0 && tinfo(tn).lora();
         RowKeep nk;
-        if (next_lora) nk = fetch_keep(tile_info<NP>(args, s_routes, tn));
+        if (next_lora) nk = fetch_keep(tinfo(tn));
         const int row = cta_row0(ti) + (int)(q * 32 + lane);
         mbar_wait(&tfull[0], (uint32_t)it & 1u);
         tc_fence_after();
@@ -614,7 +792,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
     } else {
     int t = seq.first();
     for (int it = 0; t >= 0; ++it) {
-      const TileInfo ti = tile_info<NP>(args, s_routes, t);
+      const TileInfo ti = tinfo(t);
       const int acc = it % NACC;
       const uint32_t aph = (it / NACC) & 1;
       int tn = -1;
@@ -622,13 +800,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if (it == 0 && ti.lora()) mask_pass(ti, 0);
         tn = seq.read(it + 1, lane == 0);
         if (tn >= 0) {
-          const TileInfo tni = tile_info<NP>(args, s_routes, tn);
+          const TileInfo tni = tinfo(tn);
           if (tni.lora()) mask_pass(tni, it + 1);
         }
       }
       const int row = cta_row0(ti) + (int)(q * 32 + lane);
-      const int n0 = ti.nb * BN;
-      __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(args.C) + (int64_t)row * args.ldc;
+      int n0, nlim;
+      __nv_bfloat16* crow = out_base(ti, row, n0, nlim);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * Cfg::ACC_COLS;
@@ -652,7 +830,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int c = 0; c < BN / 2; c += 8) {
             const int col = n0 + c_lo + c;
-            if (col < args.N)
+            if (col < nlim)
               store_c8(crow + col, make_uint4(pk[c / 2], pk[c / 2 + 1], pk[c / 2 + 2], pk[c / 2 + 3]), ACC);
           }
         }
@@ -676,7 +854,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
                                pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (col0 + 8 * j < args.N) store_c8(crow + col0 + 8 * j, pk[j], ACC);
+            if (col0 + 8 * j < nlim) store_c8(crow + col0 + 8 * j, pk[j], ACC);
         }
       }
       tc_fence_before();
@@ -696,20 +874,79 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-template <bool B_MN, bool MASKED, int STAGES, bool WIDE, int CL, bool ACC = false>
+template <bool B_MN, bool MASKED, int STAGES, bool WIDE, int CL, bool ACC = false, bool GRP = false>
 static int launch_one(const GemmMaps& maps, const GemmArgs& args, int num_sms, cudaStream_t stream) {
   using Cfg = GemmCfg<B_MN, STAGES, WIDE>;
-  auto kern = lf_gemm_kernel<B_MN, MASKED, STAGES, WIDE, CL, ACC>;
+  auto kern = lf_gemm_kernel<B_MN, MASKED, STAGES, WIDE, CL, ACC, GRP>;
   static std::atomic<uint64_t> attr_done{0};  // per instantiation, per device
   if (ensure_smem_attr(kern, Cfg::SMEM_BYTES, attr_done)) return -1;
   const int tiles = args.tiles_m * args.tiles_n;
   // dynamic: one cluster per tile (the resident clusters take over the rest through CLC);
   // static: one persistent cluster per CL SMs, round-robin tiles
   const int clusters = args.dynamic ? tiles : (tiles < num_sms / CL ? tiles : num_sms / CL);
-  if (launch_k(kern, dim3(CL * clusters), dim3(kGemmThreads), Cfg::SMEM_BYTES, stream, maps.a, maps.b, maps.a2,
-               maps.b2, args))
+  if (launch_k(kern, dim3(CL * clusters), dim3(kGemmThreads), Cfg::SMEM_BYTES, stream, maps, args))
     return -1;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+static int env_int_or(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+// tile width, tile schedule and raster of one launch (see gemm_launch); returns `wide`
+static bool gemm_schedule(GemmKind kind, GemmArgs& args, int num_sms, bool cl4, bool allow_wide) {
+  static const int wide_env = [] { const char* e = getenv("LF_WIDE"); return e ? atoi(e) : -1; }();
+  const int min_k = kind == kGemmDgradMasked ? 8192 : 4096;
+  const bool wide_fit = (int64_t)((args.M + 255) / 256) * ((args.N + 511) / 512) >= 4 * (num_sms / 2) &&
+                        args.K >= min_k;
+  const bool wide = allow_wide && (wide_env >= 0 ? wide_env == 1 : wide_fit);
+  static const int sched_env = [] { const char* e = getenv("LF_SCHED"); return e ? atoi(e) : 0; }();
+  const double operand_bytes = 2.0 * ((double)args.M + (double)args.N) * (double)args.K;
+  args.dynamic = sched_env == 1 ? 0 : sched_env == 2 ? 1 : (operand_bytes > 128.0 * (1 << 20) ? 1 : 0);
+  args.tiles_m = cl4 ? (args.M + 511) / 512 : (args.M + 255) / 256;
+  args.tiles_n = wide ? (args.N + 511) / 512 : (args.N + 255) / 256;
+  if (args.group <= 0) args.group = cl4 ? 4 : 8;
+  return wide;
+}
+
+// Shared-input group in one launch: the forward concatenates the projections' output
+// columns (q/k/v: N = 4096 + 1024 + 1024 as one 10-wave GEMM instead of a 7-wave one and two
+// 1.7-wave ones), the input gradient their reduction dims (K = n_q + n_k + n_v: dX written
+// once, no accumulation launches). Segments must be whole tiles (forward: multiples of the
+// tile width; dgrad: of 64). The masked dgrad runs on 256 x 256 tiles (its J partials take
+// turns in the second accumulator buffer).
+int gemm_launch_group(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_sms, cudaStream_t stream) {
+  GemmArgs args = a;
+  if (args.nseg < 2 || args.nseg > kMaxGroup || args.accumulate) return kGemmUnsupported;
+  // The input gradient's concatenated K widens every tile's operand footprint: a wave of
+  // 8 x 9 tiles streams ~8.8 K bytes of dY / W, which must stay in L2 for the grouped raster to
+  // reuse it — measured: q/k/v at K = 6144 one launch 314.6 vs 327.1 µs for three; gate/up at
+  // K = 28672 1346 vs 1250 µs (C2) and 11.3 vs 10.0 ms (C4). LF_GROUP_DGRAD_K overrides.
+  static const int kmax = env_int_or("LF_GROUP_DGRAD_K", 12288);
+  if (kind != kGemmFwd && args.K > kmax) return kGemmUnsupported;
+  // forward: 256 x 512 tiles only with >= 8 waves of them (q/k/v at C2: 5.2 waves of wide
+  // tiles, 294 µs, vs 10.4 of 256 x 256)
+  const bool allow_wide = kind == kGemmFwd &&
+                          (int64_t)((args.M + 255) / 256) * ((args.N + 511) / 512) >= 8 * (num_sms / 2);
+  const bool wide = gemm_schedule(kind, args, num_sms, false, allow_wide || kind == kGemmDgrad);
+  const int unit = kind == kGemmFwd ? (wide ? 512 : 256) : 64;
+  for (int j = 0; j < args.nseg; ++j) {
+    const int lo = j ? args.send[j - 1] : 0;
+    if (args.send[j] <= lo || (args.send[j] - lo) % unit != 0 || args.lcols[j] <= 0 || args.lcols[j] % 16 != 0)
+      return kGemmUnsupported;
+  }
+  switch (kind) {
+    case kGemmFwd:
+      return wide ? launch_one<false, false, 4, true, 2, false, true>(maps, args, num_sms, stream)
+                  : launch_one<false, false, 6, false, 2, false, true>(maps, args, num_sms, stream);
+    case kGemmDgrad:
+      return wide ? launch_one<true, false, 4, true, 2, false, true>(maps, args, num_sms, stream)
+                  : launch_one<true, false, 6, false, 2, false, true>(maps, args, num_sms, stream);
+    case kGemmDgradMasked:
+      return launch_one<true, true, 6, false, 2, false, true>(maps, args, num_sms, stream);
+  }
+  return -1;
 }
 
 int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_sms, cudaStream_t stream) {
@@ -722,19 +959,11 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
   // mask pass -> main loop; next tile's keep bits prefetched, stores deferred), which pays off
   // from K = 8192: C4 q/o 1.45 -> 1.40, gate/up 5.24 -> 4.91, down 5.05 -> 4.91 ms; at K = 4096
   // (C2 down) 2% slower.
-  static const int wide_env = [] { const char* e = getenv("LF_WIDE"); return e ? atoi(e) : -1; }();
-  const int min_k = kind == kGemmDgradMasked ? 8192 : 4096;
-  const bool wide_fit = (int64_t)((args.M + 255) / 256) * ((args.N + 511) / 512) >= 4 * (num_sms / 2) &&
-                        args.K >= min_k;
-  const bool wide = wide_env >= 0 ? wide_env == 1 : wide_fit;
   // Tile schedule. While both operands fit in L2 together, the static persistent
   // round-robin is ~5% faster (C2 q/kv, C1: no per-tile CLC round trip and the pairs'
   // drift costs nothing); beyond that, drifting pairs re-read their operands from DRAM
   // and the in-order CLC schedule wins (C4 q 1.49 -> 1.43 ms, gate 5.5 -> 5.08 ms; ncu,
   // profiles/r01_sched_shapes.txt). LF_SCHED=1 forces static, 2 dynamic (A/B runs).
-  static const int sched_env = [] { const char* e = getenv("LF_SCHED"); return e ? atoi(e) : 0; }();
-  const double operand_bytes = 2.0 * ((double)args.M + (double)args.N) * (double)args.K;
-  args.dynamic = sched_env == 1 ? 0 : sched_env == 2 ? 1 : (operand_bytes > 128.0 * (1 << 20) ? 1 : 0);
   // Two CTA pairs per cluster sharing B by TMA multicast (LF_CL=4; parity-green, off by
   // default): it cuts the power drawn per FLOP (C4 gate: 1.37 -> 1.47 GHz under the cap) but
   // a B200 holds only 33 four-CTA clusters at one CTA per SM — 132 of 148 SMs; pairs use
@@ -742,9 +971,7 @@ int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& a, int num_
   // (C4 step 42.0 -> 46.4 ms, C2 5.67 -> 6.56 ms; profiles/r02_cluster_multicast_ab.txt)
   static const int cl_env = [] { const char* e = getenv("LF_CL"); return e ? atoi(e) : 0; }();
   const bool cl4 = cl_env == 4;
-  args.tiles_m = cl4 ? (args.M + 511) / 512 : (args.M + 255) / 256;
-  args.tiles_n = wide ? (args.N + 511) / 512 : (args.N + 255) / 256;
-  if (args.group <= 0) args.group = cl4 ? 4 : 8;
+  const bool wide = gemm_schedule(kind, args, num_sms, cl4, true);
 #define LF_GEMM_LAUNCH(BMN, MSK, ST, WD)                                                        \
   (cl4 ? launch_one<BMN, MSK, ST, WD, 4>(maps, args, num_sms, stream)                          \
        : launch_one<BMN, MSK, ST, WD, 2>(maps, args, num_sms, stream))

@@ -56,6 +56,7 @@ inline int launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, 
 //                   accumulator, the epilogue warps zero its dropped elements in TMEM, and
 //                   the dY·W main loop accumulates on top (dropout p > 0)
 enum GemmKind { kGemmFwd = 0, kGemmDgrad = 1, kGemmDgradMasked = 2 };
+constexpr int kMaxGroup = 3;  // projections of one shared-input group (q/k/v)
 constexpr int kGemmUnsupported = -3;  // gemm_launch: valid request this build does not run (nothing launched)
 
 struct GemmArgs {
@@ -68,13 +69,30 @@ struct GemmArgs {
   int32_t accumulate;     // 1: C += result (bf16 read-modify-write in the epilogue)
   const LfRoute* routes;  // nullptr = no LoRA chunk
   LfSegTable segs;        // keep-mask source for kGemmDgradMasked
+  // shared-input groups (gemm_launch_group, nseg = J > 1 projections in one launch):
+  //   kGemmFwd    N-concat: projection j owns output columns [send[j-1], send[j]) and writes
+  //               them to Cs[j] (row pitch ldcs[j]); its LoRA K-block reads Ŝ_j / B_j
+  //   kGemmDgrad* K-concat: projection j owns reduction rows [send[j-1], send[j]) (dY_j, W_j);
+  //               its LoRA term reads dŜ_j / A_j, masked with the packed keep bits gbits[j]
+  int32_t nseg;                     // 0: single problem
+  int32_t send[kMaxGroup];          // cumulative segment ends (N forward, K dgrad)
+  int32_t lcols[kMaxGroup];         // padded rank of projection j
+  void* Cs[kMaxGroup];
+  int64_t ldcs[kMaxGroup];
+  const uint8_t* gbits[kMaxGroup];  // null: projection j keeps everything
+  int64_t ld_gbits;
 };
 
+// operand tensor maps: [0] for a single problem; per projection j for a group (forward:
+// a[0] = X, b[j] = W_j; dgrad: a[j] = dY_j, b[j] = W_j; LoRA a2[j] / b2[j])
 struct GemmMaps {
-  CUtensorMap a, b, a2, b2;
+  CUtensorMap a[kMaxGroup], b[kMaxGroup], a2[kMaxGroup], b2[kMaxGroup];
 };
 
 int gemm_launch(GemmKind kind, const GemmMaps& maps, const GemmArgs& args, int num_sms, cudaStream_t stream);
+// one GEMM for a shared-input group (args.nseg = J >= 2; see GemmArgs); kGemmUnsupported when
+// the group's shape has no group variant (nothing launched: run the projections one by one)
+int gemm_launch_group(GemmKind kind, const GemmMaps& maps, const GemmArgs& args, int num_sms, cudaStream_t stream);
 
 // ① dropout + down projection
 struct DownArgs {
@@ -120,7 +138,6 @@ struct GradDownArgs {
 // projection, back to back, so only the first load of a tile comes from DRAM (the
 // projection-major layout of separate launches reads X J times from DRAM); each projection
 // has its own keep bits (TMA'd per stage), dŜ and accumulators.
-constexpr int kMaxGroup = 3;
 struct GroupDownArgs {
   int32_t m, k, J;
   int32_t ctas;

@@ -519,26 +519,32 @@ def lora_group_fwd(x: torch.Tensor, ws: list[torch.Tensor], a: list[torch.Tensor
     lib = _lib.load()
     m, k = x.shape
     st = _stream(x.device)
-    ys, shats, bits, acs, bcs = [], [], [], [], []
+    ys, shats, bits, acs, bcs, plans = [], [], [], [], [], []
     pre = _group_operands(a, b, ranks) if not cache_id else None  # shadows / cache: per projection below
-    for j, w in enumerate(ws):
+    for j, w in enumerate(ws):  # ① per projection (own adapter, seed and mask)
         plan = _group_plan(j, m, k, w.shape[0], ranks, scalings, ps, seeds, offset, offset_dev, training)
         plan.bind(x.device)
-        pp = ctypes.byref(plan.problem)
         if pre is not None:
             a_cat, b_cat = pre[0][j], pre[1][j]
         else:
             a_cat, b_cat = _rank_concat_operands(plan, [a[j]], [b[j]], cache_id)
         s_hat = torch.empty((m, plan.rank_total), dtype=_BF16, device=x.device)
-        y = torch.empty((m, w.shape[0]), dtype=_BF16, device=x.device)
-        _call("dropout_down_fwd", lib.lf_dropout_down_fwd, pp, _ptr(x), _ptr(a_cat), _ptr(s_hat), st)
-        _call("base_fwd", lib.lf_base_fwd, pp, _ptr(x), _ptr(w), _ptr(s_hat), _ptr(b_cat), _ptr(y), st)
-        ys.append(y)
+        _call("dropout_down_fwd", lib.lf_dropout_down_fwd, ctypes.byref(plan.problem), _ptr(x), _ptr(a_cat),
+              _ptr(s_hat), st)
+        ys.append(torch.empty((m, w.shape[0]), dtype=_BF16, device=x.device))
         shats.append(s_hat)
         bits.append(plan.keep_bits if plan.keep_bits is not None
                     else torch.empty((0,), dtype=torch.uint8, device=x.device))
         acs.append(_own(a_cat, a, None, x))
         bcs.append(_own(b_cat, b, None, x))
+        plans.append(plan)
+    # ② for the whole group: one GEMM over the concatenated output columns (the library runs
+    # the projections one by one where the group shape has no one-launch variant)
+    J = len(ws)
+    probs = (ctypes.POINTER(_lib.LfProblem) * J)(*[ctypes.pointer(pl.problem) for pl in plans])
+    arr = lambda ts: (ctypes.c_void_p * J)(*[t_.data_ptr() for t_ in ts])  # noqa: E731
+    _call("base_fwd", lib.lf_base_fwd_group, probs, J, _ptr(x), arr(ws), arr(shats),
+          arr(bcs), arr(ys), st)
     return ys, shats, bits, acs, bcs
 
 
@@ -591,22 +597,11 @@ def lora_group_bwd(dys: list[torch.Tensor], x: torch.Tensor, ws: list[torch.Tens
     ds_ptrs = (ctypes.c_void_p * J)(*[d_.data_ptr() for d_ in dss])
     da_ptrs = (ctypes.c_void_p * J)(*[a_.data_ptr() for a_ in daccs])
     _call("grad_down", lib.lf_grad_down_group, probs, J, _ptr(x), ds_ptrs, da_ptrs, st)
-    if need_dx:  # ⑤: the first writes dX, the others add into it in their epilogues
-        for j, w in enumerate(ws):
-            args = (ctypes.byref(plans[j].problem), _ptr(dys[j]), _ptr(w), _ptr(dss[j]), _ptr(acs[j]))
-            if j == 0:
-                _call("grad_input", lib.lf_grad_input, *args, _ptr(dx), st)
-                continue
-            st_ = _STATS
-            tok = st_.begin("grad_input") if st_ is not None else None
-            rc = lib.lf_grad_input_accum(*args, _ptr(dx), st)
-            if rc == _lib.LF_E_UNSUPPORTED:  # 256x512-tile shapes: their own output, then one add
-                tmp = torch.empty_like(dx)
-                rc = lib.lf_grad_input(*args, _ptr(tmp), st)
-                dx.add_(tmp)
-            if st_ is not None:
-                st_.end("grad_input", tok)
-            _lib.check(rc, "grad_input")
+    if need_dx:  # ⑤: one GEMM over the concatenated reduction dims (dX written once), or per
+        # projection where the group has no one-launch variant (the first writes dX, the others
+        # add into it in their epilogues)
+        arr = lambda ts: (ctypes.c_void_p * J)(*[t_.data_ptr() for t_ in ts])  # noqa: E731
+        _call("grad_input", lib.lf_grad_input_group, probs, J, arr(dys), arr(ws), arr(dss), arr(acs), _ptr(dx), st)
     return dx, dacc
 
 

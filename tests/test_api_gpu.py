@@ -177,19 +177,22 @@ def test_slot_grads_split_unshared_blocks():
     torch.testing.assert_close(total_b, layer.lora_B[0].weight.grad, rtol=1e-5, atol=1e-6)
 
 
-@pytest.mark.parametrize("p,ranks", [(0.0, [16, 8, 16]), (0.1, [16, 8, 16]), (0.1, [64, 16, 32])],
-                         ids=["p0", "p01", "p01_r64"])
-def test_group_matches_separate_projections(p, ranks):
+@pytest.mark.parametrize("p,ranks,kv", [(0.0, [16, 8, 16], 128), (0.1, [16, 8, 16], 128), (0.1, [64, 16, 32], 128),
+                                       (0.0, [16, 8, 16], 256), (0.1, [64, 16, 32], 256)],
+                         ids=["p0", "p01", "p01_r64", "p0_onegemm", "p01_r64_onegemm"])
+def test_group_matches_separate_projections(p, ranks, kv):
     """FusedLoRAGroup (q/k/v sharing X) = three FusedLoRA layers at the same Philox offset:
-    identical outputs, the same dX as autograd's sequential sum of the three input gradients
-    (the ⑤ epilogues add in the same order and rounding), same dA/dB (④ runs as one launch for
-    the group, lf_grad_down_group)."""
+    identical outputs, the same dX as autograd's sum of the three input gradients up to bf16
+    rounding (the group's ⑤ is one GEMM over the concatenated reduction dims — dX rounded once
+    instead of per projection), same dA/dB (④ runs as one launch for the group). kv = 256:
+    whole 256-column tiles, so ② also runs as one GEMM over the concatenated outputs
+    (lf_base_fwd_group); kv = 128 exercises its per-projection fallback."""
     from paper_2510_00206_b200 import FusedLoRAGroup
 
     g = torch.Generator(device=DEV).manual_seed(11)
     k = 512
     bases = {nm: (torch.randn(n, k, device=DEV, generator=g) / k**0.5).to(torch.bfloat16)
-             for nm, n in (("q_proj", 512), ("k_proj", 128), ("v_proj", 128))}
+             for nm, n in (("q_proj", 512), ("k_proj", kv), ("v_proj", kv))}
     grp = FusedLoRAGroup(bases, rank=ranks, scaling=[2.0, 1.0, 0.5], dropout_p=[p, p, 0.0], seeds=[3, 4, 5],
                          init="gaussian", generator=g, dropout_rng="counter")
     x0 = torch.randn(640, k, device=DEV, generator=g).to(torch.bfloat16)
@@ -213,9 +216,9 @@ def test_group_matches_separate_projections(p, ranks):
         # dA/dB: the same fp32 products summed in another split-K partition (one ④ launch for
         # the group vs one per projection; red.global.add order) — reduction-order noise only
         assert _rel(layer.lora_A.weight.grad, got[j][1]) < 1e-4 and _rel(layer.lora_B.weight.grad, got[j][2]) < 1e-4
-    # the sums of the three input gradients in the same order and rounding; dŜ (③'s atomic
-    # split-K) may round differently run to run, hence a tolerance instead of equality
-    assert _rel(dx_group, xs.grad) < 1e-3
+    # one rounding of the summed input gradient (group) vs three bf16 dX_j added in bf16
+    # (autograd): bf16-level differences only (SPEC.md §5 tolerance)
+    assert _rel(dx_group, xs.grad) < 4e-3
 
 
 def test_group_compiles_fullgraph():
@@ -240,3 +243,55 @@ def test_group_compiles_fullgraph():
     eager = run(grp)
     got = run(torch.compile(grp, backend="aot_eager", fullgraph=True))
     assert torch.equal(got[0], eager[0]) and _rel(got[1], eager[1]) < 1e-3 and _rel(got[2], eager[2]) < 1e-4
+
+
+@pytest.mark.parametrize("m,k,ns,wide", [(8192, 4096, (4096, 1024, 1024), ""), (2048, 1024, (2048, 512, 512), "0")],
+                         ids=["c2_qkv", "small_narrow_tiles"])
+def test_group_one_gemm_vs_fp32_torch(m, k, ns, wide):
+    """The shared-input group at a full BASELINE C2 q/k/v size through lf_base_fwd_group (one
+    GEMM over N = 6144 — 256 x 512 tiles) and lf_grad_input_group (one GEMM over K = 6144 with
+    three masked LoRA terms entering the accumulator in turn) against a torch fp32
+    restatement of Eq. 1 on the kernels' own keep masks: rel-Fro <= 4e-3 (SPEC.md §5)."""
+    import os
+    import subprocess
+    import sys
+
+    if wide:  # the 256 x 256 group tiles: another process (LF_WIDE is read once)
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        r = subprocess.run([sys.executable, "-c", f"import tests.test_api_gpu as t; t._group_vs_fp32({m}, {k}, {ns})"],
+                           cwd=root, env=dict(os.environ, LF_WIDE=wide), capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+        return
+    _group_vs_fp32(m, k, ns)
+
+
+def _group_vs_fp32(m, k, ns, p=0.1):
+    from paper_2510_00206_b200 import AdapterConfig, Segment, dropout_keep_mask, fused_lora_group
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    g = torch.Generator(device=DEV).manual_seed(21)
+    x = torch.randn(m, k, device=DEV, generator=g).to(torch.bfloat16).requires_grad_(True)
+    ws = [(torch.randn(n, k, device=DEV, generator=g) / k**0.5).to(torch.bfloat16) for n in ns]
+    As = [((torch.rand(16, k, device=DEV, generator=g) * 2 - 1) / k**0.5).requires_grad_(True) for _ in ns]
+    Bs = [(torch.randn(n, 16, device=DEV, generator=g) / 4).requires_grad_(True) for n in ns]
+    dys = [torch.randn(m, n, device=DEV, generator=g).to(torch.bfloat16) for n in ns]
+    ads = [AdapterConfig(16, 2.0, p if j < 2 else 0.0, 40 + j) for j in range(len(ns))]
+    ys = fused_lora_group(x, ws, As, Bs, ads, offset=5)
+    torch.autograd.backward(ys, dys)
+    rel = lambda g_, r_: float((g_.float() - r_).norm() / r_.norm())  # noqa: E731
+    dx_ref = torch.zeros(m, k, device=DEV)
+    errs = {}
+    for j, (w, a, b, dy, ad) in enumerate(zip(ws, As, Bs, dys, ads)):
+        keep = dropout_keep_mask(m, k, [ad], [Segment(0, 0, m)], offset=5, device=DEV).float()
+        sc = ad.scaling / (1.0 - ad.dropout_p)
+        ab, bb = a.detach().bfloat16().float(), b.detach().bfloat16().float()
+        xm = x.detach().float() * keep
+        s = ((xm @ ab.T) * sc).bfloat16().float()
+        errs[f"y{j}"] = rel(ys[j].detach(), x.detach().float() @ w.float().T + s @ bb.T)
+        ds = ((dy.float() @ bb) * sc).bfloat16().float()
+        errs[f"dA{j}"] = rel(a.grad, ds.T @ xm)
+        errs[f"dB{j}"] = rel(b.grad, dy.float().T @ s)
+        dx_ref += dy.float() @ w.float() + keep * (ds @ ab)
+        del xm, keep
+    errs["dx"] = rel(x.grad, dx_ref)
+    assert all(v < 4e-3 for v in errs.values()), errs
