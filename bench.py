@@ -470,13 +470,42 @@ def graphed_runner(step_local, world, layers, warmup):
 
     g = GraphedStep(step_local, warmup=warmup)
     if world == 1:
-        return g.replay
+        def run():
+            return g.replay()
+    else:
+        def run():
+            g.replay()
+            allreduce_grads(layers)
 
-    def run():
-        g.replay()
-        allreduce_grads(layers)
-
+    run.graphed = g  # the per-launcher timing pass captures beside it in the same memory pool
     return run
+
+
+def graph_launch_durations(step_local, graphed, steps: int) -> dict:
+    """{launcher: [ms per launch, ...]} over `steps` replays of a graph of the step captured
+    with timing events around every launcher (external events: recorded inside the graph)."""
+    import torch
+
+    from paper_2510_00206_b200 import functional as F_
+    from paper_2510_00206_b200.functional import refresh_stale_operand_shadows
+
+    stats = F_.LaunchStats(timed=True, external=True)
+    F_.set_launch_stats(stats)
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, pool=graphed.graph.pool()):
+            step_local()
+    finally:
+        F_.set_launch_stats(None)
+    out: dict = {}
+    for _ in range(steps):
+        refresh_stale_operand_shadows()
+        g.replay()
+        torch.cuda.synchronize()
+        for name, pairs in stats.events.items():
+            out.setdefault(name, []).extend(a.elapsed_time(b) for a, b in pairs)
+    del g
+    return out
 
 
 def zero_grads(layers, inputs=None):
@@ -656,14 +685,26 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     barrier()
     ms = max_over_ranks(t0.elapsed_time(t1) / args.steps)
     # per-launcher CUDA-event timing in a separate pass over the same steps (events on the
-    # launching stream bracket every launcher; kept out of the headline loop)
-    stats = F_.LaunchStats(timed=True)
-    F_.set_launch_stats(stats)
-    for _ in range(args.steps):
-        step()
-    torch.cuda.synchronize()
-    F_.set_launch_stats(None)
-    durs = stats.durations_ms()
+    # launching stream bracket every launcher; kept out of the headline loop). Graphed runs
+    # capture the step once more with the events inside the graph, so each launcher is timed
+    # on the device as it runs in the graph (an eager pass would add the host's launch gaps
+    # to every small kernel: C1's GEMMs read 0.56 of peak that way)
+    durs = None
+    per_kernel_timing = "CUDA events around each launcher, eager steps"
+    if args.graph and getattr(run, "graphed", None) is not None:
+        try:
+            durs = graph_launch_durations(step_local, run.graphed, args.steps)
+            per_kernel_timing = "CUDA events around each launcher inside a CUDA-graph capture of the step"
+        except Exception as e:
+            print(f"[bench] graphed launcher timing failed ({type(e).__name__}: {e}); timing eagerly", file=sys.stderr)
+    if durs is None:
+        stats = F_.LaunchStats(timed=True)
+        F_.set_launch_stats(stats)
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        F_.set_launch_stats(None)
+        durs = stats.durations_ms()
 
     breakdown = None
     if True:  # every rank replays (the replay may hold a collective)
@@ -784,6 +825,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             }
         # the bulky parts last, so a truncated tail of the line keeps the headline keys
         line["per_kernel"] = kernels
+        line["per_kernel_timing"] = per_kernel_timing
         if multi is not None:
             line["multi_lora"] = multi
         line["step_breakdown"] = breakdown

@@ -49,23 +49,29 @@ class LaunchStats:
     """Counts kernel launches and (optionally) times each launcher with CUDA events on the
     launching stream. Install with ``set_launch_stats``; used by bench.py."""
 
-    def __init__(self, timed: bool = False):
+    def __init__(self, timed: bool = False, external: bool = False):
         self.timed = timed
+        self.external = external  # events recorded inside a CUDA-graph capture (timing per replay)
         self.launches: dict[str, int] = {}
         self.events: dict[str, list] = {}
+
+    def _event(self):
+        if self.external:
+            return torch.cuda.Event(enable_timing=True, external=True)
+        return torch.cuda.Event(enable_timing=True)
 
     def begin(self, name: str):
         self.launches[name] = self.launches.get(name, 0) + 1
         if not self.timed:
             return None
-        ev = torch.cuda.Event(enable_timing=True)
+        ev = self._event()
         ev.record()
         return ev
 
     def end(self, name: str, start) -> None:
         if start is None:
             return
-        ev = torch.cuda.Event(enable_timing=True)
+        ev = self._event()
         ev.record()
         self.events.setdefault(name, []).append((start, ev))
 
