@@ -52,18 +52,28 @@ def main():
     by_grp: dict = {}
     for name, k, n, grp in bench.projections(config):
         by_grp.setdefault(grp, []).append(name)
+    # a group's ② is one launch over the concatenated outputs (lf_base_fwd_group) when every
+    # width tiles; its ⑤ one launch over the concatenated reduction dims while that stays
+    # <= 12288 (lf_gemm.cu gemm_launch_group), else one launch per projection
     for grp, names in by_grp.items():
         if grouped and config != "c3" and grp in bench.SHARED_INPUT_GROUPS and len(names) > 1:
-            order += [(nm, "base_fwd") for nm in names] + [(nm, "grad_input") for nm in names]
+            ns = [shapes[nm][1] for nm in names]
+            fwd_one = all(n_ % 256 == 0 for n_ in ns)
+            bwd_one = sum(ns) <= 12288 and all(n_ % 64 == 0 for n_ in ns)
+            order += [(tuple(names), "base_fwd")] if fwd_one else [((nm,), "base_fwd") for nm in names]
+            order += [(tuple(names), "grad_input")] if bwd_one else [((nm,), "grad_input") for nm in names]
         else:
             for nm in names:
-                order += [(nm, "base_fwd"), (nm, "grad_input")]
+                order += [((nm,), "base_fwd"), ((nm,), "grad_input")]
     alg = []
-    for name, kind in order:
-        k, n = shapes[name]
-        b = (2 * (m * k + k * n + m * r + r * n) + 2 * m * n if kind == "base_fwd"
-             else 2 * (m * n + k * n + m * r + k * r) + 2 * m * k)
-        alg.append((f"{name} {kind}", b))
+    for names, kind in order:
+        k = shapes[names[0]][0]
+        ns = [shapes[nm][1] for nm in names]
+        if kind == "base_fwd":  # X once, every W_j / Ŝ_j / B_j once, every Y_j written once
+            b = 2 * m * k + sum(2 * (k * n_ + m * r + r * n_) + 2 * m * n_ for n_ in ns)
+        else:  # every dY_j / W_j / dŜ_j / A_j once, dX written once
+            b = sum(2 * (m * n_ + k * n_ + m * r + k * r) for n_ in ns) + 2 * m * k
+        alg.append(("/".join(names) + f" {kind}", b))
     n = min(len(launches), len(alg))
     dram = sum(l["dram_read"] + l["dram_write"] for l in launches[:n])
     algb = sum(a for _, a in alg[:n])

@@ -11,11 +11,11 @@ python bench.py --config c5 --steps 4 --warmup 3 > $OUT/bench_c5.json 2> $OUT/be
 python bench.py --impl reference --steps 5 --warmup 3 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-multi > /dev/null 2>&1
-ncu --set full --clock-control none -k regex:lf_gemm -c 14 -o $OUT/gemm_step \
+ncu --set full --clock-control none -k regex:lf_gemm -c 9 -o $OUT/gemm_step \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-multi --no-graph > /dev/null 2>&1
 ncu --set full --clock-control none -k "regex:lf_(down|gradup|finalize|dgrad_a)" -c 24 -o $OUT/lowrank_step \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-multi --no-graph > /dev/null 2>&1
-ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:lf_gemm -c 14 -o $OUT/gemm_step_c4 \
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:lf_gemm -c 9 -o $OUT/gemm_step_c4 \
   python bench.py --config c4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > /dev/null 2>&1
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:lf_gemm -c 2 -o $OUT/gemm_step_c1 \
   python bench.py --config c1 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > /dev/null 2>&1
