@@ -156,6 +156,30 @@ def test_null_and_misaligned_pointers_rejected(lib):
     assert lib.lf_grad_up(None, None, None, None, None, None, None) == _lib.LF_E_INVALID
 
 
+def test_group_entry_points_reject_bad_arguments(lib):
+    """ABI 5 group launchers (lf_base_fwd_group / lf_grad_input_group) and the ABI 4 one
+    (lf_grad_down_group): projection counts outside 1..3, missing arrays and projections that
+    do not share the input are LF_E_INVALID before anything touches a GPU."""
+    P = ctypes.POINTER(_lib.LfProblem)
+    V = ctypes.c_void_p
+    a, b = _problem(), _problem(k=128)
+    a.routes = b.routes = 4096
+    probs = (P * 2)(ctypes.pointer(a), ctypes.pointer(b))
+    arr = (V * 3)(16, 16, 16)
+    x = V(16)
+    assert lib.lf_base_fwd_group(probs, 0, x, arr, arr, arr, arr, None) == _lib.LF_E_INVALID
+    assert lib.lf_base_fwd_group(probs, 4, x, arr, arr, arr, arr, None) == _lib.LF_E_INVALID
+    assert lib.lf_base_fwd_group(probs, 2, x, None, arr, arr, arr, None) == _lib.LF_E_INVALID
+    assert lib.lf_base_fwd_group(probs, 2, x, arr, arr, arr, arr, None) == _lib.LF_E_INVALID
+    assert "share the input" in _lib.last_error()
+    assert lib.lf_grad_input_group(probs, 0, arr, arr, arr, arr, x, None) == _lib.LF_E_INVALID
+    assert lib.lf_grad_input_group(probs, 2, arr, arr, arr, None, x, None) == _lib.LF_E_INVALID
+    assert lib.lf_grad_input_group(probs, 2, arr, arr, arr, arr, None, None) == _lib.LF_E_INVALID
+    assert lib.lf_grad_input_group(probs, 2, arr, arr, arr, arr, x, None) == _lib.LF_E_INVALID
+    assert "share the input" in _lib.last_error()
+    assert lib.lf_grad_down_group(probs, 4, x, arr, arr, None) == _lib.LF_E_INVALID
+
+
 def test_no_gpu_reports_cuda_error_not_crash(lib):
     """A valid problem on a machine without a B200 fails with LF_E_CUDA/UNSUPPORTED, never a crash."""
     import torch
