@@ -128,15 +128,15 @@ LF_API int lf_grad_down(const LfProblem* p, const uint16_t* x, const uint16_t* d
 /* ④ for projections that read the same input X (q/k/v, gate/up):
  * da_accum[j] (R_j x k, fp32) += dŜ_jᵀ·(M_j⊙X) for j < nproj (<= 3), one launch that reads
  * each X tile from DRAM once (projection j's copy is masked with its own keep bits).
- * probs[j] is projection j's problem (same m, k; one segment over all rows). Falls back to
- * per-projection lf_grad_down when a problem does not have that shape. ABI 4. */
+ * probs[j] is projection j's problem (same m, k; any segment table since ABI 5). Falls back
+ * to per-projection lf_grad_down when the accumulators do not fit one launch. ABI 4. */
 LF_API int lf_grad_down_group(const LfProblem* const* probs, int32_t nproj, const uint16_t* x,
                               const uint16_t* const* ds, float* const* da_accum, void* stream);
 
 /* ② for a shared-input group (q/k/v): y[j] = X·W_jᵀ + Ŝ_j·B_jᵀ for j < nproj (<= 3) as ONE
  * GEMM over the concatenated output columns (k/v's narrow N no longer runs as its own
- * under-filled launch). probs[j]: projection j's problem (same m, k; one segment over all
- * rows); w / s_hat / b_cat / y: per-projection arrays as for lf_base_fwd. Falls back to
+ * under-filled launch). probs[j]: projection j's problem (same m, k; any segment table);
+ * w / s_hat / b_cat / y: per-projection arrays as for lf_base_fwd. Falls back to
  * per-projection lf_base_fwd for other shapes. ABI 5. */
 LF_API int lf_base_fwd_group(const LfProblem* const* probs, int32_t nproj, const uint16_t* x,
                              const uint16_t* const* w, const uint16_t* const* s_hat, const uint16_t* const* b_cat,

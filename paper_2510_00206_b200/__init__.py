@@ -2,8 +2,10 @@
 
 Public API
   FusedLoRA, FusedMultiLoRA          nn.Modules (PEFT parameter names lora_A / lora_B)
-  FusedLoRAGroup                     projections sharing one input (q/k/v, gate/up), dX summed in-GEMM
+  FusedLoRAGroup, FusedMultiLoRAGroup  projections sharing one input (q/k/v, gate/up): ②/④/⑤ as
+                                     one launch each for the group
   fused_lora, fused_multi_lora       functional forms (autograd; torch.ops.lorafusion_b200.lora_fwd/_bwd)
+  fused_lora_group, fused_multi_lora_group   the group forms (torch.ops.lorafusion_b200.lora_group_*)
   invalidate_operand_caches          forget cached bf16 adapter operands after out-of-optimizer updates
   AdapterConfig, Segment, LayerPlan  adapter hyper-parameters and microbatch segment tables
   dropout_keep_mask                  SPEC.md §3 mask the kernels regenerate
@@ -15,8 +17,9 @@ The compute path is the sm_100a shared library liblorafusion_b200.so (C ABI in
 include/lorafusion_b200.h). There is no CPU fallback.
 """
 from .errors import ExtensionMissingError, KernelError, LoRAFusionError, ValidationError
-from .functional import dropout_keep_mask, fused_lora, fused_lora_group, fused_multi_lora, invalidate_operand_caches
-from .modules import FusedLoRA, FusedLoRAGroup, FusedMultiLoRA
+from .functional import (dropout_keep_mask, fused_lora, fused_lora_group, fused_multi_lora, fused_multi_lora_group,
+                         invalidate_operand_caches)
+from .modules import FusedLoRA, FusedLoRAGroup, FusedMultiLoRA, FusedMultiLoRAGroup
 from .plan import AdapterConfig, LayerPlan, Segment, padded_rank, segments_from_lengths
 from .costmodel import (
     B200,
@@ -41,6 +44,7 @@ __all__ = [
     "FusedLoRA",
     "FusedLoRAGroup",
     "FusedMultiLoRA",
+    "FusedMultiLoRAGroup",
     "GemmShape",
     "H100_SXM",
     "HardwareProfile",
@@ -58,6 +62,7 @@ __all__ = [
     "fused_lora",
     "fused_lora_group",
     "fused_multi_lora",
+    "fused_multi_lora_group",
     "invalidate_operand_caches",
     "lora_memory_bytes",
     "padded_rank",

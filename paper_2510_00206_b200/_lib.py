@@ -15,6 +15,7 @@ from .errors import ExtensionMissingError, KernelError, ValidationError
 
 LF_ABI_VERSION = 5
 LF_MAX_SEGMENTS = 32
+LF_MAX_GROUP = 3  # projections of one shared-input group launch (lf_*_group)
 LF_MAX_RANK_TOTAL = 128
 ROUTE_TILE_ROWS = 128  # ls/costmodel.py:25
 ROUTE_ENTRY_BYTES = 16  # ls/costmodel.py:26

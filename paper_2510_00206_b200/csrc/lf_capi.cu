@@ -502,9 +502,9 @@ int lf_grad_down(const LfProblem* p, const uint16_t* x, const uint16_t* ds, floa
   return LF_OK;
 }
 
-// ④ over a shared-input group: one launch when every projection is a single segment over
-// all rows whose keep bits (if any) ①'s launch left 16-byte pitched; otherwise (and for
-// J = 1) the per-projection lf_grad_down.
+// ④ over a shared-input group: one launch when every projection's keep bits (if any) ①'s
+// launch left 16-byte pitched and the J accumulators fit TMEM; otherwise (and for J = 1) the
+// per-projection lf_grad_down. Any segment table: dŜ_j is zero off each row's segment.
 int lf_grad_down_group(const LfProblem* const* probs, int32_t nproj, const uint16_t* x, const uint16_t* const* ds,
                        float* const* da_accum, void* stream) {
   if (!probs || nproj < 1 || nproj > lf::kMaxGroup || !ds || !da_accum)
@@ -521,10 +521,10 @@ int lf_grad_down_group(const LfProblem* const* probs, int32_t nproj, const uint1
     LF_TRY(check_ptr(da_accum[j], "da_accum"));
     if (p->m != probs[0]->m || p->k != probs[0]->k)
       return fail(LF_E_INVALID, "lf_grad_down_group: projections must share the input (m, k)");
-    const bool single = p->num_segments == 1 && p->segments[0].row_start == 0 && p->segments[0].row_end == p->m &&
-                        p->segments[0].col_start == 0 && p->segments[0].rank == p->rank_total && p->row_base == 0;
+    // any segment table (dŜ_j is zero off each row's segment; ① leaves all-ones keep bits
+    // on rows of p = 0 segments)
     const bool bits_ok = t[j].mask_mode == 0 || (t[j].mask_mode == 1 && t[j].bits && t[j].ld_bits % 16 == 0);
-    if (!single || !bits_ok) fused = false;
+    if (p->row_base != 0 || !bits_ok) fused = false;
     rsum += p->rank_total;
     if (p->rank_total > rmax) rmax = p->rank_total;
   }
@@ -548,7 +548,7 @@ int lf_grad_down_group(const LfProblem* const* probs, int32_t nproj, const uint1
     const LfProblem* p = probs[j];
     if (!make_map(&maps.d[j], ds[j], p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B))
       return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (ds)");
-    a.masked[j] = t[j].mask_mode == 1 && t[j].seg[0].thr != 0;
+    a.masked[j] = t[j].mask_mode == 1;
     if (a.masked[j] && !make_map_u8(&maps.bits[j], t[j].bits, p->m, t[j].ld_bits, t[j].ld_bits, 16, 128))
       return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (keep bits)");
     a.R[j] = p->rank_total;
@@ -621,14 +621,12 @@ static int grad_input_impl(const LfProblem* p, const uint16_t* dy, const uint16_
 }
 
 // shared-input groups (② / ⑤ over J projections that read the same input): one GEMM when
-// every projection is a single adapter segment over all rows (the FusedLoRAGroup case) and
-// its width fits the group tiling; otherwise the projections run one by one (⑤: the first
-// writes dX, the others add into it). LF_GROUP_GEMM=0 forces the per-projection path.
-static bool group_single(const LfProblem* p) {
-  return p->num_segments == 1 && p->segments[0].row_start == 0 && p->segments[0].row_end == p->m &&
-         p->segments[0].col_start == 0 && p->segments[0].rank == p->rank_total && p->row_base == 0 &&
-         p->rank_total >= 16;
-}
+// the group's widths fit the group tiling; otherwise the projections run one by one (⑤: the
+// first writes dX, the others add into it). LF_GROUP_GEMM=0 forces the per-projection path.
+// The group kernels take each projection's whole rank-concat width as its LoRA K-range
+// (no routing table): Ŝ_j / dŜ_j are zero off each row's segment, and ① leaves all-ones
+// keep bits on rows of p = 0 segments, so any segment table works.
+static bool group_ok(const LfProblem* p) { return p->row_base == 0 && p->rank_total >= 16; }
 
 int lf_base_fwd_group(const LfProblem* const* probs, int32_t nproj, const uint16_t* x, const uint16_t* const* w,
                       const uint16_t* const* s_hat, const uint16_t* const* b_cat, uint16_t* const* y, void* stream) {
@@ -645,7 +643,7 @@ int lf_base_fwd_group(const LfProblem* const* probs, int32_t nproj, const uint16
       return fail(LF_E_INVALID, "lf_base_fwd_group: projections must share the input (m, k)");
     LF_TRY(check_ptr(w[j], "w"));
     LF_TRY(check_ptr(y[j], "y"));
-    if (!group_single(p)) fused = false;
+    if (!group_ok(p)) fused = false;
   }
   static const int group_env = env_int("LF_GROUP_GEMM", 1);
   if (fused && group_env) {
@@ -704,8 +702,8 @@ int lf_grad_input_group(const LfProblem* const* probs, int32_t nproj, const uint
       return fail(LF_E_INVALID, "lf_grad_input_group: projections must share the input (m, k)");
     LF_TRY(check_ptr(dy[j], "dy"));
     LF_TRY(check_ptr(w[j], "w"));
-    if (!group_single(p)) fused = false;
-    const bool m_j = t[j].mask_mode != 0 && t[j].seg[0].thr != 0;
+    if (!group_ok(p)) fused = false;
+    const bool m_j = t[j].mask_mode != 0;  // some segment drops (Philox) or an explicit mask
     if (m_j && !(t[j].mask_mode == 1 && t[j].bits)) fused = false;  // packed bits from ① only
     masked = masked || m_j;
   }
@@ -732,7 +730,7 @@ int lf_grad_input_group(const LfProblem* const* probs, int32_t nproj, const uint
       kk += p->n;
       a.send[j] = kk;
       a.lcols[j] = p->rank_total;
-      a.gbits[j] = (t[j].mask_mode == 1 && t[j].seg[0].thr != 0) ? t[j].bits : nullptr;
+      a.gbits[j] = t[j].mask_mode == 1 ? t[j].bits : nullptr;
     }
     a.ld_gbits = t[0].ld_bits;
     a.nseg = nproj;

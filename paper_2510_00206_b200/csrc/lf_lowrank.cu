@@ -209,8 +209,10 @@ __global__ void __launch_bounds__(kDownThreads, 2)
         const bool my_mask = seg >= 0 && (EXPLICIT || args.segs.seg[seg].thr != 0);
         const PhiloxRow pr = philox_row(args.segs.seg[seg >= 0 ? seg : 0], (uint32_t)(row + args.segs.row_base), step_offset);
         // Philox runs once per step: ④ and ⑤ read the packed bits written here (4 bytes per
-        // k-block and thread; word stores when the row pitch keeps them aligned)
-        uint8_t* bits_row = (!EXPLICIT && my_mask && args.segs.bits) ? args.segs.bits + (int64_t)row * nbytes : nullptr;
+        // k-block and thread; word stores when the row pitch keeps them aligned). Rows of
+        // p = 0 segments get all-ones bits, so the group launchers (one mask per projection,
+        // no segment table) can apply the bits of every row that carries a LoRA term.
+        uint8_t* bits_row = (!EXPLICIT && seg >= 0 && args.segs.bits) ? args.segs.bits + (int64_t)row * nbytes : nullptr;
         const bool bits_words = (nbytes & 3) == 0 && ((reinterpret_cast<uintptr_t>(args.segs.bits) & 3u) == 0);
         for (int kb = sp.k0; kb < sp.k1; ++kb) {
           // the keep bits depend only on (row, column, seed, offset): generate them while the

@@ -509,31 +509,58 @@ def _padr(r: int) -> int:
     return -(-int(r) // 16) * 16
 
 
-def _group_plan(j, x_rows, k, n, ranks, scalings, ps, seeds, offset, offset_dev, training) -> LayerPlan:
-    return _plan(x_rows, k, n, [ranks[j]], [scalings[j]], [ps[j]], [seeds[j]], [0, 0, x_rows, 0], offset, offset_dev,
-                 None, training, True, 0)
+def _group_split(nads, *flat):
+    """Per-projection slices of flat per-(projection, adapter) lists."""
+    out, pos = [], 0
+    for n_ in nads:
+        out.append(tuple(list(f[pos:pos + n_]) for f in flat))
+        pos += n_
+    return out
+
+
+def _group_layout(m, nads, ranks, segs):
+    """(segments, [(col_starts_j, R_j)]) of a group call: the projections share the segment
+    table (none: one segment over all rows, adapter 0) and each lays out its own adapters."""
+    segs = list(segs) if segs else [0, 0, m, 0]
+    segments = [Segment(*segs[i:i + 4]) for i in range(0, len(segs), 4)]
+    lays = []
+    for (r_j,) in _group_split(nads, ranks):
+        cs, _, R = rank_layout(r_j, segments, True)
+        lays.append((cs, R))
+    return segs, segments, lays
+
+
+def _group_plan(j, x_rows, k, n, nads, ranks, scalings, ps, seeds, segs, offset, offset_dev,
+                training) -> LayerPlan:
+    r_j, s_j, p_j, sd_j = _group_split(nads, ranks, scalings, ps, seeds)[j]
+    return _plan(x_rows, k, n, r_j, s_j, p_j, sd_j, segs, offset, offset_dev, None, training, True, 0)
 
 
 @torch.library.custom_op(f"{_NS}::lora_group_fwd", mutates_args=(), device_types="cuda")
 def lora_group_fwd(x: torch.Tensor, ws: list[torch.Tensor], a: list[torch.Tensor], b: list[torch.Tensor],
-                   ranks: list[int], scalings: list[float], ps: list[float], seeds: list[int], offset: int,
-                   offset_dev: Optional[torch.Tensor], training: bool,
+                   nads: list[int], ranks: list[int], scalings: list[float], ps: list[float], seeds: list[int],
+                   segs: list[int], offset: int, offset_dev: Optional[torch.Tensor], training: bool,
                    cache_id: int) -> tuple[list[torch.Tensor], list[torch.Tensor], list[torch.Tensor],
                                            list[torch.Tensor], list[torch.Tensor]]:
-    """① + ② of every projection j (own adapter, seed and dropout mask, one shared Philox
-    offset): returns ([Y_j], [Ŝ_j], [packed keep mask_j or empty], [A_j bf16], [B_j bf16])."""
+    """① + ② of every projection j of a shared-input group (its own adapters — nads[j] of
+    them, flat in a / b / ranks / … — seeds and dropout masks, one shared Philox offset and
+    segment table): returns ([Y_j], [Ŝ_j], [packed keep mask_j or empty], [A_cat_j bf16],
+    [B_cat_j bf16])."""
     lib = _lib.load()
     m, k = x.shape
     st = _stream(x.device)
+    segs, _, _ = _group_layout(m, nads, ranks, segs)
     ys, shats, bits, acs, bcs, plans = [], [], [], [], [], []
-    pre = _group_operands(a, b, ranks) if not cache_id else None  # shadows / cache: per projection below
-    for j, w in enumerate(ws):  # ① per projection (own adapter, seed and mask)
-        plan = _group_plan(j, m, k, w.shape[0], ranks, scalings, ps, seeds, offset, offset_dev, training)
+    single = all(n_ == 1 for n_ in nads) and len(segs) == 4
+    pre = _group_operands(a, b, ranks) if (single and not cache_id) else None  # one multi-tensor cast
+    per = _group_split(nads, a, b)
+    for j, w in enumerate(ws):  # ① per projection (own adapters, seeds and masks)
+        plan = _group_plan(j, m, k, w.shape[0], nads, ranks, scalings, ps, seeds, segs, offset, offset_dev, training)
         plan.bind(x.device)
         if pre is not None:
             a_cat, b_cat = pre[0][j], pre[1][j]
         else:
-            a_cat, b_cat = _rank_concat_operands(plan, [a[j]], [b[j]], cache_id)
+            a_cat, b_cat = _rank_concat_operands(plan, per[j][0], per[j][1], cache_id)
         s_hat = torch.empty((m, plan.rank_total), dtype=_BF16, device=x.device)
         _call("dropout_down_fwd", lib.lf_dropout_down_fwd, ctypes.byref(plan.problem), _ptr(x), _ptr(a_cat),
               _ptr(s_hat), st)
@@ -549,44 +576,44 @@ def lora_group_fwd(x: torch.Tensor, ws: list[torch.Tensor], a: list[torch.Tensor
     J = len(ws)
     probs = (ctypes.POINTER(_lib.LfProblem) * J)(*[ctypes.pointer(pl.problem) for pl in plans])
     arr = lambda ts: (ctypes.c_void_p * J)(*[t_.data_ptr() for t_ in ts])  # noqa: E731
-    _call("base_fwd", lib.lf_base_fwd_group, probs, J, _ptr(x), arr(ws), arr(shats),
-          arr(bcs), arr(ys), st)
+    _call("base_fwd", lib.lf_base_fwd_group, probs, J, _ptr(x), arr(ws), arr(shats), arr(bcs), arr(ys), st)
     return ys, shats, bits, acs, bcs
 
 
 @lora_group_fwd.register_fake
-def _lora_group_fwd_fake(x, ws, a, b, ranks, scalings, ps, seeds, offset, offset_dev, training, cache_id):
+def _lora_group_fwd_fake(x, ws, a, b, nads, ranks, scalings, ps, seeds, segs, offset, offset_dev, training, cache_id):
     m, k = x.shape
+    segs, segments, lays = _group_layout(m, nads, ranks, segs)
     ys = [x.new_empty((m, w.shape[0])) for w in ws]
-    shats = [x.new_empty((m, -(-r // 16) * 16)) for r in ranks]
-    bits = [x.new_empty((m, k // 8), dtype=torch.uint8) if (training and p_ > 0) else
-            x.new_empty((0,), dtype=torch.uint8) for p_ in ps]
-    acs = [x.new_empty((-(-r // 16) * 16, k)) for r in ranks]
-    bcs = [x.new_empty((w.shape[0], -(-r // 16) * 16)) for r, w in zip(ranks, ws)]
+    shats = [x.new_empty((m, R)) for _, R in lays]
+    bits = [x.new_empty((m, k // 8), dtype=torch.uint8) if _needs_bits(p_j, segs, None, training) else
+            x.new_empty((0,), dtype=torch.uint8) for (p_j,) in _group_split(nads, ps)]
+    acs = [x.new_empty((R, k)) for _, R in lays]
+    bcs = [x.new_empty((w.shape[0], R)) for (_, R), w in zip(lays, ws)]
     return ys, shats, bits, acs, bcs
 
 
 @torch.library.custom_op(f"{_NS}::lora_group_bwd", mutates_args=(), device_types="cuda")
 def lora_group_bwd(dys: list[torch.Tensor], x: torch.Tensor, ws: list[torch.Tensor], acs: list[torch.Tensor],
-                   bcs: list[torch.Tensor], shats: list[torch.Tensor], bits: list[torch.Tensor], ranks: list[int],
-                   scalings: list[float], ps: list[float], seeds: list[int], offset: int,
-                   offset_dev: Optional[torch.Tensor], training: bool, cache_id: int,
+                   bcs: list[torch.Tensor], shats: list[torch.Tensor], bits: list[torch.Tensor], nads: list[int],
+                   ranks: list[int], scalings: list[float], ps: list[float], seeds: list[int], segs: list[int],
+                   offset: int, offset_dev: Optional[torch.Tensor], training: bool, cache_id: int,
                    need_dx: bool) -> tuple[torch.Tensor, torch.Tensor]:
-    """③ + ④ + ⑤ of every projection: returns (dX = Σ_j dX_j, [dA_0 | dB_0 | dA_1 | dB_1 ...]
-    fp32 flat, one zero-fill for the whole group).
-    The first ⑤ writes dX, the others add into it in their epilogues (lf_grad_input_accum):
-    no separate gradient-sum kernels."""
+    """③ + ④ + ⑤ of every projection: returns (dX = Σ_j dX_j, [dA_cat_0 | dB_cat_0 | dA_cat_1 |
+    dB_cat_1 ...] fp32 flat, one zero-fill for the whole group). ④ runs as one launch and ⑤
+    as one GEMM over the concatenated reduction dims where the group allows it."""
     lib = _lib.load()
     m, k = x.shape
     st = _stream(x.device)
+    segs, _, lays = _group_layout(m, nads, ranks, segs)
     dx = torch.empty((m, k) if need_dx else (0,), dtype=_BF16, device=x.device)
-    sizes = [_padr(r) * (k + w.shape[0]) for r, w in zip(ranks, ws)]
+    sizes = [R * (k + w.shape[0]) for (_, R), w in zip(lays, ws)]
     dacc = torch.zeros(sum(sizes), dtype=torch.float32, device=x.device)
     plans, daccs, dss = [], [], []
     pos = 0
     for j, w in enumerate(ws):  # ③ per projection (each reads its own dY)
         n = w.shape[0]
-        plan = _group_plan(j, m, k, n, ranks, scalings, ps, seeds, offset, offset_dev, training)
+        plan = _group_plan(j, m, k, n, nads, ranks, scalings, ps, seeds, segs, offset, offset_dev, training)
         plan.bind(x.device, keep_bits=bits[j])
         R = plan.rank_total
         acc = dacc[pos:pos + sizes[j]]
@@ -600,26 +627,25 @@ def lora_group_bwd(dys: list[torch.Tensor], x: torch.Tensor, ws: list[torch.Tens
     # ④ for all projections in one launch: each X tile leaves DRAM once
     J = len(ws)
     probs = (ctypes.POINTER(_lib.LfProblem) * J)(*[ctypes.pointer(pl.problem) for pl in plans])
-    ds_ptrs = (ctypes.c_void_p * J)(*[d_.data_ptr() for d_ in dss])
-    da_ptrs = (ctypes.c_void_p * J)(*[a_.data_ptr() for a_ in daccs])
-    _call("grad_down", lib.lf_grad_down_group, probs, J, _ptr(x), ds_ptrs, da_ptrs, st)
+    arr = lambda ts: (ctypes.c_void_p * J)(*[t_.data_ptr() for t_ in ts])  # noqa: E731
+    _call("grad_down", lib.lf_grad_down_group, probs, J, _ptr(x), arr(dss), arr(daccs), st)
     if need_dx:  # ⑤: one GEMM over the concatenated reduction dims (dX written once), or per
         # projection where the group has no one-launch variant (the first writes dX, the others
         # add into it in their epilogues)
-        arr = lambda ts: (ctypes.c_void_p * J)(*[t_.data_ptr() for t_ in ts])  # noqa: E731
         _call("grad_input", lib.lf_grad_input_group, probs, J, arr(dys), arr(ws), arr(dss), arr(acs), _ptr(dx), st)
     return dx, dacc
 
 
 @lora_group_bwd.register_fake
-def _lora_group_bwd_fake(dys, x, ws, acs, bcs, shats, bits, ranks, scalings, ps, seeds, offset, offset_dev, training,
-                         cache_id, need_dx):
+def _lora_group_bwd_fake(dys, x, ws, acs, bcs, shats, bits, nads, ranks, scalings, ps, seeds, segs, offset,
+                         offset_dev, training, cache_id, need_dx):
     m, k = x.shape
+    _, _, lays = _group_layout(m, nads, ranks, segs)
     dx = x.new_empty((m, k) if need_dx else (0,))
-    return dx, x.new_empty((sum(_padr(r) * (k + w.shape[0]) for r, w in zip(ranks, ws)),), dtype=torch.float32)
+    return dx, x.new_empty((sum(R * (k + w.shape[0]) for (_, R), w in zip(lays, ws)),), dtype=torch.float32)
 
 
-_GROUP_ARGS = ("ranks", "scalings", "ps", "seeds", "offset", "offset_dev", "training", "cache_id")
+_GROUP_ARGS = ("nads", "ranks", "scalings", "ps", "seeds", "segs", "offset", "offset_dev", "training", "cache_id")
 
 
 def _group_setup_context(ctx, inputs, output):
@@ -628,18 +654,22 @@ def _group_setup_context(ctx, inputs, output):
     ctx.mark_non_differentiable(*shats, *bits, *acs, *bcs)
     ctx.set_materialize_grads(False)
     args = dict(zip(_GROUP_ARGS, rest))
+    # non-tensor arguments get None, except an empty list (no segment table), which
+    # flattens like a list of tensors and must come back as []
+    ctx.none_grads = tuple([] if isinstance(v, list) and not v else None for v in rest)
     offset_dev = args.pop("offset_dev")
     ctx.has_off = offset_dev is not None
     ctx.J = len(ws)
+    ctx.NA = len(a)
     ctx.param_dtypes = [p.dtype for p in a] + [p.dtype for p in b]
     ctx.args = args
     ctx.save_for_backward(x, *ws, *acs, *bcs, *shats, *bits, *([offset_dev] if ctx.has_off else []))
 
 
 def _group_backward(ctx, gys, _gs=None, _gbits=None, _ga=None, _gb=None):
-    J = ctx.J
+    J, NA = ctx.J, ctx.NA
     x, *rest = ctx.saved_tensors
-    ws, a, b = rest[:J], rest[J:2 * J], rest[2 * J:3 * J]
+    ws, acs, bcs = rest[:J], rest[J:2 * J], rest[2 * J:3 * J]
     shats, bits = rest[3 * J:4 * J], rest[4 * J:5 * J]
     offset_dev = rest[5 * J] if ctx.has_off else None
     A = ctx.args
@@ -647,18 +677,31 @@ def _group_backward(ctx, gys, _gs=None, _gbits=None, _ga=None, _gb=None):
     dys = [(g if g is not None else torch.zeros((x.shape[0], w.shape[0]), dtype=_BF16, device=x.device))
            .to(_BF16).contiguous() for g, w in zip(gys, ws)]
     dx, dacc = torch.ops.lorafusion_b200.lora_group_bwd(
-        dys, x, list(ws), list(a), list(b), list(shats), list(bits), A["ranks"], A["scalings"], A["ps"], A["seeds"],
-        A["offset"], offset_dev, A["training"], A["cache_id"], need_dx)
-    k = x.shape[1]
-    ga, gb = [], []
-    pos = 0
-    for j, (r, w) in enumerate(zip(A["ranks"], ws)):
-        R = _padr(r)
-        acc = dacc[pos:pos + R * (k + w.shape[0])]
-        pos += R * (k + w.shape[0])
-        ga.append(acc[:R * k].view(R, k)[:r].to(ctx.param_dtypes[j]))
-        gb.append(acc[R * k:].view(w.shape[0], R)[:, :r].to(ctx.param_dtypes[J + j]))
-    return (dx if need_dx else None, [None] * J, ga, gb) + (None,) * len(_GROUP_ARGS)
+        dys, x, list(ws), list(acs), list(bcs), list(shats), list(bits), A["nads"], A["ranks"], A["scalings"],
+        A["ps"], A["seeds"], A["segs"], A["offset"], offset_dev, A["training"], A["cache_id"], need_dx)
+    m, k = x.shape
+    _, segments, lays = _group_layout(m, A["nads"], A["ranks"], A["segs"])
+    # each projection's rank-concat gradients back to its adapters' parameters (a block per
+    # adapter present in the segment table; absent adapters get no gradient)
+    ga: list = [None] * NA
+    gb: list = [None] * NA
+    pos, base = 0, 0
+    for j, ((cs, R), w, (r_j,)) in enumerate(zip(lays, ws, _group_split(A["nads"], A["ranks"]))):
+        n = w.shape[0]
+        acc = dacc[pos:pos + R * (k + n)]
+        pos += R * (k + n)
+        da, db = acc[:R * k].view(R, k), acc[R * k:].view(n, R)
+        seen = set()
+        for s_, c0 in zip(segments, cs):
+            if s_.adapter in seen:
+                continue
+            seen.add(s_.adapter)
+            i = base + s_.adapter
+            r = r_j[s_.adapter]
+            ga[i] = da[c0:c0 + r].to(ctx.param_dtypes[i])
+            gb[i] = db[:, c0:c0 + r].to(ctx.param_dtypes[NA + i])
+        base += len(r_j)
+    return (dx if need_dx else None, [None] * J, ga, gb) + ctx.none_grads
 
 
 torch.library.register_autograd(f"{_NS}::lora_group_fwd", _group_backward, setup_context=_group_setup_context)
@@ -670,22 +713,61 @@ def fused_lora_group(x: torch.Tensor, weights: Sequence[torch.Tensor], lora_a: S
                      operand_cache: OperandCache | None = None) -> list[torch.Tensor]:
     """Several LoRA linears that read the same input (q/k/v, gate/up): Y_j = X·W_jᵀ +
     s_j·dropout_j(X)·A_jᵀ·B_jᵀ, each with its own adapter, seed and mask (one Philox offset
-    for the call). Same results as separate fused_lora calls, but the input gradient
-    Σ_j dX_j is summed inside the ⑤ GEMM epilogues (SURVEY §8(f)#4)."""
+    for the call). Same results as separate fused_lora calls up to bf16 rounding; ②, ④ and
+    ⑤ run as one launch each for the group where its shape allows (SURVEY §8(f)#4)."""
     if not weights or len(weights) != len(lora_a) or len(weights) != len(lora_b) or len(weights) != len(adapters):
         raise ValidationError("fused_lora_group needs one weight, lora_a, lora_b and adapter per projection")
+    return fused_multi_lora_group(x, weights, [[a_] for a_ in lora_a], [[b_] for b_ in lora_b],
+                                  [[ad] for ad in adapters], None, offset, training, offset_dev, operand_cache)
+
+
+def fused_multi_lora_group(x: torch.Tensor, weights: Sequence[torch.Tensor],
+                           lora_a: Sequence[Sequence[torch.Tensor]], lora_b: Sequence[Sequence[torch.Tensor]],
+                           adapters: Sequence[Sequence[AdapterConfig]], segments: Sequence[Segment] | None = None,
+                           offset: int = 0, training: bool = True, offset_dev: torch.Tensor | None = None,
+                           operand_cache: OperandCache | None = None) -> list[torch.Tensor]:
+    """FusedMultiLoRA for projections that read the same input: projection j has its own
+    adapter slots (lora_a[j][i], lora_b[j][i], adapters[j][i]: rank, scale, dropout, seed) and
+    all share one microbatch segment table (None: every row to slot 0). Y_j equals
+    fused_multi_lora(x, weights[j], lora_a[j], lora_b[j], adapters[j], segments) up to bf16
+    rounding. A microbatch beyond one launch's limits (> 32 segments, rank-concat > 128) runs
+    projection by projection through fused_multi_lora."""
+    J = len(weights)
+    if not J or len(lora_a) != J or len(lora_b) != J or len(adapters) != J:
+        raise ValidationError("fused_multi_lora_group needs weights, lora_a, lora_b and adapters per projection")
+    if J > _lib.LF_MAX_GROUP:
+        raise ValidationError(f"at most {_lib.LF_MAX_GROUP} projections per group, got {J}")
     k = weights[0].shape[1]
     x2, lead = _flatten_input(x, k)
-    packed = pack_adapters(adapters)
+    m = x2.shape[0]
+    segs_list = list(segments) if segments is not None else None
+    nads, flat_a, flat_b, flat_ad = [], [], [], []
     for j, w in enumerate(weights):
         if w.shape[1] != k:
             raise ValidationError(f"weights[{j}] has in_features {w.shape[1]}, expected {k} (one shared input)")
-        _check_call(x2, w, [lora_a[j]], [lora_b[j]], [packed[0][j]], k, w.shape[0], None, offset_dev)
-    if x2.shape[0] == 0:
-        return [_EmptyBatchFn.apply(x2, w.shape[0], a_, b_).reshape(lead + (w.shape[0],))
-                for w, a_, b_ in zip(weights, lora_a, lora_b)]
+        if len(lora_a[j]) != len(adapters[j]) or len(lora_b[j]) != len(adapters[j]) or not adapters[j]:
+            raise ValidationError(f"projection {j}: one lora_a, lora_b and adapter per slot (at least one)")
+        if segs_list is not None:
+            validate_segments(segs_list, m, len(adapters[j]), max_segments=None)
+        packed_j = pack_adapters(adapters[j])
+        _check_call(x2, w, lora_a[j], lora_b[j], packed_j[0], k, w.shape[0], None, offset_dev)
+        nads.append(len(adapters[j]))
+        flat_a += list(lora_a[j])
+        flat_b += list(lora_b[j])
+        flat_ad += list(adapters[j])
+    if m == 0 or segs_list == []:  # no rows, or no LoRA rows: the per-projection path
+        return [fused_multi_lora(x, w, lora_a[j], lora_b[j], adapters[j], segs_list or [], offset, None, training,
+                                 offset_dev=offset_dev) for j, w in enumerate(weights)]
+    if segs_list is not None:
+        fits = all(len(split_segments(adapters[j], segs_list, m)) == 1 for j in range(J))
+        if not fits:  # beyond one launch: the per-projection path splits the microbatch
+            return [fused_multi_lora(x, w, lora_a[j], lora_b[j], adapters[j], segs_list, offset, None, training,
+                                     offset_dev=offset_dev, operand_cache=operand_cache)
+                    for j, w in enumerate(weights)]
+    packed = pack_adapters(flat_ad)
+    segs = pack_segments(segs_list) if segs_list else []
     ys = torch.ops.lorafusion_b200.lora_group_fwd(
-        x2, list(weights), list(lora_a), list(lora_b), *packed, int(offset), offset_dev, bool(training),
+        x2, list(weights), flat_a, flat_b, nads, *packed, segs, int(offset), offset_dev, bool(training),
         _cache_handle(operand_cache))[0]
     return [y.reshape(lead + (y.shape[1],)) for y in ys]
 

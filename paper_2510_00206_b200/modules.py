@@ -32,6 +32,7 @@ from typing import Sequence
 import torch
 from torch import nn
 
+from . import _lib
 from .errors import ValidationError
 from .functional import (OperandCache, ShadowOperands, _apply, _cache_handle, _check_call, _EmptyBatchFn,
                          _flatten_input, fused_multi_lora, pack_adapters)
@@ -419,11 +420,106 @@ class FusedLoRAGroup(nn.Module):
         else:
             off, off_dev = _step_offsets(self, x2.device, self._has_dropout)
             ys = torch.ops.lorafusion_b200.lora_group_fwd(
-                x2, ws, a, b, *self._packed, off, off_dev, self.training, _cache_handle(self._operands))[0]
+                x2, ws, a, b, [1] * len(ws), *self._packed, [], off, off_dev, self.training,
+                _cache_handle(self._operands))[0]
         out = []
         for p, y in zip(projs, ys):
             y = y.reshape(lead + (p.out_features,))
             if p.base_bias is not None:
                 y = y + p.base_bias.to(y.dtype)
+            out.append(y)
+        return tuple(out)
+
+
+class FusedMultiLoRAGroup(nn.Module):
+    """FusedMultiLoRA layers that read the same input (q/k/v, gate/up) as one module: every
+    projection is a :class:`FusedMultiLoRA` child with its own adapter slots, seeds and
+    masks, and all share the microbatch segment table. ``forward(x, segments)`` returns the
+    projections' outputs in order; ②, ④ and ⑤ run as one launch each for the group where
+    its shape allows (fused_multi_lora_group)."""
+
+    def __init__(self, projections: "dict[str, nn.Linear | torch.Tensor]", adapters: Sequence[AdapterConfig], *,
+                 seeds: Sequence[Sequence[int]] | None = None, init: str = "peft", dtype: torch.dtype = torch.float32,
+                 generator: torch.Generator | None = None, capturable: bool = False, dropout_rng: str | None = None):
+        super().__init__()
+        names = list(projections)
+        layers = {}
+        for j, nm in enumerate(names):
+            ads = list(adapters)
+            if seeds is not None:
+                ads = [AdapterConfig(a.rank, a.scaling, a.dropout_p, seed=sd) for a, sd in zip(ads, seeds[j])]
+            layers[nm] = FusedMultiLoRA(projections[nm], ads, init=init, dtype=dtype, generator=generator,
+                                        capturable=capturable, dropout_rng=dropout_rng)
+        self._adopt(layers, capturable, dropout_rng)
+
+    @classmethod
+    def from_layers(cls, layers: "dict[str, FusedMultiLoRA]", capturable: bool | None = None,
+                    dropout_rng: str | None = None) -> "FusedMultiLoRAGroup":
+        """Group existing FusedMultiLoRA layers that read the same input (parameters shared)."""
+        if not layers:
+            raise ValidationError("FusedMultiLoRAGroup needs at least one projection")
+        first = next(iter(layers.values()))
+        obj = cls.__new__(cls)
+        nn.Module.__init__(obj)
+        obj._adopt(dict(layers), first.capturable if capturable is None else capturable,
+                   first.dropout_rng if dropout_rng is None else dropout_rng)
+        return obj
+
+    def _adopt(self, layers: "dict[str, FusedMultiLoRA]", capturable: bool, dropout_rng: str) -> None:
+        names = list(layers)
+        if not names:
+            raise ValidationError("FusedMultiLoRAGroup needs at least one projection")
+        if len(names) > _lib.LF_MAX_GROUP:
+            raise ValidationError(f"at most {_lib.LF_MAX_GROUP} projections per group, got {len(names)}")
+        self.names = names
+        for nm in names:
+            if not nm.isidentifier():
+                raise ValidationError(f"projection name {nm!r} must be a Python identifier")
+            if not isinstance(layers[nm], FusedMultiLoRA):
+                raise ValidationError(f"projection {nm!r} must be a FusedMultiLoRA layer")
+            self.add_module(nm, layers[nm])
+        ks = {self.proj(nm).in_features for nm in names}
+        if len(ks) != 1:
+            raise ValidationError(f"all projections of a group read the same input: in_features {sorted(ks)}")
+        nslots = {len(self.proj(nm).adapters) for nm in names}
+        if len(nslots) != 1:
+            raise ValidationError("all projections of a group need the same adapter slots (one segment table)")
+        self.in_features = ks.pop()
+        _init_capturable(self, capturable, self.proj(names[0]).base_weight.device, dropout_rng)
+        self._offset = 0
+        self._operands = ShadowOperands() if capturable else OperandCache(capacity=2 * len(names))
+        self._has_dropout = any(a.dropout_p > 0 for nm in names for a in self.proj(nm).adapters)
+
+    def proj(self, name: str) -> "FusedMultiLoRA":
+        return self._modules[name]
+
+    def next_offset(self) -> int:
+        off = self._offset
+        self._offset += 1
+        return off
+
+    def dropout_state(self) -> dict:
+        return _dropout_state(self)
+
+    def load_dropout_state(self, state: dict) -> None:
+        _load_dropout_state(self, state)
+
+    def invalidate_operands(self) -> None:
+        self._operands.clear()
+
+    def forward(self, x: torch.Tensor, segments: Sequence[Segment]) -> tuple[torch.Tensor, ...]:
+        from .functional import fused_multi_lora_group
+
+        projs = [self._modules[nm] for nm in self.names]
+        has_dropout = any(p.adapters[s_.adapter].dropout_p > 0 for p in projs for s_ in segments)
+        off, off_dev = _step_offsets(self, projs[0].base_weight.device, has_dropout)
+        ys = fused_multi_lora_group(
+            x, [p.base_weight for p in projs], [[la.weight for la in p.lora_A] for p in projs],
+            [[lb.weight for lb in p.lora_B] for p in projs], [p.adapters for p in projs], segments, offset=off,
+            training=self.training, offset_dev=off_dev, operand_cache=self._operands)
+        out = []
+        for p, y in zip(projs, ys):
+            if p.base is not None and p.base.bias is not None:
+                y = y + p.base.bias.to(y.dtype)
             out.append(y)
         return tuple(out)

@@ -295,3 +295,48 @@ def _group_vs_fp32(m, k, ns, p=0.1):
         del xm, keep
     errs["dx"] = rel(x.grad, dx_ref)
     assert all(v < 4e-3 for v in errs.values()), errs
+
+
+@pytest.mark.parametrize("ranks,ps", [((8, 16, 32, 64), (0.0, 0.05, 0.1, 0.1)), ((8, 16), (0.1, 0.0))],
+                         ids=["c3_like", "rsum_small"])
+def test_multi_lora_group_matches_separate_layers(ranks, ps):
+    """FusedMultiLoRAGroup (q/k/v sharing X, 4 or 2 adapter slots each, one segment table) =
+    three FusedMultiLoRA layers at the same Philox offset: identical Y (the group GEMM's LoRA
+    K-range covers each projection's whole rank-concat width — zero off-segment columns add
+    exact zeros), dA/dB up to reduction order, dX up to bf16 rounding. rsum_small: the
+    accumulators of all three fit one ④ launch; c3_like (R = 128 each): ④ per projection."""
+    from paper_2510_00206_b200 import FusedMultiLoRAGroup, segments_from_lengths
+
+    g = torch.Generator(device=DEV).manual_seed(13)
+    k = 512
+    bases = {nm: (torch.randn(n, k, device=DEV, generator=g) / k**0.5).to(torch.bfloat16)
+             for nm, n in (("q_proj", 512), ("k_proj", 256), ("v_proj", 256))}
+    ads = [AdapterConfig(r, 2.0 / (i + 1), p_, seed=50 + i) for i, (r, p_) in enumerate(zip(ranks, ps))]
+    seeds = [[100 * j + i for i in range(len(ads))] for j in range(3)]
+    grp = FusedMultiLoRAGroup(bases, ads, seeds=seeds, init="gaussian", generator=g, dropout_rng="counter")
+    lens = [200, 184, 128, 128][:len(ads)]
+    segs = segments_from_lengths(list(range(len(ads))), lens)
+    m = sum(lens)
+    x0 = torch.randn(m, k, device=DEV, generator=g).to(torch.bfloat16)
+    dys = [torch.randn(m, b_.shape[0], device=DEV, generator=g).to(torch.bfloat16) for b_ in bases.values()]
+    grp._offset = 3
+    x = x0.clone().requires_grad_(True)
+    ys = grp(x, segs)
+    torch.autograd.backward(ys, dys)
+    dx_group = x.grad.clone()
+    got = [(y.detach(), [la.weight.grad.clone() for la in grp.proj(nm).lora_A],
+            [lb.weight.grad.clone() for lb in grp.proj(nm).lora_B]) for y, nm in zip(ys, grp.names)]
+    xs = x0.clone().requires_grad_(True)
+    for j, nm in enumerate(grp.names):
+        layer = grp.proj(nm)
+        for p_ in layer.parameters():
+            p_.grad = None
+        layer.dropout_rng = "counter"
+        layer._offset = 3
+        y = layer(xs, segs)
+        y.backward(dys[j])
+        assert torch.equal(y, got[j][0])
+        for ga, gl in zip(got[j][1] + got[j][2], [la.weight.grad for la in layer.lora_A] +
+                          [lb.weight.grad for lb in layer.lora_B]):
+            assert _rel(gl, ga) < 1e-4
+    assert _rel(dx_group, xs.grad) < 4e-3
