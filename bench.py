@@ -415,7 +415,7 @@ _UNITS: dict = {}
 
 def step_units(config: str, layers: dict):
     """How one step calls the layers: [(group input, [names], module or FusedLoRAGroup)]."""
-    from paper_2510_00206_b200 import FusedLoRAGroup
+    from paper_2510_00206_b200 import FusedLoRAGroup, FusedMultiLoRAGroup
 
     cache = _UNITS
     key = (id(layers), config, GROUPED)
@@ -424,8 +424,9 @@ def step_units(config: str, layers: dict):
         for name, k, n, grp in projections(config):
             by_grp.setdefault(grp, []).append(name)
         for grp, names in by_grp.items():
-            if GROUPED and config != "c3" and grp in SHARED_INPUT_GROUPS and len(names) > 1:
-                units.append((grp, names, FusedLoRAGroup.from_layers({nm: layers[nm] for nm in names})))
+            if GROUPED and grp in SHARED_INPUT_GROUPS and len(names) > 1:
+                kind = FusedMultiLoRAGroup if config == "c3" else FusedLoRAGroup
+                units.append((grp, names, kind.from_layers({nm: layers[nm] for nm in names})))
             else:
                 units.extend((grp, [nm], layers[nm]) for nm in names)
         cache[key] = units
@@ -439,7 +440,7 @@ def fused_step(config, layers, inputs, grads, world, flat_grad=None):
     call = layer_call(config)
     for grp, names, mod in step_units(config, layers):
         if len(names) > 1:
-            ys = mod(inputs[grp])
+            ys = call(mod, inputs[grp])
             torch.autograd.backward(ys, [grads[nm] for nm in names])
         else:
             y = call(mod, inputs[grp])

@@ -702,7 +702,10 @@ int lf_grad_input_group(const LfProblem* const* probs, int32_t nproj, const uint
       return fail(LF_E_INVALID, "lf_grad_input_group: projections must share the input (m, k)");
     LF_TRY(check_ptr(dy[j], "dy"));
     LF_TRY(check_ptr(w[j], "w"));
-    if (!group_ok(p)) fused = false;
+    // the J masked LoRA partials take turns in the accumulator over each projection's whole
+    // rank-concat width: wide multi-adapter widths (C3: R = 128, routing hulls of 64) make the
+    // turns longer than the per-projection launches' hull-sized partials (C3 ⑤ 2.33 -> 2.40 ms)
+    if (!group_ok(p) || p->rank_total > 32) fused = false;
     const bool m_j = t[j].mask_mode != 0;  // some segment drops (Philox) or an explicit mask
     if (m_j && !(t[j].mask_mode == 1 && t[j].bits)) fused = false;  // packed bits from ① only
     masked = masked || m_j;

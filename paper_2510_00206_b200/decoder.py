@@ -18,6 +18,7 @@ torch projections (:func:`.baseline.unfused_multi_lora`) — the end-to-end base
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -28,7 +29,7 @@ from torch import nn
 from .baseline import unfused_multi_lora
 from .errors import ValidationError
 from .functional import refresh_stale_operand_shadows
-from .modules import FusedMultiLoRA
+from .modules import FusedMultiLoRA, FusedMultiLoRAGroup
 from .plan import AdapterConfig, Segment
 
 PROJECTIONS = ("q", "k", "v", "o", "gate", "up", "down")
@@ -199,14 +200,27 @@ class DecoderLayer(nn.Module):
                 self.proj[name] = FusedMultiLoRA(w, ads, init="gaussian", generator=generator, capturable=capturable)
             else:
                 self.proj[name] = TorchMultiLoRA(w, ads, generator=generator)
+        # projections that read the same input run as shared-input groups (②/④/⑤ one launch
+        # each); kept outside the module registry so parameter names and state dicts stay the
+        # per-projection ones
+        self._groups = None
+        if fused and os.environ.get("LF_DECODER_GROUPS", "1") != "0":  # =0: per-projection calls (A/B)
+            self._groups = (FusedMultiLoRAGroup.from_layers({nm: self.proj[nm] for nm in ("q", "k", "v")}),
+                            FusedMultiLoRAGroup.from_layers({nm: self.proj[nm] for nm in ("gate", "up")}))
 
     def forward(self, h, mb: PackedMicrobatch, rope: Rotary):
         s = self.shape
         m, segs = h.shape[0], mb.segments
         x = self.ln1(h)
-        q = self.proj["q"](x, segs).view(m, s.heads, s.head_dim)
-        k = self.proj["k"](x, segs).view(m, s.kv_heads, s.head_dim)
-        v = self.proj["v"](x, segs).view(m, s.kv_heads, s.head_dim)
+        if self._groups is not None:
+            for grp in self._groups:  # not registered submodules: follow train() / eval() here
+                grp.training = self.training
+            q, k, v = self._groups[0](x, segs)
+        else:
+            q, k, v = (self.proj[nm](x, segs) for nm in ("q", "k", "v"))
+        q = q.view(m, s.heads, s.head_dim)
+        k = k.view(m, s.kv_heads, s.head_dim)
+        v = v.view(m, s.kv_heads, s.head_dim)
         cos, sin = rope.tables(mb.positions)
         q, k = apply_rope(q, k, cos, sin)
         if self.attention == "flash":
@@ -218,8 +232,10 @@ class DecoderLayer(nn.Module):
             o = varlen_attention_sdpa(q, k, v, mb.cu_seqlens)
         h = h + self.proj["o"](o.reshape(m, s.hidden), segs)
         x = self.ln2(h)
-        g = self.proj["gate"](x, segs)
-        u = self.proj["up"](x, segs)
+        if self._groups is not None:
+            g, u = self._groups[1](x, segs)
+        else:
+            g, u = self.proj["gate"](x, segs), self.proj["up"](x, segs)
         return h + self.proj["down"](F.silu(g) * u, segs)
 
 

@@ -56,7 +56,7 @@ def main():
     # width tiles; its ⑤ one launch over the concatenated reduction dims while that stays
     # <= 12288 (lf_gemm.cu gemm_launch_group), else one launch per projection
     for grp, names in by_grp.items():
-        if grouped and config != "c3" and grp in bench.SHARED_INPUT_GROUPS and len(names) > 1:
+        if grouped and grp in bench.SHARED_INPUT_GROUPS and len(names) > 1:
             ns = [shapes[nm][1] for nm in names]
             fwd_one = all(n_ % 256 == 0 for n_ in ns)
             bwd_one = sum(ns) <= 12288 and all(n_ % 64 == 0 for n_ in ns)
