@@ -122,6 +122,14 @@ LF_API int lf_base_fwd(const LfProblem* p, const uint16_t* x, const uint16_t* w,
 LF_API int lf_grad_up(const LfProblem* p, const uint16_t* dy, const uint16_t* b_cat, const uint16_t* s_hat, uint16_t* ds,
                float* db_accum, void* stream);
 
+/* ③ for projections that read the same input (q/k/v, gate/up): lf_grad_up for j < nproj
+ * (<= 3) as one launch plus one dŜ finalize launch (the per-launch fixed cost paid once).
+ * Each problem needs its own workspace (one launch holds all their split-K partials); falls
+ * back to per-projection lf_grad_up when workspaces are shared. ABI 5. */
+LF_API int lf_grad_up_group(const LfProblem* const* probs, int32_t nproj, const uint16_t* const* dy,
+                            const uint16_t* const* b_cat, const uint16_t* const* s_hat, uint16_t* const* ds,
+                            float* const* db_accum, void* stream);
+
 /* ④ da_accum (R x k, fp32) += dŜᵀ·(M⊙X). */
 LF_API int lf_grad_down(const LfProblem* p, const uint16_t* x, const uint16_t* ds, float* da_accum, void* stream);
 

@@ -41,6 +41,7 @@ EXPORTED_SYMBOLS = (
     "lf_grad_up",
     "lf_grad_down",
     "lf_grad_down_group",
+    "lf_grad_up_group",
     "lf_grad_input",
     "lf_grad_input_accum",
     "lf_base_fwd_group",
@@ -96,6 +97,8 @@ _SIGNATURES = {
     "lf_grad_down": (ctypes.c_int, [_P, _V, _V, _V, _V]),
     "lf_grad_down_group": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int32, _V, ctypes.POINTER(_V),
                                           ctypes.POINTER(_V), _V]),
+    "lf_grad_up_group": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int32, ctypes.POINTER(_V), ctypes.POINTER(_V),
+                                        ctypes.POINTER(_V), ctypes.POINTER(_V), ctypes.POINTER(_V), _V]),
     "lf_grad_input": (ctypes.c_int, [_P, _V, _V, _V, _V, _V, _V]),
     "lf_grad_input_accum": (ctypes.c_int, [_P, _V, _V, _V, _V, _V, _V]),
     "lf_base_fwd_group": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int32, _V, ctypes.POINTER(_V),

@@ -502,6 +502,71 @@ int lf_grad_down(const LfProblem* p, const uint16_t* x, const uint16_t* ds, floa
   return LF_OK;
 }
 
+// ③ over a shared-input group: one ③ launch and one dŜ finalize launch for the J projections
+// (each its own grid, sized by its share of the dY bytes, and its own split-K workspace —
+// the problems must not share one); otherwise (J = 1, LF_GROUP_UP=0) per projection.
+int lf_grad_up_group(const LfProblem* const* probs, int32_t nproj, const uint16_t* const* dy,
+                     const uint16_t* const* b_cat, const uint16_t* const* s_hat, uint16_t* const* ds,
+                     float* const* db_accum, void* stream) {
+  if (!probs || nproj < 1 || nproj > lf::kMaxGroup || !dy || !b_cat || !s_hat || !ds || !db_accum)
+    return fail(LF_E_INVALID, "lf_grad_up_group: 1..%d projections with dy / b_cat / s_hat / ds / db arrays",
+                lf::kMaxGroup);
+  static const int group_env = env_int("LF_GROUP_UP", 1);
+  bool fused = nproj > 1 && group_env;
+  lf::LfSegTable t[lf::kMaxGroup];
+  double bytes[lf::kMaxGroup], total = 0;
+  for (int j = 0; j < nproj; ++j) {
+    const LfProblem* p = probs[j];
+    if (!p) return fail(LF_E_INVALID, "lf_grad_up_group: projection %d has no problem", j);
+    LF_TRY(validate(p, true, &t[j]));
+    if (p->num_segments == 0) return fail(LF_E_INVALID, "lf_grad_up_group needs at least one segment");
+    LF_TRY(check_ptr(dy[j], "dy"));
+    LF_TRY(check_ptr(b_cat[j], "b_cat"));
+    LF_TRY(check_ptr(s_hat[j], "s_hat"));
+    LF_TRY(check_ptr(ds[j], "ds"));
+    LF_TRY(check_ptr(db_accum[j], "db_accum"));
+    LF_TRY(check_workspace(p));
+    for (int i = 0; i < j; ++i)
+      if (probs[i]->workspace == p->workspace) fused = false;  // one launch needs disjoint workspaces
+    bytes[j] = (double)p->m * p->n;
+    total += bytes[j];
+  }
+  if (!fused) {
+    for (int j = 0; j < nproj; ++j) LF_TRY(lf_grad_up(probs[j], dy[j], b_cat[j], s_hat[j], ds[j], db_accum[j], stream));
+    return LF_OK;
+  }
+  Dev d;
+  LF_TRY(current_device(&d));
+  lf::GroupUpMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  lf::GroupUpArgs g;
+  memset(&g, 0, sizeof(g));
+  g.J = nproj;
+  for (int j = 0; j < nproj; ++j) {
+    const LfProblem* p = probs[j];
+    if (!make_map(&maps.dy[j], dy[j], p->m, p->n, p->n, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_map(&maps.b[j], b_cat[j], p->n, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B) ||
+        !make_map(&maps.s[j], s_hat[j], p->m, p->rank_total, p->rank_total, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B))
+      return fail(LF_E_CUDA, "cuTensorMapEncodeTiled failed (dy / b_cat / s_hat)");
+    lf::GradUpArgs& a = g.p[j];
+    a.m = p->m;
+    a.n = p->n;
+    a.rtot = p->rank_total;
+    a.ds = ds[j];
+    a.db = db_accum[j];
+    split_workspace(p, &a.ws, &a.counters);
+    a.routes = reinterpret_cast<const lf::LfRoute*>(p->routes);
+    a.segs = t[j];
+    // this projection's share of the SMs, by its dY bytes (one resident wave for the group)
+    int sms_j = (int)(d.sms * bytes[j] / total);
+    if (sms_j < 1) sms_j = 1;
+    lf::grad_up_grid(p->m, p->n, p->rank_total, t[j].wmax, sms_j, 1, &a.n_split, &a.m_split, &a.nacc);
+    if (a.n_split <= 0) return fail(LF_E_INVALID, "rank_total=%d too large for grad_up TMEM budget", p->rank_total);
+  }
+  if (lf::grad_up_group_launch(maps, g, (cudaStream_t)stream)) return cuda_fail("grad_up_group launch");
+  return LF_OK;
+}
+
 // ④ over a shared-input group: one launch when every projection's keep bits (if any) ①'s
 // launch left 16-byte pitched and the J accumulators fit TMEM; otherwise (and for J = 1) the
 // per-projection lf_grad_down. Any segment table: dŜ_j is zero off each row's segment.

@@ -13,6 +13,8 @@
 // epilogue kernel (lf_finalize_kernel, lf_lowrank.cu) then scales, masks off-segment
 // columns, converts to bf16 and re-zeroes the workspace.
 #include "lf_device.cuh"
+#include <cstring>
+
 #include "lf_kernels.h"
 
 namespace lf {
@@ -22,10 +24,9 @@ constexpr int DY_BYTES = 2 * 128 * 64 * 2;  // 32 KB: two 64-column SW128 boxes 
 constexpr int MAX_SMEM = 200 * 1024;
 }  // namespace gup
 
-__global__ void __launch_bounds__(192, 2)
-    lf_gradup_kernel(const __grid_constant__ CUtensorMap tmDy, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmS, const __grid_constant__ GradUpArgs args, int stages,
-                     int stage_bytes) {
+// one CTA's share of ③: n-subtiles [bx·tiles_n/n_split, ...) x m-tiles [by·tiles_m/m_split, ...)
+__device__ __forceinline__ void gradup_cta(const CUtensorMap& tmDy, const CUtensorMap& tmB, const CUtensorMap& tmS,
+                                           const GradUpArgs& args, int stages, int stage_bytes, int bx, int by) {
   using namespace gup;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
@@ -45,10 +46,10 @@ __global__ void __launch_bounds__(192, 2)
   const uint32_t warp = warp_id(), lane = lane_id();
   const int tiles_m = (args.m + 127) / 128;
   const int tiles_n = (args.n + 127) / 128;
-  const int nt0 = (int)((int64_t)blockIdx.x * tiles_n / args.n_split);
-  const int nt1 = (int)((int64_t)(blockIdx.x + 1) * tiles_n / args.n_split);
-  const int mt0 = (int)((int64_t)blockIdx.y * tiles_m / args.m_split);
-  const int mt1 = (int)((int64_t)(blockIdx.y + 1) * tiles_m / args.m_split);
+  const int nt0 = (int)((int64_t)bx * tiles_n / args.n_split);
+  const int nt1 = (int)((int64_t)(bx + 1) * tiles_n / args.n_split);
+  const int mt0 = (int)((int64_t)by * tiles_m / args.m_split);
+  const int mt1 = (int)((int64_t)(by + 1) * tiles_m / args.m_split);
   const int nsub = nt1 - nt0;
   // NA independent accumulators per chain (consecutive K-steps rotate through them): small-N
   // MMAs into a single accumulator serialise on its latency
@@ -258,6 +259,24 @@ __global__ void __launch_bounds__(192, 2)
   }
 }
 
+__global__ void __launch_bounds__(192, 2)
+    lf_gradup_kernel(const __grid_constant__ CUtensorMap tmDy, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmS, const __grid_constant__ GradUpArgs args, int stages,
+                     int stage_bytes) {
+  gradup_cta(tmDy, tmB, tmS, args, stages, stage_bytes, (int)blockIdx.x, (int)blockIdx.y);
+}
+
+// ③ for a shared-input group in one launch: CTAs [cta_end[j-1], cta_end[j]) run projection j's
+// grid (n_split_j x m_split_j, its own stage ring); one launch pays the fixed costs once
+__global__ void __launch_bounds__(192, 2)
+    lf_gradup_group_kernel(const __grid_constant__ GroupUpMaps maps, const __grid_constant__ GroupUpArgs g) {
+  int j = 0;
+  while (j + 1 < g.J && (int)blockIdx.x >= g.cta_end[j]) ++j;
+  const int local = (int)blockIdx.x - (j ? g.cta_end[j - 1] : 0);
+  const GradUpArgs& a = g.p[j];
+  gradup_cta(maps.dy[j], maps.b[j], maps.s[j], a, g.stages[j], g.stage_bytes[j], local % a.n_split, local / a.n_split);
+}
+
 // CTA grid: n_split x m_split blocks of (n-subtiles x m-tiles). The dB accumulators of a
 // CTA's n-range must fit TMEM next to the two dŜ buffers: (2 + nsub) * R <= 512.
 // Among admissible splits pick the smallest critical path (waves x max units of one 32 KB
@@ -299,15 +318,51 @@ void grad_up_grid(int m, int n, int rtot, int wmax, int sms, int per_sm, int* n_
   }
 }
 
-int grad_up_launch(const CUtensorMap& tm_dy, const CUtensorMap& tm_b, const CUtensorMap& tm_s,
-                   const GradUpArgs& args, int num_sms, int per_sm, cudaStream_t stream) {
-  (void)num_sms;
+// stage ring of one ③ problem: (stages, stage_bytes, dynamic smem bytes), or -1
+static int gradup_ring(const GradUpArgs& args, int per_sm, int* stages_out, int* stage_bytes_out) {
   const int sh_bytes = (args.segs.wmax / 16) * 4096;
   const int stage_bytes = gup::DY_BYTES + sh_bytes;
   int stages = (gup::MAX_SMEM / per_sm - 2 * sh_bytes) / stage_bytes;
   if (stages > 6) stages = 6;  // deep ring: ~180 KB of dY in flight per SM
   if (stages < 2) return -1;
-  const int smem = stages * stage_bytes + 2 * sh_bytes + 1024 + 1024;
+  *stages_out = stages;
+  *stage_bytes_out = stage_bytes;
+  return stages * stage_bytes + 2 * sh_bytes + 1024 + 1024;
+}
+
+int grad_up_group_launch(const GroupUpMaps& maps, GroupUpArgs& g, cudaStream_t stream) {
+  int smem = 0, ctas = 0;
+  for (int j = 0; j < g.J; ++j) {
+    const int sm_j = gradup_ring(g.p[j], 1, &g.stages[j], &g.stage_bytes[j]);
+    if (sm_j < 0 || g.p[j].n_split <= 0) return -1;
+    if (sm_j > smem) smem = sm_j;
+    ctas += g.p[j].n_split * g.p[j].m_split;
+    g.cta_end[j] = ctas;
+  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (ensure_smem_attr(lf_gradup_group_kernel, gup::MAX_SMEM + 2048, attr_done)) return -1;
+  if (launch_k(lf_gradup_group_kernel, dim3(ctas), dim3(192), smem, stream, maps, g)) return -1;
+  GroupFinArgs f;
+  memset(&f, 0, sizeof(f));
+  f.J = g.J;
+  int64_t chunks = 0;
+  for (int j = 0; j < g.J; ++j) {
+    chunks += (int64_t)g.p[j].segs.m * (g.p[j].segs.rtot / 8);
+    f.chunk_end[j] = chunks;
+    f.segs[j] = g.p[j].segs;
+    f.routes[j] = g.p[j].routes;
+    f.ws[j] = g.p[j].ws;
+    f.out[j] = reinterpret_cast<__nv_bfloat16*>(g.p[j].ds);
+  }
+  return launch_k(lf_finalize_group_kernel, dim3((unsigned)((chunks + 127) / 128)), dim3(128), 0, stream, f);
+}
+
+int grad_up_launch(const CUtensorMap& tm_dy, const CUtensorMap& tm_b, const CUtensorMap& tm_s,
+                   const GradUpArgs& args, int num_sms, int per_sm, cudaStream_t stream) {
+  (void)num_sms;
+  int stages = 0, stage_bytes = 0;
+  const int smem = gradup_ring(args, per_sm, &stages, &stage_bytes);
+  if (smem < 0) return -1;
   static std::atomic<uint64_t> attr_done{0};
   if (ensure_smem_attr(lf_gradup_kernel, gup::MAX_SMEM + 2048, attr_done)) return -1;
   dim3 grid(args.n_split, args.m_split);

@@ -3,6 +3,7 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 #include <atomic>
@@ -121,6 +122,27 @@ struct GradUpArgs {
   LfSegTable segs;
 };
 void grad_up_grid(int m, int n, int rtot, int wmax, int sms, int per_sm, int* n_split, int* m_split, int* nacc);
+// ③ for a shared-input group: one launch for the J projections (each its own grid, ring and
+// split-K workspace), then one dŜ finalize launch for all of them
+struct GroupUpMaps {
+  CUtensorMap dy[kMaxGroup], b[kMaxGroup], s[kMaxGroup];
+};
+struct GroupUpArgs {
+  int32_t J;
+  int32_t cta_end[kMaxGroup];     // cumulative CTA counts (set by grad_up_group_launch)
+  int32_t stages[kMaxGroup], stage_bytes[kMaxGroup];
+  GradUpArgs p[kMaxGroup];
+};
+struct GroupFinArgs {
+  int32_t J;
+  int64_t chunk_end[kMaxGroup];   // cumulative 8-column chunk counts
+  LfSegTable segs[kMaxGroup];
+  const LfRoute* routes[kMaxGroup];
+  float* ws[kMaxGroup];
+  __nv_bfloat16* out[kMaxGroup];
+};
+int grad_up_group_launch(const GroupUpMaps& maps, GroupUpArgs& args, cudaStream_t stream);
+__global__ void lf_finalize_group_kernel(const __grid_constant__ GroupFinArgs f);
 int grad_up_launch(const CUtensorMap& tm_dy, const CUtensorMap& tm_b, const CUtensorMap& tm_s,
                    const GradUpArgs& args, int num_sms, int per_sm, cudaStream_t stream);
 

@@ -319,6 +319,23 @@ __global__ void __launch_bounds__(128) lf_finalize_kernel(const __grid_constant_
   finalize_chunk(segs, routes[row / LF_TILE_M], row, c, ws, out);
 }
 
+// the dŜ finalize of several ③ problems (a shared-input group) in one launch
+__global__ void __launch_bounds__(128) lf_finalize_group_kernel(const __grid_constant__ GroupFinArgs f) {
+  pdl_wait();
+  pdl_launch_dependents();
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int j = 0;
+  while (j + 1 < f.J && idx >= f.chunk_end[j]) ++j;
+  if (idx >= f.chunk_end[j]) return;
+  idx -= j ? f.chunk_end[j - 1] : 0;
+  const LfSegTable& segs = f.segs[j];
+  if (segs.debug & 16) return;
+  const int chunks = segs.rtot / 8;
+  const int row = (int)(idx / chunks);
+  const int c = (int)(idx - (int64_t)row * chunks) * 8;
+  finalize_chunk(segs, f.routes[j][row / LF_TILE_M], row, c, f.ws[j], f.out[j]);
+}
+
 int finalize_launch(const LfSegTable& segs, const LfRoute* routes, float* ws, void* out, cudaStream_t stream) {
   const int64_t threads = (int64_t)segs.m * (segs.rtot / 8);
   return launch_k(lf_finalize_kernel, dim3((unsigned)((threads + 127) / 128)), dim3(128), 0, stream, segs, routes, ws,

@@ -30,6 +30,7 @@ from torch.optim.optimizer import register_optimizer_step_post_hook
 from . import _lib
 from .errors import ValidationError
 from .plan import AdapterConfig, LayerPlan, Segment, rank_layout, split_segments, validate_segments
+from .plan import workspace as group_workspace
 
 _BF16 = torch.bfloat16
 _NS = "lorafusion_b200"
@@ -611,23 +612,30 @@ def lora_group_bwd(dys: list[torch.Tensor], x: torch.Tensor, ws: list[torch.Tens
     dacc = torch.zeros(sum(sizes), dtype=torch.float32, device=x.device)
     plans, daccs, dss = [], [], []
     pos = 0
-    for j, w in enumerate(ws):  # ③ per projection (each reads its own dY)
+    for j, w in enumerate(ws):
         n = w.shape[0]
         plan = _group_plan(j, m, k, n, nads, ranks, scalings, ps, seeds, segs, offset, offset_dev, training)
         plan.bind(x.device, keep_bits=bits[j])
-        R = plan.rank_total
         acc = dacc[pos:pos + sizes[j]]
         pos += sizes[j]
-        ds = torch.empty((m, R), dtype=_BF16, device=x.device)
-        _call("grad_up", lib.lf_grad_up, ctypes.byref(plan.problem), _ptr(dys[j]), _ptr(bcs[j]), _ptr(shats[j]),
-              _ptr(ds), _ptr(acc[R * k:]), st)
         plans.append(plan)
         daccs.append(acc)
-        dss.append(ds)
-    # ④ for all projections in one launch: each X tile leaves DRAM once
+        dss.append(torch.empty((m, plan.rank_total), dtype=_BF16, device=x.device))
     J = len(ws)
+    # ③ for the group in one launch: each projection keeps its split-K partials in its own
+    # slice of the (self-cleaning, per-stream) workspace
+    wsz = [-(-_lib.workspace_bytes(m, pl.rank_total) // 256) * 256 for pl in plans]
+    buf = group_workspace(x.device, st.value or 0, sum(wsz))
+    off = 0
+    for pl, sz in zip(plans, wsz):
+        pl.problem.workspace = buf.data_ptr() + off
+        pl.problem.workspace_bytes = sz
+        off += sz
     probs = (ctypes.POINTER(_lib.LfProblem) * J)(*[ctypes.pointer(pl.problem) for pl in plans])
     arr = lambda ts: (ctypes.c_void_p * J)(*[t_.data_ptr() for t_ in ts])  # noqa: E731
+    _call("grad_up", lib.lf_grad_up_group, probs, J, arr(dys), arr(bcs), arr(shats), arr(dss),
+          arr([acc[pl.rank_total * k:] for acc, pl in zip(daccs, plans)]), st)
+    # ④ for all projections in one launch: each X tile leaves DRAM once
     _call("grad_down", lib.lf_grad_down_group, probs, J, _ptr(x), arr(dss), arr(daccs), st)
     if need_dx:  # ⑤: one GEMM over the concatenated reduction dims (dX written once), or per
         # projection where the group has no one-launch variant (the first writes dX, the others
