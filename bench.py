@@ -951,7 +951,7 @@ def run_e2e(args, layers, inputs, grads, device, world, barrier, max_over_ranks)
             if grp not in leaves:  # activation leaf: dX is computed as in a real layer
                 leaves[grp] = dev_in[grp].detach().requires_grad_(True)
             if len(names) > 1:
-                torch.autograd.backward(mod(leaves[grp]), [dev_dy[nm] for nm in names])
+                torch.autograd.backward(call(mod, leaves[grp]), [dev_dy[nm] for nm in names])
             else:
                 call(mod, leaves[grp]).backward(dev_dy[names[0]])
         done[b].record(cur)

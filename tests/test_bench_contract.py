@@ -65,3 +65,18 @@ def test_our_arm_two_ranks_sharing_one_gpu():
     d = lines[0]
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["steps"] == 2 and d["warmup"] >= 3
     assert d["gpu_launches"] > 0 and d["roofline"]["frac"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config,extra", [("c1", []), ("c3", []), ("c4", ["--tokens", "2048"])])
+def test_each_config_prints_a_full_line(config, extra):
+    """Every bench config end to end on one GPU, the e2e leg included (short runs): one JSON
+    line with the contract keys — the paths the driver only runs at round end."""
+    res = subprocess.run([sys.executable, "bench.py", "--config", config, "--steps", "2", "--warmup", "3",
+                          "--no-cpu-baseline", *extra], cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-3000:]
+    lines = _json_lines(res.stdout)
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    assert d["roofline"]["frac"] > 0 and d["unfused_torch"]["speedup"] > 0
