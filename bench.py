@@ -592,6 +592,14 @@ def step_breakdown(run, steps: int = 1) -> dict:
         ent[0] += 1
         ent[1] += gain
     span = covered - t0
+    if os.environ.get("LF_BREAKDOWN_NAMES"):  # raw kernel names behind the classes (stderr)
+        raw: dict = {}
+        for e in evs:
+            ent = raw.setdefault(e.name[:160], [0, 0.0])
+            ent[0] += 1
+            ent[1] += e.time_range.end - e.time_range.start
+        for nm, (cnt, us) in sorted(raw.items(), key=lambda kv: -kv[1][1]):
+            print(f"[breakdown] {us / steps:9.1f} us  x{cnt / steps:g}  {nm}", file=sys.stderr)
     out = {nm: {"ms_per_step": v[1] / 1e3 / steps, "kernels_per_step": v[0] / steps}
            for nm, v in sorted(parts.items(), key=lambda kv: -kv[1][1])}
     out["idle (gaps between kernels)"] = {"ms_per_step": idle / 1e3 / steps}

@@ -143,12 +143,14 @@ register_optimizer_step_post_hook(invalidate_operand_caches)
 
 
 class ShadowOperands:
-    """Persistent bf16 operand copies (A (R,k), B (n,R), zero-padded to R = rank rounded up
-    to 16) of single-adapter projections, for ``capturable`` modules: a CUDA graph reads them
-    at fixed addresses, so no cast runs inside the graph. They are refreshed in place — all
-    of them in one multi-tensor copy per device — after every optimizer step (the global
-    post-hook above), and by a lookup that sees a parameter's in-place version change; an
-    update through ``p.data`` needs ``invalidate_operand_caches()`` (or the module's
+    """Persistent bf16 rank-concat operands (A_cat (R,k), B_cat (n,R)) for ``capturable``
+    modules: a CUDA graph reads them at fixed addresses, so no cast, pad or concatenation
+    runs inside the graph. Each entry covers one column-block layout — one adapter
+    (FusedLoRA) or several (FusedMultiLoRA: every block is an adapter's lora_A/lora_B cast
+    into its columns; padding columns stay zero). They are refreshed in place — all of them
+    in one multi-tensor copy per device — after every optimizer step (the global post-hook
+    above), and by a lookup that sees a parameter's in-place version change; an update
+    through ``p.data`` needs ``invalidate_operand_caches()`` (or the module's
     ``invalidate_operands()``)."""
 
     def __init__(self):
@@ -156,45 +158,60 @@ class ShadowOperands:
         _SHADOW_SETS.add(self)
 
     def lookup(self, a: torch.Tensor, b: torch.Tensor, R: int) -> tuple[torch.Tensor, torch.Tensor]:
-        key = (a.data_ptr(), b.data_ptr(), R)
+        """One adapter: A (r,k) / B (n,r) into columns [0, r) of R."""
+        return self.lookup_blocks([(a, b, 0)], R)
+
+    def lookup_blocks(self, blocks, R: int) -> tuple[torch.Tensor, torch.Tensor]:
+        """``blocks``: (lora_A weight, lora_B weight, first column) per column block; R the
+        total (padded) column count."""
+        key = (R,) + tuple((a.data_ptr(), b.data_ptr(), c0) for a, b, c0 in blocks)
         ent = self._d.get(key)
         if ent is None:
-            if len(self._d) >= 16:  # parameters moved (module.to): drop the stale copies
+            if len(self._d) >= 32:  # parameters moved (module.to) or layouts churn: drop the stale copies
                 self._d.clear()
-            ent = [torch.zeros((R, a.shape[1]), dtype=_BF16, device=a.device),
-                   torch.zeros((b.shape[0], R), dtype=_BF16, device=b.device), -1, -1,
-                   weakref.ref(a), weakref.ref(b)]
-            self._d[key] = ent
-        if ent[2] != a._version or ent[3] != b._version:
-            self._copy([ent])
+            a0, b0 = blocks[0][0], blocks[0][1]
+            a_cat = torch.zeros((R, a0.shape[1]), dtype=_BF16, device=a0.device)
+            b_cat = torch.zeros((b0.shape[0], R), dtype=_BF16, device=b0.device)
+            # piece: [A_cat rows, B_cat columns, weakref A, weakref B, A version, B version]
+            pieces = [[a_cat[c0:c0 + a.shape[0]], b_cat[:, c0:c0 + a.shape[0]], weakref.ref(a), weakref.ref(b), -1, -1]
+                      for a, b, c0 in blocks]
+            ent = self._d[key] = (a_cat, b_cat, pieces)
+        if any(pc[4] != a._version or pc[5] != b._version for pc, (a, b, _c) in zip(ent[2], blocks)):
+            self._copy(ent[2])
         return ent[0], ent[1]
 
     @staticmethod
-    def _copy(ents) -> None:
+    def _copy(pieces) -> None:
         by_dev: dict = {}
-        for ent in ents:
-            a, b = ent[4](), ent[5]()
+        for pc in pieces:
+            a, b = pc[2](), pc[3]()
             if a is None or b is None:
                 continue
-            r = a.shape[0]
             dst, src = by_dev.setdefault(a.device, ([], []))
-            dst += [ent[0][:r], ent[1][:, :r]]
+            dst += [pc[0], pc[1]]
             src += [a.detach(), b.detach()]
-            ent[2], ent[3] = a._version, b._version
+            pc[4], pc[5] = a._version, b._version
         with torch.no_grad():
             for dst, src in by_dev.values():
                 torch._foreach_copy_(dst, src)
 
+    def _pieces(self) -> list:
+        return [pc for ent in self._d.values() for pc in ent[2]]
+
     def refresh_all(self) -> None:
-        self._copy(list(self._d.values()))
+        self._copy(self._pieces())
+
+    def clear(self) -> None:
+        """Re-copy every persistent operand (the addresses a captured graph reads stay put)."""
+        self.refresh_all()
 
     def stale(self) -> list:
-        """Entries whose parameters changed in place since their last copy (host check)."""
+        """Pieces whose parameters changed in place since their last copy (host check)."""
         out = []
-        for ent in self._d.values():
-            a, b = ent[4](), ent[5]()
-            if a is not None and b is not None and (ent[2] != a._version or ent[3] != b._version):
-                out.append(ent)
+        for pc in self._pieces():
+            a, b = pc[2](), pc[3]()
+            if a is not None and b is not None and (pc[4] != a._version or pc[5] != b._version):
+                out.append(pc)
         return out
 
 
@@ -202,12 +219,9 @@ def refresh_stale_operand_shadows() -> None:
     """Re-copy the persistent bf16 operands whose fp32 parameters changed in place (version
     counter) since their last copy — a host-side check, one multi-tensor copy only when
     something changed. GraphedStep.replay() calls it before every replay."""
-    ents = [e for sh in list(_SHADOW_SETS) for e in sh.stale()]
-    if ents:
-        ShadowOperands._copy(ents)
-
-    def clear(self) -> None:
-        self.refresh_all()
+    pcs = [pc for sh in list(_SHADOW_SETS) for pc in sh.stale()]
+    if pcs:
+        ShadowOperands._copy(pcs)
 
 
 class OperandCache:
@@ -262,11 +276,7 @@ def _own(t: torch.Tensor | None, inputs: Sequence[torch.Tensor], empty_shape, li
 def _rank_concat_operands(plan: LayerPlan, a: Sequence[torch.Tensor], b: Sequence[torch.Tensor], cache_id: int):
     cache = _CACHES.get(cache_id) if cache_id else None
     if isinstance(cache, ShadowOperands):
-        blocks = plan.column_blocks()
-        if len(blocks) == 1:
-            ad = blocks[0][0]
-            return cache.lookup(a[ad], b[ad], blocks[0][2])
-        cache = None  # several adapters in one call: gather per call
+        return cache.lookup_blocks([(a[ad], b[ad], c0) for ad, c0, _r in plan.column_blocks()], plan.rank_total)
     key = None
     if cache is not None:
         blocks = plan.column_blocks()

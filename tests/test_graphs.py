@@ -59,8 +59,8 @@ def test_graphed_fused_lora_matches_eager_offset_and_redraws_mask():
 
 
 def test_graphed_multi_lora_replays_track_weight_updates():
-    """capturable layers re-cast the fp32 master weights inside the graph: an in-place
-    update between replays is seen by the next replay."""
+    """capturable multi-adapter layers read persistent bf16 rank-concat copies of the fp32
+    master weights: an in-place update between replays is re-copied before the next replay."""
     g = torch.Generator(device=DEV).manual_seed(2)
     m, k, n = 768, 256, 256
     w = (torch.randn(n, k, device=DEV, generator=g) / k**0.5).to(torch.bfloat16)
@@ -122,4 +122,45 @@ def test_graphed_fused_lora_sees_optimizer_and_inplace_updates():
         check()
     with torch.no_grad():
         cap.lora_B.weight.mul_(2.0)  # in place: version bump, refreshed before the replay
+    check()
+
+
+def test_graphed_multi_lora_sees_optimizer_updates_bitwise():
+    """Capturable FusedMultiLoRA (ranks 8 / 32 / 16: padded and unpadded column blocks) reads
+    persistent rank-concat copies inside the graph — no cast, pad or concatenation per call —
+    refreshed by every optimizer step and by invalidate_operands(); the graphed step matches
+    a non-capturable layer with the same weights bit for bit."""
+    g = torch.Generator(device=DEV).manual_seed(9)
+    m, k, n = 640, 256, 384
+    w = (torch.randn(n, k, device=DEV, generator=g) / 16).to(torch.bfloat16)
+    ads = [AdapterConfig(8, 2.0, 0.0, 1), AdapterConfig(32, 1.0, 0.0, 2), AdapterConfig(16, 0.5, 0.0, 3)]
+    cap = FusedMultiLoRA(w, ads, init="gaussian", capturable=True, generator=g)
+    ref = FusedMultiLoRA(w, ads, init="gaussian")
+    x = torch.randn(m, k, device=DEV, generator=g).to(torch.bfloat16)
+    segs = segments_from_lengths([0, 1, 2], [128, 256, 256])
+    opt = torch.optim.AdamW(cap.parameters(), lr=1e-2, fused=True)
+
+    def step():
+        y = cap(x, segs)
+        y.float().square().mean().backward()
+        return y.detach()
+
+    graphed = GraphedStep(step, warmup=2)
+
+    def check():
+        y = graphed.replay()
+        with torch.no_grad():
+            for pr, pc in zip(ref.parameters(), cap.parameters()):
+                pr.copy_(pc)
+            ref.invalidate_operands()
+            assert torch.equal(y, ref(x, segs))
+
+    check()
+    for _ in range(2):
+        opt.step()
+        opt.zero_grad(set_to_none=False)
+        check()
+    with torch.no_grad():
+        cap.lora_A[0].weight.data.mul_(-1.0)  # through .data: no version bump
+    cap.invalidate_operands()
     check()

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--p", type=float, default=0.1)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--rounds", type=int, default=2)
+    ap.add_argument("--only", default="", help="comma-separated variants (e.g. dgrad_group)")
     args = ap.parse_args()
     import torch
 
@@ -80,6 +81,8 @@ def main():
         _lib.check(lib.lf_grad_input_group(pp, J, arr(DY), arr(W), arr(S), arr(A), P(DX), s_), "dgrad_group")
 
     variants = {"fwd_separate": fwd_sep, "fwd_group": fwd_grp, "dgrad_separate": dg_sep, "dgrad_group": dg_grp}
+    if args.only:
+        variants = {k_: v_ for k_, v_ in variants.items() if k_ in args.only.split(",")}
     flops = {"fwd": 2 * m * k * sum(ns), "dgrad": 2 * m * k * sum(ns)}
     graphs = {}
     for name, fn in variants.items():
