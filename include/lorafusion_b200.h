@@ -49,9 +49,10 @@ extern "C" {
 #define LF_API
 #endif
 
-#define LF_ABI_VERSION 5
+#define LF_ABI_VERSION 6
 #define LF_MAX_SEGMENTS 32
 #define LF_MAX_RANK_TOTAL 128
+#define LF_MAX_COPY_BLOCKS 64 /* lf_copy_column_blocks blocks per call */
 #define LF_ROUTE_TILE_ROWS 128 /* ls/costmodel.py:25 ROUTING_TILE_ROWS */
 #define LF_ROUTE_ENTRY_BYTES 16 /* ls/costmodel.py:26 ROUTING_ENTRY_BYTES */
 
@@ -177,6 +178,15 @@ LF_API int lf_dropout_mask(const LfProblem* p, uint8_t* keep_out, void* stream);
 /* Packed keep bits of the same mask (m x k/8 bytes, 16-byte aligned; bit c of byte j of a
  * row = column 8j + c). Input-free, so callers may run it on a side stream ahead of ①. */
 LF_API int lf_keep_bits(const LfProblem* p, uint8_t* bits_out, void* stream);
+
+/* Column blocks of fp32 row-major matrices copied out contiguously, all in one launch: for
+ * block i, dst[i] (rows[i] x width[i], row-major) = src[i][:, col[i] : col[i] + width[i]] of a
+ * rows[i] x ld[i] matrix. Turns dB_cat's per-adapter column blocks (n x R) into the
+ * contiguous n x r gradients an optimizer expects (a multi-adapter call's lora_B grads);
+ * no reference counterpart (the reference has no gradient layout). 0 <= nblocks <=
+ * LF_MAX_COPY_BLOCKS. ABI 6. */
+LF_API int lf_copy_column_blocks(int32_t nblocks, const float* const* src, const int32_t* rows, const int32_t* ld,
+                                 const int32_t* col, const int32_t* width, float* const* dst, void* stream);
 
 /* Thread-local message describing the last failure (never NULL). */
 LF_API const char* lf_last_error(void);

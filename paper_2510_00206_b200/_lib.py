@@ -13,8 +13,9 @@ from pathlib import Path
 
 from .errors import ExtensionMissingError, KernelError, ValidationError
 
-LF_ABI_VERSION = 5
+LF_ABI_VERSION = 6
 LF_MAX_SEGMENTS = 32
+LF_MAX_COPY_BLOCKS = 64  # lf_copy_column_blocks blocks per call
 LF_MAX_GROUP = 3  # projections of one shared-input group launch (lf_*_group)
 LF_MAX_RANK_TOTAL = 128
 ROUTE_TILE_ROWS = 128  # ls/costmodel.py:25
@@ -48,6 +49,7 @@ EXPORTED_SYMBOLS = (
     "lf_grad_input_group",
     "lf_dropout_mask",
     "lf_keep_bits",
+    "lf_copy_column_blocks",
     "lf_last_error",
     "lf_abi_version",
 )
@@ -107,6 +109,9 @@ _SIGNATURES = {
                                            ctypes.POINTER(_V), ctypes.POINTER(_V), ctypes.POINTER(_V), _V, _V]),
     "lf_dropout_mask": (ctypes.c_int, [_P, _V, _V]),
     "lf_keep_bits": (ctypes.c_int, [_P, _V, _V]),
+    "lf_copy_column_blocks": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(_V), ctypes.POINTER(ctypes.c_int32),
+                                             ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                             ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_V), _V]),
     "lf_last_error": (ctypes.c_char_p, []),
     "lf_abi_version": (ctypes.c_int, []),
 }

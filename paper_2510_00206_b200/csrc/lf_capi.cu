@@ -332,6 +332,29 @@ int lf_keep_bits(const LfProblem* p, uint8_t* bits_out, void* stream) {
   return LF_OK;
 }
 
+// Per-adapter dB gradients out of dB_cat's column blocks in one launch (see the header)
+int lf_copy_column_blocks(int32_t nblocks, const float* const* src, const int32_t* rows, const int32_t* ld,
+                          const int32_t* col, const int32_t* width, float* const* dst, void* stream) {
+  if (nblocks < 0 || nblocks > LF_MAX_COPY_BLOCKS)
+    return fail(LF_E_INVALID, "lf_copy_column_blocks: nblocks %d outside [0, %d]", nblocks, LF_MAX_COPY_BLOCKS);
+  if (nblocks == 0) return LF_OK;
+  if (!src || !rows || !ld || !col || !width || !dst)
+    return fail(LF_E_INVALID, "lf_copy_column_blocks: NULL argument array");
+  lf::CopyBlocksArgs a;
+  a.n = nblocks;
+  for (int i = 0; i < nblocks; ++i) {
+    if (!src[i] || !dst[i]) return fail(LF_E_INVALID, "lf_copy_column_blocks: block %d has a NULL pointer", i);
+    if (rows[i] <= 0 || width[i] <= 0 || col[i] < 0 || (int64_t)col[i] + width[i] > ld[i])
+      return fail(LF_E_INVALID, "lf_copy_column_blocks: block %d: rows %d, columns [%d, %d) of a row of %d", i,
+                  rows[i], col[i], col[i] + width[i], ld[i]);
+    a.blk[i] = lf::CopyBlock{src[i], dst[i], rows[i], ld[i], col[i], width[i]};
+  }
+  Dev d;
+  LF_TRY(current_device(&d));
+  if (lf::copy_blocks_launch(a, d.sms, (cudaStream_t)stream)) return cuda_fail("copy_column_blocks launch");
+  return LF_OK;
+}
+
 int lf_dropout_down_fwd(const LfProblem* p, const uint16_t* x, const uint16_t* a_cat, uint16_t* s_hat,
                         void* stream) {
   lf::LfSegTable t;

@@ -189,4 +189,17 @@ int routes_launch(const LfSegTable& segs, int32_t* routes, int ntiles, cudaStrea
 int mask_launch(const LfSegTable& segs, int32_t k, uint8_t* keep, cudaStream_t stream);
 int keep_bits_launch(const LfSegTable& segs, int32_t k, uint8_t* bits, int64_t ld, int num_sms, cudaStream_t stream);
 
+// lf_copy_column_blocks: dst (rows x width, contiguous) = src[:, col : col + width] of a rows x ld matrix
+constexpr int kMaxCopyBlocks = 64;
+struct CopyBlock {
+  const float* src;
+  float* dst;
+  int32_t rows, ld, col, width;
+};
+struct CopyBlocksArgs {
+  int32_t n;
+  CopyBlock blk[kMaxCopyBlocks];
+};
+int copy_blocks_launch(const CopyBlocksArgs& a, int num_sms, cudaStream_t stream);
+
 }  // namespace lf

@@ -917,4 +917,44 @@ int mask_launch(const LfSegTable& segs, int32_t k, uint8_t* keep, cudaStream_t s
   return launch_k(lf_mask_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, stream, segs, k, keep);
 }
 
+// Column blocks out of fp32 row-major matrices into contiguous buffers (dB_cat n x R ->
+// each adapter's n x r gradient): one launch for every block of a call; blockIdx.y picks the
+// block, the x grid strides over its elements (4 floats per thread where alignment allows).
+__global__ void __launch_bounds__(256) lf_copy_blocks_kernel(const __grid_constant__ CopyBlocksArgs a) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const CopyBlock& b = a.blk[blockIdx.y];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool vec = ((b.width | b.ld | b.col) & 3) == 0 && ((reinterpret_cast<uintptr_t>(b.src) | reinterpret_cast<uintptr_t>(b.dst)) & 15u) == 0;
+  if (vec) {
+    const int w4 = b.width >> 2;
+    const int64_t total = (int64_t)b.rows * w4;
+    for (int64_t i = t0; i < total; i += stride) {
+      const int64_t r = i / w4;
+      const int c = (int)(i - r * w4) * 4;
+      const float4 v = *reinterpret_cast<const float4*>(b.src + r * b.ld + b.col + c);
+      *reinterpret_cast<float4*>(b.dst + r * b.width + c) = v;
+    }
+  } else {
+    const int64_t total = (int64_t)b.rows * b.width;
+    for (int64_t i = t0; i < total; i += stride) {
+      const int64_t r = i / b.width;
+      const int c = (int)(i - r * b.width);
+      b.dst[r * b.width + c] = b.src[r * b.ld + b.col + c];
+    }
+  }
+}
+
+int copy_blocks_launch(const CopyBlocksArgs& a, int num_sms, cudaStream_t stream) {
+  if (a.n <= 0) return 0;
+  int64_t most = 0;
+  for (int i = 0; i < a.n; ++i) most = max(most, (int64_t)a.blk[i].rows * a.blk[i].width);
+  int64_t gx = (most / 4 + 255) / 256;
+  const int64_t cap = (4LL * num_sms + a.n - 1) / a.n;  // ~4 CTAs per SM over all blocks
+  if (gx > cap) gx = cap;
+  if (gx < 1) gx = 1;
+  return launch_k(lf_copy_blocks_kernel, dim3((unsigned)gx, (unsigned)a.n), dim3(256), 0, stream, a);
+}
+
 }  // namespace lf

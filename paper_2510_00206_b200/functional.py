@@ -153,22 +153,26 @@ class ShadowOperands:
     through ``p.data`` needs ``invalidate_operand_caches()`` (or the module's
     ``invalidate_operands()``)."""
 
-    def __init__(self):
+    def __init__(self, capacity: int = 64):
+        self.capacity = capacity
         self._d: dict = {}
         _SHADOW_SETS.add(self)
 
-    def lookup(self, a: torch.Tensor, b: torch.Tensor, R: int) -> tuple[torch.Tensor, torch.Tensor]:
+    def lookup(self, a: torch.Tensor, b: torch.Tensor, R: int) -> tuple[torch.Tensor, torch.Tensor] | None:
         """One adapter: A (r,k) / B (n,r) into columns [0, r) of R."""
         return self.lookup_blocks([(a, b, 0)], R)
 
-    def lookup_blocks(self, blocks, R: int) -> tuple[torch.Tensor, torch.Tensor]:
+    def lookup_blocks(self, blocks, R: int) -> tuple[torch.Tensor, torch.Tensor] | None:
         """``blocks``: (lora_A weight, lora_B weight, first column) per column block; R the
-        total (padded) column count."""
+        total (padded) column count. None when the module's entry cap is reached."""
         key = (R,) + tuple((a.data_ptr(), b.data_ptr(), c0) for a, b, c0 in blocks)
         ent = self._d.get(key)
         if ent is None:
-            if len(self._d) >= 32:  # parameters moved (module.to) or layouts churn: drop the stale copies
-                self._d.clear()
+            # entries are never dropped: a captured graph may read them. Past the cap (layouts
+            # churning, parameters moved) or first seen inside a capture, the caller gathers
+            # per call instead.
+            if len(self._d) >= self.capacity or torch.cuda.is_current_stream_capturing():
+                return None  # (inside a capture: a new copy would be valid only after a replay)
             a0, b0 = blocks[0][0], blocks[0][1]
             a_cat = torch.zeros((R, a0.shape[1]), dtype=_BF16, device=a0.device)
             b_cat = torch.zeros((b0.shape[0], R), dtype=_BF16, device=b0.device)
@@ -276,7 +280,10 @@ def _own(t: torch.Tensor | None, inputs: Sequence[torch.Tensor], empty_shape, li
 def _rank_concat_operands(plan: LayerPlan, a: Sequence[torch.Tensor], b: Sequence[torch.Tensor], cache_id: int):
     cache = _CACHES.get(cache_id) if cache_id else None
     if isinstance(cache, ShadowOperands):
-        return cache.lookup_blocks([(a[ad], b[ad], c0) for ad, c0, _r in plan.column_blocks()], plan.rank_total)
+        hit = cache.lookup_blocks([(a[ad], b[ad], c0) for ad, c0, _r in plan.column_blocks()], plan.rank_total)
+        if hit is not None:
+            return hit
+        cache = None
     key = None
     if cache is not None:
         blocks = plan.column_blocks()
@@ -309,6 +316,44 @@ def _group_operands(a: Sequence[torch.Tensor], b: Sequence[torch.Tensor], ranks)
     bcs = [torch.empty(t.shape, dtype=_BF16, device=t.device) for t in b]
     torch._foreach_copy_(acs + bcs, [t.detach() for t in a] + [t.detach() for t in b])
     return acs, bcs
+
+
+# --------------------------------------------------------------------------------------
+# dB column blocks -> contiguous per-adapter gradients
+# --------------------------------------------------------------------------------------
+def _gather_db_blocks(flat: torch.Tensor, specs) -> list[torch.Tensor]:
+    """Contiguous (n, r) fp32 gradients of the column blocks ``specs`` = ((offset, n, R, c0,
+    r), ...) of n x R row-major matrices inside ``flat``. dB_cat[:, c0:c0 + r] is a strided
+    view, which autograd would copy into a contiguous .grad with one elementwise launch per
+    adapter and projection (28 per C3 step): blocks spanning their whole rows stay views,
+    the others are copied out by one lf_copy_column_blocks launch per call."""
+    res: list = [None] * len(specs)
+    part = []
+    for i, (off, n, R, c0, r) in enumerate(specs):
+        if c0 == 0 and r == R:
+            res[i] = flat[off:off + n * R].view(n, R)
+        else:
+            part.append(i)
+    if not part:
+        return res
+    out = torch.empty(sum(specs[i][1] * specs[i][4] for i in part), dtype=flat.dtype, device=flat.device)
+    lib = _lib.load()
+    st = _stream(flat.device)
+    base, esz = flat.data_ptr(), flat.element_size()
+    pos = 0
+    for c in range(0, len(part), _lib.LF_MAX_COPY_BLOCKS):
+        chunk = part[c:c + _lib.LF_MAX_COPY_BLOCKS]
+        nb = len(chunk)
+        src, dst = (ctypes.c_void_p * nb)(), (ctypes.c_void_p * nb)()
+        rows, ld, col, wid = ((ctypes.c_int32 * nb)() for _ in range(4))
+        for t, i in enumerate(chunk):
+            off, n, R, c0, r = specs[i]
+            src[t], dst[t] = base + off * esz, out.data_ptr() + pos * esz
+            rows[t], ld[t], col[t], wid[t] = n, R, c0, r
+            res[i] = out[pos:pos + n * r].view(n, r)
+            pos += n * r
+        _call("copy_column_blocks", lib.lf_copy_column_blocks, nb, src, rows, ld, col, wid, dst, st)
+    return res
 
 
 # --------------------------------------------------------------------------------------
@@ -495,15 +540,17 @@ def _backward(ctx, dy, _ds=None, _dbits=None, _da=None, _db=None):
     # blocks of one adapter when its segments do not share one, e.g. per-batch slots)
     ga: list = [None] * na
     gb: list = [None] * na
-    seen = set()
+    seen, blocks = set(), []
     for s, c0 in zip(segments, col_starts):
         if (s.adapter, c0) in seen:
             continue
         seen.add((s.adapter, c0))
-        r = A["ranks"][s.adapter]
-        a_part, b_part = da[c0:c0 + r], db[:, c0:c0 + r]
-        ga[s.adapter] = a_part if ga[s.adapter] is None else ga[s.adapter] + a_part
-        gb[s.adapter] = b_part if gb[s.adapter] is None else gb[s.adapter] + b_part
+        blocks.append((s.adapter, c0, A["ranks"][s.adapter]))
+    b_parts = _gather_db_blocks(dacc, [(R * k, n, R, c0, r) for _ad, c0, r in blocks])
+    for (ad, c0, r), b_part in zip(blocks, b_parts):
+        a_part = da[c0:c0 + r]
+        ga[ad] = a_part if ga[ad] is None else ga[ad] + a_part
+        gb[ad] = b_part if gb[ad] is None else gb[ad] + b_part
     dts = ctx.param_dtypes
     ga = [g.to(dts[i]) if g is not None else None for i, g in enumerate(ga)]
     gb = [g.to(dts[na + i]) if g is not None else None for i, g in enumerate(gb)]
@@ -704,11 +751,10 @@ def _group_backward(ctx, gys, _gs=None, _gbits=None, _ga=None, _gb=None):
     ga: list = [None] * NA
     gb: list = [None] * NA
     pos, base = 0, 0
+    b_specs, b_slots = [], []
     for j, ((cs, R), w, (r_j,)) in enumerate(zip(lays, ws, _group_split(A["nads"], A["ranks"]))):
         n = w.shape[0]
-        acc = dacc[pos:pos + R * (k + n)]
-        pos += R * (k + n)
-        da, db = acc[:R * k].view(R, k), acc[R * k:].view(n, R)
+        da = dacc[pos:pos + R * k].view(R, k)
         seen = set()
         for s_, c0 in zip(segments, cs):
             if s_.adapter in seen:
@@ -717,8 +763,13 @@ def _group_backward(ctx, gys, _gs=None, _gbits=None, _ga=None, _gb=None):
             i = base + s_.adapter
             r = r_j[s_.adapter]
             ga[i] = da[c0:c0 + r].to(ctx.param_dtypes[i])
-            gb[i] = db[:, c0:c0 + r].to(ctx.param_dtypes[NA + i])
+            b_specs.append((pos + R * k, n, R, c0, r))
+            b_slots.append(i)
+        pos += R * (k + n)
         base += len(r_j)
+    # every projection's dB blocks in one gather (contiguous per-adapter gradients)
+    for i, g in zip(b_slots, _gather_db_blocks(dacc, b_specs)):
+        gb[i] = g.to(ctx.param_dtypes[NA + i])
     return (dx if need_dx else None, [None] * J, ga, gb) + ctx.none_grads
 
 

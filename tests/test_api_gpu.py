@@ -340,3 +340,72 @@ def test_multi_lora_group_matches_separate_layers(ranks, ps):
                           [lb.weight.grad for lb in layer.lora_B]):
             assert _rel(gl, ga) < 1e-4
     assert _rel(dx_group, xs.grad) < 4e-3
+
+
+@pytest.mark.parametrize("grouped", [False, True], ids=["layer", "group"])
+def test_capturable_multi_lora_step_has_no_operand_or_grad_copies(grouped):
+    """A capturable multi-adapter step (ranks 8/16/32/64: padded and full blocks) reads the
+    persistent rank-concat operands and gathers every dB column block in one index_select:
+    after the first call the fwd+bwd launches no cast, pad, cat or strided-copy kernels, and
+    its outputs and gradients equal the non-capturable layer's bit for bit."""
+    from torch.profiler import ProfilerActivity, profile
+
+    from paper_2510_00206_b200 import FusedMultiLoRAGroup
+
+    g = torch.Generator(device=DEV).manual_seed(21)
+    k = 256
+    ads = [AdapterConfig(r, 2.0, 0.0, seed=i + 1) for i, r in enumerate((8, 16, 32, 64))]
+    segs = segments_from_lengths([0, 1, 2, 3], [128, 256, 128, 128])
+    m = 640
+    names = ("q", "k") if grouped else ("q",)
+    bases = {nm: (torch.randn(n, k, device=DEV, generator=g) / 16).to(torch.bfloat16) for nm, n in zip(names, (384, 128))}
+    caps = {nm: FusedMultiLoRA(w, ads, init="gaussian", generator=g, capturable=True) for nm, w in bases.items()}
+    refs = {nm: FusedMultiLoRA(w, ads, init="gaussian") for nm, w in bases.items()}
+    with torch.no_grad():
+        for nm in names:
+            for pr, pc in zip(refs[nm].parameters(), caps[nm].parameters()):
+                pr.copy_(pc)
+    mod = FusedMultiLoRAGroup.from_layers(caps) if grouped else caps["q"]
+    ref = FusedMultiLoRAGroup.from_layers(refs) if grouped else refs["q"]
+    x = torch.randn(m, k, device=DEV, generator=g).to(torch.bfloat16)
+    dys = [torch.randn(m, w.shape[0], device=DEV, generator=g).to(torch.bfloat16) for w in bases.values()]
+
+    def step(layer):
+        for p_ in layer.parameters():
+            p_.grad = None
+        ys = layer(x, segs)
+        ys = ys if isinstance(ys, tuple) else (ys,)
+        torch.autograd.backward(ys, dys)
+        return ys
+
+    step(mod)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        ys = step(mod)
+        torch.cuda.synchronize()
+    names_run = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    bad = [nm_ for nm_ in names_run if any(t in nm_ for t in ("copy_kernel", "CatArray", "bfloat16_copy"))]
+    assert not bad, bad
+    ys_ref = step(ref)
+    for y, yr in zip(ys, ys_ref):
+        assert torch.equal(y, yr)
+    for pc, pr in zip(mod.parameters(), ref.parameters()):
+        assert pc.grad.is_contiguous()
+        assert torch.equal(pc.grad, pr.grad)
+
+
+def test_copy_column_blocks_matches_slicing():
+    """lf_copy_column_blocks (through functional._gather_db_blocks): vectorised blocks (widths
+    and offsets multiples of 4), scalar ones (width 3, column 5) and whole-row blocks (views,
+    no copy) all equal the torch slices, over several matrices of one flat buffer."""
+    from paper_2510_00206_b200.functional import _gather_db_blocks
+
+    g = torch.Generator(device=DEV).manual_seed(4)
+    flat = torch.randn(300 * 128 + 77 * 48 + 9 * 16, device=DEV, generator=g)
+    specs = [(0, 300, 128, 0, 8), (0, 300, 128, 16, 64), (0, 300, 128, 5, 3), (300 * 128, 77, 48, 32, 16),
+             (300 * 128 + 77 * 48, 9, 16, 0, 16)]
+    got = _gather_db_blocks(flat, specs)
+    for (off, n, R, c0, r), t in zip(specs, got):
+        ref = flat[off:off + n * R].view(n, R)[:, c0:c0 + r]
+        assert t.is_contiguous() and torch.equal(t, ref)
+    assert got[-1].data_ptr() == flat[300 * 128 + 77 * 48:].data_ptr()  # whole rows: a view

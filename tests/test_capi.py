@@ -180,6 +180,23 @@ def test_group_entry_points_reject_bad_arguments(lib):
     assert lib.lf_grad_down_group(probs, 4, x, arr, arr, None) == _lib.LF_E_INVALID
 
 
+def test_copy_column_blocks_rejects_bad_arguments(lib):
+    """ABI 6 lf_copy_column_blocks: block counts outside 0..LF_MAX_COPY_BLOCKS, NULL arrays
+    or pointers and column ranges past the row are LF_E_INVALID; zero blocks is a no-op."""
+    V, I = ctypes.c_void_p, ctypes.c_int32
+    src, dst = (V * 2)(16, 16), (V * 2)(32, 32)
+    rows, ld, col, wid = (I * 2)(4, 4), (I * 2)(128, 128), (I * 2)(0, 64), (I * 2)(64, 64)
+    assert lib.lf_copy_column_blocks(0, None, None, None, None, None, None, None) == _lib.LF_OK
+    assert lib.lf_copy_column_blocks(-1, src, rows, ld, col, wid, dst, None) == _lib.LF_E_INVALID
+    assert lib.lf_copy_column_blocks(_lib.LF_MAX_COPY_BLOCKS + 1, src, rows, ld, col, wid, dst, None) == _lib.LF_E_INVALID
+    assert lib.lf_copy_column_blocks(2, src, rows, ld, col, None, dst, None) == _lib.LF_E_INVALID
+    bad = (I * 2)(0, 65)
+    assert lib.lf_copy_column_blocks(2, src, rows, ld, bad, wid, dst, None) == _lib.LF_E_INVALID
+    assert "block 1" in _lib.last_error()
+    nul = (V * 2)(16, None)
+    assert lib.lf_copy_column_blocks(2, nul, rows, ld, col, wid, dst, None) == _lib.LF_E_INVALID
+
+
 def test_no_gpu_reports_cuda_error_not_crash(lib):
     """A valid problem on a machine without a B200 fails with LF_E_CUDA/UNSUPPORTED, never a crash."""
     import torch
