@@ -485,6 +485,9 @@ __device__ __forceinline__ uint32_t philox_keep8(uint32_t col8, uint32_t row, co
 // Per-(segment, row) Philox state hoisted out of the column loop: the round keys, the
 // constant counter words (row, offset) and the packed 16-bit threshold. One call then
 // costs 10 x (2 IMAD.WIDE + 2 LOP3) plus a SIMD compare of the eight 16-bit lanes.
+#ifndef LF_PHILOX_KEYS_INLINE
+#define LF_PHILOX_KEYS_INLINE 0  // 1: philox_masks adds the Weyl constants per round instead of reading k0[]/k1[]
+#endif
 struct PhiloxRow {
   uint32_t k0[10], k1[10];
   uint32_t c1, c2, c3;
@@ -634,14 +637,24 @@ __device__ __forceinline__ uint64_t philox_masks(const PhiloxRow& pr, int col, u
     c2[j] = pr.c2;
     c3[j] = pr.c3;
   }
+#if LF_PHILOX_KEYS_INLINE
+  uint32_t ka = pr.k0[0], kb = pr.k1[0];
+#endif
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
+#if LF_PHILOX_KEYS_INLINE
+    const uint32_t ki0 = ka, ki1 = kb;
+    ka += 0x9E3779B9u;
+    kb += 0xBB67AE85u;
+#else
+    const uint32_t ki0 = pr.k0[i], ki1 = pr.k1[i];
+#endif
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
       const uint64_t p0 = (uint64_t)0xD2511F53u * c0[j];
       const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2[j];
-      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1[j] ^ pr.k0[i];
-      const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3[j] ^ pr.k1[i];
+      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1[j] ^ ki0;
+      const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3[j] ^ ki1;
       c1[j] = (uint32_t)p1;
       c3[j] = (uint32_t)p0;
       c0[j] = n0;

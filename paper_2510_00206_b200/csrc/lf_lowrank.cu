@@ -35,10 +35,16 @@ __device__ __forceinline__ bool tile_needs_mask(const LfSegTable& t, const LfRou
 // ------------------------------------------------------------------------------------
 // ① dropout + down projection
 // ------------------------------------------------------------------------------------
+#ifndef LF_DOWN_MINB
+#define LF_DOWN_MINB 2  // resident CTAs per SM (register bound)
+#endif
+#ifndef LF_DOWN_SMEM_KB
+#define LF_DOWN_SMEM_KB 100
+#endif
 namespace down {
 constexpr int X_BYTES = 128 * 64 * 2;  // 16 KB
 // 2 CTAs / SM (register bound): ~2 x 100 KB of X tiles in flight per SM
-constexpr int SMEM_BUDGET = 100 * 1024;
+constexpr int SMEM_BUDGET = LF_DOWN_SMEM_KB * 1024;
 }  // namespace down
 
 // wmax: the widest routing hull (LfSegTable::wmax), the most A_cat columns a stage holds
@@ -76,7 +82,7 @@ struct UnitWalker {
 // EXPLICIT: the keep mask comes from a caller's uint8 mask (mask_mode 2) instead of Philox —
 // a separate instantiation, so the Philox hot loop carries no per-k-block mode test
 template <bool EXPLICIT>
-__global__ void __launch_bounds__(kDownThreads, 2)
+__global__ void __launch_bounds__(kDownThreads, LF_DOWN_MINB)
     lf_down_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ DownArgs args, int STAGES, int STAGE_BYTES) {
   using namespace down;
@@ -226,12 +232,18 @@ __global__ void __launch_bounds__(kDownThreads, 2)
               bits = 0;
 #pragma unroll
               for (int c = 0; c < 4; ++c) bits |= explicit_keep8(mrow, col + 8 * c, args.k) << (8 * c);
+            } else if (args.segs.debug & 4096) {  // profiling: a fixed pattern instead of Philox
+              bits = 0xFBFFFFFEu ^ (uint32_t)kb;
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) msk[c][i] = (c | i) ? 0xFFFFFFFFu : 0xFFFF0000u;
             } else {
               bits = (uint32_t)philox_masks<4>(pr, col, msk);
             }
           }
           mbar_wait(&full[stage], phase);
-          if (my_mask && bits != ~0u) {
+          if (my_mask && bits != ~0u && !(args.segs.debug & 8192)) {  // 8192, profiling: no smem pass
             const uint32_t so = (uint32_t)(stage * STAGE_BYTES);
             uint4 v[4];
 #pragma unroll
@@ -245,7 +257,7 @@ __global__ void __launch_bounds__(kDownThreads, 2)
                                                 v[c].w & msk[c][3]));
             }
           }
-          if (bits_row) {
+          if (bits_row && !(args.segs.debug & 16384)) {  // 16384, profiling: no keep-bit stores
             const int b0 = kb * 8 + 4 * half;
             if (bits_words && b0 + 4 <= nbytes) {
               *reinterpret_cast<uint32_t*>(bits_row + b0) = bits;
