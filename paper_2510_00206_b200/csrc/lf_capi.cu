@@ -383,7 +383,7 @@ int lf_dropout_down_fwd(const LfProblem* p, const uint16_t* x, const uint16_t* a
   const int nkb = (p->k + 63) / 64;
   int stages = 0, stage_bytes = 0;
   lf::down_config(t.wmax, &stages, &stage_bytes);
-  const int occ = occupancy_for_smem(stages * stage_bytes + 2048);
+  const int occ = occupancy_for_smem(stages * stage_bytes + 2048 + lf::down_extra_smem(t.mask_mode));
   // one resident wave sharing the units evenly (stream-K); at least 4 k-blocks per CTA so
   // the split-K partial traffic stays small next to the X stream
   const long units = (long)tiles_m * nkb;

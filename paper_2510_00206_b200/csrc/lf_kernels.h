@@ -106,6 +106,7 @@ struct DownArgs {
   LfSegTable segs;
 };
 void down_config(int wmax, int* stages, int* stage_bytes);
+int down_extra_smem(int mask_mode);  // ①'s keep-bit ring (LF_DOWN_SPLIT), bytes
 int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs& args, int num_sms,
                 cudaStream_t stream);
 

@@ -41,8 +41,13 @@ __device__ __forceinline__ bool tile_needs_mask(const LfSegTable& t, const LfRou
 #ifndef LF_DOWN_SMEM_KB
 #define LF_DOWN_SMEM_KB 100
 #endif
+#ifndef LF_DOWN_SPLIT
+#define LF_DOWN_SPLIT 1  // Philox keep bits by 4 generator warps running ahead, masks applied by 4 others
+#endif
 namespace down {
 constexpr int X_BYTES = 128 * 64 * 2;  // 16 KB
+constexpr int BITS_SLOTS = 8;          // LF_DOWN_SPLIT: keep-bit ring depth (k-blocks the generators run ahead)
+constexpr int BITS_SLOT_BYTES = 128 * 8;  // one k-block's 64 keep bits per tile row
 // 2 CTAs / SM (register bound): ~2 x 100 KB of X tiles in flight per SM
 constexpr int SMEM_BUDGET = LF_DOWN_SMEM_KB * 1024;
 }  // namespace down
@@ -52,6 +57,10 @@ void down_config(int wmax, int* stages, int* stage_bytes) {
   *stage_bytes = down::X_BYTES + wmax * 128;
   int s = down::SMEM_BUDGET / *stage_bytes;
   *stages = s < 2 ? 2 : (s > 8 ? 8 : s);
+}
+
+int down_extra_smem(int mask_mode) {
+  return (LF_DOWN_SPLIT && mask_mode != 2) ? down::BITS_SLOTS * (down::BITS_SLOT_BYTES + 16) : 0;
 }
 
 constexpr int kDownThreads = 320;  // producer, MMA, 8 mask warps (2 per row quadrant; 4 also do the epilogue)
@@ -88,12 +97,19 @@ __global__ void __launch_bounds__(kDownThreads, LF_DOWN_MINB)
   using namespace down;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  // SPLIT (Philox path): warps 6..9 generate each k-block's keep bits into a ring of
+  // BITS_SLOTS slots (bits_full / bits_empty), up to BITS_SLOTS k-blocks ahead of the data;
+  // warps 2..5 apply them to the X tiles and flush. Otherwise all 8 mask warps do both.
+  constexpr bool SPLIT = LF_DOWN_SPLIT && !EXPLICIT;
+  uint8_t* sbits = smem + STAGES * STAGE_BYTES;  // SPLIT: [BITS_SLOTS][128 rows] x 8 bytes
+  uint64_t* full = reinterpret_cast<uint64_t*>(sbits + (SPLIT ? BITS_SLOTS * BITS_SLOT_BYTES : 0));
   uint64_t* empty = full + STAGES;
   uint64_t* masked = empty + STAGES;
   uint64_t* tfull = masked + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bits_full = tempty + 2;   // [BITS_SLOTS] SPLIT
+  uint64_t* bits_empty = bits_full + BITS_SLOTS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bits_empty + BITS_SLOTS);
   __shared__ int s_last;
 
   const uint32_t warp = warp_id(), lane = lane_id();
@@ -105,11 +121,17 @@ __global__ void __launch_bounds__(kDownThreads, LF_DOWN_MINB)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&masked[s], 8);
+      mbar_init(&masked[s], SPLIT ? 4 : 8);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4);
+    }
+    if constexpr (SPLIT) {
+      for (int i = 0; i < BITS_SLOTS; ++i) {
+        mbar_init(&bits_full[i], 4);
+        mbar_init(&bits_empty[i], 4);
+      }
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmX);
@@ -184,6 +206,100 @@ __global__ void __launch_bounds__(kDownThreads, LF_DOWN_MINB)
       ++it;
     }
     __syncwarp();
+  } else if (SPLIT && warp >= 6) {
+    // keep-bit generators (warps 6..9): thread <-> tile row 32*(warp&3) + lane; per k-block
+    // the row's 64 keep bits (8 Philox4x32-10 calls) into the ring and to the packed global
+    // mask ④ / ⑤ read. They never wait for X, only for a free slot.
+    const uint32_t q = warp & 3u;
+    const int rit = (int)(q * 32 + lane);
+    const uint64_t step_offset = table_offset(args.segs);
+    const int nbytes = (int)args.segs.ld_bits;
+    int slot = 0;
+    uint32_t bphase = 0;
+    if (gated) {
+      while (walk.next(sp)) {
+        const LfRoute rt = args.routes[sp.tile];
+        if (rt.col_hi - rt.col_lo <= 0) continue;
+        const int row = sp.tile * 128 + rit;
+        const int seg = row < args.m ? find_segment(args.segs, rt.seg_lo, rt.seg_hi, row) : -1;
+        const bool my_mask = seg >= 0 && args.segs.seg[seg].thr != 0;
+        const PhiloxRow pr = philox_row(args.segs.seg[seg >= 0 ? seg : 0], (uint32_t)(row + args.segs.row_base), step_offset);
+        // rows of p = 0 segments get all-ones bits (see the unsplit path below)
+        uint8_t* bits_row = (seg >= 0 && args.segs.bits) ? args.segs.bits + (int64_t)row * nbytes : nullptr;
+        for (int kb = sp.k0; kb < sp.k1; ++kb) {
+          uint64_t bits = ~0ull;
+          if (my_mask) {
+            if (args.segs.debug & 4096) {  // profiling: a fixed pattern instead of Philox
+              bits = 0xFBFFFFFEFBFFFFFEull ^ (uint64_t)kb;
+            } else {
+              uint32_t msk[8][4];  // unused here: the appliers expand the bits themselves
+              bits = philox_masks<8>(pr, kb * 64, msk);
+            }
+          }
+          mbar_wait(&bits_empty[slot], bphase ^ 1);
+          sts64(smem_u32(sbits + slot * BITS_SLOT_BYTES + rit * 8), bits);
+          if (bits_row && !(args.segs.debug & 16384)) store_bits64(bits_row, kb * 8, nbytes, bits);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bits_full[slot]);
+          if (++slot == BITS_SLOTS) { slot = 0; bphase ^= 1; }
+        }
+      }
+    }
+  } else if (SPLIT) {
+    // appliers (warps 2..5): thread <-> tile row; per k-block zero the dropped elements of
+    // the whole 128-byte row from the ring's bits, then release stage and slot; each span's
+    // partial sums are flushed here too
+    const uint32_t q = warp & 3u;
+    const int rit = (int)(q * 32 + lane);
+    int stage = 0, it = 0, slot = 0;
+    uint32_t phase = 0, bphase = 0;
+    while (walk.next(sp)) {
+      const LfRoute rt = args.routes[sp.tile];
+      const int N = rt.col_hi - rt.col_lo;
+      const int row = sp.tile * 128 + rit;
+      if (N <= 0) {  // no adapter in this row tile: its Ŝ rows are zero (written once, by the span at k = 0)
+        if (sp.k0 == 0 && row < args.m) zero_row(args.rtot, row, reinterpret_cast<__nv_bfloat16*>(args.s_hat));
+        continue;
+      }
+      for (int kb = sp.k0; kb < sp.k1; ++kb) {
+        if (gated) {
+          mbar_wait(&bits_full[slot], bphase);
+          const uint64_t bits = lds64(smem_u32(sbits + slot * BITS_SLOT_BYTES + rit * 8));
+          mbar_wait(&full[stage], phase);
+          if (!(args.segs.debug & 8192)) apply_row_sw128(smem + stage * STAGE_BYTES, rit, bits);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&masked[stage]);
+            mbar_arrive(&bits_empty[slot]);
+          }
+          if (++slot == BITS_SLOTS) { slot = 0; bphase ^= 1; }
+        }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      const int b = it & 1;
+      mbar_wait(&tfull[b], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + ((q * 32u) << 16) + b * args.rtot;
+      float* wrow = args.ws + (int64_t)row * args.rtot + rt.col_lo;
+      for (int c = 0; c < N; c += 16) {
+        uint32_t v[16];
+        tmem_ld16(taddr + c, v);
+        tmem_ld_wait();
+        if (row < args.m && !(args.segs.debug & 2)) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            red_add_v4(wrow + c + j, __uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                       __uint_as_float(v[j + 3]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+      tile_contribute(args.segs, rt, sp.tile, rit, sp.k1 - sp.k0, nkb, args.counters, args.ws,
+                      reinterpret_cast<__nv_bfloat16*>(args.s_hat), 1, &s_last);
+      ++it;
+    }
   } else {
     // mask warps 2..9: thread <-> tile row 32*(warp&3) + lane, half = which 4 of the row's 8
     // 16-byte chunks it masks; warps 2..5 (half 0) also flush each span's partial sums
@@ -358,8 +474,8 @@ int down_launch(const CUtensorMap& tm_x, const CUtensorMap& tm_a, const DownArgs
                 cudaStream_t stream) {
   int stages = 0, stage_bytes = 0;
   down_config(args.segs.wmax, &stages, &stage_bytes);
-  const int smem = stages * stage_bytes + 1024 + 256;
   const bool expl = args.segs.mask_mode == 2;
+  const int smem = stages * stage_bytes + 1024 + 256 + down_extra_smem(args.segs.mask_mode);
   auto kern = expl ? lf_down_kernel<true> : lf_down_kernel<false>;
   static std::atomic<uint64_t> attr_done[2] = {0, 0};
   if (ensure_smem_attr(kern, 200 * 1024, attr_done[expl ? 1 : 0])) return -1;
