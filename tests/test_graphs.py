@@ -164,3 +164,33 @@ def test_graphed_multi_lora_sees_optimizer_updates_bitwise():
         cap.lora_A[0].weight.data.mul_(-1.0)  # through .data: no version bump
     cap.invalidate_operands()
     check()
+
+
+def test_capture_with_a_layout_first_seen_inside_the_graph():
+    """A capturable multi-adapter layer whose column-block layout is first seen during a
+    capture gathers its operands inside the graph (no persistent copy is created mid-capture)
+    and the replay equals the eager layer; a later eager call creates the persistent copy."""
+    g = torch.Generator(device=DEV).manual_seed(12)
+    m, k, n = 512, 256, 256
+    w = (torch.randn(n, k, device=DEV, generator=g) / 16).to(torch.bfloat16)
+    ads = [AdapterConfig(8, 2.0, 0.0, 1), AdapterConfig(32, 1.0, 0.0, 2)]
+    layer = FusedMultiLoRA(w, ads, init="gaussian", capturable=True, generator=g)
+    x = torch.randn(m, k, device=DEV, generator=g).to(torch.bfloat16)
+    warm_segs = segments_from_lengths([1], [m])  # layout {adapter 1}
+    new_segs = segments_from_lengths([0, 1], [256, 256])  # layout {0, 1}: first seen in the capture
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side), torch.no_grad():
+        layer(x, warm_segs)
+    torch.cuda.current_stream().wait_stream(side)
+    n_before = len(layer._operands._d)
+    graph = torch.cuda.CUDAGraph()
+    with torch.no_grad(), torch.cuda.graph(graph):
+        y = layer(x, new_segs)
+    assert len(layer._operands._d) == n_before  # nothing persistent created inside the capture
+    graph.replay()
+    with torch.no_grad():
+        ref = layer(x, new_segs)
+    torch.cuda.synchronize()
+    assert torch.equal(y, ref)
+    assert len(layer._operands._d) == n_before + 1
