@@ -837,7 +837,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if constexpr (!MASKED) tn = seq.read(it + 1, lane == 0);
         t = tn;
         continue;
-      }
+      } else {
 #pragma unroll 1
       for (int c = c_lo; c < c_hi; c += 32) {
         const int col0 = n0 + c;
@@ -862,6 +862,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kGemmThreads, 1)
       if (lane == 0) mbar_arrive_cluster(tempty_leader[acc]);
       if constexpr (!MASKED) tn = seq.read(it + 1, lane == 0);
       t = tn;
+      }  // NACC == 2
     }
     }
   }
