@@ -409,3 +409,18 @@ def test_copy_column_blocks_matches_slicing():
         ref = flat[off:off + n * R].view(n, R)[:, c0:c0 + r]
         assert t.is_contiguous() and torch.equal(t, ref)
     assert got[-1].data_ptr() == flat[300 * 128 + 77 * 48:].data_ptr()  # whole rows: a view
+
+
+def test_copy_column_blocks_more_blocks_than_one_launch_holds():
+    """More than LF_MAX_COPY_BLOCKS blocks in one call: copied in several launches, each
+    block still equal to its torch slice."""
+    from paper_2510_00206_b200 import _lib
+    from paper_2510_00206_b200.functional import _gather_db_blocks
+
+    g = torch.Generator(device=DEV).manual_seed(6)
+    n, R = 96, 128
+    flat = torch.randn(n * R, device=DEV, generator=g)
+    specs = [(0, n, R, (8 * i) % 120, 8) for i in range(_lib.LF_MAX_COPY_BLOCKS + 6)]
+    got = _gather_db_blocks(flat, specs)
+    for (off, n_, R_, c0, r), t in zip(specs, got):
+        assert torch.equal(t, flat[off:off + n_ * R_].view(n_, R_)[:, c0:c0 + r])
